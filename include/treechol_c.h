@@ -1,0 +1,158 @@
+/*
+ * treechol_c.h -- C ABI of the B200-native nested recursive mixed-precision
+ * Cholesky (libtreechol_b200.so).
+ *
+ * This is the drop-in boundary: plain pointers, sizes and int status codes,
+ * no C++ or torch types.  Each entry point names the reference interface it
+ * replaces (file:line under /root/reference/proj).  The C++ headers in
+ * include/treechol/ (same API as the reference's proj/include/treechol) are
+ * implemented on top of these calls; INTEGRATION.md shows the ctypes and C++
+ * bindings a maintainer would add.
+ *
+ * Storage contract (matrix.hpp:11-24): matrices are column-major doubles,
+ * element (i,j) at a[j*lda + i].  The factor L overwrites the lower
+ * triangle; the strict upper triangle is never read or written.  Every value
+ * written is a double holding a value of its block's precision level.
+ */
+#ifndef TREECHOL_C_H
+#define TREECHOL_C_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes.  The C++ shim maps them back onto the reference exception
+ * types (errors.hpp:8-62) with identical what() text. */
+typedef enum {
+    TC_OK = 0,
+    TC_NOT_POSITIVE_DEFINITE = 1, /* NotPositiveDefinite, kernels.cpp:57-60  */
+    TC_NUMERICAL_BREAKDOWN = 2,   /* NumericalBreakdown, tree.cpp:19-31     */
+    TC_SINGULAR_DIAGONAL = 3,     /* SingularDiagonal, kernels.cpp:79-81    */
+    TC_INVALID_ARGUMENT = 4,      /* InvalidArgument, tree.cpp:72-76        */
+    TC_SYNTAX_ERROR = 5,          /* SyntaxError, precision.cpp:52-100      */
+    TC_VALIDATION_ERROR = 6,      /* ValidationError, precision.cpp:103-109 */
+    TC_CUDA_ERROR = 7,            /* device/runtime failure (no reference)  */
+    TC_NO_DEVICE = 8              /* no CUDA device: there is no CPU path   */
+} tc_status;
+
+/* Precision tags, identical to treechol::Precision (precision.hpp:14). */
+enum { TC_F16 = 0, TC_F32 = 1, TC_F64 = 2 };
+/* Kernel tags, identical to treechol::Kernel (flops.hpp:10). */
+enum { TC_K_POTRF = 0, TC_K_TRSM = 1, TC_K_SYRK = 2, TC_K_GEMM = 3 };
+
+/* FlopBreakdown (flops.hpp:17-48) */
+typedef struct {
+    uint64_t by_level[3];
+    uint64_t by_kernel[4];
+    uint64_t calls[4];
+} tc_flops;
+
+/* Failure details of the last factorization on a plan. */
+typedef struct {
+    int status;      /* tc_status */
+    int index;       /* NPD / singular: global row index (errors.hpp:27-43) */
+    int row0, row1;  /* breakdown: block rows a..b, cols c..d (tree.cpp:23-27) */
+    int col0, col1;
+    int elem_row;    /* breakdown: global element (i, j) */
+    int elem_col;
+    int diagonal;    /* breakdown: 1 = "diagonal" block, 0 = "off-diagonal" */
+} tc_info;
+
+typedef struct tc_plan tc_plan;
+
+/* ---- configuration (precision.hpp:81-99, precision.cpp:17-111) -------- */
+
+/* PrecisionConfig::parse.  levels must hold >= 16 ints. */
+int tc_config_parse(const char* text, int* levels, int* nlevels);
+/* PrecisionConfig::to_string into buf (NUL-terminated). */
+int tc_config_to_string(const int* levels, int nlevels, char* buf, int buflen);
+
+/* ---- planning (build_tree, tree.cpp:42-78; flop_breakdown, analysis.cpp:64-120) */
+
+/* flop_breakdown(n, b, config): static count, no device needed. */
+int tc_flop_breakdown(int n, int b, const int* levels, int nlevels, tc_flops* out);
+
+/* build_tree(view, config, b, quantize) + SolveOptions{leaf_size}: plans
+ * the factorization of an order-n matrix.  Pure host work: no device memory
+ * is touched until the first factorization.  leaf_size <= 0 means b. */
+int tc_plan_create(int n, int b, const int* levels, int nlevels, int quantize,
+                   int leaf_size, tc_plan** out);
+void tc_plan_destroy(tc_plan* plan);
+/* the flops tree_potrf adds to SolveOptions::flops (tree.cpp:106-152) */
+int tc_plan_flops(const tc_plan* plan, tc_flops* out);
+/* plan statistics: number of device ops / kernel launches per factorization */
+int tc_plan_stats(const tc_plan* plan, int* n_ops, int* n_launches, int* n_gemm_problems);
+/* execution knobs: use_graph (default 1), n_streams (default 6),
+ * use_tc (default 1: tcgen05 for FP16-operand GEMMs; 0 = SIMT path) */
+int tc_plan_set_option(tc_plan* plan, const char* key, int value);
+
+/* ---- factorization (tree_potrf, tree.cpp:106-125) ---------------------- */
+
+/* Device-resident factorization.  Reads A (column-major doubles, lda) from
+ * device memory dA_in and writes L's lower triangle into dL_out (may equal
+ * dA_in for the in-place drop-in).  stream: a cudaStream_t or NULL.
+ * If info != NULL the call synchronizes and reports the outcome; with
+ * info == NULL it only enqueues (read the outcome with tc_plan_status). */
+int tc_potrf_device(tc_plan* plan, const double* dA_in, int lda_in, double* dL_out,
+                    int lda_out, void* stream, tc_info* info);
+/* Host buffers: H2D copy, device factorization, D2H of the lower triangle,
+ * in place on A (exactly the reference's TileView contract). */
+int tc_potrf_host(tc_plan* plan, double* A, int lda, tc_info* info);
+/* Serialized, eagerly launched run with a CUDA event after every op:
+ * op_ms[i] = device time of op i (cap entries).  For roofline accounting. */
+int tc_plan_profile(tc_plan* plan, const double* dA_in, int lda_in, double* dL_out,
+                    int lda_out, void* stream, float* op_ms, int cap);
+/* op i of the plan: type (0 import, 1 export, 2 check, 3 quant, 4 dequant,
+ * 5 shadow, 6 potrf leaf, 7 trsm leaf, 8 gemm), gemm class (0 = tcgen05
+ * FP16, 1..5 SIMT classes, -1 otherwise), level, algorithmic flops, rect */
+int tc_plan_op_info(const tc_plan* plan, int i, int* type, int* gclass, int* level,
+                    double* flops, int* rect4);
+/* flops of the last run as SolveOptions::flops would hold them: the full
+ * plan on success, the calls completed before the failure otherwise */
+int tc_plan_run_flops(const tc_plan* plan, tc_flops* out);
+/* Synchronize the plan's last factorization and decode its status. */
+int tc_plan_status(tc_plan* plan, tc_info* info);
+/* Human-readable text identical to the reference exception's what(). */
+int tc_info_message(const tc_plan* plan, const tc_info* info, char* buf, int buflen);
+
+/* ---- solve (no reference counterpart) -------------- */
+
+/* Solves A X = B with the factor in dL (column-major doubles, lower
+ * triangle), B overwritten by X (n x nrhs, ldb).  Forward then backward
+ * substitution in FP64 on the device. */
+int tc_potrs_device(int n, const double* dL, int ldl, double* dB, int ldb, int nrhs,
+                    void* stream);
+
+/* ---- analysis (analysis.cpp) ------------------------------------------- */
+
+/* spd_generate(n, seed) into a host column-major buffer (lda >= n);
+ * bit-identical to analysis.cpp:12-28 (mt19937_64). */
+int tc_spd_generate_host(int n, uint64_t seed, double* A, int lda);
+/* the same matrix straight into device memory: the host streams the raw
+ * mt19937_64 draws, the device symmetrizes them (bit-identical) */
+int tc_spd_generate_device(int n, uint64_t seed, double* dA, int lda, void* stream);
+/* ||A - L L^T||_F / ||A||_F on the device in FP64 (analysis.cpp:30-62):
+ * only lower triangles are read; NaN if any lower entry is non-finite. */
+int tc_factorization_error_device(int n, const double* dA, int lda, const double* dL,
+                                  int ldl, double* out, void* stream);
+/* ||b - A x||_2 / (||A||_F ||x||_2 + ||b||_2) with A symmetric (lower read) */
+int tc_solve_residual_device(int n, const double* dA, int lda, const double* dX,
+                             const double* dB, double* out, void* stream);
+
+/* ---- misc --------------------------------------------------------------- */
+
+/* thread-local text of the last error (argument / CUDA failures) */
+const char* tc_last_error(void);
+/* 1 if a CUDA device is usable */
+int tc_device_available(void);
+/* library build tag */
+const char* tc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TREECHOL_C_H */

@@ -1,0 +1,519 @@
+"""treechol-b200: B200-native nested recursive mixed-precision Cholesky.
+
+Python host mirror of the reference's public interface
+(/root/reference/proj/include/treechol/*.hpp) over the C ABI of
+``libtreechol_b200.so`` (include/treechol_c.h).  Names, argument meaning and
+error behaviour follow the reference:
+
+    PrecisionConfig.parse / to_string / at_depth / leaf   precision.hpp:81-99
+    flop_breakdown(n, b, config)                          analysis.hpp:44
+    factor_matrix(a, config, b, quantize) -> FactorReport analysis.hpp:48
+    spd_generate(n, seed), factorization_error(a, l)      analysis.hpp:33-38
+    NotPositiveDefinite / NumericalBreakdown / ...        errors.hpp:8-62
+
+plus the device API the reference does not have: ``Plan`` (build once, factor
+device-resident matrices through a cached CUDA graph), ``potrs`` and the
+GPU backward-error metrics.  There is no CPU fallback: every compute call
+needs a CUDA device and raises ``NoDevice`` without one.
+
+Matrices are column-major doubles exactly like the reference's TileView.  On
+the host that is a Fortran-ordered numpy array; on the device a torch tensor
+``t`` of shape (n, n) whose memory is column-major, i.e. ``t[j, i] = A(i, j)``
+(``to_device`` / ``from_device`` convert).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtreechol_b200.so")
+
+HALF, SINGLE, DOUBLE = 0, 1, 2
+_LEVEL_NAMES = ("F16", "F32", "F64")
+POTRF, TRSM, SYRK, GEMM = 0, 1, 2, 3
+KERNEL_NAMES = ("POTRF-leaf", "TRSM-leaf", "SYRK-leaf", "GEMM")  # flops.cpp:5-12
+
+TC_OK, TC_NPD, TC_BREAKDOWN, TC_SINGULAR, TC_INVALID, TC_SYNTAX, TC_VALIDATION, TC_CUDA, TC_NO_DEVICE = range(9)
+
+OP_TYPES = ("import", "export", "check", "quant", "dequant", "shadow", "potrf", "trsm", "gemm")
+GEMM_CLASSES = ("tc16", "simt_f16", "simt_f32", "simt_f16d", "simt_f32d", "simt_f64")
+
+
+# ---------------------------------------------------------------- errors.hpp
+class Error(RuntimeError):
+    """treechol::Error"""
+
+
+class SyntaxError_(Error):
+    """treechol::SyntaxError (config grammar)"""
+
+
+class ValidationError(Error):
+    """treechol::ValidationError (non-monotone config)"""
+
+
+class InvalidArgument(Error):
+    """treechol::InvalidArgument"""
+
+
+class NotPositiveDefinite(Error):
+    def __init__(self, index: int, msg: str = ""):
+        super().__init__(msg or f"matrix is not positive definite: pivot {index} is non-positive or non-finite")
+        self.index = index
+
+
+class SingularDiagonal(Error):
+    def __init__(self, index: int, msg: str = ""):
+        super().__init__(msg or f"singular triangular factor: diagonal entry {index} is zero or non-finite")
+        self.index = index
+
+
+class NumericalBreakdown(Error):
+    """treechol::NumericalBreakdown"""
+
+
+class CudaError(Error):
+    """device / runtime failure (no reference counterpart)"""
+
+
+class NoDevice(Error):
+    """no CUDA device: the library has no CPU path"""
+
+
+# ---------------------------------------------------------------- C structs
+class _Flops(C.Structure):
+    _fields_ = [("by_level", C.c_uint64 * 3), ("by_kernel", C.c_uint64 * 4), ("calls", C.c_uint64 * 4)]
+
+
+class _Info(C.Structure):
+    _fields_ = [(n, C.c_int) for n in
+                ("status", "index", "row0", "row1", "col0", "col1", "elem_row", "elem_col", "diagonal")]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (make -C paper_2601_08082_b200/csrc)")
+    lib = C.CDLL(LIB_PATH)
+    I, D, P, U64 = C.c_int, C.c_double, C.c_void_p, C.c_uint64
+    PI = C.POINTER(C.c_int)
+    sig = {
+        "tc_config_parse": (I, [C.c_char_p, PI, PI]),
+        "tc_config_to_string": (I, [PI, I, C.c_char_p, I]),
+        "tc_flop_breakdown": (I, [I, I, PI, I, C.POINTER(_Flops)]),
+        "tc_plan_create": (I, [I, I, PI, I, I, I, C.POINTER(P)]),
+        "tc_plan_destroy": (None, [P]),
+        "tc_plan_flops": (I, [P, C.POINTER(_Flops)]),
+        "tc_plan_run_flops": (I, [P, C.POINTER(_Flops)]),
+        "tc_plan_stats": (I, [P, PI, PI, PI]),
+        "tc_plan_set_option": (I, [P, C.c_char_p, I]),
+        "tc_plan_op_info": (I, [P, I, PI, PI, PI, C.POINTER(D), PI]),
+        "tc_potrf_device": (I, [P, P, I, P, I, P, C.POINTER(_Info)]),
+        "tc_potrf_host": (I, [P, P, I, C.POINTER(_Info)]),
+        "tc_plan_profile": (I, [P, P, I, P, I, P, C.POINTER(C.c_float), I]),
+        "tc_plan_status": (I, [P, C.POINTER(_Info)]),
+        "tc_info_message": (I, [P, C.POINTER(_Info), C.c_char_p, I]),
+        "tc_potrs_device": (I, [I, P, I, P, I, I, P]),
+        "tc_spd_generate_host": (I, [I, U64, P, I]),
+        "tc_spd_generate_device": (I, [I, U64, P, I, P]),
+        "tc_factorization_error_device": (I, [I, P, I, P, I, C.POINTER(D), P]),
+        "tc_solve_residual_device": (I, [I, P, I, P, P, C.POINTER(D), P]),
+        "tc_last_error": (C.c_char_p, []),
+        "tc_device_available": (I, []),
+        "tc_version": (C.c_char_p, []),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+_lib = _load()
+EXPORTED = tuple(n for n in dir(_lib) if n.startswith("tc_"))
+
+
+def lib():
+    return _lib
+
+
+def _last_error() -> str:
+    return (_lib.tc_last_error() or b"").decode()
+
+
+def _raise(code: int, info: _Info | None = None):
+    msg = _last_error()
+    if code == TC_OK:
+        return
+    if code == TC_NPD:
+        raise NotPositiveDefinite(info.index if info else -1, msg)
+    if code == TC_SINGULAR:
+        raise SingularDiagonal(info.index if info else -1, msg)
+    if code == TC_BREAKDOWN:
+        raise NumericalBreakdown(msg)
+    if code == TC_SYNTAX:
+        raise SyntaxError_(msg)
+    if code == TC_VALIDATION:
+        raise ValidationError(msg)
+    if code == TC_INVALID:
+        raise InvalidArgument(msg)
+    if code == TC_NO_DEVICE:
+        raise NoDevice(msg)
+    raise CudaError(msg)
+
+
+def version() -> str:
+    return _lib.tc_version().decode()
+
+
+def device_available() -> bool:
+    return bool(_lib.tc_device_available())
+
+
+# ---------------------------------------------------------------- precision.hpp
+class Precision:
+    Half, Single, Double = HALF, SINGLE, DOUBLE
+
+
+def range_max(p: int) -> float:  # precision.hpp:20-26
+    return (65504.0, 3.4028234663852886e38, 1.7976931348623157e308)[p]
+
+
+def unit_roundoff(p: int) -> float:  # precision.hpp:28-34
+    return (2.0 ** -11, 2.0 ** -24, 2.0 ** -53)[p]
+
+
+def precision_name(p: int) -> str:
+    return _LEVEL_NAMES[p]
+
+
+@dataclass(frozen=True)
+class PrecisionConfig:
+    """precision.hpp:81-99: outer -> inner levels, saturating at the last."""
+    levels: tuple
+
+    def at_depth(self, d: int) -> int:
+        return self.levels[min(d, len(self.levels) - 1)]
+
+    def leaf(self) -> int:
+        return self.levels[-1]
+
+    def to_string(self) -> str:
+        arr = (C.c_int * len(self.levels))(*self.levels)
+        buf = C.create_string_buffer(128)
+        _raise(_lib.tc_config_to_string(arr, len(self.levels), buf, 128))
+        return buf.value.decode()
+
+    def __str__(self):
+        return self.to_string()
+
+    @staticmethod
+    def parse(text: str) -> "PrecisionConfig":
+        arr = (C.c_int * 16)()
+        n = C.c_int(0)
+        _raise(_lib.tc_config_parse(text.encode(), arr, C.byref(n)))
+        return PrecisionConfig(tuple(arr[i] for i in range(n.value)))
+
+
+def _cfg(config) -> PrecisionConfig:
+    if isinstance(config, PrecisionConfig):
+        return config
+    if isinstance(config, str):
+        return PrecisionConfig.parse(config)
+    return PrecisionConfig(tuple(int(x) for x in config))
+
+
+# ---------------------------------------------------------------- flops.hpp
+@dataclass
+class FlopBreakdown:
+    by_level: list = field(default_factory=lambda: [0, 0, 0])
+    by_kernel: list = field(default_factory=lambda: [0, 0, 0, 0])
+    calls: list = field(default_factory=lambda: [0, 0, 0, 0])
+
+    @classmethod
+    def _from(cls, f: _Flops):
+        return cls(list(f.by_level), list(f.by_kernel), list(f.calls))
+
+    def total(self) -> int:
+        return sum(self.by_level)
+
+    def level_fraction(self, p: int) -> float:
+        t = self.total()
+        return 0.0 if t == 0 else self.by_level[p] / t
+
+    def kernel_fraction(self, k: int) -> float:
+        t = self.total()
+        return 0.0 if t == 0 else self.by_kernel[k] / t
+
+    def as_tuple(self):
+        return tuple(self.by_level) + tuple(self.by_kernel) + tuple(self.calls)
+
+
+def flop_breakdown(n: int, b: int, config) -> FlopBreakdown:
+    """analysis.cpp:64-120 (static, no device)."""
+    cfg = _cfg(config)
+    arr = (C.c_int * len(cfg.levels))(*cfg.levels)
+    out = _Flops()
+    _raise(_lib.tc_flop_breakdown(n, b, arr, len(cfg.levels), C.byref(out)))
+    return FlopBreakdown._from(out)
+
+
+def potrf_flops(n: int) -> int:
+    """n(n+1)(2n+1)/6, the total of every tree (analysis.cpp:66-68)."""
+    return n * (n + 1) * (2 * n + 1) // 6
+
+
+# ---------------------------------------------------------------- device glue
+def _ptr(t) -> int:
+    """raw device / host pointer of a torch tensor or numpy array"""
+    if hasattr(t, "data_ptr"):
+        return t.data_ptr()
+    return t.ctypes.data
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        return None
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def to_device(a: np.ndarray, device="cuda"):
+    """Fortran float64 (n, m) -> torch tensor with the same column-major memory."""
+    import torch
+    a = np.asfortranarray(a, dtype=np.float64)
+    return torch.from_numpy(a.T).to(device)
+
+
+def from_device(t) -> np.ndarray:
+    """inverse of to_device: a Fortran-ordered numpy array"""
+    return np.asfortranarray(t.detach().cpu().numpy().T)
+
+
+def _check_dev(t, n, what):
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float64:
+        raise InvalidArgument(f"{what} must be a CUDA float64 tensor")
+    if t.dim() != 2 or t.shape[1] < n or not t.is_contiguous():
+        raise InvalidArgument(f"{what} must be a contiguous (cols, ld>=n) tensor")
+    return t.shape[1]
+
+
+@dataclass
+class FactorStatus:
+    status: str            # ok | not-positive-definite | numerical-breakdown | singular-diagonal
+    detail: str = ""
+    index: int = -1
+    info: _Info | None = None
+
+
+_STATUS_NAMES = {TC_OK: "ok", TC_NPD: "not-positive-definite", TC_BREAKDOWN: "numerical-breakdown",
+                 TC_SINGULAR: "singular-diagonal"}
+
+
+class Plan:
+    """build_tree + tree_potrf for one (n, b, config, quantize), planned once
+    (tree.hpp:42-66).  Device workspace is allocated on the first factor."""
+
+    def __init__(self, n: int, b: int, config, quantize: bool = True, leaf_size: int = 0, use_tc: bool = True,
+                 use_graph: bool = True, n_streams: int = 0):
+        self.cfg = _cfg(config)
+        self.n, self.b, self.quantize = int(n), int(b), bool(quantize)
+        arr = (C.c_int * len(self.cfg.levels))(*self.cfg.levels)
+        h = C.c_void_p()
+        _raise(_lib.tc_plan_create(self.n, self.b, arr, len(self.cfg.levels), int(self.quantize), int(leaf_size),
+                                   C.byref(h)))
+        self._h = h
+        if not use_tc:
+            self.set_option("use_tc", 0)
+        if not use_graph:
+            self.set_option("use_graph", 0)
+        if n_streams:
+            self.set_option("n_streams", n_streams)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _lib.tc_plan_destroy(h)
+            self._h = None
+
+    def set_option(self, key: str, value: int):
+        _raise(_lib.tc_plan_set_option(self._h, key.encode(), int(value)))
+
+    def flops(self) -> FlopBreakdown:
+        out = _Flops()
+        _raise(_lib.tc_plan_flops(self._h, C.byref(out)))
+        return FlopBreakdown._from(out)
+
+    def run_flops(self) -> FlopBreakdown:
+        out = _Flops()
+        _raise(_lib.tc_plan_run_flops(self._h, C.byref(out)))
+        return FlopBreakdown._from(out)
+
+    def stats(self):
+        a, b, c = C.c_int(), C.c_int(), C.c_int()
+        _raise(_lib.tc_plan_stats(self._h, C.byref(a), C.byref(b), C.byref(c)))
+        return {"ops": a.value, "launches": b.value, "gemm_problems": c.value}
+
+    def op_info(self, i: int):
+        t, g, lv = C.c_int(), C.c_int(), C.c_int()
+        fl = C.c_double()
+        r = (C.c_int * 4)()
+        _raise(_lib.tc_plan_op_info(self._h, i, C.byref(t), C.byref(g), C.byref(lv), C.byref(fl), r))
+        return {"type": OP_TYPES[t.value], "gclass": GEMM_CLASSES[g.value] if g.value >= 0 else None,
+                "level": lv.value, "flops": fl.value, "rect": tuple(r)}
+
+    def _status(self, code: int, info: _Info) -> FactorStatus:
+        if code in (TC_OK, TC_NPD, TC_BREAKDOWN, TC_SINGULAR):
+            buf = C.create_string_buffer(512)
+            _lib.tc_info_message(self._h, C.byref(info), buf, 512)
+            return FactorStatus(_STATUS_NAMES[code], buf.value.decode(), info.index, info)
+        _raise(code, info)
+
+    def factor_device(self, a_in, l_out=None, stream=None, sync: bool = True):
+        """Device-resident tree_potrf: reads a_in, writes L's lower triangle
+        into l_out (default: in place).  Returns FactorStatus when sync."""
+        n = self.n
+        lda = _check_dev(a_in, n, "a_in")
+        l_out = a_in if l_out is None else l_out
+        ldl = _check_dev(l_out, n, "l_out")
+        info = _Info()
+        code = _lib.tc_potrf_device(self._h, _ptr(a_in), lda, _ptr(l_out), ldl, _stream_ptr(stream),
+                                    C.byref(info) if sync else None)
+        if not sync:
+            _raise(code)
+            return None
+        return self._status(code, info)
+
+    def status(self) -> FactorStatus:
+        info = _Info()
+        code = _lib.tc_plan_status(self._h, C.byref(info))
+        return self._status(code, info)
+
+    def factor_host(self, a: np.ndarray) -> FactorStatus:
+        """tree_potrf on a host Fortran float64 array, in place (TileView contract)."""
+        if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.f_contiguous):
+            raise InvalidArgument("a must be a Fortran-ordered float64 array")
+        info = _Info()
+        code = _lib.tc_potrf_host(self._h, a.ctypes.data, a.shape[0], C.byref(info))
+        return self._status(code, info)
+
+    def profile(self, a_in, l_out, stream=None):
+        """serialized eager run; per-op device milliseconds"""
+        n_ops = self.stats()["ops"]
+        out = (C.c_float * n_ops)()
+        _raise(_lib.tc_plan_profile(self._h, _ptr(a_in), _check_dev(a_in, self.n, "a_in"), _ptr(l_out),
+                                    _check_dev(l_out, self.n, "l_out"), _stream_ptr(stream), out, n_ops))
+        return list(out)
+
+
+# ---------------------------------------------------------------- analysis.hpp
+def spd_generate(n: int, seed: int) -> np.ndarray:
+    """analysis.cpp:12-28, bit-identical (mt19937_64), Fortran float64."""
+    a = np.empty((n, n), dtype=np.float64, order="F")
+    _raise(_lib.tc_spd_generate_host(n, C.c_uint64(seed), a.ctypes.data, n))
+    return a
+
+
+def spd_generate_device(n: int, seed: int, device="cuda"):
+    """spd_generate(n, seed) straight into a device tensor (column-major
+    memory, bit-identical to analysis.cpp:12-28)."""
+    import torch
+    t = torch.empty((n, n), dtype=torch.float64, device=device)
+    _raise(_lib.tc_spd_generate_device(n, C.c_uint64(seed), _ptr(t), n, None))
+    return t
+
+
+def factorization_error_device(a_dev, l_dev, n: int | None = None, stream=None) -> float:
+    """||A - L L^T||_F / ||A||_F in FP64 on the device (analysis.cpp:30-62)."""
+    n = n or a_dev.shape[0]
+    out = C.c_double()
+    _raise(_lib.tc_factorization_error_device(n, _ptr(a_dev), _check_dev(a_dev, n, "a"), _ptr(l_dev),
+                                              _check_dev(l_dev, n, "l"), C.byref(out), _stream_ptr(stream)))
+    return out.value
+
+
+def factorization_error(a: np.ndarray, l: np.ndarray) -> float:
+    """host-array convenience wrapper over the device metric"""
+    return factorization_error_device(to_device(a), to_device(l))
+
+
+def potrs_device(l_dev, b_dev, n: int | None = None, stream=None):
+    """A X = B with the factor L (lower, column-major); B (n x nrhs column-
+    major, i.e. torch shape (nrhs, ldb)) is overwritten by X."""
+    n = n or l_dev.shape[0]
+    ldl = _check_dev(l_dev, n, "L")
+    import torch
+    if not (isinstance(b_dev, torch.Tensor) and b_dev.is_cuda and b_dev.dtype == torch.float64):
+        raise InvalidArgument("B must be a CUDA float64 tensor")
+    b2 = b_dev if b_dev.dim() == 2 else b_dev.view(1, -1)
+    _raise(_lib.tc_potrs_device(n, _ptr(l_dev), ldl, _ptr(b2), b2.shape[1], b2.shape[0], _stream_ptr(stream)))
+    return b_dev
+
+
+def solve_residual_device(a_dev, x_dev, b_dev, n: int | None = None, stream=None) -> float:
+    n = n or a_dev.shape[0]
+    out = C.c_double()
+    _raise(_lib.tc_solve_residual_device(n, _ptr(a_dev), _check_dev(a_dev, n, "a"), _ptr(x_dev), _ptr(b_dev),
+                                         C.byref(out), _stream_ptr(stream)))
+    return out.value
+
+
+@dataclass
+class FactorReport:
+    """analysis.hpp:15-27"""
+    n: int = 0
+    config: str = ""
+    b: int = 0
+    quantize: bool = True
+    seed: int = 0
+    status: str = ""
+    detail: str = ""
+    rel_error: float = float("nan")
+    digits: float = float("nan")
+    flops: FlopBreakdown = field(default_factory=FlopBreakdown)
+    wall_ms: float = 0.0
+
+
+def factor_matrix(a: np.ndarray, config, b: int, quantize: bool = True, plan: Plan | None = None) -> FactorReport:
+    """analysis.cpp:122-155 on the device: copy A (the one permitted copy),
+    factor it, map failures to a status, measure ||A - LL^T||/||A||."""
+    import torch
+    cfg = _cfg(config)
+    n = a.shape[0]
+    rep = FactorReport(n=n, config=cfg.to_string(), b=b, quantize=quantize)
+    plan = plan or Plan(n, b, cfg, quantize)
+    a_dev = to_device(a)
+    l_dev = torch.empty_like(a_dev)
+    l_dev.copy_(a_dev)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    st = plan.factor_device(a_dev, l_dev)
+    rep.wall_ms = (time.perf_counter() - t0) * 1e3
+    rep.flops = plan.run_flops()
+    if st.status == "ok":
+        rep.status = "ok"
+        rep.rel_error = factorization_error_device(a_dev, l_dev)
+        rep.digits = -math.log10(rep.rel_error) if rep.rel_error > 0 else float("inf")
+    elif st.status == "singular-diagonal":
+        raise SingularDiagonal(st.index, st.detail)
+    else:
+        rep.status, rep.detail = st.status, st.detail
+    return rep
+
+
+def accuracy_sweep(sizes, configs, b, seeds, quantize=True):
+    """analysis.cpp:157-173: n-major, then config, then seed."""
+    out = []
+    for n in sizes:
+        for cfg in configs:
+            plan = Plan(n, b, _cfg(cfg), quantize)
+            for s in seeds:
+                r = factor_matrix(spd_generate(n, s), cfg, b, quantize, plan=plan)
+                r.seed = s
+                out.append(r)
+    return out

@@ -1,0 +1,440 @@
+// capi.cpp -- extern "C" entry points of libtreechol_b200.so (treechol_c.h).
+// No exception crosses this boundary: every entry point returns a tc_status
+// and leaves a thread-local message for tc_last_error().
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/treechol_c.h"
+#include "engine.hpp"
+#include "launch.hpp"
+#include "plan.hpp"
+
+using namespace tcb;
+
+struct tc_plan {
+    std::unique_ptr<Engine> eng;
+    Failure last;
+    bool have_result = false;
+    double* d_host_stage = nullptr;  // device copy used by tc_potrf_host
+    ~tc_plan() {
+        if (d_host_stage) cudaFree(d_host_stage);
+    }
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    return fail(TC_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+bool levels_ok(const int* levels, int nlevels) {
+    if (!levels || nlevels < 1) return false;
+    for (int i = 0; i < nlevels; ++i)
+        if (levels[i] < 0 || levels[i] > 2) return false;
+    return true;
+}
+
+void fill_info(const Failure& f, tc_info* info) {
+    if (!info) return;
+    std::memset(info, 0, sizeof(*info));
+    info->status = f.status;
+    info->index = f.index;
+    info->row0 = f.block.r0;
+    info->row1 = f.block.r0 + f.block.m - 1;
+    info->col0 = f.block.c0;
+    info->col1 = f.block.c0 + f.block.n - 1;
+    info->elem_row = f.elem_row;
+    info->elem_col = f.elem_col;
+    info->diagonal = f.diagonal;
+}
+
+std::string message_of(const tc_info& info) {
+    char buf[256];
+    switch (info.status) {
+        case TC_NOT_POSITIVE_DEFINITE:
+            std::snprintf(buf, sizeof buf, "matrix is not positive definite: pivot %d is non-positive or non-finite",
+                          info.index);
+            return buf;
+        case TC_SINGULAR_DIAGONAL:
+            std::snprintf(buf, sizeof buf, "singular triangular factor: diagonal entry %d is zero or non-finite",
+                          info.index);
+            return buf;
+        case TC_NUMERICAL_BREAKDOWN:
+            std::snprintf(buf, sizeof buf,
+                          "non-finite value in %s block (rows %d..%d, cols %d..%d) at element (%d, %d)",
+                          info.diagonal ? "diagonal" : "off-diagonal", info.row0, info.row1, info.col0, info.col1,
+                          info.elem_row, info.elem_col);
+            return buf;
+        default:
+            return "";
+    }
+}
+
+void flops_out(const uint64_t L[3], const uint64_t K[4], const uint64_t C[4], tc_flops* out) {
+    for (int i = 0; i < 3; ++i) out->by_level[i] = L[i];
+    for (int i = 0; i < 4; ++i) {
+        out->by_kernel[i] = K[i];
+        out->calls[i] = C[i];
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tc_last_error(void) { return g_err.c_str(); }
+
+const char* tc_version(void) { return "treechol-b200 0.1 (sm_100a)"; }
+
+int tc_device_available(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n > 0 ? 1 : 0;
+}
+
+int tc_config_parse(const char* text, int* levels, int* nlevels) {
+    if (!text || !levels || !nlevels) return fail(TC_INVALID_ARGUMENT, "null argument");
+    std::vector<int> lv;
+    std::string err;
+    const int r = parse_config(text, lv, err);
+    if (r == 1) return fail(TC_SYNTAX_ERROR, err);
+    if (r == 2) return fail(TC_VALIDATION_ERROR, err);
+    if (lv.size() > 16) return fail(TC_INVALID_ARGUMENT, "more than 16 precision levels");
+    for (size_t i = 0; i < lv.size(); ++i) levels[i] = lv[i];
+    *nlevels = int(lv.size());
+    return TC_OK;
+}
+
+int tc_config_to_string(const int* levels, int nlevels, char* buf, int buflen) {
+    if (!levels_ok(levels, nlevels) || !buf || buflen < 1) return fail(TC_INVALID_ARGUMENT, "bad config");
+    const std::string s = config_to_string(std::vector<int>(levels, levels + nlevels));
+    std::snprintf(buf, size_t(buflen), "%s", s.c_str());
+    return TC_OK;
+}
+
+int tc_flop_breakdown(int n, int b, const int* levels, int nlevels, tc_flops* out) {
+    if (!out) return fail(TC_INVALID_ARGUMENT, "null output");
+    if (n < 1 || b < 1) return fail(TC_INVALID_ARGUMENT, "flop_breakdown: n, b >= 1");
+    if (!levels_ok(levels, nlevels)) return fail(TC_INVALID_ARGUMENT, "empty precision config");
+    uint64_t L[3], K[4], C[4];
+    static_flop_breakdown(n, b, std::vector<int>(levels, levels + nlevels), L, K, C);
+    flops_out(L, K, C, out);
+    return TC_OK;
+}
+
+int tc_plan_create(int n, int b, const int* levels, int nlevels, int quantize, int leaf_size, tc_plan** out) {
+    if (!out) return fail(TC_INVALID_ARGUMENT, "null output");
+    *out = nullptr;
+    if (b < 1) return fail(TC_INVALID_ARGUMENT, "leaf size must be >= 1");
+    if (!levels || nlevels < 1) return fail(TC_INVALID_ARGUMENT, "empty precision config");
+    if (!levels_ok(levels, nlevels)) return fail(TC_INVALID_ARGUMENT, "precision level out of range");
+    if (n < 1) return fail(TC_INVALID_ARGUMENT, "tree requires a square matrix of order >= 1");
+    if (n >= (1 << 20)) return fail(TC_INVALID_ARGUMENT, "order too large (n < 2^20)");
+    try {
+        PlanOptions po;
+        Plan p = Plan::make(n, b, std::vector<int>(levels, levels + nlevels), quantize != 0, leaf_size, po);
+        auto* h = new tc_plan;
+        h->eng = std::make_unique<Engine>(std::move(p));
+        *out = h;
+        return TC_OK;
+    } catch (const std::invalid_argument& e) {
+        return fail(TC_INVALID_ARGUMENT, e.what());
+    } catch (const std::exception& e) {
+        return fail(TC_INVALID_ARGUMENT, e.what());
+    }
+}
+
+void tc_plan_destroy(tc_plan* plan) { delete plan; }
+
+int tc_plan_flops(const tc_plan* plan, tc_flops* out) {
+    if (!plan || !out) return fail(TC_INVALID_ARGUMENT, "null argument");
+    uint64_t L[3], K[4], C[4];
+    plan->eng->plan.flop_totals(L, K, C);
+    flops_out(L, K, C, out);
+    return TC_OK;
+}
+
+// flops the reference would have added before stopping (partial on failure)
+int tc_plan_run_flops(const tc_plan* plan, tc_flops* out) {
+    if (!plan || !out) return fail(TC_INVALID_ARGUMENT, "null argument");
+    uint64_t L[3], K[4], C[4];
+    const uint32_t lim = (plan->have_result && plan->last.status) ? plan->last.seq : 0xffffffffu;
+    plan->eng->plan.flop_totals(L, K, C, lim);
+    flops_out(L, K, C, out);
+    return TC_OK;
+}
+
+int tc_plan_stats(const tc_plan* plan, int* n_ops, int* n_launches, int* n_gemm_problems) {
+    if (!plan) return fail(TC_INVALID_ARGUMENT, "null plan");
+    if (n_ops) *n_ops = int(plan->eng->plan.ops.size());
+    if (n_launches) *n_launches = plan->eng->launches_per_run();
+    if (n_gemm_problems) *n_gemm_problems = int(plan->eng->plan.probs.size());
+    return TC_OK;
+}
+
+int tc_plan_set_option(tc_plan* plan, const char* key, int value) {
+    if (!plan || !key) return fail(TC_INVALID_ARGUMENT, "null argument");
+    Engine& e = *plan->eng;
+    const std::string k = key;
+    if (k == "use_graph") {
+        e.use_graph = value != 0;
+        return TC_OK;
+    }
+    if (k == "n_streams") {
+        if (e.ready()) return fail(TC_INVALID_ARGUMENT, "n_streams must be set before the first run");
+        e.n_streams = value < 1 ? 1 : value;
+        return TC_OK;
+    }
+    if (k == "use_tc") {
+        if (e.ready()) return fail(TC_INVALID_ARGUMENT, "use_tc must be set before the first run");
+        if (bool(value) == e.plan.opt.use_tc) return TC_OK;
+        PlanOptions po = e.plan.opt;
+        po.use_tc = value != 0;
+        Plan p = Plan::make(e.plan.n, e.plan.b, e.plan.levels, e.plan.quantize, e.plan.leaf_size, po);
+        const bool g = e.use_graph;
+        const int s = e.n_streams;
+        plan->eng = std::make_unique<Engine>(std::move(p));
+        plan->eng->use_graph = g;
+        plan->eng->n_streams = s;
+        return TC_OK;
+    }
+    return fail(TC_INVALID_ARGUMENT, "unknown option '" + k + "'");
+}
+
+// per-op metadata for profiling: type, gemm class, level, flops, rect
+int tc_plan_op_info(const tc_plan* plan, int i, int* type, int* gclass, int* level, double* flops, int* rect4) {
+    if (!plan || i < 0 || i >= int(plan->eng->plan.ops.size())) return fail(TC_INVALID_ARGUMENT, "bad op index");
+    const Op& op = plan->eng->plan.ops[i];
+    if (type) *type = op.type;
+    if (gclass) *gclass = op.type == OP_GEMM ? op.gclass : -1;
+    if (level) *level = op.level;
+    if (flops) *flops = op.flops;
+    if (rect4) {
+        rect4[0] = op.rect.r0;
+        rect4[1] = op.rect.c0;
+        rect4[2] = op.rect.m;
+        rect4[3] = op.rect.n;
+    }
+    return TC_OK;
+}
+
+int tc_potrf_device(tc_plan* plan, const double* dA_in, int lda_in, double* dL_out, int lda_out, void* stream,
+                    tc_info* info) {
+    if (!plan || !dA_in || !dL_out) return fail(TC_INVALID_ARGUMENT, "null argument");
+    const int n = plan->eng->plan.n;
+    if (lda_in < n || lda_out < n) return fail(TC_INVALID_ARGUMENT, "leading dimension < n");
+    if (!tc_device_available()) return fail(TC_NO_DEVICE, "no CUDA device (there is no CPU fallback)");
+    std::string err;
+    plan->have_result = false;
+    if (!plan->eng->enqueue(dA_in, lda_in, dL_out, lda_out, static_cast<cudaStream_t>(stream), &err))
+        return fail(TC_CUDA_ERROR, err);
+    if (!info) return TC_OK;
+    return tc_plan_status(plan, info);
+}
+
+int tc_plan_status(tc_plan* plan, tc_info* info) {
+    if (!plan) return fail(TC_INVALID_ARGUMENT, "null plan");
+    std::string err;
+    Failure f;
+    if (!plan->eng->result(&f, &err)) return fail(TC_CUDA_ERROR, err);
+    plan->last = f;
+    plan->have_result = true;
+    fill_info(f, info);
+    if (f.status) {
+        tc_info tmp;
+        fill_info(f, &tmp);
+        g_err = message_of(tmp);
+    }
+    return f.status;
+}
+
+int tc_info_message(const tc_plan*, const tc_info* info, char* buf, int buflen) {
+    if (!info || !buf || buflen < 1) return fail(TC_INVALID_ARGUMENT, "null argument");
+    std::snprintf(buf, size_t(buflen), "%s", message_of(*info).c_str());
+    return TC_OK;
+}
+
+int tc_potrf_host(tc_plan* plan, double* A, int lda, tc_info* info) {
+    if (!plan || !A) return fail(TC_INVALID_ARGUMENT, "null argument");
+    const int n = plan->eng->plan.n;
+    if (lda < n) return fail(TC_INVALID_ARGUMENT, "leading dimension < n");
+    if (!tc_device_available()) return fail(TC_NO_DEVICE, "no CUDA device (there is no CPU fallback)");
+    cudaError_t e;
+    if (!plan->d_host_stage) {
+        e = cudaMalloc(&plan->d_host_stage, sizeof(double) * size_t(n) * size_t(n));
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+    }
+    cudaStream_t s = nullptr;
+    e = cudaMemcpy2DAsync(plan->d_host_stage, sizeof(double) * size_t(n), A, sizeof(double) * size_t(lda),
+                          sizeof(double) * size_t(n), size_t(n), cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(e, "H2D");
+    tc_info local;
+    int st = tc_potrf_device(plan, plan->d_host_stage, n, plan->d_host_stage, n, s, &local);
+    if (st == TC_CUDA_ERROR || st == TC_NO_DEVICE || st == TC_INVALID_ARGUMENT) return st;
+    // lower triangle back (upper columns untouched on both sides)
+    for (int j0 = 0; j0 < n; j0 += 256) {
+        const int w = std::min(256, n - j0);
+        // rows j0..n-1 of columns j0..j0+w-1: a trapezoid covering the lower part
+        e = cudaMemcpy2DAsync(A + size_t(j0) * lda + j0, sizeof(double) * size_t(lda),
+                              plan->d_host_stage + size_t(j0) * n + j0, sizeof(double) * size_t(n),
+                              sizeof(double) * size_t(n - j0), size_t(w), cudaMemcpyDeviceToHost, s);
+        if (e != cudaSuccess) return cuda_fail(e, "D2H");
+    }
+    e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, "sync");
+    if (info) *info = local;
+    return st;
+}
+
+int tc_plan_profile(tc_plan* plan, const double* dA_in, int lda_in, double* dL_out, int lda_out, void* stream,
+                    float* op_ms, int cap) {
+    if (!plan || !dA_in || !dL_out || !op_ms) return fail(TC_INVALID_ARGUMENT, "null argument");
+    std::vector<float> ms;
+    std::string err;
+    if (!plan->eng->profile(dA_in, lda_in, dL_out, lda_out, static_cast<cudaStream_t>(stream), ms, &err))
+        return fail(TC_CUDA_ERROR, err);
+    for (int i = 0; i < cap && i < int(ms.size()); ++i) op_ms[i] = ms[i];
+    return TC_OK;
+}
+
+// ---------------------------------------------------------------- analysis
+
+int tc_spd_generate_host(int n, uint64_t seed, double* A, int lda) {
+    if (!A || n < 1 || lda < n) return fail(TC_INVALID_ARGUMENT, "bad arguments");
+    // analysis.cpp:12-28 streamed in one pass: draw t = j*n + i is R(i,j);
+    // the first-drawn partner of each pair is parked in the lower triangle
+    std::mt19937_64 rng(seed);
+    const double dn = double(n);
+    for (int j = 0; j < n; ++j) {
+        double* col = A + size_t(j) * lda;
+        for (int i = 0; i < n; ++i) {
+            const double r = double(rng() >> 11) * 0x1p-53;
+            if (i < j) {
+                double& lo = A[size_t(i) * lda + j];  // holds R(j, i)
+                const double v = 0.5 * (r + lo);      // 0.5 * (R(i,j) + R(j,i))
+                col[i] = v;
+                lo = v;
+            } else if (i == j) {
+                col[i] = 0.5 * (r + r) + dn;
+            } else {
+                col[i] = r;
+            }
+        }
+    }
+    return TC_OK;
+}
+
+int tc_spd_generate_device(int n, uint64_t seed, double* dA, int lda, void* stream) {
+    if (!dA || n < 1 || lda < n) return fail(TC_INVALID_ARGUMENT, "bad arguments");
+    if (!tc_device_available()) return fail(TC_NO_DEVICE, "no CUDA device");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    // the draw stream is sequential (mt19937_64): the host produces whole
+    // columns of raw R into two pinned buffers while the previous chunk is in
+    // flight; the device then symmetrizes in place (bit-identical)
+    const size_t ccols = std::max<size_t>(1, (size_t(64) << 20) / size_t(n));  // ~512 MB chunks
+    double* hbuf[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    cudaError_t e = cudaSuccess;
+    for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
+        e = cudaMallocHost(&hbuf[k], sizeof(double) * ccols * size_t(n));
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming);
+    }
+    std::mt19937_64 rng(seed);
+    int k = 0;
+    for (size_t c0 = 0; c0 < size_t(n) && e == cudaSuccess; c0 += ccols, k ^= 1) {
+        const size_t w = std::min(ccols, size_t(n) - c0);
+        e = cudaEventSynchronize(ev[k]);
+        if (e != cudaSuccess) break;
+        double* h = hbuf[k];
+        const size_t cnt = w * size_t(n);
+        for (size_t t = 0; t < cnt; ++t) h[t] = double(rng() >> 11) * 0x1p-53;
+        e = cudaMemcpy2DAsync(dA + c0 * size_t(lda), sizeof(double) * size_t(lda), h, sizeof(double) * size_t(n),
+                              sizeof(double) * size_t(n), w, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess) e = cudaEventRecord(ev[k], s);
+    }
+    if (e == cudaSuccess) {
+        launch_symmetrize(dA, lda, n, s);
+        e = cudaStreamSynchronize(s);
+    }
+    if (e == cudaSuccess) e = cudaGetLastError();
+    for (int j = 0; j < 2; ++j) {
+        if (hbuf[j]) cudaFreeHost(hbuf[j]);
+        if (ev[j]) cudaEventDestroy(ev[j]);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "spd_generate_device");
+    return TC_OK;
+}
+
+int tc_factorization_error_device(int n, const double* dA, int lda, const double* dL, int ldl, double* out,
+                                  void* stream) {
+    if (!dA || !dL || !out || n < 1) return fail(TC_INVALID_ARGUMENT, "bad arguments");
+    if (!tc_device_available()) return fail(TC_NO_DEVICE, "no CUDA device");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int T = 0;
+    const int tiles = fact_error_partials(n, &T);
+    double* d_part = nullptr;
+    int* d_flag = nullptr;
+    cudaError_t e = cudaMallocAsync(&d_part, sizeof(double) * (2 * size_t(tiles) + 1), s);
+    if (e != cudaSuccess) return cuda_fail(e, "alloc");
+    e = cudaMallocAsync(&d_flag, sizeof(int), s);
+    if (e != cudaSuccess) return cuda_fail(e, "alloc");
+    launch_fact_error(n, dA, lda, dL, ldl, d_part, d_flag, T, s);
+    e = cudaMemcpyAsync(out, d_part + 2 * size_t(tiles), sizeof(double), cudaMemcpyDeviceToHost, s);
+    cudaFreeAsync(d_part, s);
+    cudaFreeAsync(d_flag, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "factorization_error");
+    return TC_OK;
+}
+
+int tc_potrs_device(int n, const double* dL, int ldl, double* dB, int ldb, int nrhs, void* stream) {
+    if (!dL || !dB || n < 1 || nrhs < 1 || ldl < n || ldb < n) return fail(TC_INVALID_ARGUMENT, "bad arguments");
+    if (!tc_device_available()) return fail(TC_NO_DEVICE, "no CUDA device");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int nb = (n + 63) / 64;
+    int* d_cnt = nullptr;
+    cudaError_t e = cudaMallocAsync(&d_cnt, sizeof(int) * size_t(nb + 1) * size_t(nrhs), s);
+    if (e != cudaSuccess) return cuda_fail(e, "alloc");
+    launch_potrs(n, dL, ldl, dB, ldb, nrhs, d_cnt, nullptr, s);
+    cudaFreeAsync(d_cnt, s);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "potrs");
+    return TC_OK;
+}
+
+int tc_solve_residual_device(int n, const double* dA, int lda, const double* dX, const double* dB, double* out,
+                             void* stream) {
+    if (!dA || !dX || !dB || !out || n < 1) return fail(TC_INVALID_ARGUMENT, "bad arguments");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int nb = residual_partials(n);
+    double* d_part = nullptr;
+    cudaError_t e = cudaMallocAsync(&d_part, sizeof(double) * (4 * size_t(nb) + 1), s);
+    if (e != cudaSuccess) return cuda_fail(e, "alloc");
+    launch_residual(n, dA, lda, dX, dB, d_part, s);
+    e = cudaMemcpyAsync(out, d_part + 4 * size_t(nb), sizeof(double), cudaMemcpyDeviceToHost, s);
+    cudaFreeAsync(d_part, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, "residual");
+    return TC_OK;
+}
+
+}  // extern "C"

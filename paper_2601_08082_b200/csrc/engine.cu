@@ -1,0 +1,341 @@
+// engine.cu -- see engine.hpp.
+#include "engine.hpp"
+
+#include <algorithm>
+#include <cstring>
+
+#include "launch.hpp"
+
+namespace tcb {
+
+namespace {
+
+constexpr int kRaRing = 16;
+
+#define TC_TRY(expr)                                                        \
+    do {                                                                    \
+        cudaError_t e_ = (expr);                                            \
+        if (e_ != cudaSuccess) {                                            \
+            if (err) *err = std::string(#expr) + ": " + cudaGetErrorString(e_); \
+            return false;                                                   \
+        }                                                                   \
+    } while (0)
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+Engine::~Engine() {
+    if (gexec_) cudaGraphExecDestroy(gexec_);
+    if (graph_) cudaGraphDestroy(graph_);
+    for (auto e : events_) cudaEventDestroy(e);
+    if (fork_) cudaEventDestroy(fork_);
+    for (auto s : streams_) cudaStreamDestroy(s);
+    if (d_bufs_) cudaFree(d_bufs_);
+    if (d_words_) cudaFree(d_words_);
+    if (d_arena_) cudaFree(d_arena_);
+    if (d_ra_) cudaFree(d_ra_);
+    if (h_ra_) cudaFreeHost(h_ra_);
+    if (h_status_) cudaFreeHost(h_status_);
+}
+
+int Engine::launches_per_run() const {
+    int k = 2;  // status / alpha resets
+    for (const Op& op : plan.ops) k += op.type == OP_QUANT ? 2 : 1;
+    return k;
+}
+
+bool Engine::prepare(std::string* err) {
+    if (ready_) return true;
+    TC_TRY(cudaGetDevice(&device_));
+    init_leaf_attributes();
+    init_tc_attributes();
+    const int n = plan.n;
+    const long long ldw = (long long)align_up(size_t(n), 64);
+    ctx_.ldw = ldw;
+    // level buffers: one allocation, 256-byte aligned sub-buffers
+    size_t sz[3] = {0, 0, 0}, off[3] = {0, 0, 0}, total = 0;
+    const size_t esz[3] = {2, 4, 8};
+    for (int l = 0; l < 3; ++l)
+        if (plan.needs_buf[l]) {
+            sz[l] = size_t(n) * size_t(ldw) * esz[l];
+            off[l] = total;
+            total = align_up(total + sz[l], 256);
+        }
+    if (total) TC_TRY(cudaMalloc(&d_bufs_, total));
+    unsigned char* base = static_cast<unsigned char*>(d_bufs_);
+    ctx_.b16 = plan.needs_buf[0] ? reinterpret_cast<__half*>(base + off[0]) : nullptr;
+    ctx_.b32 = plan.needs_buf[1] ? reinterpret_cast<float*>(base + off[1]) : nullptr;
+    ctx_.b64 = plan.needs_buf[2] ? reinterpret_cast<double*>(base + off[2]) : nullptr;
+    TC_TRY(cudaMalloc(&d_words_, sizeof(unsigned long long) * size_t(1 + std::max(1, plan.n_alpha_slots))));
+    ctx_.status = d_words_;
+    ctx_.alpha_bits = d_words_ + 1;
+    TC_TRY(cudaMalloc(&d_ra_, sizeof(RunArgs)));
+    ctx_.ra = d_ra_;
+    TC_TRY(cudaMallocHost(&h_ra_, sizeof(RunArgs) * kRaRing));
+    TC_TRY(cudaMallocHost(&h_status_, sizeof(unsigned long long)));
+
+    // launch tables
+    std::vector<unsigned char> host;
+    launch_.assign(plan.ops.size(), OpLaunch{});
+    auto append = [&](const void* p, size_t bytes) {
+        const size_t o = align_up(host.size(), 128);
+        host.resize(o + bytes);
+        if (bytes) std::memcpy(host.data() + o, p, bytes);
+        return o;
+    };
+    for (size_t i = 0; i < plan.ops.size(); ++i) {
+        const Op& op = plan.ops[i];
+        OpLaunch& L = launch_[i];
+        if (op.type == OP_IMPORT || op.type == OP_EXPORT || op.type == OP_SHADOW) {
+            std::vector<BlockDescHost> bh;
+            for (int b : op.blocks) {
+                const Block& blk = plan.blocks[b];
+                bh.push_back({blk.rect.r0, blk.rect.c0, blk.rect.m, blk.rect.n, blk.level, blk.leaf ? 1 : 0});
+            }
+            std::vector<BlockDesc> bd;
+            L.tiles = make_block_table(bh, bd);
+            L.count = int(bd.size());
+            L.offset = append(bd.data(), bd.size() * sizeof(BlockDesc));
+        } else if (op.type == OP_GEMM) {
+            std::vector<DevProb> dp;
+            for (int p = op.prob_begin; p < op.prob_end; ++p) {
+                const GemmProb& g = plan.probs[p];
+                DevProb d{};
+                d.m = g.m;
+                d.n = g.n;
+                d.k = g.k;
+                d.a_r0 = g.a_r0;
+                d.a_c0 = g.a_c0;
+                d.b_r0 = g.b_r0;
+                d.b_c0 = g.b_c0;
+                d.c_r0 = g.c_r0;
+                d.c_c0 = g.c_c0;
+                d.exec_level = g.exec_level;
+                d.lower = g.lower;
+                d.alpha = g.alpha;
+                d.beta = g.beta;
+                dp.push_back(d);
+            }
+            L.count = int(dp.size());
+            if (op.gclass == GC_TC16) {
+                std::vector<unsigned char> tp;
+                L.tiles = tc_build_probs(ctx_, dp, tp, err);
+                if (L.tiles < 0) return false;
+                L.offset = append(tp.data(), tp.size());
+            } else {
+                L.tiles = simt_tiles(dp);
+                L.offset = append(dp.data(), dp.size() * sizeof(DevProb));
+            }
+        }
+    }
+    if (!host.empty()) {
+        TC_TRY(cudaMalloc(&d_arena_, host.size()));
+        TC_TRY(cudaMemcpy(d_arena_, host.data(), host.size(), cudaMemcpyHostToDevice));
+    }
+    seq_op_.assign(size_t(plan.n_seq) + 1, -1);
+    for (size_t i = 0; i < plan.ops.size(); ++i) {
+        const Op& op = plan.ops[i];
+        if (op.seq) seq_op_[op.seq] = int(i);
+        if (op.type == OP_GEMM)
+            for (int p = op.prob_begin; p < op.prob_end; ++p) seq_op_[plan.probs[p].seq] = int(i);
+    }
+    ready_ = true;
+    return true;
+}
+
+void Engine::launch_op(int i, cudaStream_t s) {
+    const Op& op = plan.ops[i];
+    const OpLaunch& L = launch_[i];
+    const Rect& r = op.rect;
+    unsigned char* tab = d_arena_ + L.offset;
+    switch (op.type) {
+        case OP_IMPORT: launch_import(ctx_, reinterpret_cast<BlockDesc*>(tab), L.count, L.tiles, s); break;
+        case OP_EXPORT: launch_export(ctx_, reinterpret_cast<BlockDesc*>(tab), L.count, L.tiles, s); break;
+        case OP_SHADOW: launch_shadow(ctx_, reinterpret_cast<BlockDesc*>(tab), L.count, L.tiles, op.level, s); break;
+        case OP_CHECK: launch_check(ctx_, op.src, r.r0, r.c0, r.m, r.n, op.lower, op.seq, s); break;
+        case OP_QUANT: launch_quant(ctx_, op.level, r.r0, r.c0, r.m, r.n, op.slot, op.seq, s); break;
+        case OP_DEQUANT: launch_dequant(ctx_, op.level, r.r0, r.c0, r.m, r.n, op.slot, s); break;
+        case OP_POTRF: launch_potrf_leaf(ctx_, op.level, r.r0, r.m, op.seq, s); break;
+        case OP_TRSM: launch_trsm_leaf(ctx_, op.level, r.r0, r.c0, r.m, r.n, op.lrect.r0, op.seq, s); break;
+        case OP_GEMM:
+            if (op.gclass == GC_TC16) launch_gemm_tc(ctx_, tab, L.count, L.tiles, s);
+            else launch_gemm_simt(ctx_, op.gclass, reinterpret_cast<DevProb*>(tab), L.count, L.tiles, s);
+            break;
+    }
+}
+
+void Engine::reset_words(cudaStream_t s) {
+    cudaMemsetAsync(d_words_, 0xFF, sizeof(unsigned long long), s);
+    if (plan.n_alpha_slots > 0)
+        cudaMemsetAsync(d_words_ + 1, 0, sizeof(unsigned long long) * size_t(plan.n_alpha_slots), s);
+}
+
+// enqueue every op on the stream pool (works eagerly or under capture)
+bool Engine::enqueue_ops(cudaStream_t origin, std::string* err) {
+    const int N = int(plan.ops.size());
+    const int S = std::max(1, n_streams);
+    if (int(streams_.size()) < S) {
+        for (int s = int(streams_.size()); s < S; ++s) {
+            cudaStream_t st;
+            TC_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+            streams_.push_back(st);
+        }
+    }
+    if (int(events_.size()) < N + S) {
+        for (int e = int(events_.size()); e < N + S; ++e) {
+            cudaEvent_t ev;
+            TC_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            events_.push_back(ev);
+        }
+    }
+    if (!fork_) TC_TRY(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming));
+    // stream assignment: continue a dep's stream when that dep is its tail
+    std::vector<int> sid(N, 0), tail(S, -1), last_use(S, -1);
+    std::vector<char> need_ev(N, 0);
+    std::vector<std::vector<int>> waits(N);
+    for (int i = 0; i < N; ++i) {
+        int pick = -1;
+        for (int d : plan.ops[i].deps)
+            if (tail[sid[d]] == d) {
+                pick = sid[d];
+                break;
+            }
+        if (pick < 0) {
+            pick = 0;
+            for (int s = 1; s < S; ++s)
+                if (last_use[s] < last_use[pick]) pick = s;
+        }
+        sid[i] = pick;
+        for (int d : plan.ops[i].deps)
+            if (sid[d] != pick || tail[pick] != d) {
+                // same-stream deps are ordered already unless another op intervened (still ordered)
+                if (sid[d] != pick) {
+                    waits[i].push_back(d);
+                    need_ev[d] = 1;
+                }
+            }
+        tail[pick] = i;
+        last_use[pick] = i;
+    }
+    reset_words(origin);
+    TC_TRY(cudaEventRecord(fork_, origin));
+    for (int s = 0; s < S; ++s) TC_TRY(cudaStreamWaitEvent(streams_[s], fork_, 0));
+    for (int i = 0; i < N; ++i) {
+        cudaStream_t st = streams_[sid[i]];
+        for (int d : waits[i]) TC_TRY(cudaStreamWaitEvent(st, events_[d], 0));
+        launch_op(i, st);
+        if (need_ev[i]) TC_TRY(cudaEventRecord(events_[i], st));
+    }
+    for (int s = 0; s < S; ++s) {
+        TC_TRY(cudaEventRecord(events_[N + s], streams_[s]));
+        TC_TRY(cudaStreamWaitEvent(origin, events_[N + s], 0));
+    }
+    TC_TRY(cudaGetLastError());
+    return true;
+}
+
+bool Engine::enqueue(const double* a_in, long long lda_in, double* l_out, long long lda_out, cudaStream_t stream,
+                     std::string* err) {
+    if (!prepare(err)) return false;
+    static int ring = 0;
+    RunArgs* slot = h_ra_ + (ring++ % kRaRing);
+    slot->a_in = a_in;
+    slot->l_out = l_out;
+    slot->lda_in = lda_in;
+    slot->lda_out = lda_out;
+    TC_TRY(cudaMemcpyAsync(d_ra_, slot, sizeof(RunArgs), cudaMemcpyHostToDevice, stream));
+    if (use_graph) {
+        if (!gexec_) {
+            cudaStream_t cap;
+            TC_TRY(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+            TC_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+            std::string e2;
+            const bool ok = enqueue_ops(cap, &e2);
+            cudaGraph_t g = nullptr;
+            const cudaError_t ce = cudaStreamEndCapture(cap, &g);
+            cudaStreamDestroy(cap);
+            if (!ok) {
+                if (err) *err = e2;
+                if (g) cudaGraphDestroy(g);
+                return false;
+            }
+            TC_TRY(ce);
+            graph_ = g;
+            TC_TRY(cudaGraphInstantiate(&gexec_, graph_, 0));
+        }
+        TC_TRY(cudaGraphLaunch(gexec_, stream));
+    } else {
+        if (!enqueue_ops(stream, err)) return false;
+    }
+    last_stream_ = stream;
+    return true;
+}
+
+bool Engine::result(Failure* f, std::string* err) {
+    TC_TRY(cudaMemcpyAsync(h_status_, d_words_, sizeof(unsigned long long), cudaMemcpyDeviceToHost, last_stream_));
+    TC_TRY(cudaStreamSynchronize(last_stream_));
+    *f = Failure{};
+    const unsigned long long key = *h_status_;
+    if (key == ~0ull) return true;
+    const uint32_t seq = uint32_t(key >> 40);
+    const uint64_t local = key & ((1ull << 40) - 1);
+    f->seq = seq;
+    const int oi = seq < seq_op_.size() ? seq_op_[seq] : -1;
+    if (oi < 0) {
+        if (err) *err = "corrupt status word";
+        return false;
+    }
+    const Op& op = plan.ops[oi];
+    switch (op.type) {
+        case OP_CHECK:
+        case OP_QUANT:
+            f->status = 2;
+            f->block = op.rect;
+            f->elem_row = op.rect.r0 + int(local & 0xFFFFF);
+            f->elem_col = op.rect.c0 + int(local >> 20);
+            f->diagonal = op.type == OP_CHECK ? op.diagonal : 0;
+            break;
+        case OP_POTRF:
+            f->status = 1;
+            f->index = op.rect.r0 + int(local);
+            break;
+        case OP_TRSM:
+            f->status = 3;
+            f->index = op.lrect.r0 + int(local);
+            break;
+        default:
+            if (err) *err = "status from an op that cannot fail";
+            return false;
+    }
+    return true;
+}
+
+bool Engine::profile(const double* a_in, long long lda_in, double* l_out, long long lda_out, cudaStream_t stream,
+                     std::vector<float>& op_ms, std::string* err) {
+    if (!prepare(err)) return false;
+    RunArgs* slot = h_ra_;
+    slot->a_in = a_in;
+    slot->l_out = l_out;
+    slot->lda_in = lda_in;
+    slot->lda_out = lda_out;
+    TC_TRY(cudaMemcpyAsync(d_ra_, slot, sizeof(RunArgs), cudaMemcpyHostToDevice, stream));
+    const int N = int(plan.ops.size());
+    std::vector<cudaEvent_t> ev(N + 1);
+    for (auto& e : ev) TC_TRY(cudaEventCreate(&e));
+    reset_words(stream);
+    TC_TRY(cudaEventRecord(ev[0], stream));
+    for (int i = 0; i < N; ++i) {
+        launch_op(i, stream);
+        TC_TRY(cudaEventRecord(ev[i + 1], stream));
+    }
+    TC_TRY(cudaStreamSynchronize(stream));
+    TC_TRY(cudaGetLastError());
+    op_ms.assign(N, 0.f);
+    for (int i = 0; i < N; ++i) cudaEventElapsedTime(&op_ms[i], ev[i], ev[i + 1]);
+    for (auto& e : ev) cudaEventDestroy(e);
+    last_stream_ = stream;
+    return true;
+}
+
+}  // namespace tcb

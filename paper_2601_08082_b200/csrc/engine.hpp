@@ -1,0 +1,85 @@
+// engine.hpp -- executes a Plan on one device (internal).
+//
+// The op list is enqueued on a pool of CUDA streams, each op waiting on the
+// events of the deps that live on other streams; the whole enqueue is
+// captured once into a CUDA graph (cached per plan) and replayed per call.
+// Device state per plan: the level buffers, the status word, the quantize
+// alpha slots, the launch tables, and a RunArgs block the kernels read the
+// caller's pointers from (so one graph serves every call).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "device.cuh"
+#include "plan.hpp"
+
+namespace tcb {
+
+struct OpLaunch {
+    int tiles = 0;
+    int count = 0;
+    size_t offset = 0;  // into the table arena
+};
+
+struct Failure {
+    int status = 0;  // tc_status
+    int index = -1;
+    Rect block;
+    int elem_row = -1, elem_col = -1;
+    int diagonal = 0;
+    uint32_t seq = 0;
+};
+
+class Engine {
+   public:
+    explicit Engine(Plan p) : plan(std::move(p)) {}
+    ~Engine();
+    Engine(const Engine&) = delete;
+    Engine& operator=(const Engine&) = delete;
+
+    Plan plan;
+    bool use_graph = true;
+    int n_streams = 6;
+
+    // enqueue one factorization (import .. export) on `stream`
+    bool enqueue(const double* a_in, long long lda_in, double* l_out, long long lda_out, cudaStream_t stream,
+                 std::string* err);
+    // wait for the last enqueue and decode the status word
+    bool result(Failure* f, std::string* err);
+    // serialized eager run with an event after every op (per-op timing)
+    bool profile(const double* a_in, long long lda_in, double* l_out, long long lda_out, cudaStream_t stream,
+                 std::vector<float>& op_ms, std::string* err);
+    // partial flops of a failed run: calls with seq < failing seq
+    int launches_per_run() const;
+
+    bool ready() const { return ready_; }
+    bool prepare(std::string* err);
+
+   private:
+    bool ready_ = false;
+    int device_ = -1;
+    DevCtx ctx_{};
+    RunArgs* d_ra_ = nullptr;
+    RunArgs* h_ra_ = nullptr;
+    unsigned long long* h_status_ = nullptr;
+    void* d_bufs_ = nullptr;
+    unsigned long long* d_words_ = nullptr;  // status + alpha slots
+    unsigned char* d_arena_ = nullptr;
+    std::vector<OpLaunch> launch_;
+    std::vector<cudaStream_t> streams_;
+    std::vector<cudaEvent_t> events_;
+    cudaEvent_t fork_ = nullptr;
+    cudaStream_t last_stream_ = nullptr;
+    cudaGraph_t graph_ = nullptr;
+    cudaGraphExec_t gexec_ = nullptr;
+    std::vector<int> seq_op_;  // seq -> op index
+
+    void launch_op(int i, cudaStream_t s);
+    void reset_words(cudaStream_t s);
+    bool enqueue_ops(cudaStream_t origin, std::string* err);
+};
+
+}  // namespace tcb

@@ -1,0 +1,305 @@
+// k_elementwise.cu -- HBM-bound passes over blocks of the matrix:
+//   import   caller doubles (col-major) -> level buffers (row-major), rounding
+//            to each block's level (build_tree rounding, tree.cpp:47-60)
+//   export   level buffers -> caller doubles, lower triangle only
+//   shadow   final L block -> p-rounded copy in buffer p (kernels.cpp:29,78)
+//   check    require_finite (tree.cpp:19-31) -> first bad element
+//   quant    quantize_block of a spine panel (tree.cpp:80-95), fused with its
+//            require_finite and the absmax reduction
+//   dequant  dequantize_block (tree.cpp:97-104)
+// Transposing kernels stage a 32x32 tile in shared memory so both the
+// column-major and the row-major side are coalesced.
+#include "device.cuh"
+#include "launch.hpp"
+
+namespace tcb {
+
+namespace {
+
+constexpr int TS = 32;  // tile side
+
+__global__ void __launch_bounds__(256) k_import(DevCtx c, const BlockDesc* blocks, int nb) {
+    __shared__ double tile[TS][TS + 1];
+    const int t = blockIdx.x;
+    const BlockDesc bd = blocks[find_block(blocks, nb, t)];
+    const int lt = t - bd.tile0;
+    const int i0 = (lt / bd.tiles_n) * TS, j0 = (lt % bd.tiles_n) * TS;
+    const double* a = c.ra->a_in;
+    const long long lda = c.ra->lda_in;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+#pragma unroll
+    for (int r = 0; r < TS; r += 8) {
+        const int i = i0 + tx, j = j0 + ty + r;
+        double v = 0.0;
+        if (i < bd.m && j < bd.n) v = a[(long long)(bd.c0 + j) * lda + bd.r0 + i];
+        tile[ty + r][tx] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < TS; r += 8) {
+        const int i = i0 + ty + r, j = j0 + tx;
+        if (i < bd.m && j < bd.n) {
+            double v = tile[tx][ty + r];
+            if (bd.lower && j > i) v = 0.0;  // strict upper of a leaf square: unused
+            store_level(c, bd.level, (long long)(bd.r0 + i) * c.ldw + bd.c0 + j, v);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_export(DevCtx c, const BlockDesc* blocks, int nb) {
+    __shared__ double tile[TS][TS + 1];
+    const int t = blockIdx.x;
+    const BlockDesc bd = blocks[find_block(blocks, nb, t)];
+    const int lt = t - bd.tile0;
+    const int i0 = (lt / bd.tiles_n) * TS, j0 = (lt % bd.tiles_n) * TS;
+    double* l = c.ra->l_out;
+    const long long ldl = c.ra->lda_out;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+#pragma unroll
+    for (int r = 0; r < TS; r += 8) {
+        const int i = i0 + ty + r, j = j0 + tx;
+        double v = 0.0;
+        if (i < bd.m && j < bd.n) v = load_level(c, bd.level, (long long)(bd.r0 + i) * c.ldw + bd.c0 + j);
+        tile[ty + r][tx] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < TS; r += 8) {
+        const int i = i0 + tx, j = j0 + ty + r;
+        if (i < bd.m && j < bd.n && !(bd.lower && j > i))
+            l[(long long)(bd.c0 + j) * ldl + bd.r0 + i] = tile[tx][ty + r];
+    }
+}
+
+// shadow: blocks carry their source level; target is `p`
+__global__ void __launch_bounds__(256) k_shadow(DevCtx c, const BlockDesc* blocks, int nb, int p) {
+    const int t = blockIdx.x;
+    const BlockDesc bd = blocks[find_block(blocks, nb, t)];
+    const int lt = t - bd.tile0;
+    const int i0 = (lt / bd.tiles_n) * TS, j0 = (lt % bd.tiles_n) * TS;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+#pragma unroll
+    for (int r = 0; r < TS; r += 8) {
+        const int i = i0 + ty + r, j = j0 + tx;
+        if (i < bd.m && j < bd.n) {
+            const long long off = (long long)(bd.r0 + i) * c.ldw + bd.c0 + j;
+            double v = load_level(c, bd.level, off);
+            if (bd.lower && j > i) v = 0.0;
+            store_level(c, p, off, v);
+        }
+    }
+}
+
+// require_finite over rect (lower: leaf lower triangle) of buffer `lv`
+__global__ void __launch_bounds__(256) k_check(DevCtx c, int lv, int r0, int c0, int m, int n, int lower,
+                                               uint32_t seq) {
+    const int j = blockIdx.x * 256 + threadIdx.x;
+    const int ib = blockIdx.y * 16;
+    unsigned long long best = ~0ull;
+    if (j < n) {
+        for (int ii = 0; ii < 16; ++ii) {
+            const int i = ib + ii;
+            if (i >= m) break;
+            if (lower && j > i) continue;
+            const double v = load_level(c, lv, (long long)(r0 + i) * c.ldw + c0 + j);
+            if (!isfinite(v)) {
+                best = fail_key(seq, elem_local(i, j));
+                break;
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long x = __shfl_xor_sync(0xffffffffu, best, o);
+        best = x < best ? x : best;
+    }
+    if ((threadIdx.x & 31) == 0 && best != ~0ull) atomicMin(c.status, best);
+}
+
+// quantize pass 1: require_finite on the caller's doubles, max|B| into the
+// alpha slot, and a speculative alpha == 1 conversion into buffer lv
+__global__ void __launch_bounds__(256) k_quant1(DevCtx c, int lv, int r0, int c0, int m, int n, int slot,
+                                                uint32_t seq) {
+    __shared__ double tile[TS][TS + 1];
+    __shared__ unsigned long long smax[8], skey[8];
+    const int tiles_n = (n + TS - 1) / TS;
+    const int i0 = (blockIdx.x / tiles_n) * TS, j0 = (blockIdx.x % tiles_n) * TS;
+    const double* a = c.ra->a_in;
+    const long long lda = c.ra->lda_in;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    unsigned long long mx = 0, key = ~0ull;
+#pragma unroll
+    for (int r = 0; r < TS; r += 8) {
+        const int i = i0 + tx, j = j0 + ty + r;
+        double v = 0.0;
+        if (i < m && j < n) {
+            v = a[(long long)(c0 + j) * lda + r0 + i];
+            if (!isfinite(v)) {
+                const unsigned long long k = fail_key(seq, elem_local(i, j));
+                key = k < key ? k : key;
+            }
+            const unsigned long long bits = __double_as_longlong(fabs(v));
+            mx = bits > mx ? bits : mx;
+        }
+        tile[ty + r][tx] = v;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long x = __shfl_xor_sync(0xffffffffu, mx, o);
+        const unsigned long long y = __shfl_xor_sync(0xffffffffu, key, o);
+        mx = x > mx ? x : mx;
+        key = y < key ? y : key;
+    }
+    if (tx == 0) {
+        smax[ty] = mx;
+        skey[ty] = key;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long M = 0, K = ~0ull;
+        for (int w = 0; w < 8; ++w) {
+            M = smax[w] > M ? smax[w] : M;
+            K = skey[w] < K ? skey[w] : K;
+        }
+        if (M) atomicMax(c.alpha_bits + slot, M);
+        if (K != ~0ull) atomicMin(c.status, K);
+    }
+#pragma unroll
+    for (int r = 0; r < TS; r += 8) {
+        const int i = i0 + ty + r, j = j0 + tx;
+        if (i < m && j < n) store_level(c, lv, (long long)(r0 + i) * c.ldw + c0 + j, tile[tx][ty + r]);
+    }
+}
+
+__device__ __forceinline__ double slot_alpha(const DevCtx& c, int lv, int slot) {
+    const double amax = __longlong_as_double((long long)c.alpha_bits[slot]);
+    double alpha = amax / range_max(lv);
+    if (!(alpha > 1.0)) alpha = 1.0;
+    return alpha;
+}
+
+// quantize pass 2: only when alpha != 1, B <- rn(B / alpha) from the doubles
+__global__ void __launch_bounds__(256) k_quant2(DevCtx c, int lv, int r0, int c0, int m, int n, int slot) {
+    const double alpha = slot_alpha(c, lv, slot);
+    if (alpha == 1.0) return;
+    __shared__ double tile[TS][TS + 1];
+    const int tiles_n = (n + TS - 1) / TS;
+    const int i0 = (blockIdx.x / tiles_n) * TS, j0 = (blockIdx.x % tiles_n) * TS;
+    const double* a = c.ra->a_in;
+    const long long lda = c.ra->lda_in;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+#pragma unroll
+    for (int r = 0; r < TS; r += 8) {
+        const int i = i0 + tx, j = j0 + ty + r;
+        tile[ty + r][tx] = (i < m && j < n) ? a[(long long)(c0 + j) * lda + r0 + i] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < TS; r += 8) {
+        const int i = i0 + ty + r, j = j0 + tx;
+        if (i < m && j < n) store_level(c, lv, (long long)(r0 + i) * c.ldw + c0 + j, tile[tx][ty + r] / alpha);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_dequant(DevCtx c, int lv, int r0, int c0, int m, int n, int slot) {
+    const double alpha = slot_alpha(c, lv, slot);
+    if (alpha == 1.0) return;  // tree.cpp:98
+    const int j = blockIdx.x * 256 + threadIdx.x;
+    if (j >= n) return;
+    for (int ii = 0; ii < 16; ++ii) {
+        const int i = blockIdx.y * 16 + ii;
+        if (i >= m) break;
+        const long long off = (long long)(r0 + i) * c.ldw + c0 + j;
+        store_level(c, lv, off, load_level(c, lv, off) * alpha);
+    }
+}
+
+int tiles_of(int m, int n) { return ((m + TS - 1) / TS) * ((n + TS - 1) / TS); }
+
+// spd_generate's symmetrization (analysis.cpp:22-26) in place on the raw
+// column-major draws R: A(i,j) = A(j,i) = 0.5 * (R(i,j) + R(j,i)), A(j,j) +=
+// n.  One CTA per lower tile pair; explicit _rn ops forbid contraction, so
+// the result is bit-identical to the host reference.
+__global__ void __launch_bounds__(256) k_symmetrize(double* a, long long lda, int n) {
+    __shared__ double t1[TS][TS + 1], t2[TS][TS + 1];
+    const int t = blockIdx.x;
+    int I = int((sqrt(8.0 * t + 1.0) - 1.0) / 2.0);
+    while ((I + 1) * (I + 2) / 2 <= t) ++I;
+    while (I * (I + 1) / 2 > t) --I;
+    const int J = t - I * (I + 1) / 2;  // I >= J
+    const int i0 = I * TS, j0 = J * TS;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    for (int r = 0; r < TS; r += 8) {
+        const int i = i0 + tx, j = j0 + ty + r;  // tile (I,J): rows i, cols j
+        t1[ty + r][tx] = (i < n && j < n) ? a[(long long)j * lda + i] : 0.0;
+        const int i2 = j0 + tx, j2 = i0 + ty + r;  // tile (J,I)
+        t2[ty + r][tx] = (i2 < n && j2 < n) ? a[(long long)j2 * lda + i2] : 0.0;
+    }
+    __syncthreads();
+    const double dn = double(n);
+    for (int r = 0; r < TS; r += 8) {
+        // element (i, j) of tile (I,J) pairs with (j, i) of tile (J,I)
+        const int jl = ty + r, il = tx;
+        const int i = i0 + il, j = j0 + jl;
+        if (i < n && j < n) {
+            double v = __dmul_rn(0.5, __dadd_rn(t1[jl][il], t2[il][jl]));
+            if (i == j) v = __dadd_rn(v, dn);
+            a[(long long)j * lda + i] = v;
+            a[(long long)i * lda + j] = v;
+        }
+    }
+}
+
+}  // namespace
+
+void launch_symmetrize(double* a, long long lda, int n, cudaStream_t s) {
+    const int T = (n + TS - 1) / TS;
+    k_symmetrize<<<T * (T + 1) / 2, 256, 0, s>>>(a, lda, n);
+}
+
+// host-side block table construction
+int make_block_table(const std::vector<BlockDescHost>& in, std::vector<BlockDesc>& out) {
+    out.clear();
+    int tiles = 0;
+    for (const auto& h : in) {
+        BlockDesc d;
+        d.r0 = h.r0;
+        d.c0 = h.c0;
+        d.m = h.m;
+        d.n = h.n;
+        d.level = h.level;
+        d.lower = h.lower;
+        d.tile0 = tiles;
+        d.tiles_n = (h.n + TS - 1) / TS;
+        out.push_back(d);
+        tiles += tiles_of(h.m, h.n);
+    }
+    return tiles;
+}
+
+void launch_import(const DevCtx& c, const BlockDesc* d_blocks, int nb, int tiles, cudaStream_t s) {
+    if (tiles > 0) k_import<<<tiles, 256, 0, s>>>(c, d_blocks, nb);
+}
+void launch_export(const DevCtx& c, const BlockDesc* d_blocks, int nb, int tiles, cudaStream_t s) {
+    if (tiles > 0) k_export<<<tiles, 256, 0, s>>>(c, d_blocks, nb);
+}
+void launch_shadow(const DevCtx& c, const BlockDesc* d_blocks, int nb, int tiles, int p, cudaStream_t s) {
+    if (tiles > 0) k_shadow<<<tiles, 256, 0, s>>>(c, d_blocks, nb, p);
+}
+void launch_check(const DevCtx& c, int lv, int r0, int c0, int m, int n, int lower, uint32_t seq,
+                  cudaStream_t s) {
+    dim3 g((n + 255) / 256, (m + 15) / 16);
+    k_check<<<g, 256, 0, s>>>(c, lv, r0, c0, m, n, lower, seq);
+}
+void launch_quant(const DevCtx& c, int lv, int r0, int c0, int m, int n, int slot, uint32_t seq,
+                  cudaStream_t s) {
+    const int t = tiles_of(m, n);
+    k_quant1<<<t, 256, 0, s>>>(c, lv, r0, c0, m, n, slot, seq);
+    k_quant2<<<t, 256, 0, s>>>(c, lv, r0, c0, m, n, slot);
+}
+void launch_dequant(const DevCtx& c, int lv, int r0, int c0, int m, int n, int slot, cudaStream_t s) {
+    dim3 g((n + 255) / 256, (m + 15) / 16);
+    k_dequant<<<g, 256, 0, s>>>(c, lv, r0, c0, m, n, slot);
+}
+
+}  // namespace tcb

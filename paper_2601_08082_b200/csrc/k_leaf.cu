@@ -1,0 +1,306 @@
+// k_leaf.cu -- diagonal leaf POTRF and leaf TRSM (kernels.cpp:42-92).
+//
+// Both keep the reference's per-element arithmetic (dot_update, kernels.cpp:
+// 23-38): the dot product accumulates in Acc (FP32 for the F16/F32 levels,
+// FP64 for F64) and is never rounded to the level mid-way; the result is
+// rn_level(rn_acc(c - s)), then pivots / divisions round to the level.  Only
+// the summation order differs (blocked by 32 columns).
+//
+// potrf_leaf: one CTA per leaf.  The lower triangle lives in shared memory
+// (packed rows) when it fits, else it is worked on in place in global memory
+// (L2-resident).  Columns are processed in 32-wide panels:
+//   a) P = partial dot products against all finished columns (register-
+//      blocked 4x4 per thread),
+//   b1) the 32x32 diagonal block factored by one warp with shuffles,
+//   b2) rows below solved against it, one thread per row, no barriers.
+// trsm_leaf: one thread per row of B, 128 rows per CTA; the current 32-column
+// chunk of L is staged (transposed) in shared memory and broadcast.
+#include "device.cuh"
+#include "launch.hpp"
+
+namespace tcb {
+
+namespace {
+
+constexpr int PW = 32;  // panel width
+constexpr int TRSM_ROWS = 32;  // rows per trsm CTA (4 threads per row)
+constexpr int POTRF_THREADS = 512;
+constexpr int KT = 16;  // potrf phase (a): finished columns staged per step
+
+template <typename Acc>
+constexpr size_t potrf_smem(int n, bool smem) {
+    return (size_t(n) * PW + size_t(KT) * (n + 4) + size_t(KT) * (PW + 4) +
+            (smem ? size_t(n) * (n + 1) / 2 : 0)) * sizeof(Acc);
+}
+
+template <int L, bool SMEM>
+struct LeafAcc {
+    using T = typename LvT<L>::T;
+    using Acc = typename LvT<L>::Acc;
+    Acc* s;             // packed rows (SMEM)
+    T* g;               // global leaf origin (row-major, ld)
+    long long ld;
+    __device__ __forceinline__ Acc get(int i, int j) const {
+        if constexpr (SMEM) return s[(i * (i + 1)) / 2 + j];
+        else return Acc(to_d(g[(long long)i * ld + j]));
+    }
+    __device__ __forceinline__ void set(int i, int j, Acc v) const {
+        if constexpr (SMEM) s[(i * (i + 1)) / 2 + j] = v;
+        else g[(long long)i * ld + j] = from_double<T>(double(v));
+    }
+};
+
+template <int L, bool SMEM>
+__global__ void __launch_bounds__(POTRF_THREADS) k_potrf_leaf(DevCtx c, int r0, int n, uint32_t seq) {
+    using T = typename LvT<L>::T;
+    using Acc = typename LvT<L>::Acc;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int ldS = n + 4;                        // staged rows, padded
+    Acc* P = reinterpret_cast<Acc*>(smem_raw);    // [n][PW] partial sums
+    Acc* As = P + size_t(n) * PW;                 // [KT][ldS]  A(J+r, t0+tt) transposed
+    Acc* Bs = As + size_t(KT) * ldS;              // [KT][PW+4] A(J+jj, t0+tt)
+    Acc* S = Bs + size_t(KT) * (PW + 4);          // packed lower triangle (SMEM)
+    T* g = lvbuf<L>(c) + (long long)r0 * c.ldw + r0;
+    LeafAcc<L, SMEM> A{S, g, c.ldw};
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = POTRF_THREADS / 32;
+
+    if constexpr (SMEM) {
+        for (int i = warp; i < n; i += NW)
+            for (int j = lane; j <= i; j += 32) S[(i * (i + 1)) / 2 + j] = Acc(to_d(g[(long long)i * c.ldw + j]));
+        __syncthreads();
+    }
+
+    for (int J = 0; J < n; J += PW) {
+        const int w = min(PW, n - J);
+        const int R = n - J;  // rows of this panel
+        // (a) P[r][jj] = sum_{t<J} A(J+r, t) * A(J+jj, t): a small SIMT GEMM,
+        // KT finished columns at a time staged transposed (conflict-free
+        // float4 reads), one 4x4 register block per thread
+        const int units = 8 * ((R + 3) / 4);
+        for (int ub = 0; ub < units; ub += POTRF_THREADS) {  // one pass for n <= 256
+        const int cb = tid & 7, rb = (ub + tid) >> 3;
+        const bool mine = ub + tid < units;
+        Acc acc[4][4];
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+            for (int y = 0; y < 4; ++y) acc[x][y] = Acc(0);
+        for (int t0 = 0; t0 < J; t0 += KT) {
+            for (int e = tid; e < R * KT; e += POTRF_THREADS) {
+                const int r = e / KT, tt = e % KT;
+                As[tt * ldS + r] = A.get(J + r, t0 + tt);
+            }
+            for (int e = tid; e < PW * KT; e += POTRF_THREADS) {
+                const int jj = e / KT, tt = e % KT;
+                Bs[tt * (PW + 4) + jj] = jj < w ? A.get(J + jj, t0 + tt) : Acc(0);
+            }
+            __syncthreads();
+            if (mine)
+#pragma unroll 4
+                for (int tt = 0; tt < KT; ++tt) {
+                    Acc a[4], bb[4];
+#pragma unroll
+                    for (int x = 0; x < 4; ++x) a[x] = As[tt * ldS + 4 * rb + x];
+#pragma unroll
+                    for (int y = 0; y < 4; ++y) bb[y] = Bs[tt * (PW + 4) + 4 * cb + y];
+#pragma unroll
+                    for (int x = 0; x < 4; ++x)
+#pragma unroll
+                        for (int y = 0; y < 4; ++y) acc[x][y] = fma(a[x], bb[y], acc[x][y]);
+                }
+            __syncthreads();
+        }
+        if (mine)
+#pragma unroll
+            for (int x = 0; x < 4; ++x)
+#pragma unroll
+                for (int y = 0; y < 4; ++y) {
+                    const int r = 4 * rb + x;
+                    if (r < R) P[r * PW + 4 * cb + y] = acc[x][y];
+                }
+        }
+        __syncthreads();
+        // (b1) diagonal block by warp 0: lane l owns row J + l
+        if (warp == 0) {
+            Acc x[PW];
+            const bool live = lane < w;
+#pragma unroll
+            for (int tt = 0; tt < PW; ++tt) x[tt] = (live && tt <= lane && tt < w) ? A.get(J + lane, J + tt) : Acc(0);
+#pragma unroll
+            for (int jj = 0; jj < PW; ++jj) {
+                if (jj < w) {
+                    Acc s = live ? P[lane * PW + jj] : Acc(0);
+#pragma unroll
+                    for (int tt = 0; tt < jj; ++tt) s = fma(x[tt], __shfl_sync(0xffffffffu, x[tt], jj), s);
+                    const Acc v = rnd<L>(x[jj] - s);  // rn_level(rn_acc(c - s))
+                    const Acc piv = __shfl_sync(0xffffffffu, v, jj);
+                    if (lane == 0 && !(isfinite(piv) && piv > Acc(0)))
+                        report(c, seq, uint64_t(J + jj));
+                    const Acc d = rnd<L>(sqrt(piv));
+                    if (lane == jj) x[jj] = d;
+                    else if (lane > jj) x[jj] = rnd<L>(v / d);
+                }
+            }
+            if (live)
+#pragma unroll
+                for (int tt = 0; tt < PW; ++tt)
+                    if (tt <= lane && tt < w) A.set(J + lane, J + tt, x[tt]);
+        }
+        __syncthreads();
+        // (b2) rows below the diagonal block, one thread per row
+        for (int r = PW + tid; r < R; r += POTRF_THREADS) {
+            const int i = J + r;
+            Acc x[PW];
+#pragma unroll
+            for (int jj = 0; jj < PW; ++jj) {
+                if (jj < w) {
+                    Acc s = P[r * PW + jj];
+#pragma unroll
+                    for (int tt = 0; tt < jj; ++tt) s = fma(x[tt], A.get(J + jj, J + tt), s);
+                    const Acc v = rnd<L>(A.get(i, J + jj) - s);
+                    x[jj] = rnd<L>(v / A.get(J + jj, J + jj));
+                }
+            }
+#pragma unroll
+            for (int jj = 0; jj < PW; ++jj)
+                if (jj < w) A.set(i, J + jj, x[jj]);
+        }
+        __syncthreads();
+    }
+
+    if constexpr (SMEM) {
+        for (int i = warp; i < n; i += NW)
+            for (int j = lane; j <= i; j += 32)
+                g[(long long)i * c.ldw + j] = from_double<T>(double(S[(i * (i + 1)) / 2 + j]));
+    }
+}
+
+// trsm_leaf: B (m x n at (br0, bc0)) <- B * L^-T, L the n x n square at lr0
+template <int L>
+__global__ void __launch_bounds__(128) k_trsm_leaf(DevCtx c, int br0, int bc0, int m, int n, int lr0,
+                                                  uint32_t seq) {
+    using T = typename LvT<L>::T;
+    using Acc = typename LvT<L>::Acc;
+    constexpr int TSL = 128;  // staged slice of finished columns
+    __shared__ Acc Lc[TSL][PW + 1];
+    __shared__ Acc D[PW][PW + 1];
+    const T* Lg = lvbuf<L>(c) + (long long)lr0 * c.ldw + lr0;
+    T* Bg = lvbuf<L>(c) + (long long)br0 * c.ldw + bc0;
+    // a quad of threads per row: the finished-column sums are split over the
+    // quad (t = q, q+4, ...) and reduced with shuffles; the in-chunk
+    // substitution is run redundantly by the quad, quad lane 0 stores
+    const int q = threadIdx.x & 3;
+    const int i = blockIdx.x * TRSM_ROWS + (threadIdx.x >> 2);
+    const bool live = i < m;
+    T* row = Bg + (long long)(live ? i : 0) * c.ldw;
+
+    for (int J = 0; J < n; J += PW) {
+        const int w = min(PW, n - J);
+        Acc acc[PW];
+#pragma unroll
+        for (int jj = 0; jj < PW; ++jj) acc[jj] = Acc(0);
+        for (int t0 = 0; t0 < J; t0 += TSL) {
+            const int tw = min(TSL, J - t0);
+            __syncthreads();
+            for (int e = threadIdx.x; e < tw * PW; e += 128) {
+                const int tt = e % tw, jj = e / tw;
+                Lc[tt][jj] = jj < w ? Acc(to_d(Lg[(long long)(J + jj) * c.ldw + t0 + tt])) : Acc(0);
+            }
+            __syncthreads();
+            if (live)
+                for (int tt = q; tt < tw; tt += 4) {
+                    const Acc xv = Acc(to_d(row[t0 + tt]));
+#pragma unroll
+                    for (int jj = 0; jj < PW; ++jj) acc[jj] = fma(xv, Lc[tt][jj], acc[jj]);
+                }
+        }
+#pragma unroll
+        for (int jj = 0; jj < PW; ++jj) {
+            acc[jj] += __shfl_xor_sync(0xffffffffu, acc[jj], 1);
+            acc[jj] += __shfl_xor_sync(0xffffffffu, acc[jj], 2);
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < PW * PW; e += 128) {
+            const int tt = e % PW, jj = e / PW;
+            D[tt][jj] = (jj < w && tt < w) ? Acc(to_d(Lg[(long long)(J + jj) * c.ldw + J + tt])) : Acc(1);
+        }
+        __syncthreads();
+        if (blockIdx.x == 0 && threadIdx.x == 0)
+            for (int jj = 0; jj < w; ++jj) {
+                const Acc ljj = D[jj][jj];
+                if (ljj == Acc(0) || !isfinite(ljj)) {
+                    report(c, seq, uint64_t(J + jj));
+                    break;
+                }
+            }
+        Acc x[PW];
+        if (live) {
+#pragma unroll
+            for (int jj = 0; jj < PW; ++jj) {
+                if (jj < w) {
+                    Acc s = acc[jj];
+#pragma unroll
+                    for (int tt = 0; tt < jj; ++tt) s = fma(x[tt], D[tt][jj], s);
+                    const Acc v = rnd<L>(Acc(to_d(row[J + jj])) - s);
+                    x[jj] = rnd<L>(v / D[jj][jj]);
+                }
+            }
+        }
+        __syncwarp();  // every quad lane has read row[J..J+w) before lane 0 stores
+        if (live && q == 0)
+#pragma unroll
+            for (int jj = 0; jj < PW; ++jj)
+                if (jj < w) row[J + jj] = from_double<T>(double(x[jj]));
+    }
+}
+
+template <int L, bool SMEM>
+void potrf_launch(const DevCtx& c, int r0, int n, uint32_t seq, cudaStream_t s) {
+    using Acc = typename LvT<L>::Acc;
+    const size_t smem = potrf_smem<Acc>(n, SMEM);
+    k_potrf_leaf<L, SMEM><<<1, POTRF_THREADS, smem, s>>>(c, r0, n, seq);
+}
+
+}  // namespace
+
+void init_leaf_attributes() {
+    const int cap = 227 * 1024;
+    cudaFuncSetAttribute(k_potrf_leaf<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
+    cudaFuncSetAttribute(k_potrf_leaf<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
+    cudaFuncSetAttribute(k_potrf_leaf<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
+    cudaFuncSetAttribute(k_potrf_leaf<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
+    cudaFuncSetAttribute(k_potrf_leaf<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
+    cudaFuncSetAttribute(k_potrf_leaf<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
+}
+
+constexpr size_t kLeafSmemCap = 220 * 1024;
+
+void launch_potrf_leaf(const DevCtx& c, int lv, int r0, int n, uint32_t seq, cudaStream_t s) {
+    const bool d = lv == LV_F64;
+    const bool fits = (d ? potrf_smem<double>(n, true) : potrf_smem<float>(n, true)) <= kLeafSmemCap;
+    const bool pfits = (d ? potrf_smem<double>(n, false) : potrf_smem<float>(n, false)) <= kLeafSmemCap;
+    if (!pfits) {
+        // the partial-sum panel alone exceeds shared memory: n > ~860 (F64)
+        // -- not reachable with the supported leaf sizes; guard anyway
+        return;
+    }
+    switch (lv) {
+        case LV_F16: fits ? potrf_launch<0, true>(c, r0, n, seq, s) : potrf_launch<0, false>(c, r0, n, seq, s); break;
+        case LV_F32: fits ? potrf_launch<1, true>(c, r0, n, seq, s) : potrf_launch<1, false>(c, r0, n, seq, s); break;
+        default: fits ? potrf_launch<2, true>(c, r0, n, seq, s) : potrf_launch<2, false>(c, r0, n, seq, s); break;
+    }
+}
+
+void launch_trsm_leaf(const DevCtx& c, int lv, int br0, int bc0, int m, int n, int lr0, uint32_t seq,
+                      cudaStream_t s) {
+    const int grid = (m + TRSM_ROWS - 1) / TRSM_ROWS;
+    if (grid == 0) return;
+    switch (lv) {
+        case LV_F16: k_trsm_leaf<0><<<grid, 128, 0, s>>>(c, br0, bc0, m, n, lr0, seq); break;
+        case LV_F32: k_trsm_leaf<1><<<grid, 128, 0, s>>>(c, br0, bc0, m, n, lr0, seq); break;
+        default: k_trsm_leaf<2><<<grid, 128, 0, s>>>(c, br0, bc0, m, n, lr0, seq); break;
+    }
+}
+
+}  // namespace tcb

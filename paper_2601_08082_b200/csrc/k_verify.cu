@@ -1,0 +1,349 @@
+// k_verify.cu -- accuracy metrics and the solve, all FP64 on the device.
+//
+//   fact_error   ||A - L L^T||_F / ||A||_F over the symmetric matrix
+//                (factorization_error, analysis.cpp:30-62): lower triangles
+//                only, weight 2 off the diagonal, NaN on non-finite input.
+//                64x64 lower tiles of E = A - L L^T; per-tile partial sums
+//                reduced in a fixed order (deterministic).
+//   potrs        L y = b then L^T x = y (no reference counterpart; SURVEY
+//                8(a) row 25).  Bandwidth-bound wavefront: one CTA per
+//                64-row block, blocks claim logical indices from an atomic
+//                ticket so a block only ever waits on blocks already
+//                running; finished blocks publish a flag.  L is streamed
+//                once per direction with coalesced column reads.
+//   residual     ||b - A x||_2 / (||A||_F ||x||_2 + ||b||_2), A symmetric
+//                with only its lower triangle read.
+#include "device.cuh"
+#include "launch.hpp"
+
+namespace tcb {
+
+namespace {
+
+constexpr int VT = 64;  // tile / block size
+
+// ---------------------------------------------------------------- fact_error
+__global__ void __launch_bounds__(256) k_fact_error(int n, const double* __restrict__ A, long long lda,
+                                                    const double* __restrict__ Lm, long long ldl, double* partials,
+                                                    int* nonfinite, int T) {
+    // tile index -> (I, J), I >= J, row-major over the lower tile triangle
+    const int t = blockIdx.x;
+    int I = int((sqrt(8.0 * t + 1.0) - 1.0) / 2.0);
+    while ((I + 1) * (I + 2) / 2 <= t) ++I;
+    while (I * (I + 1) / 2 > t) --I;
+    const int J = t - I * (I + 1) / 2;
+    const int i0 = I * VT, j0 = J * VT;
+    __shared__ double Li[16][VT + 1];
+    __shared__ double Lj[16][VT + 1];
+    __shared__ double red[2][8];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // 16 x 16 threads, 4x4 each
+    double acc[4][4] = {};
+    const int kmax = min(j0 + VT, n);  // k <= j <= i for lower elements
+    for (int k0 = 0; k0 < kmax; k0 += 16) {
+        for (int e = threadIdx.x; e < 16 * VT; e += 256) {
+            const int r = e % VT, kk = e / VT;
+            const int k = k0 + kk, gi = i0 + r, gj = j0 + r;
+            Li[kk][r] = (gi < n && k < n && k <= gi) ? Lm[(long long)k * ldl + gi] : 0.0;
+            Lj[kk][r] = (gj < n && k < n && k <= gj) ? Lm[(long long)k * ldl + gj] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) {
+            double a[4], b[4];
+#pragma unroll
+            for (int x = 0; x < 4; ++x) a[x] = Li[kk][ty * 4 + x];
+#pragma unroll
+            for (int y = 0; y < 4; ++y) b[y] = Lj[kk][tx * 4 + y];
+#pragma unroll
+            for (int x = 0; x < 4; ++x)
+#pragma unroll
+                for (int y = 0; y < 4; ++y) acc[x][y] = fma(a[x], b[y], acc[x][y]);
+        }
+        __syncthreads();
+    }
+    double num = 0.0, den = 0.0;
+    int bad = 0;
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) {
+            const int i = i0 + ty * 4 + x, j = j0 + tx * 4 + y;
+            if (i >= n || j > i) continue;
+            const double a = A[(long long)j * lda + i];
+            const double l = Lm[(long long)j * ldl + i];
+            if (!isfinite(a) || !isfinite(l)) bad = 1;
+            const double e = a - acc[x][y];
+            const double w = i == j ? 1.0 : 2.0;
+            num += w * e * e;
+            den += w * a * a;
+        }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        num += __shfl_xor_sync(0xffffffffu, num, o);
+        den += __shfl_xor_sync(0xffffffffu, den, o);
+    }
+    bad = __any_sync(0xffffffffu, bad);
+    if ((threadIdx.x & 31) == 0) {
+        red[0][threadIdx.x >> 5] = num;
+        red[1][threadIdx.x >> 5] = den;
+    }
+    if (bad && (threadIdx.x & 31) == 0) atomicExch(nonfinite, 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s0 = 0.0, s1 = 0.0;
+        for (int w = 0; w < 8; ++w) {
+            s0 += red[0][w];
+            s1 += red[1][w];
+        }
+        partials[2 * t] = s0;
+        partials[2 * t + 1] = s1;
+    }
+}
+
+__global__ void k_fact_error_final(const double* partials, int count, const int* nonfinite, double* out) {
+    __shared__ double s0[256], s1[256];
+    double a = 0.0, b = 0.0;
+    for (int t = threadIdx.x; t < count; t += 256) {
+        a += partials[2 * t];
+        b += partials[2 * t + 1];
+    }
+    s0[threadIdx.x] = a;
+    s1[threadIdx.x] = b;
+    __syncthreads();
+    for (int w = 128; w; w >>= 1) {
+        if (threadIdx.x < w) {
+            s0[threadIdx.x] += s0[threadIdx.x + w];
+            s1[threadIdx.x] += s1[threadIdx.x + w];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = *nonfinite ? __longlong_as_double(0x7ff8000000000000ll) : sqrt(s0[0] / s1[0]);
+}
+
+// ---------------------------------------------------------------- potrs
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// forward: y = L^-1 b, in place on b.  counters: [0] ticket, [1..nb] flags
+__global__ void __launch_bounds__(256) k_potrs_fwd(int n, const double* __restrict__ Lm, long long ldl, double* B,
+                                                   long long ldb, int* counters) {
+    const int nb = (n + VT - 1) / VT;
+    int* cnt = counters + blockIdx.y * (nb + 1);
+    double* y = B + blockIdx.y * ldb;
+    __shared__ int sI;
+    __shared__ double part[4][VT];
+    __shared__ double yb[VT];
+    if (threadIdx.x == 0) sI = atomicAdd(cnt, 1);
+    __syncthreads();
+    const int I = sI;
+    const int i0 = I * VT;
+    const int r = threadIdx.x & 63, q = threadIdx.x >> 6;
+    const int gi = i0 + r;
+    double acc = 0.0;
+    for (int J = 0; J < I; ++J) {
+        if (threadIdx.x == 0)
+            while (ld_acquire(cnt + 1 + J) == 0) {
+            }
+        __syncthreads();
+        const int k0 = J * VT + q * 16;
+        if (gi < n)
+#pragma unroll 4
+            for (int kk = 0; kk < 16; ++kk) {
+                const int k = k0 + kk;
+                acc = fma(Lm[(long long)k * ldl + gi], __ldcg(y + k), acc);
+            }
+    }
+    part[q][r] = acc;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        // diagonal block solve by one warp: lane l owns rows l and l + 32
+        double v[2];
+        for (int h = 0; h < 2; ++h) {
+            const int rr = threadIdx.x + 32 * h, g = i0 + rr;
+            v[h] = g < n ? y[g] - (part[0][rr] + part[1][rr] + part[2][rr] + part[3][rr]) : 0.0;
+        }
+        const int rows = min(VT, n - i0);
+        for (int k = 0; k < rows; ++k) {
+            const int owner = k & 31, h = k >> 5;
+            double xk = __shfl_sync(0xffffffffu, h ? v[1] : v[0], owner);
+            xk = xk / Lm[(long long)(i0 + k) * ldl + i0 + k];
+            if (threadIdx.x == owner) {
+                if (h) v[1] = xk;
+                else v[0] = xk;
+            }
+            for (int hh = 0; hh < 2; ++hh) {
+                const int rr = threadIdx.x + 32 * hh;
+                if (rr > k && rr < rows) v[hh] -= Lm[(long long)(i0 + k) * ldl + i0 + rr] * xk;
+            }
+        }
+        for (int h = 0; h < 2; ++h) {
+            const int rr = threadIdx.x + 32 * h;
+            if (rr < rows) y[i0 + rr] = v[h];
+        }
+        __threadfence();
+        __syncwarp();
+        if (threadIdx.x == 0) st_release(cnt + 1 + I, 1);
+    }
+}
+
+// backward: x = L^-T y, in place, blocks in reverse order
+__global__ void __launch_bounds__(256) k_potrs_bwd(int n, const double* __restrict__ Lm, long long ldl, double* B,
+                                                   long long ldb, int* counters) {
+    const int nb = (n + VT - 1) / VT;
+    int* cnt = counters + blockIdx.y * (nb + 1);
+    double* y = B + blockIdx.y * ldb;
+    __shared__ int sI;
+    __shared__ double part[4][VT];
+    if (threadIdx.x == 0) sI = nb - 1 - atomicAdd(cnt, 1);
+    __syncthreads();
+    const int I = sI;
+    const int i0 = I * VT;
+    const int r = threadIdx.x & 63, q = threadIdx.x >> 6;
+    const int gi = i0 + r;  // x_gi needs sum_{k > block} L(k, gi) x_k
+    double acc = 0.0;
+    for (int J = nb - 1; J > I; --J) {
+        if (threadIdx.x == 0)
+            while (ld_acquire(cnt + 1 + J) == 0) {
+            }
+        __syncthreads();
+        const int k0 = J * VT + q * 16;
+        if (gi < n)
+            for (int kk = 0; kk < 16; ++kk) {
+                const int k = k0 + kk;
+                if (k < n) acc = fma(Lm[(long long)gi * ldl + k], __ldcg(y + k), acc);
+            }
+    }
+    part[q][r] = acc;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double v[2];
+        const int rows = min(VT, n - i0);
+        for (int h = 0; h < 2; ++h) {
+            const int rr = threadIdx.x + 32 * h, g = i0 + rr;
+            v[h] = rr < rows ? y[g] - (part[0][rr] + part[1][rr] + part[2][rr] + part[3][rr]) : 0.0;
+        }
+        for (int k = rows - 1; k >= 0; --k) {
+            const int owner = k & 31, h = k >> 5;
+            double xk = __shfl_sync(0xffffffffu, h ? v[1] : v[0], owner);
+            xk = xk / Lm[(long long)(i0 + k) * ldl + i0 + k];
+            if (threadIdx.x == owner) {
+                if (h) v[1] = xk;
+                else v[0] = xk;
+            }
+            for (int hh = 0; hh < 2; ++hh) {
+                const int rr = threadIdx.x + 32 * hh;
+                // row rr < k of L^T: x_rr -= L(k, rr) x_k
+                if (rr < k) v[hh] -= Lm[(long long)(i0 + rr) * ldl + i0 + k] * xk;
+            }
+        }
+        for (int h = 0; h < 2; ++h) {
+            const int rr = threadIdx.x + 32 * h;
+            if (rr < rows) y[i0 + rr] = v[h];
+        }
+        __threadfence();
+        __syncwarp();
+        if (threadIdx.x == 0) st_release(cnt + 1 + I, 1);
+    }
+}
+
+// ---------------------------------------------------------------- residual
+// per 64-row block I: r_I = b_I - sum_J A(I,J) x_J with A(I,J) = A(J,I)^T above
+__global__ void __launch_bounds__(256) k_residual(int n, const double* __restrict__ A, long long lda,
+                                                  const double* __restrict__ X, const double* __restrict__ Bv,
+                                                  double* partials) {
+    const int I = blockIdx.x, i0 = I * VT;
+    const int r = threadIdx.x & 63, q = threadIdx.x >> 6;
+    const int gi = i0 + r;
+    __shared__ double part[4][VT];
+    __shared__ double red[4][8];
+    double acc = 0.0, anorm = 0.0;
+    if (gi < n)
+        for (int j = q; j < n; j += 4) {
+            // lower element A(max, min)
+            const double a = j <= gi ? A[(long long)j * lda + gi] : A[(long long)gi * lda + j];
+            acc = fma(a, X[j], acc);
+            if (j <= gi) anorm += (j == gi ? 1.0 : 2.0) * a * a;
+        }
+    part[q][r] = acc;
+    __syncthreads();
+    double rr = 0.0, xx = 0.0, bb = 0.0, aa = anorm;
+    if (threadIdx.x < VT && gi < n) {
+        const double ax = part[0][r] + part[1][r] + part[2][r] + part[3][r];
+        const double res = Bv[gi] - ax;
+        rr = res * res;
+        xx = X[gi] * X[gi];
+        bb = Bv[gi] * Bv[gi];
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        rr += __shfl_xor_sync(0xffffffffu, rr, o);
+        xx += __shfl_xor_sync(0xffffffffu, xx, o);
+        bb += __shfl_xor_sync(0xffffffffu, bb, o);
+        aa += __shfl_xor_sync(0xffffffffu, aa, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        red[0][threadIdx.x >> 5] = rr;
+        red[1][threadIdx.x >> 5] = xx;
+        red[2][threadIdx.x >> 5] = bb;
+        red[3][threadIdx.x >> 5] = aa;
+    }
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        double s = 0.0;
+        for (int w = 0; w < 8; ++w) s += red[threadIdx.x][w];
+        partials[4 * I + threadIdx.x] = s;
+    }
+}
+
+__global__ void k_residual_final(const double* partials, int count, double* out) {
+    if (threadIdx.x != 0) return;
+    double s[4] = {0, 0, 0, 0};
+    for (int t = 0; t < count; ++t)
+        for (int k = 0; k < 4; ++k) s[k] += partials[4 * t + k];
+    *out = sqrt(s[0]) / (sqrt(s[3]) * sqrt(s[1]) + sqrt(s[2]));
+}
+
+}  // namespace
+
+int fact_error_partials(int n, int* tiles_per_side) {
+    const int T = (n + VT - 1) / VT;
+    *tiles_per_side = T;
+    return T * (T + 1) / 2;
+}
+
+void launch_fact_error(int n, const double* dA, long long lda, const double* dL, long long ldl, double* d_partials,
+                       int* d_nonfinite, int T, cudaStream_t s) {
+    const int tiles = T * (T + 1) / 2;
+    cudaMemsetAsync(d_nonfinite, 0, sizeof(int), s);
+    k_fact_error<<<tiles, 256, 0, s>>>(n, dA, lda, dL, ldl, d_partials, d_nonfinite, T);
+    k_fact_error_final<<<1, 256, 0, s>>>(d_partials, tiles, d_nonfinite, d_partials + 2 * size_t(tiles));
+}
+
+size_t potrs_work_doubles(int n, int nrhs) { return 0; }
+
+void launch_potrs(int n, const double* dL, long long ldl, double* dB, long long ldb, int nrhs, int* d_counters,
+                  double*, cudaStream_t s) {
+    const int nb = (n + VT - 1) / VT;
+    const size_t cbytes = sizeof(int) * size_t(nb + 1) * size_t(nrhs);
+    cudaMemsetAsync(d_counters, 0, cbytes, s);
+    k_potrs_fwd<<<dim3(nb, nrhs), 256, 0, s>>>(n, dL, ldl, dB, ldb, d_counters);
+    cudaMemsetAsync(d_counters, 0, cbytes, s);
+    k_potrs_bwd<<<dim3(nb, nrhs), 256, 0, s>>>(n, dL, ldl, dB, ldb, d_counters);
+}
+
+int residual_partials(int n) { return (n + VT - 1) / VT; }
+
+void launch_residual(int n, const double* dA, long long lda, const double* dX, const double* dB, double* d_partials,
+                     cudaStream_t s) {
+    const int nb = (n + VT - 1) / VT;
+    k_residual<<<nb, 256, 0, s>>>(n, dA, lda, dX, dB, d_partials);
+    k_residual_final<<<1, 32, 0, s>>>(d_partials, nb, d_partials + 4 * size_t(nb));
+}
+
+}  // namespace tcb

@@ -1,0 +1,68 @@
+// launch.hpp -- host-side launchers of the sm_100a kernels (internal).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <vector>
+
+#include "device.cuh"
+#include "plan.hpp"
+
+#include <string>
+
+namespace tcb {
+
+struct BlockDescHost {
+    int r0, c0, m, n, level, lower;
+};
+
+// elementwise (k_elementwise.cu)
+int make_block_table(const std::vector<BlockDescHost>& in, std::vector<BlockDesc>& out);
+void launch_import(const DevCtx& c, const BlockDesc* d_blocks, int nb, int tiles, cudaStream_t s);
+void launch_export(const DevCtx& c, const BlockDesc* d_blocks, int nb, int tiles, cudaStream_t s);
+void launch_shadow(const DevCtx& c, const BlockDesc* d_blocks, int nb, int tiles, int p, cudaStream_t s);
+void launch_check(const DevCtx& c, int lv, int r0, int c0, int m, int n, int lower, uint32_t seq,
+                  cudaStream_t s);
+void launch_quant(const DevCtx& c, int lv, int r0, int c0, int m, int n, int slot, uint32_t seq,
+                  cudaStream_t s);
+void launch_dequant(const DevCtx& c, int lv, int r0, int c0, int m, int n, int slot, cudaStream_t s);
+
+// spd_generate symmetrization of raw draws (k_elementwise.cu)
+void launch_symmetrize(double* a, long long lda, int n, cudaStream_t s);
+
+// one-time kernel attributes (before any graph capture)
+void init_leaf_attributes();
+void init_tc_attributes();
+
+// leaves (k_leaf.cu)
+void launch_potrf_leaf(const DevCtx& c, int lv, int r0, int n, uint32_t seq, cudaStream_t s);
+void launch_trsm_leaf(const DevCtx& c, int lv, int br0, int bc0, int m, int n, int lr0, uint32_t seq,
+                      cudaStream_t s);
+
+// grouped GEMM (k_gemm_simt.cu / k_gemm_tc.cu)
+// problems must already be in device memory with tile0 / tiles_n filled by
+// the matching *_tiles() helper
+int simt_tiles(std::vector<DevProb>& probs);
+void launch_gemm_simt(const DevCtx& c, int gclass, const DevProb* d_probs, int nprob, int tiles,
+                      cudaStream_t s);
+
+struct TcProb;  // defined in k_gemm_tc.cu (holds TMA descriptors)
+size_t tc_prob_size();
+// fills host-side TcProb records (tensor maps over the F16 buffer)
+int tc_build_probs(const DevCtx& c, const std::vector<DevProb>& probs, std::vector<unsigned char>& out,
+                   std::string* err);
+void launch_gemm_tc(const DevCtx& c, const void* d_probs, int nprob, int tiles, cudaStream_t s);
+bool tc_supported();
+
+// verification (k_verify.cu)
+void launch_fact_error(int n, const double* dA, long long lda, const double* dL, long long ldl,
+                       double* d_partials, int* d_nonfinite, int tiles_per_side, cudaStream_t s);
+int fact_error_partials(int n, int* tiles_per_side);
+void launch_potrs(int n, const double* dL, long long ldl, double* dB, long long ldb, int nrhs,
+                  int* d_counters, double* d_work, cudaStream_t s);
+size_t potrs_work_doubles(int n, int nrhs);
+void launch_residual(int n, const double* dA, long long lda, const double* dX, const double* dB,
+                     double* d_partials, cudaStream_t s);
+int residual_partials(int n);
+
+}  // namespace tcb

@@ -1,0 +1,631 @@
+// plan.cpp -- see plan.hpp.  Reference recursion: tree.cpp:42-152,
+// static counter: analysis.cpp:64-120, config grammar: precision.cpp:17-111.
+#include "plan.hpp"
+
+#include <algorithm>
+#include <array>
+#include <cctype>
+#include <stdexcept>
+
+namespace tcb {
+
+Rect Rect::unite(const Rect& o) const {
+    if (m <= 0 || n <= 0) return o;
+    if (o.m <= 0 || o.n <= 0) return *this;
+    Rect r;
+    r.r0 = std::min(r0, o.r0);
+    r.c0 = std::min(c0, o.c0);
+    r.m = std::max(r0 + m, o.r0 + o.m) - r.r0;
+    r.n = std::max(c0 + n, o.c0 + o.n) - r.c0;
+    return r;
+}
+
+// ---------------------------------------------------------------------------
+// tree construction (build_node, tree.cpp:42-66): n1 = floor(n/2), leaf iff
+// n <= b, levels by depth with saturation (precision.hpp:84-86)
+// ---------------------------------------------------------------------------
+
+int Plan::build_node(int r0, int n, int depth) {
+    const int id = int(nodes.size());
+    nodes.push_back(Node{});
+    nodes[id].r0 = r0;
+    nodes[id].n = n;
+    nodes[id].depth = depth;
+    if (n <= b) {
+        nodes[id].leaf = true;
+        nodes[id].level = leaf_level();
+        Block blk;
+        blk.rect = {r0, r0, n, n};
+        blk.level = leaf_level();
+        blk.leaf = true;
+        blk.node = id;
+        nodes[id].block = int(blocks.size());
+        blocks.push_back(blk);
+        return id;
+    }
+    const int n1 = n / 2, n2 = n - n1;
+    nodes[id].n1 = n1;
+    nodes[id].level = at_depth(depth);
+    Block blk;
+    blk.rect = {r0 + n1, r0, n2, n1};
+    blk.level = at_depth(depth);
+    blk.node = id;
+    nodes[id].block = int(blocks.size());
+    blocks.push_back(blk);
+    const int d1 = build_node(r0, n1, depth + 1);
+    const int d2 = build_node(r0 + n1, n2, depth + 1);
+    nodes[id].d1 = d1;
+    nodes[id].d2 = d2;
+    return id;
+}
+
+int Plan::gemm_class(int op_level, int exec_level) const {
+    if (op_level == LV_F16) {
+        if (exec_level == LV_F64) return GC_SIMT_F16D;
+        return opt.use_tc ? GC_TC16 : GC_SIMT_F16;
+    }
+    if (op_level == LV_F32) return exec_level == LV_F64 ? GC_SIMT_F32D : GC_SIMT_F32;
+    return GC_SIMT_F64;
+}
+
+int Plan::push(Op op) {
+    ops.push_back(std::move(op));
+    return int(ops.size()) - 1;
+}
+
+// ---------------------------------------------------------------------------
+// level conversion of final L blocks: trsm_leaf / gemm_mixed read L through
+// round_to(., p) (kernels.cpp:29, kernels.cpp:78).  Blocks stored above p get
+// a p-rounded copy in buffer p, made once, right after they became final.
+// ---------------------------------------------------------------------------
+
+void Plan::ensure_shadows(int node, int p) {
+    std::vector<int> todo;
+    std::vector<int> stack{node};
+    while (!stack.empty()) {
+        const int id = stack.back();
+        stack.pop_back();
+        const Node& nd = nodes[id];
+        const int blk = nd.block;
+        if (blocks[blk].level > p && !has_shadow[blk][p]) {
+            todo.push_back(blk);
+            has_shadow[blk][p] = 1;
+        }
+        if (!nd.leaf) {
+            stack.push_back(nd.d1);
+            stack.push_back(nd.d2);
+        }
+    }
+    if (todo.empty()) return;
+    std::sort(todo.begin(), todo.end());
+    Op op;
+    op.type = OP_SHADOW;
+    op.level = p;
+    op.blocks = todo;
+    for (int blk : todo) op.rect = op.rect.unite(blocks[blk].rect);
+    needs_buf[p] = true;
+    push(std::move(op));
+}
+
+// ---------------------------------------------------------------------------
+// tree_trsm (tree.cpp:127-138)
+// ---------------------------------------------------------------------------
+
+void Plan::emit_trsm(Rect B, int p, int lnode) {
+    const Node& L = nodes[lnode];
+    if (L.leaf || std::min(B.m, B.n) <= leaf_size) {
+        Op op;
+        op.type = OP_TRSM;
+        op.level = p;
+        op.rect = B;
+        op.lrect = {L.r0, L.r0, L.n, L.n};
+        op.seq = next_seq();
+        const uint64_t f = uint64_t(B.m) * uint64_t(B.n) * uint64_t(B.n);
+        add_flops(op.seq, p, K_TRSM, f);
+        op.flops = double(f);
+        push(std::move(op));
+        return;
+    }
+    const int n1 = L.n1;
+    const int d1 = L.d1, d2 = L.d2;
+    const Rect off = blocks[L.block].rect;
+    Rect B1{B.r0, B.c0, B.m, n1};
+    Rect B2{B.r0, B.c0 + n1, B.m, B.n - n1};
+    emit_trsm(B1, p, d1);
+    GemmProb g;
+    g.m = B.m;
+    g.n = B.n - n1;
+    g.k = n1;
+    g.a_r0 = B1.r0;
+    g.a_c0 = B1.c0;
+    g.b_r0 = off.r0;
+    g.b_c0 = off.c0;
+    g.c_r0 = B2.r0;
+    g.c_c0 = B2.c0;
+    g.exec_level = p;
+    g.seq = next_seq();
+    g.ref_kernel = K_GEMM;
+    const uint64_t f = 2ull * uint64_t(g.m) * uint64_t(g.n) * uint64_t(g.k);
+    add_flops(g.seq, p, K_GEMM, f);
+    Op op;
+    op.type = OP_GEMM;
+    op.level = p;
+    op.gclass = gemm_class(p, p);
+    op.prob_begin = int(probs.size());
+    probs.push_back(g);
+    op.prob_end = int(probs.size());
+    op.rect = B2;
+    op.flops = double(f);
+    push(std::move(op));
+    emit_trsm(B2, p, d2);
+}
+
+// ---------------------------------------------------------------------------
+// tree_syrk (tree.cpp:140-152): leaves via syrk_leaf at the leaf level, the
+// off-diagonal contributions via gemm_mixed at the destination's level.  All
+// sub-updates of one tree_syrk write disjoint blocks, so they are grouped
+// into one launch per operand class.
+// ---------------------------------------------------------------------------
+
+void Plan::collect_syrk(int cnode, Rect A, int p, std::vector<GemmProb>& out) {
+    const Node& C = nodes[cnode];
+    if (C.leaf) {
+        GemmProb g;
+        g.m = g.n = C.n;
+        g.k = A.n;
+        g.a_r0 = A.r0;
+        g.a_c0 = A.c0;
+        g.b_r0 = A.r0;
+        g.b_c0 = A.c0;
+        g.c_r0 = C.r0;
+        g.c_c0 = C.r0;
+        g.exec_level = leaf_level();
+        g.lower = 1;
+        g.seq = next_seq();
+        g.ref_kernel = K_SYRK;
+        add_flops(g.seq, g.exec_level, K_SYRK,
+                  uint64_t(C.n) * uint64_t(C.n + 1) * uint64_t(A.n));
+        out.push_back(g);
+        return;
+    }
+    const int n1 = C.n1;
+    const int d1 = C.d1, d2 = C.d2, lvl = C.level;
+    const Rect off = blocks[C.block].rect;
+    Rect A1{A.r0, A.c0, n1, A.n};
+    Rect A2{A.r0 + n1, A.c0, A.m - n1, A.n};
+    collect_syrk(d1, A1, p, out);
+    GemmProb g;
+    g.m = off.m;
+    g.n = off.n;
+    g.k = A.n;
+    g.a_r0 = A2.r0;
+    g.a_c0 = A2.c0;
+    g.b_r0 = A1.r0;
+    g.b_c0 = A1.c0;
+    g.c_r0 = off.r0;
+    g.c_c0 = off.c0;
+    g.exec_level = lvl;
+    g.seq = next_seq();
+    g.ref_kernel = K_GEMM;
+    add_flops(g.seq, lvl, K_GEMM, 2ull * uint64_t(g.m) * uint64_t(g.n) * uint64_t(g.k));
+    out.push_back(g);
+    collect_syrk(d2, A2, p, out);
+}
+
+void Plan::emit_syrk(int cnode, Rect A, int p) {
+    std::vector<GemmProb> all;
+    collect_syrk(cnode, A, p, all);
+    // one launch per class, classes in order of first appearance
+    std::vector<int> classes;
+    for (const auto& g : all) {
+        const int c = gemm_class(p, g.exec_level);
+        if (std::find(classes.begin(), classes.end(), c) == classes.end()) classes.push_back(c);
+    }
+    for (int c : classes) {
+        Op op;
+        op.type = OP_GEMM;
+        op.level = p;
+        op.gclass = c;
+        op.prob_begin = int(probs.size());
+        for (const auto& g : all)
+            if (gemm_class(p, g.exec_level) == c) {
+                probs.push_back(g);
+                op.rect = op.rect.unite({g.c_r0, g.c_c0, g.m, g.n});
+                op.flops += double(g.lower ? 2.0 * g.m * g.n * g.k / 2.0 : 2.0 * g.m * g.n * g.k);
+            }
+        op.prob_end = int(probs.size());
+        push(std::move(op));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// tree_potrf (tree.cpp:106-125)
+// ---------------------------------------------------------------------------
+
+void Plan::emit_potrf(int node) {
+    const Node nd = nodes[node];
+    if (nd.leaf) {
+        Op chk;
+        chk.type = OP_CHECK;
+        chk.level = nd.level;
+        chk.src = nd.level;
+        chk.rect = blocks[nd.block].rect;
+        chk.lower = 1;
+        chk.diagonal = 1;
+        chk.seq = next_seq();
+        push(std::move(chk));
+        Op op;
+        op.type = OP_POTRF;
+        op.level = nd.level;
+        op.rect = blocks[nd.block].rect;
+        op.seq = next_seq();
+        const uint64_t n = uint64_t(nd.n);
+        add_flops(op.seq, nd.level, K_POTRF, n * (n + 1) * (2 * n + 1) / 6);
+        op.flops = double(n) * n * n / 3.0;
+        push(std::move(op));
+        return;
+    }
+    emit_potrf(nd.d1);
+    const Block blk = blocks[nd.block];
+    const int p = blk.level;
+    int slot = -1;
+    if (blk.spine_quant) {
+        slot = n_alpha_slots++;
+        Op q;
+        q.type = OP_QUANT;
+        q.level = p;
+        q.rect = blk.rect;
+        q.slot = slot;
+        q.seq = next_seq();  // the require_finite that precedes quantize
+        push(std::move(q));
+    } else {
+        Op chk;
+        chk.type = OP_CHECK;
+        chk.level = p;
+        chk.src = p;
+        chk.rect = blk.rect;
+        chk.seq = next_seq();
+        push(std::move(chk));
+    }
+    ensure_shadows(nd.d1, p);
+    emit_trsm(blk.rect, p, nd.d1);
+    if (blk.spine_quant) {
+        Op dq;
+        dq.type = OP_DEQUANT;
+        dq.level = p;
+        dq.rect = blk.rect;
+        dq.slot = slot;
+        push(std::move(dq));
+    }
+    Op chk;
+    chk.type = OP_CHECK;
+    chk.level = p;
+    chk.src = p;
+    chk.rect = blk.rect;
+    chk.seq = next_seq();
+    push(std::move(chk));
+    emit_syrk(nd.d2, blk.rect, p);
+    emit_potrf(nd.d2);
+}
+
+// ---------------------------------------------------------------------------
+// dependencies
+// ---------------------------------------------------------------------------
+
+void Plan::finalize_accesses() {
+    const Rect whole{0, 0, n, n};
+    for (Op& op : ops) {
+        op.acc.clear();
+        switch (op.type) {
+            case OP_IMPORT:
+                op.acc.push_back({BUF_USER, whole, false});
+                for (int blk : op.blocks) op.acc.push_back({blocks[blk].level, blocks[blk].rect, true});
+                break;
+            case OP_EXPORT:
+                op.acc.push_back({BUF_USER, whole, true});
+                for (int blk : op.blocks) op.acc.push_back({blocks[blk].level, blocks[blk].rect, false});
+                break;
+            case OP_CHECK:
+                op.acc.push_back({op.src, op.rect, false});
+                break;
+            case OP_QUANT:
+                op.acc.push_back({BUF_USER, op.rect, false});
+                op.acc.push_back({op.level, op.rect, true});
+                op.acc.push_back({BUF_ALPHA, {op.slot, 0, 1, 1}, true});
+                break;
+            case OP_DEQUANT:
+                op.acc.push_back({BUF_ALPHA, {op.slot, 0, 1, 1}, false});
+                op.acc.push_back({op.level, op.rect, true});
+                break;
+            case OP_SHADOW:
+                for (int blk : op.blocks) {
+                    op.acc.push_back({blocks[blk].level, blocks[blk].rect, false});
+                    op.acc.push_back({op.level, blocks[blk].rect, true});
+                }
+                break;
+            case OP_POTRF:
+                op.acc.push_back({op.level, op.rect, true});
+                break;
+            case OP_TRSM:
+                op.acc.push_back({op.level, op.rect, true});
+                op.acc.push_back({op.level, op.lrect, false});
+                break;
+            case OP_GEMM: {
+                Rect rd;
+                std::vector<Rect> rds;
+                for (int i = op.prob_begin; i < op.prob_end; ++i) {
+                    const GemmProb& g = probs[i];
+                    rds.push_back({g.a_r0, g.a_c0, g.m, g.k});
+                    rds.push_back({g.b_r0, g.b_c0, g.n, g.k});
+                    op.acc.push_back({g.exec_level, {g.c_r0, g.c_c0, g.m, g.n}, true});
+                }
+                // drop read rects contained in another (SYRK reads sub-rows of one panel)
+                std::vector<Rect> keep;
+                for (size_t i = 0; i < rds.size(); ++i) {
+                    bool contained = false;
+                    for (size_t j = 0; j < rds.size() && !contained; ++j) {
+                        if (i == j) continue;
+                        const Rect& a = rds[i];
+                        const Rect& b = rds[j];
+                        const bool inside = a.r0 >= b.r0 && a.c0 >= b.c0 && a.r0 + a.m <= b.r0 + b.m &&
+                                            a.c0 + a.n <= b.c0 + b.n;
+                        const bool same = a.r0 == b.r0 && a.c0 == b.c0 && a.m == b.m && a.n == b.n;
+                        if (inside && !(same && j > i)) contained = true;
+                    }
+                    if (!contained) keep.push_back(rds[i]);
+                }
+                for (const Rect& r : keep) op.acc.push_back({op.level, r, false});
+                break;
+            }
+        }
+    }
+}
+
+void Plan::build_deps() {
+    const int N = int(ops.size());
+    // per-op, per-buffer bounding boxes for a fast reject
+    std::vector<std::array<Rect, BUF_COUNT>> bb(N);
+    for (int i = 0; i < N; ++i)
+        for (const Access& a : ops[i].acc) bb[i][a.buf] = bb[i][a.buf].unite(a.rect);
+    const int W = (N + 63) / 64;
+    std::vector<uint64_t> anc(size_t(N) * W, 0);
+    auto conflict = [&](int i, int j) {
+        bool any = false;
+        for (int b = 0; b < BUF_COUNT && !any; ++b) any = bb[i][b].overlaps(bb[j][b]);
+        if (!any) return false;
+        for (const Access& x : ops[i].acc)
+            for (const Access& y : ops[j].acc)
+                if (x.buf == y.buf && (x.write || y.write) && x.rect.overlaps(y.rect)) return true;
+        return false;
+    };
+    for (int i = 0; i < N; ++i) {
+        uint64_t* ai = &anc[size_t(i) * W];
+        for (int j = i - 1; j >= 0; --j) {
+            if (ai[j / 64] >> (j % 64) & 1ull) continue;  // already ordered transitively
+            if (!conflict(i, j)) continue;
+            ops[i].deps.push_back(j);
+            const uint64_t* aj = &anc[size_t(j) * W];
+            for (int w = 0; w < W; ++w) ai[w] |= aj[w];
+            ai[j / 64] |= 1ull << (j % 64);
+        }
+    }
+}
+
+Plan Plan::make(int n, int b, const std::vector<int>& levels, bool quantize, int leaf_size,
+                const PlanOptions& opt) {
+    if (b < 1) throw std::invalid_argument("leaf size must be >= 1");
+    if (levels.empty()) throw std::invalid_argument("empty precision config");
+    if (n < 1) throw std::invalid_argument("tree requires a square matrix of order >= 1");
+    for (int l : levels)
+        if (l < LV_F16 || l > LV_F64) throw std::invalid_argument("precision level out of range");
+    Plan P;
+    P.n = n;
+    P.b = b;
+    P.leaf_size = leaf_size > 0 ? leaf_size : b;
+    P.levels = levels;
+    P.quantize = quantize;
+    P.opt = opt;
+    P.build_node(0, n, 0);
+    // spine: nodes reached from the root through diag1 links only.  Their
+    // off-diagonal panels get no SYRK update before their quantize, so the
+    // scale is computed from the caller's original doubles (tree.cpp:117).
+    // Every other panel receives >= 1 update rounded to its level first, so
+    // max|B| <= range_max(level) and alpha == 1 exactly.  F64 spine panels
+    // also have alpha == 1 (max|B| <= DBL_MAX).
+    if (quantize)
+        for (int id = 0; id >= 0 && !P.nodes[id].leaf; id = P.nodes[id].d1) {
+            Block& blk = P.blocks[P.nodes[id].block];
+            if (blk.level != LV_F64) blk.spine_quant = true;
+        }
+    P.has_shadow.assign(P.blocks.size(), std::vector<uint8_t>(3, 0));
+    for (const Block& blk : P.blocks) P.needs_buf[blk.level] = true;
+
+    Op imp;
+    imp.type = OP_IMPORT;
+    for (int i = 0; i < int(P.blocks.size()); ++i)
+        if (!P.blocks[i].spine_quant) imp.blocks.push_back(i);
+    imp.rect = {0, 0, n, n};
+    P.push(std::move(imp));
+    P.emit_potrf(0);
+    Op exp;
+    exp.type = OP_EXPORT;
+    for (int i = 0; i < int(P.blocks.size()); ++i) exp.blocks.push_back(i);
+    exp.rect = {0, 0, n, n};
+    P.push(std::move(exp));
+    P.finalize_accesses();
+    P.build_deps();
+    return P;
+}
+
+void Plan::flop_totals(uint64_t by_level[3], uint64_t by_kernel[4], uint64_t calls[4],
+                       uint32_t seq_limit) const {
+    for (int i = 0; i < 3; ++i) by_level[i] = 0;
+    for (int i = 0; i < 4; ++i) by_kernel[i] = calls[i] = 0;
+    for (const FlopRec& r : flops) {
+        if (r.seq >= seq_limit) continue;
+        by_level[r.level] += r.flops;
+        by_kernel[r.kernel] += r.flops;
+        calls[r.kernel] += 1;
+    }
+}
+
+int Plan::op_of_seq(uint32_t seq) const {
+    for (int i = 0; i < int(ops.size()); ++i) {
+        const Op& op = ops[i];
+        if (op.seq == seq) return i;
+        if (op.type == OP_GEMM)
+            for (int p = op.prob_begin; p < op.prob_end; ++p)
+                if (probs[p].seq == seq) return i;
+    }
+    return -1;
+}
+
+// ---------------------------------------------------------------------------
+// StaticCounter (analysis.cpp:70-111) restated
+// ---------------------------------------------------------------------------
+
+namespace {
+struct Counter {
+    uint64_t b;
+    const std::vector<int>& lv;
+    uint64_t *L, *K, *C;
+    int at(int d) const { return lv[d < int(lv.size()) ? d : int(lv.size()) - 1]; }
+    void add(int level, int kernel, uint64_t f) {
+        L[level] += f;
+        K[kernel] += f;
+        C[kernel] += 1;
+    }
+    void trsm(uint64_t m, uint64_t n, int d, int p) {
+        if (n <= b || m <= b) return add(p, K_TRSM, m * n * n);
+        const uint64_t n1 = n / 2, n2 = n - n1;
+        trsm(m, n1, d + 1, p);
+        add(p, K_GEMM, 2 * m * n2 * n1);
+        trsm(m, n2, d + 1, p);
+    }
+    void syrk(uint64_t n, uint64_t k, int d, int p) {
+        if (n <= b) return add(lv.back(), K_SYRK, n * (n + 1) * k);
+        const uint64_t n1 = n / 2, n2 = n - n1;
+        syrk(n1, k, d + 1, p);
+        add(at(d), K_GEMM, 2 * n2 * n1 * k);
+        syrk(n2, k, d + 1, p);
+    }
+    void potrf(uint64_t n, int d) {
+        if (n <= b) return add(lv.back(), K_POTRF, n * (n + 1) * (2 * n + 1) / 6);
+        const uint64_t n1 = n / 2, n2 = n - n1;
+        const int p = at(d);
+        potrf(n1, d + 1);
+        trsm(n2, n1, d + 1, p);
+        syrk(n2, n1, d + 1, p);
+        potrf(n2, d + 1);
+    }
+};
+}  // namespace
+
+void static_flop_breakdown(int n, int b, const std::vector<int>& levels, uint64_t by_level[3],
+                           uint64_t by_kernel[4], uint64_t calls[4]) {
+    for (int i = 0; i < 3; ++i) by_level[i] = 0;
+    for (int i = 0; i < 4; ++i) by_kernel[i] = calls[i] = 0;
+    if (n < 1 || b < 1 || levels.empty()) throw std::invalid_argument("flop_breakdown: n, b >= 1");
+    Counter c{uint64_t(b), levels, by_level, by_kernel, calls};
+    c.potrf(uint64_t(n), 0);
+}
+
+// ---------------------------------------------------------------------------
+// PrecisionConfig grammar (precision.cpp:17-111):
+//   config := '[' fmt (',' fmt)* ']' | ['Pure'] fmt ;  fmt := ('F'|'FP')('16'|'32'|'64')
+// case-insensitive, whitespace anywhere, monotone outer -> inner.
+// ---------------------------------------------------------------------------
+
+namespace {
+struct Scan {
+    const std::string& s;
+    size_t i = 0;
+    void ws() {
+        while (i < s.size() && std::isspace((unsigned char)s[i])) ++i;
+    }
+    bool end() {
+        ws();
+        return i >= s.size();
+    }
+    char peek() {
+        ws();
+        return i < s.size() ? s[i] : '\0';
+    }
+};
+
+int read_format(Scan& sc, int& out, std::string& err) {
+    sc.ws();
+    std::string tok;
+    while (sc.i < sc.s.size() && std::isalnum((unsigned char)sc.s[sc.i]))
+        tok += char(std::toupper((unsigned char)sc.s[sc.i++]));
+    const std::string norm = tok.rfind("FP", 0) == 0 ? "F" + tok.substr(2) : tok;
+    if (norm == "F16") out = LV_F16;
+    else if (norm == "F32") out = LV_F32;
+    else if (norm == "F64") out = LV_F64;
+    else {
+        err = "unknown precision token '" + norm + "'";
+        return 1;
+    }
+    return 0;
+}
+}  // namespace
+
+int parse_config(const std::string& text, std::vector<int>& out, std::string& err) {
+    out.clear();
+    Scan sc{text};
+    if (sc.end()) {
+        err = "empty precision config";
+        return 1;
+    }
+    int lv = 0;
+    if (sc.peek() == '[') {
+        ++sc.i;
+        if (sc.peek() == ']') {
+            err = "empty precision config";
+            return 1;
+        }
+        if (read_format(sc, lv, err)) return 1;
+        out.push_back(lv);
+        while (sc.peek() == ',') {
+            ++sc.i;
+            if (read_format(sc, lv, err)) return 1;
+            out.push_back(lv);
+        }
+        if (sc.peek() != ']') {
+            err = "expected ',' or ']' in precision config";
+            return 1;
+        }
+        ++sc.i;
+    } else {
+        const size_t save = sc.i;
+        std::string word;
+        while (sc.i < text.size() && std::isalpha((unsigned char)text[sc.i]))
+            word += char(std::toupper((unsigned char)text[sc.i++]));
+        if (word != "PURE") sc.i = save;
+        if (read_format(sc, lv, err)) return 1;
+        out.push_back(lv);
+    }
+    if (!sc.end()) {
+        err = "trailing characters in precision config";
+        return 1;
+    }
+    for (size_t i = 1; i < out.size(); ++i)
+        if (out[i] < out[i - 1]) {
+            err = "precision must be non-decreasing from outer to inner: " + text;
+            return 2;
+        }
+    return 0;
+}
+
+std::string config_to_string(const std::vector<int>& levels) {
+    static const char* names[3] = {"F16", "F32", "F64"};
+    if (levels.size() == 1) return std::string("Pure ") + names[levels[0]];
+    std::string s = "[";
+    for (size_t i = 0; i < levels.size(); ++i) {
+        if (i) s += ", ";
+        s += names[levels[i]];
+    }
+    return s + "]";
+}
+
+}  // namespace tcb

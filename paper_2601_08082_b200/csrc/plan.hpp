@@ -1,0 +1,180 @@
+// plan.hpp -- host planner: the reference recursion unrolled into a flat op
+// list with explicit data dependencies (SURVEY 7.1 "planner", Appendix B).
+//
+// The reference drives tree_potrf / tree_trsm / tree_syrk recursively at run
+// time (tree.cpp:106-152).  Here the same recursion runs once, on the host,
+// at plan time, and emits device ops in the reference's sequential order:
+//   * every reference kernel call (potrf_leaf, trsm_leaf, syrk_leaf,
+//     gemm_mixed) and every check point (require_finite, pivot, singular
+//     diagonal) gets a sequence number `seq` in that order, so the device can
+//     report the FIRST failure the reference would have thrown;
+//   * the flops each call adds to SolveOptions::flops are recorded with its
+//     seq (static == instrumented, criterion 6);
+//   * ops carry (buffer, rect, read/write) accesses; dependencies are
+//     derived from conflicts, which preserves every block's update order
+//      while letting independent updates overlap.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace tcb {
+
+enum Level : int { LV_F16 = 0, LV_F32 = 1, LV_F64 = 2 };
+enum Buf : int { BUF_F16 = 0, BUF_F32 = 1, BUF_F64 = 2, BUF_USER = 3, BUF_ALPHA = 4, BUF_COUNT = 5 };
+enum RefKernel : int { K_POTRF = 0, K_TRSM = 1, K_SYRK = 2, K_GEMM = 3 };
+
+struct Rect {
+    int r0 = 0, c0 = 0, m = 0, n = 0;
+    bool overlaps(const Rect& o) const {
+        return m > 0 && n > 0 && o.m > 0 && o.n > 0 && r0 < o.r0 + o.m && o.r0 < r0 + m &&
+               c0 < o.c0 + o.n && o.c0 < c0 + n;
+    }
+    Rect unite(const Rect& o) const;
+};
+
+// one node of the precision tree (PrecisionTreeNode, tree.hpp:14-26)
+struct Node {
+    int r0 = 0, n = 0, depth = 0;
+    bool leaf = false;
+    int level = LV_F64;  // leaf_level (leaves) / offdiag_level (splits)
+    int n1 = 0;
+    int d1 = -1, d2 = -1;  // child node ids
+    int block = -1;        // storage block: the leaf square or the off-diagonal
+};
+
+// a storage block: every lower-triangle element belongs to exactly one
+struct Block {
+    Rect rect;
+    int level = LV_F64;
+    bool leaf = false;         // diagonal leaf (lower triangle only)
+    bool spine_quant = false;  // quantized from the caller's doubles (see planner)
+    int node = -1;
+};
+
+// one reference-level GEMM-shaped call: C(m x n) = epi(C, sum_t A(i,t) B(j,t))
+struct GemmProb {
+    int m = 0, n = 0, k = 0;
+    int a_r0 = 0, a_c0 = 0;
+    int b_r0 = 0, b_c0 = 0;
+    int c_r0 = 0, c_c0 = 0;
+    int exec_level = LV_F64;  // rounding level of the result (= C's level)
+    int lower = 0;            // syrk_leaf: only C(i,j) with global col <= row
+    double alpha = -1.0, beta = 1.0;
+    uint32_t seq = 0;
+    int ref_kernel = K_GEMM;
+};
+
+enum OpType : int {
+    OP_IMPORT = 0,  // caller doubles -> level buffers (build-time rounding, tree.cpp:47-60)
+    OP_EXPORT,      // level buffers -> caller doubles (lower triangle)
+    OP_CHECK,       // require_finite (tree.cpp:19-31)
+    OP_QUANT,       // quantize_block of a spine panel from the caller's doubles (tree.cpp:80-95)
+    OP_DEQUANT,     // dequantize_block (tree.cpp:97-104)
+    OP_SHADOW,      // round final L blocks down to a TRSM's level p (kernels.cpp:29, 78)
+    OP_POTRF,       // potrf_leaf (kernels.cpp:42-69)
+    OP_TRSM,        // trsm_leaf (kernels.cpp:71-92)
+    OP_GEMM,        // grouped gemm_mixed / syrk_leaf calls of one operand class
+};
+
+// GEMM launch classes
+enum GemmClass : int {
+    GC_TC16 = 0,      // FP16 operands, FP32 accumulate, tcgen05 (exec F16/F32)
+    GC_SIMT_F16 = 1,  // FP16 operands, FP32 accumulate, SIMT (validation / fallback)
+    GC_SIMT_F32 = 2,  // FP32 operands, FP32 accumulate
+    GC_SIMT_F16D = 3, // FP16 operands, FP64 accumulate (F64 exec)
+    GC_SIMT_F32D = 4, // FP32 operands, FP64 accumulate
+    GC_SIMT_F64 = 5,  // FP64 operands, FP64 accumulate
+};
+
+struct Access {
+    int buf;
+    Rect rect;
+    bool write;
+};
+
+struct Op {
+    OpType type = OP_CHECK;
+    int level = LV_F64;   // storage/exec level of the op's target
+    int src = BUF_F64;    // OP_CHECK: buffer read; OP_SHADOW: unused (per block)
+    Rect rect;            // target rect (check / quant / potrf square / trsm B)
+    Rect lrect;           // OP_TRSM: the L square (r0 == c0)
+    int lower = 0;        // OP_CHECK: lower triangle only
+    int diagonal = 0;     // OP_CHECK: "diagonal" vs "off-diagonal" wording
+    int slot = -1;        // OP_QUANT / OP_DEQUANT: alpha slot
+    uint32_t seq = 0;     // status sequence number (0 = op never fails)
+    int gclass = GC_TC16; // OP_GEMM
+    int prob_begin = 0, prob_end = 0;  // OP_GEMM: range in Plan::probs
+    std::vector<int> blocks;           // OP_IMPORT / EXPORT / SHADOW
+    std::vector<Access> acc;
+    std::vector<int> deps;
+    double flops = 0;      // algorithmic flops executed (for per-op timing)
+};
+
+struct FlopRec {
+    uint32_t seq;
+    int level, kernel;
+    uint64_t flops;
+};
+
+struct PlanOptions {
+    bool use_tc = true;      // FP16-operand GEMMs on tcgen05
+};
+
+struct Plan {
+    int n = 0, b = 0, leaf_size = 0;
+    std::vector<int> levels;
+    bool quantize = true;
+    PlanOptions opt;
+
+    std::vector<Node> nodes;
+    std::vector<Block> blocks;
+    std::vector<GemmProb> probs;
+    std::vector<Op> ops;
+    std::vector<FlopRec> flops;  // in seq order
+    int n_alpha_slots = 0;
+    uint32_t n_seq = 0;
+    bool needs_buf[3] = {false, false, false};
+
+    // build + plan (throws std::invalid_argument on bad input)
+    static Plan make(int n, int b, const std::vector<int>& levels, bool quantize,
+                     int leaf_size, const PlanOptions& opt);
+
+    int at_depth(int d) const { return levels[d < int(levels.size()) ? d : int(levels.size()) - 1]; }
+    int leaf_level() const { return levels.back(); }
+
+    // total flops (optionally only of calls with seq < limit)
+    void flop_totals(uint64_t by_level[3], uint64_t by_kernel[4], uint64_t calls[4],
+                     uint32_t seq_limit = 0xffffffffu) const;
+
+    // which op owns a sequence number
+    int op_of_seq(uint32_t seq) const;
+
+   private:
+    std::vector<std::vector<uint8_t>> has_shadow;  // [block][level]
+    int build_node(int r0, int n, int depth);
+    void emit_potrf(int node);
+    void emit_trsm(Rect brect, int p, int lnode);
+    void emit_syrk(int cnode, Rect arect, int p);
+    void collect_syrk(int cnode, Rect arect, int p, std::vector<GemmProb>& out);
+    void ensure_shadows(int node, int p);
+    int push(Op op);
+    uint32_t next_seq() { return ++n_seq; }
+    void add_flops(uint32_t seq, int level, int kernel, uint64_t f) {
+        flops.push_back({seq, level, kernel, f});
+    }
+    int gemm_class(int op_level, int exec_level) const;
+    void finalize_accesses();
+    void build_deps();
+};
+
+// static flop count (analysis.cpp:64-120 StaticCounter restated)
+void static_flop_breakdown(int n, int b, const std::vector<int>& levels, uint64_t by_level[3],
+                           uint64_t by_kernel[4], uint64_t calls[4]);
+
+// PrecisionConfig grammar (precision.cpp:52-111); returns 0 ok, 1 syntax, 2 validation
+int parse_config(const std::string& text, std::vector<int>& out, std::string& err);
+std::string config_to_string(const std::vector<int>& levels);
+
+}  // namespace tcb

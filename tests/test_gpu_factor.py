@@ -1,0 +1,214 @@
+"""GPU parity of the factorization against the oracle (the C restatement of
+the reference, itself pinned bit-exact to the compiled reference).
+
+Bar (BASELINE.json north_star): same inputs and precision tree, backward
+error ||A - LL^T||_F/||A||_F within 2x of the reference's, identical status /
+failure text / flop accounting (bit-exact partitioning).  The tolerance is
+written in each test: rel_gpu <= 2 * rel_oracle + FLOOR with FLOOR = 1e-15
+(both sides are at the FP64 rounding floor for Pure F64).
+"""
+import numpy as np
+import pytest
+
+from pyoracle import parse_levels
+
+pytestmark = pytest.mark.gpu
+
+FLOOR = 1e-15
+
+
+def _run(tc, a, b, cfg, quantize=True, **plan_kw):
+    import torch
+    plan = tc.Plan(a.shape[0], b, cfg, quantize, **plan_kw)
+    a_dev = tc.to_device(a)
+    l_dev = a_dev.clone()
+    st = plan.factor_device(a_dev, l_dev)
+    rel = tc.factorization_error_device(a_dev, l_dev) if st.status == "ok" else float("nan")
+    torch.cuda.synchronize()
+    return st, tc.from_device(l_dev), rel, plan.run_flops()
+
+
+CASES = [
+    # n, b, config, quantize, seed
+    (8, 2, "Pure F64", True, 1),
+    (7, 2, "[F16, F32]", True, 3),
+    (64, 8, "[F16, F32]", True, 7),
+    (96, 16, "[F16, F32]", True, 11),
+    (128, 16, "Pure F16", True, 2),
+    (100, 7, "[F16, F16, F16, F32]", True, 5),
+    (200, 32, "[F16, F32, F64]", True, 4),
+    (200, 32, "[F16, F32, F64]", False, 4),
+    (384, 48, "[F16, F16, F32]", True, 21),
+    (256, 32, "Pure F32", True, 9),
+    (1024, 128, "[F16, F64]", True, 42),           # C1
+    (1024, 64, "[F16, F16, F16, F32]", True, 0),   # criterion 2/3 ladder member
+    (1024, 64, "Pure F16", True, 0),
+    (512, 256, "Pure F32", True, 3),
+    (1000, 64, "[F16, F32]", True, 8),             # irregular splits (500/250/125/62/63)
+    (777, 100, "[F16, F16, F32, F64]", True, 12),
+    (2048, 256, "[F16, F32, F64]", True, 42),
+]
+
+
+@pytest.mark.parametrize("n,b,cfg,q,seed", CASES)
+def test_factor_matches_oracle(tc, oracle, n, b, cfg, q, seed):
+    a = oracle.spd_generate(n, seed)
+    st_o, det_o, l_o, rel_o, fl_o = oracle.factor(a, b, parse_levels(cfg), q)
+    st, l, rel, fl = _run(tc, a, b, cfg, q)
+    assert st.status == st_o == "ok"
+    assert fl.as_tuple() == fl_o.as_tuple()
+    # device metric == oracle metric on the same L (to FP64 rounding)
+    rel_cpu = oracle.factorization_error(a, l)
+    assert abs(rel - rel_cpu) <= 1e-6 * rel_cpu + 1e-15
+    assert rel <= 2.0 * rel_o + FLOOR, (rel, rel_o)
+    # upper triangle untouched
+    iu = np.triu_indices(n, 1)
+    assert np.array_equal(l[iu], a[iu])
+
+
+@pytest.mark.parametrize("n,b,cfg,q,seed", CASES[:8])
+def test_simt_path_matches_oracle(tc, oracle, n, b, cfg, q, seed):
+    """use_tc=0: every FP16-operand GEMM on the SIMT kernel instead of tcgen05"""
+    a = oracle.spd_generate(n, seed)
+    st_o, det_o, l_o, rel_o, fl_o = oracle.factor(a, b, parse_levels(cfg), q)
+    st, l, rel, fl = _run(tc, a, b, cfg, q, use_tc=False)
+    assert st.status == "ok"
+    assert rel <= 2.0 * rel_o + FLOOR
+
+
+def test_pure_f64_equals_textbook_cholesky(tc, oracle):
+    """acceptance criterion 1 (acceptance.cpp:69-94): 50 cases, <= 1e-13"""
+    rng = np.random.default_rng(20240901)
+    worst = 0.0
+    for c in range(50):
+        n = 1 + int(rng.integers(0, 256))
+        b = min(n, (1, 2, 7, 32, n)[c % 5])
+        a = oracle.spd_generate(n, int(rng.integers(0, 2**62)))
+        ref = np.linalg.cholesky(a)
+        st, l, rel, fl = _run(tc, a, b, "Pure F64")
+        assert st.status == "ok"
+        lo = np.tril(l)
+        d = np.sqrt(np.sum((lo - ref) ** 2) / np.sum(ref ** 2))
+        worst = max(worst, d)
+    assert worst <= 1e-13
+
+
+def _scaled(oracle, n, seed, s):
+    return np.asfortranarray(oracle.spd_generate(n, seed) * s)
+
+
+def test_quantization_rescue(tc, oracle):
+    """criterion 4 (acceptance.cpp:167-185): ok with quantization,
+    breakdown with the same detail text as the reference without"""
+    a = _scaled(oracle, 256, 4, 3.0 * 65504.0 / 0.5)
+    lv = parse_levels("[F16, F32]")
+    st, l, rel, fl = _run(tc, a, 32, "[F16, F32]", True)
+    st_o, det_o, _, rel_o, fl_o = oracle.factor(a, 32, lv, True)
+    assert st.status == st_o == "ok"
+    assert rel <= 2 * rel_o + FLOOR
+    st, l, rel, fl = _run(tc, a, 32, "[F16, F32]", False)
+    st_o, det_o, _, _, fl_o = oracle.factor(a, 32, lv, False)
+    assert st.status == "numerical-breakdown" == st_o
+    assert st.detail == det_o
+    assert fl.as_tuple() == fl_o.as_tuple()
+
+
+def test_quantization_alpha_above_one(tc, oracle):
+    """a spine panel beyond the Half range gets alpha > 1 (tree.cpp:117-120)"""
+    a = _scaled(oracle, 64, 7, 3.0 * 65504.0 / 0.5)
+    for cfg in ("[F16, F32]", "[F16, F16, F32]"):
+        st, l, rel, fl = _run(tc, a, 8, cfg, True)
+        st_o, det_o, _, rel_o, fl_o = oracle.factor(a, 8, parse_levels(cfg), True)
+        assert st.status == st_o
+        assert st.detail == det_o
+        if st_o == "ok":
+            assert rel <= 2 * rel_o + FLOOR
+
+
+def test_extreme_range_breakdown_text(tc, oracle):
+    """criterion 5 (acceptance.cpp:189-231)"""
+    n = 256
+    a = oracle.spd_generate(n, 6)
+    s = np.where(np.arange(n) < n // 2, 1e-3, 1e8)
+    a = np.asfortranarray(a * s[:, None] * s[None, :])
+    for cfg in ("Pure F16", "[F16, F32]", "[F16, F32, F64]"):
+        st, *_ = _run(tc, a, 32, cfg)
+        st_o, det_o, *_ = oracle.factor(a, 32, parse_levels(cfg))
+        assert st.status == st_o == "numerical-breakdown"
+        assert st.detail == det_o
+    st, l, rel, fl = _run(tc, a, 32, "Pure F64")
+    assert st.status == "ok" and -np.log10(rel) >= 13.0
+
+
+@pytest.mark.parametrize("n,b,i,val", [(16, 4, 9, -50.0), (24, 8, 5, -1.0)])
+def test_not_positive_definite_index(tc, oracle, n, b, i, val):
+    a = oracle.spd_generate(n, 4 if n == 16 else 8)
+    a[i, i] = val
+    st, *_, fl = _run(tc, a, b, "Pure F64")
+    st_o, det_o, _, _, fl_o = oracle.factor(a, b, parse_levels("Pure F64"))
+    assert st.status == st_o == "not-positive-definite"
+    assert st.index == i
+    assert st.detail == det_o
+    assert fl.as_tuple() == fl_o.as_tuple()  # partial flops up to the failure
+
+
+def test_pure_f16_breaks_down_on_large_diagonal(tc, oracle):
+    """n + r > 65504 on the diagonal overflows binary16 at build"""
+    n = 512
+    a = oracle.spd_generate(n, 1)
+    a[np.arange(n), np.arange(n)] += 65536.0 - n
+    st, *_ = _run(tc, a, 64, "Pure F16")
+    st_o, det_o, *_ = oracle.factor(a, 64, parse_levels("Pure F16"))
+    assert st.status == st_o == "numerical-breakdown"
+    assert st.detail == det_o
+
+
+def test_deterministic_bit_for_bit(tc, oracle):
+    """criterion 8 (acceptance.cpp:314-336)"""
+    a = oracle.spd_generate(384, 21)
+    _, l1, r1, _ = _run(tc, a, 48, "[F16, F16, F32]")
+    _, l2, r2, _ = _run(tc, a, 48, "[F16, F16, F32]")
+    assert np.array_equal(l1.view(np.uint64), l2.view(np.uint64))
+    assert r1 == r2
+
+
+def test_graph_and_eager_agree(tc, oracle):
+    a = oracle.spd_generate(512, 5)
+    _, l1, r1, _ = _run(tc, a, 64, "[F16, F16, F32]")
+    _, l2, r2, _ = _run(tc, a, 64, "[F16, F16, F32]", use_graph=False)
+    assert np.array_equal(l1.view(np.uint64), l2.view(np.uint64))
+
+
+def test_host_entry_point_in_place(tc, oracle):
+    a = oracle.spd_generate(300, 3)
+    l = np.array(a, order="F", copy=True)
+    plan = tc.Plan(300, 32, "[F16, F32]")
+    st = plan.factor_host(l)
+    assert st.status == "ok"
+    _, l_dev, _, _ = _run(tc, a, 32, "[F16, F32]")
+    assert np.array_equal(np.tril(l), np.tril(l_dev))
+    iu = np.triu_indices(300, 1)
+    assert np.array_equal(l[iu], a[iu])
+
+
+def test_ladder_ordering_n1024(tc, oracle):
+    """criteria 2-3 (acceptance.cpp:103-163) on seeds 0-2 against the
+    published medians (proj/test_output.txt:19-24, 34)"""
+    cfgs = ["Pure F64", "Pure F32", "Pure F16", "[F16, F32]", "[F16, F16, F16, F32]"]
+    med = {}
+    for cfg in cfgs:
+        plan = tc.Plan(1024, 64, cfg)
+        rels = []
+        for seed in range(3):
+            a = oracle.spd_generate(1024, seed)
+            a_dev = tc.to_device(a)
+            l_dev = a_dev.clone()
+            assert plan.factor_device(a_dev, l_dev).status == "ok"
+            rels.append(tc.factorization_error_device(a_dev, l_dev))
+        med[cfg] = float(np.median(rels))
+    d = {k: -np.log10(v) for k, v in med.items()}
+    assert d["Pure F64"] >= 14.0
+    assert 6.0 <= d["Pure F32"] <= 10.0
+    assert d["Pure F16"] < 4.0
+    assert d["[F16, F32]"] >= 5.0
+    assert med["[F16, F16, F16, F32]"] <= med["Pure F16"] / 50.0
