@@ -203,11 +203,12 @@ int tc_plan_set_option(tc_plan* plan, const char* key, int value) {
         e.n_streams = value < 1 ? 1 : value;
         return TC_OK;
     }
-    if (k == "use_tc") {
-        if (e.ready()) return fail(TC_INVALID_ARGUMENT, "use_tc must be set before the first run");
-        if (bool(value) == e.plan.opt.use_tc) return TC_OK;
+    if (k == "use_tc" || k == "inverse_trsm") {
+        if (e.ready()) return fail(TC_INVALID_ARGUMENT, k + " must be set before the first run");
         PlanOptions po = e.plan.opt;
-        po.use_tc = value != 0;
+        bool& field = k == "use_tc" ? po.use_tc : po.inverse_trsm;
+        if (bool(value) == field) return TC_OK;
+        field = value != 0;
         Plan p = Plan::make(e.plan.n, e.plan.b, e.plan.levels, e.plan.quantize, e.plan.leaf_size, po);
         const bool g = e.use_graph;
         const int s = e.n_streams;

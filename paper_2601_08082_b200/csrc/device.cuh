@@ -34,6 +34,8 @@ struct DevCtx {
     const RunArgs* ra;
     unsigned long long* status;      // first failure key (atomicMin)
     unsigned long long* alpha_bits;  // per quantize slot: bits of max|B| (atomicMax)
+    __half* w16;      // leaf inverses, hi | lo (ld kW16Ld), for inverse FP16 solves
+    float* wscale;    // per leaf (indexed by its first row): 2^-e the W16 entries carry
 };
 
 // failure key: seq in the high 24 bits, a position inside the op below.
@@ -157,6 +159,8 @@ struct DevProb {
     int tile0;      // first tile of this problem in the launch
     int tiles_n;    // tiles across n
     double alpha, beta;
+    int a_kwrap;    // A's K coordinate wraps (inverse solve); 0 = no
+    int b_buf;      // B operand buffer (BUF_W16 for inverse solves), -1 = operand level
 };
 
 }  // namespace tcb

@@ -33,6 +33,7 @@ Engine::~Engine() {
     for (auto s : streams_) cudaStreamDestroy(s);
     if (d_bufs_) cudaFree(d_bufs_);
     if (d_words_) cudaFree(d_words_);
+    if (d_w16_) cudaFree(d_w16_);
     if (d_arena_) cudaFree(d_arena_);
     if (d_ra_) cudaFree(d_ra_);
     if (h_ra_) cudaFreeHost(h_ra_);
@@ -67,6 +68,13 @@ bool Engine::prepare(std::string* err) {
     ctx_.b16 = plan.needs_buf[0] ? reinterpret_cast<__half*>(base + off[0]) : nullptr;
     ctx_.b32 = plan.needs_buf[1] ? reinterpret_cast<float*>(base + off[1]) : nullptr;
     ctx_.b64 = plan.needs_buf[2] ? reinterpret_cast<double*>(base + off[2]) : nullptr;
+    if (plan.needs_w16) {
+        // leaf inverses (hi | lo, zero outside the written triangles) + scales
+        TC_TRY(cudaMalloc(&d_w16_, sizeof(__half) * size_t(n) * kW16Ld + sizeof(float) * size_t(n)));
+        TC_TRY(cudaMemset(d_w16_, 0, sizeof(__half) * size_t(n) * kW16Ld + sizeof(float) * size_t(n)));
+        ctx_.w16 = static_cast<__half*>(d_w16_);
+        ctx_.wscale = reinterpret_cast<float*>(ctx_.w16 + size_t(n) * kW16Ld);
+    }
     TC_TRY(cudaMalloc(&d_words_, sizeof(unsigned long long) * size_t(1 + std::max(1, plan.n_alpha_slots))));
     ctx_.status = d_words_;
     ctx_.alpha_bits = d_words_ + 1;
@@ -115,6 +123,8 @@ bool Engine::prepare(std::string* err) {
                 d.lower = g.lower;
                 d.alpha = g.alpha;
                 d.beta = g.beta;
+                d.a_kwrap = g.a_kwrap;
+                d.b_buf = g.b_buf;
                 dp.push_back(d);
             }
             L.count = int(dp.size());
@@ -137,8 +147,9 @@ bool Engine::prepare(std::string* err) {
     for (size_t i = 0; i < plan.ops.size(); ++i) {
         const Op& op = plan.ops[i];
         if (op.seq) seq_op_[op.seq] = int(i);
-        if (op.type == OP_GEMM)
-            for (int p = op.prob_begin; p < op.prob_end; ++p) seq_op_[plan.probs[p].seq] = int(i);
+        if (op.type == OP_GEMM)  // GEMMs never fail: keep a failing op's claim on a shared seq
+            for (int p = op.prob_begin; p < op.prob_end; ++p)
+                if (seq_op_[plan.probs[p].seq] < 0) seq_op_[plan.probs[p].seq] = int(i);
     }
     ready_ = true;
     return true;
@@ -158,6 +169,7 @@ void Engine::launch_op(int i, cudaStream_t s) {
         case OP_DEQUANT: launch_dequant(ctx_, op.level, r.r0, r.c0, r.m, r.n, op.slot, s); break;
         case OP_POTRF: launch_potrf_leaf(ctx_, op.level, r.r0, r.m, op.seq, s); break;
         case OP_TRSM: launch_trsm_leaf(ctx_, op.level, r.r0, r.c0, r.m, r.n, op.lrect.r0, op.seq, s); break;
+        case OP_INVERSE: launch_leaf_inverse(ctx_, r.r0, r.m, op.seq, s); break;
         case OP_GEMM:
             if (op.gclass == GC_TC16) launch_gemm_tc(ctx_, tab, L.count, L.tiles, s);
             else launch_gemm_simt(ctx_, op.gclass, reinterpret_cast<DevProb*>(tab), L.count, L.tiles, s);
@@ -303,6 +315,10 @@ bool Engine::result(Failure* f, std::string* err) {
         case OP_TRSM:
             f->status = 3;
             f->index = op.lrect.r0 + int(local);
+            break;
+        case OP_INVERSE:
+            f->status = 3;
+            f->index = op.rect.r0 + int(local);
             break;
         default:
             if (err) *err = "status from an op that cannot fail";

@@ -67,6 +67,7 @@ class Engine {
     unsigned long long* h_status_ = nullptr;
     void* d_bufs_ = nullptr;
     unsigned long long* d_words_ = nullptr;  // status + alpha slots
+    void* d_w16_ = nullptr;                  // leaf inverses + scales
     unsigned char* d_arena_ = nullptr;
     std::vector<OpLaunch> launch_;
     std::vector<cudaStream_t> streams_;

@@ -40,6 +40,7 @@ struct alignas(128) TcProb {
     int a_r0, a_c0, b_r0, b_c0, c_r0, c_c0;
     int exec_level, lower, tile0, tiles_n;
     double alpha, beta;
+    int a_kwrap;  // inverse solve: A columns repeat with this period (B = [W_hi | W_lo])
 };
 
 size_t tc_prob_size() { return sizeof(TcProb); }
@@ -215,7 +216,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gemm_tc(DevCtx c, const TcProb*
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_expect_tx(&full[stage], STAGE_BYTES);
-                    tma_load_2d(sA + stage * A_BYTES, &p->ta, &full[stage], p->a_c0 + kb * BK, p->a_r0 + tm * BM);
+                    const int ka = p->a_kwrap ? (kb * BK) % p->a_kwrap : kb * BK;
+                    tma_load_2d(sA + stage * A_BYTES, &p->ta, &full[stage], p->a_c0 + ka, p->a_r0 + tm * BM);
                     tma_load_2d(sB + stage * B_BYTES, &p->tb, &full[stage], p->b_c0 + kb * BK, p->b_r0 + tn * BN);
                     if (++stage == STAGES) {
                         stage = 0;
@@ -275,6 +277,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gemm_tc(DevCtx c, const TcProb*
             const bool row_ok = i < p.m;
             const long long rowoff = (long long)(p.c_r0 + (row_ok ? i : 0)) * c.ldw + p.c_c0;
             const int lvl = p.exec_level;
+            // inverse solves carry W scaled by 2^e; undo it exactly here
+            const double alpha = p.a_kwrap ? double(c.wscale[p.b_r0]) : p.alpha;
             for (int cc = 0; cc < BN; cc += 32) {
                 float v[32];
                 __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge first
@@ -302,8 +306,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gemm_tc(DevCtx c, const TcProb*
 #pragma unroll
                             for (int e = 0; e < 4; ++e) {
                                 const float2 cf = __half22float2(h[e]);
-                                const float r0 = epi_f(v[8 * g + 2 * e], cf.x, p.alpha, p.beta);
-                                const float r1 = epi_f(v[8 * g + 2 * e + 1], cf.y, p.alpha, p.beta);
+                                const float r0 = epi_f(v[8 * g + 2 * e], cf.x, alpha, p.beta);
+                                const float r1 = epi_f(v[8 * g + 2 * e + 1], cf.y, alpha, p.beta);
                                 h[e] = __halves2half2(f2h(r0), f2h(r1));
                             }
                             *reinterpret_cast<uint4*>(C + 8 * g) = raw;
@@ -311,7 +315,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gemm_tc(DevCtx c, const TcProb*
                     } else {
                         for (int e = 0; e < jmax; ++e) {
                             const float cv = p.beta != 0.0 ? __half2float(C[e]) : 0.f;
-                            C[e] = f2h(epi_f(v[e], cv, p.alpha, p.beta));
+                            C[e] = f2h(epi_f(v[e], cv, alpha, p.beta));
                         }
                     }
                 } else {
@@ -321,16 +325,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gemm_tc(DevCtx c, const TcProb*
 #pragma unroll
                         for (int g = 0; g < 8; ++g) {
                             float4 cv = p.beta != 0.0 ? *reinterpret_cast<const float4*>(C + 4 * g) : make_float4(0, 0, 0, 0);
-                            cv.x = epi_f(v[4 * g + 0], cv.x, p.alpha, p.beta);
-                            cv.y = epi_f(v[4 * g + 1], cv.y, p.alpha, p.beta);
-                            cv.z = epi_f(v[4 * g + 2], cv.z, p.alpha, p.beta);
-                            cv.w = epi_f(v[4 * g + 3], cv.w, p.alpha, p.beta);
+                            cv.x = epi_f(v[4 * g + 0], cv.x, alpha, p.beta);
+                            cv.y = epi_f(v[4 * g + 1], cv.y, alpha, p.beta);
+                            cv.z = epi_f(v[4 * g + 2], cv.z, alpha, p.beta);
+                            cv.w = epi_f(v[4 * g + 3], cv.w, alpha, p.beta);
                             *reinterpret_cast<float4*>(C + 4 * g) = cv;
                         }
                     } else {
                         for (int e = 0; e < jmax; ++e) {
                             const float cv = p.beta != 0.0 ? C[e] : 0.f;
-                            C[e] = epi_f(v[e], cv, p.alpha, p.beta);
+                            C[e] = epi_f(v[e], cv, alpha, p.beta);
                         }
                     }
                 }
@@ -399,8 +403,13 @@ int tc_build_probs(const DevCtx& c, const std::vector<DevProb>& probs, std::vect
     for (size_t i = 0; i < probs.size(); ++i) {
         const DevProb& d = probs[i];
         TcProb& p = tp[i];
-        if (!make_map(&p.ta, c.b16, c.ldw, d.a_r0 + d.m, d.a_c0 + d.k, BM, err)) return -1;
-        if (!make_map(&p.tb, c.b16, c.ldw, d.b_r0 + d.n, d.b_c0 + d.k, BN, err)) return -1;
+        // A extent ends at the problem's K edge (an inverse solve's A is the
+        // n-wide leaf column block read twice: its extent is n, period a_kwrap)
+        if (!make_map(&p.ta, c.b16, c.ldw, d.a_r0 + d.m, d.a_c0 + (d.a_kwrap ? d.n : d.k), BM, err)) return -1;
+        const bool w = d.b_buf == BUF_W16;
+        if (!make_map(&p.tb, w ? c.w16 : c.b16, w ? kW16Ld : c.ldw, d.b_r0 + d.n, d.b_c0 + d.k, BN, err))
+            return -1;
+        p.a_kwrap = d.a_kwrap;
         p.m = d.m;
         p.n = d.n;
         p.k = d.k;

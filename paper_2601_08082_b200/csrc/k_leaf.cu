@@ -255,6 +255,85 @@ __global__ void __launch_bounds__(128) k_trsm_leaf(DevCtx c, int br0, int bc0, i
     }
 }
 
+// W = inv(rn16(L)) for one leaf (L the F16-level copy: the leaf itself or its
+// shadow), FP32 arithmetic, written as an FP16 pair W*2^e = hi + lo into the
+// W16 workspace (row r0+i: hi at [0,n), lo at [kW16Lo, kW16Lo+n)); 2^-e goes
+// to wscale[r0].  Column t of W is a forward substitution L w = e_t that only
+// reads L and its own earlier entries, so columns are independent: a quad of
+// threads per column splits each dot product.  CTA = 32 columns.
+// Also the singular-diagonal check of the first solve against this leaf
+// (kernels.cpp:79-81: rn16(l(j,j)) zero or non-finite).
+constexpr int INV_COLS = 32;
+
+__global__ void __launch_bounds__(128) k_leaf_inverse(DevCtx c, int r0, int n, uint32_t seq) {
+    extern __shared__ __align__(16) float inv_smem[];
+    float* Ls = inv_smem;                          // packed lower triangle, n(n+1)/2
+    float* Wc = Ls + (n * (n + 1)) / 2;            // [INV_COLS][n] this CTA's columns
+    __shared__ float colmax[INV_COLS];
+    const __half* g = c.b16 + (long long)r0 * c.ldw + r0;
+    const int c0 = blockIdx.x * INV_COLS;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = c0 + warp; i < n; i += 4)
+        for (int j = c0 + lane; j <= i; j += 32) Ls[(i * (i + 1)) / 2 + j] = __half2float(g[(long long)i * c.ldw + j]);
+    __syncthreads();
+    const int q = threadIdx.x & 3;
+    const int tl = threadIdx.x >> 2;  // local column
+    const int t = c0 + tl;
+    const bool live = t < n;
+    float amax = 0.f;
+    if (threadIdx.x == 0)
+        for (int j = c0; j < min(n, c0 + INV_COLS); ++j) {
+            const float d = Ls[(j * (j + 1)) / 2 + j];
+            if (d == 0.f || !isfinite(d)) {
+                report(c, seq, uint64_t(j));
+                break;
+            }
+        }
+    for (int i = c0; i < n; ++i) {
+        float s = 0.f;
+        if (live && i > t) {
+            const float* Li = Ls + (i * (i + 1)) / 2;
+            const float* Wt = Wc + tl * n;
+            for (int k = t + q; k < i; k += 4) s = fmaf(Li[k], Wt[k], s);
+        }
+        s += __shfl_xor_sync(0xffffffffu, s, 1);
+        s += __shfl_xor_sync(0xffffffffu, s, 2);
+        if (live && i >= t) {
+            const float lii = Ls[(i * (i + 1)) / 2 + i];
+            const float w = i == t ? 1.0f / lii : -s / lii;
+            if (q == 0) Wc[tl * n + i] = w;
+            amax = fmaxf(amax, fabsf(w));
+        }
+        __syncwarp();
+    }
+    if (q == 0 && tl < INV_COLS) colmax[tl] = live ? amax : 0.f;
+    __syncthreads();
+    // per-leaf scale: all CTAs of the leaf must agree, so it is derived from
+    // the diagonal (|W(t,t)| = 1/|L(t,t)| dominates a diagonally dominant
+    // leaf) of the whole leaf, not from this CTA's columns
+    float dmax = 0.f;
+    for (int j = lane; j < n; j += 32) dmax = fmaxf(dmax, fabsf(1.0f / Ls[(j * (j + 1)) / 2 + j]));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+    int e = 0;
+    if (dmax > 0.f && isfinite(dmax)) (void)frexpf(dmax, &e);  // dmax = f * 2^e, f in [0.5, 1)
+    const float up = ldexpf(1.0f, -e), down = ldexpf(1.0f, e);
+    if (blockIdx.x == 0 && threadIdx.x == 0) c.wscale[r0] = down;
+    __half* W = c.w16 + (long long)r0 * kW16Ld;
+    // write rows i = 0..n-1 of this CTA's columns: hi, lo (upper part zero)
+    for (int e2 = threadIdx.x; e2 < n * INV_COLS; e2 += 128) {
+        const int i = e2 / INV_COLS, tc = e2 % INV_COLS, tt = c0 + tc;
+        if (tt >= n) continue;
+        const float w = i >= tt ? Wc[tc * n + i] * up : 0.f;
+        const __half hi = __float2half_rn(w);
+        const __half lo = __float2half_rn(w - __half2float(hi));
+        W[(long long)i * kW16Ld + tt] = hi;
+        W[(long long)i * kW16Ld + kW16Lo + tt] = lo;
+    }
+}
+
+size_t inverse_smem(int n) { return (size_t(n) * (n + 1) / 2 + size_t(INV_COLS) * n) * sizeof(float); }
+
 template <int L, bool SMEM>
 void potrf_launch(const DevCtx& c, int r0, int n, uint32_t seq, cudaStream_t s) {
     using Acc = typename LvT<L>::Acc;
@@ -264,8 +343,13 @@ void potrf_launch(const DevCtx& c, int r0, int n, uint32_t seq, cudaStream_t s) 
 
 }  // namespace
 
+void launch_leaf_inverse(const DevCtx& c, int r0, int n, uint32_t seq, cudaStream_t s) {
+    k_leaf_inverse<<<(n + INV_COLS - 1) / INV_COLS, 128, inverse_smem(n), s>>>(c, r0, n, seq);
+}
+
 void init_leaf_attributes() {
     const int cap = 227 * 1024;
+    cudaFuncSetAttribute(k_leaf_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
     cudaFuncSetAttribute(k_potrf_leaf<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
     cudaFuncSetAttribute(k_potrf_leaf<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
     cudaFuncSetAttribute(k_potrf_leaf<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);

@@ -38,6 +38,7 @@ void init_tc_attributes();
 void launch_potrf_leaf(const DevCtx& c, int lv, int r0, int n, uint32_t seq, cudaStream_t s);
 void launch_trsm_leaf(const DevCtx& c, int lv, int br0, int bc0, int m, int n, int lr0, uint32_t seq,
                       cudaStream_t s);
+void launch_leaf_inverse(const DevCtx& c, int r0, int n, uint32_t seq, cudaStream_t s);
 
 // grouped GEMM (k_gemm_simt.cu / k_gemm_tc.cu)
 // problems must already be in device memory with tile0 / tiles_n filled by

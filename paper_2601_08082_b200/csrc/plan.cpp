@@ -59,10 +59,13 @@ int Plan::build_node(int r0, int n, int depth) {
     return id;
 }
 
-int Plan::gemm_class(int op_level, int exec_level) const {
+int Plan::gemm_class(int op_level, int exec_level, const GemmProb* g) const {
     if (op_level == LV_F16) {
         if (exec_level == LV_F64) return GC_SIMT_F16D;
-        return opt.use_tc ? GC_TC16 : GC_SIMT_F16;
+        // TMA needs 16-byte aligned rows: column offsets and K multiples of 8
+        // halves (always true for power-of-two n and b >= 8)
+        const bool aligned = !g || (g->a_c0 % 8 == 0 && g->b_c0 % 8 == 0 && g->k % 8 == 0);
+        return (opt.use_tc && aligned) ? GC_TC16 : GC_SIMT_F16;
     }
     if (op_level == LV_F32) return exec_level == LV_F64 ? GC_SIMT_F32D : GC_SIMT_F32;
     return GC_SIMT_F64;
@@ -114,14 +117,61 @@ void Plan::ensure_shadows(int node, int p) {
 void Plan::emit_trsm(Rect B, int p, int lnode) {
     const Node& L = nodes[lnode];
     if (L.leaf || std::min(B.m, B.n) <= leaf_size) {
+        const uint32_t seq = next_seq();
+        const uint64_t f = uint64_t(B.m) * uint64_t(B.n) * uint64_t(B.n);
+        add_flops(seq, p, K_TRSM, f);
+        // large FP16 leaf solve on the tensor cores: X = rn16(B (W_hi + W_lo)^T)
+        // with W = inv(rn16(L)) from the leaf's inverse op.  Rows are
+        // independent, so the tile owning a row block reads and overwrites it.
+        const bool inv = opt.use_tc && opt.inverse_trsm && p == LV_F16 && L.leaf && L.n <= kW16Lo &&
+                         B.m >= kInvMinRows && B.c0 % 8 == 0 && L.r0 % 8 == 0;
+        if (inv) {
+            const int lb = nodes[lnode].block;
+            if (!has_inverse[lb]) {
+                has_inverse[lb] = 1;
+                needs_w16 = true;
+                Op iv;
+                iv.type = OP_INVERSE;
+                iv.level = p;
+                iv.rect = {L.r0, L.r0, L.n, L.n};
+                iv.seq = seq;  // singular diagonal is reported for its first solve
+                push(std::move(iv));
+            }
+            GemmProb g;
+            g.m = B.m;
+            g.n = L.n;
+            g.k = 2 * kW16Lo;
+            g.a_r0 = B.r0;
+            g.a_c0 = B.c0;
+            g.a_kwrap = kW16Lo;
+            g.b_r0 = L.r0;
+            g.b_c0 = 0;
+            g.b_buf = BUF_W16;
+            g.c_r0 = B.r0;
+            g.c_c0 = B.c0;
+            g.exec_level = p;
+            g.alpha = 1.0;
+            g.beta = 0.0;
+            g.seq = seq;
+            g.ref_kernel = K_TRSM;
+            Op op;
+            op.type = OP_GEMM;
+            op.level = p;
+            op.gclass = GC_TC16;
+            op.prob_begin = int(probs.size());
+            probs.push_back(g);
+            op.prob_end = int(probs.size());
+            op.rect = B;
+            op.flops = double(f);
+            push(std::move(op));
+            return;
+        }
         Op op;
         op.type = OP_TRSM;
         op.level = p;
         op.rect = B;
         op.lrect = {L.r0, L.r0, L.n, L.n};
-        op.seq = next_seq();
-        const uint64_t f = uint64_t(B.m) * uint64_t(B.n) * uint64_t(B.n);
-        add_flops(op.seq, p, K_TRSM, f);
+        op.seq = seq;
         op.flops = double(f);
         push(std::move(op));
         return;
@@ -150,7 +200,7 @@ void Plan::emit_trsm(Rect B, int p, int lnode) {
     Op op;
     op.type = OP_GEMM;
     op.level = p;
-    op.gclass = gemm_class(p, p);
+    op.gclass = gemm_class(p, p, &g);
     op.prob_begin = int(probs.size());
     probs.push_back(g);
     op.prob_end = int(probs.size());
@@ -218,7 +268,7 @@ void Plan::emit_syrk(int cnode, Rect A, int p) {
     // one launch per class, classes in order of first appearance
     std::vector<int> classes;
     for (const auto& g : all) {
-        const int c = gemm_class(p, g.exec_level);
+        const int c = gemm_class(p, g.exec_level, &g);
         if (std::find(classes.begin(), classes.end(), c) == classes.end()) classes.push_back(c);
     }
     for (int c : classes) {
@@ -228,7 +278,7 @@ void Plan::emit_syrk(int cnode, Rect A, int p) {
         op.gclass = c;
         op.prob_begin = int(probs.size());
         for (const auto& g : all)
-            if (gemm_class(p, g.exec_level) == c) {
+            if (gemm_class(p, g.exec_level, &g) == c) {
                 probs.push_back(g);
                 op.rect = op.rect.unite({g.c_r0, g.c_c0, g.m, g.n});
                 op.flops += double(g.lower ? 2.0 * g.m * g.n * g.k / 2.0 : 2.0 * g.m * g.n * g.k);
@@ -346,6 +396,10 @@ void Plan::finalize_accesses() {
             case OP_POTRF:
                 op.acc.push_back({op.level, op.rect, true});
                 break;
+            case OP_INVERSE:
+                op.acc.push_back({op.level, op.rect, false});
+                op.acc.push_back({BUF_W16, {op.rect.r0, 0, op.rect.m, kW16Ld}, true});
+                break;
             case OP_TRSM:
                 op.acc.push_back({op.level, op.rect, true});
                 op.acc.push_back({op.level, op.lrect, false});
@@ -355,8 +409,9 @@ void Plan::finalize_accesses() {
                 std::vector<Rect> rds;
                 for (int i = op.prob_begin; i < op.prob_end; ++i) {
                     const GemmProb& g = probs[i];
-                    rds.push_back({g.a_r0, g.a_c0, g.m, g.k});
-                    rds.push_back({g.b_r0, g.b_c0, g.n, g.k});
+                    rds.push_back({g.a_r0, g.a_c0, g.m, g.a_kwrap ? g.a_kwrap : g.k});
+                    if (g.b_buf >= 0) op.acc.push_back({g.b_buf, {g.b_r0, g.b_c0, g.n, g.k}, false});
+                    else rds.push_back({g.b_r0, g.b_c0, g.n, g.k});
                     op.acc.push_back({g.exec_level, {g.c_r0, g.c_c0, g.m, g.n}, true});
                 }
                 // drop read rects contained in another (SYRK reads sub-rows of one panel)
@@ -438,6 +493,7 @@ Plan Plan::make(int n, int b, const std::vector<int>& levels, bool quantize, int
             if (blk.level != LV_F64) blk.spine_quant = true;
         }
     P.has_shadow.assign(P.blocks.size(), std::vector<uint8_t>(3, 0));
+    P.has_inverse.assign(P.blocks.size(), 0);
     for (const Block& blk : P.blocks) P.needs_buf[blk.level] = true;
 
     Op imp;

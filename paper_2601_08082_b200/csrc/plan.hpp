@@ -22,7 +22,13 @@
 namespace tcb {
 
 enum Level : int { LV_F16 = 0, LV_F32 = 1, LV_F64 = 2 };
-enum Buf : int { BUF_F16 = 0, BUF_F32 = 1, BUF_F64 = 2, BUF_USER = 3, BUF_ALPHA = 4, BUF_COUNT = 5 };
+enum Buf : int { BUF_F16 = 0, BUF_F32 = 1, BUF_F64 = 2, BUF_USER = 3, BUF_ALPHA = 4, BUF_W16 = 5, BUF_COUNT = 6 };
+
+// inverse-based FP16 leaf solves: W = inv(rn16(L_leaf)) as an FP16 hi/lo pair
+// in the W16 workspace (row r0+j of a leaf at columns [0,n) hi, [256, 256+n) lo)
+constexpr int kW16Ld = 512;
+constexpr int kW16Lo = 256;
+constexpr int kInvMinRows = 512;  // below this the substitution kernel is used
 enum RefKernel : int { K_POTRF = 0, K_TRSM = 1, K_SYRK = 2, K_GEMM = 3 };
 
 struct Rect {
@@ -64,6 +70,8 @@ struct GemmProb {
     double alpha = -1.0, beta = 1.0;
     uint32_t seq = 0;
     int ref_kernel = K_GEMM;
+    int a_kwrap = 0;        // A's K coordinate wraps at this period (inverse solve: hi|lo)
+    int b_buf = -1;         // buffer of the B operand (-1: the operand level's)
 };
 
 enum OpType : int {
@@ -76,6 +84,7 @@ enum OpType : int {
     OP_POTRF,       // potrf_leaf (kernels.cpp:42-69)
     OP_TRSM,        // trsm_leaf (kernels.cpp:71-92)
     OP_GEMM,        // grouped gemm_mixed / syrk_leaf calls of one operand class
+    OP_INVERSE,     // W16 = inv(rn16(L_leaf)) hi/lo, for inverse-based FP16 leaf solves
 };
 
 // GEMM launch classes
@@ -120,6 +129,7 @@ struct FlopRec {
 
 struct PlanOptions {
     bool use_tc = true;      // FP16-operand GEMMs on tcgen05
+    bool inverse_trsm = true; // FP16 leaf solves with m >= kInvMinRows as tcgen05 GEMMs
 };
 
 struct Plan {
@@ -136,6 +146,7 @@ struct Plan {
     int n_alpha_slots = 0;
     uint32_t n_seq = 0;
     bool needs_buf[3] = {false, false, false};
+    bool needs_w16 = false;
 
     // build + plan (throws std::invalid_argument on bad input)
     static Plan make(int n, int b, const std::vector<int>& levels, bool quantize,
@@ -153,6 +164,7 @@ struct Plan {
 
    private:
     std::vector<std::vector<uint8_t>> has_shadow;  // [block][level]
+    std::vector<uint8_t> has_inverse;              // [block] W16 ready
     int build_node(int r0, int n, int depth);
     void emit_potrf(int node);
     void emit_trsm(Rect brect, int p, int lnode);
@@ -164,7 +176,7 @@ struct Plan {
     void add_flops(uint32_t seq, int level, int kernel, uint64_t f) {
         flops.push_back({seq, level, kernel, f});
     }
-    int gemm_class(int op_level, int exec_level) const;
+    int gemm_class(int op_level, int exec_level, const GemmProb* g) const;
     void finalize_accesses();
     void build_deps();
 };

@@ -19,7 +19,10 @@ FLOOR = 1e-15
 
 def _run(tc, a, b, cfg, quantize=True, **plan_kw):
     import torch
+    inverse = plan_kw.pop("inverse", True)
     plan = tc.Plan(a.shape[0], b, cfg, quantize, **plan_kw)
+    if not inverse:
+        plan.set_option("inverse_trsm", 0)
     a_dev = tc.to_device(a)
     l_dev = a_dev.clone()
     st = plan.factor_device(a_dev, l_dev)
@@ -212,3 +215,38 @@ def test_ladder_ordering_n1024(tc, oracle):
     assert d["Pure F16"] < 4.0
     assert d["[F16, F32]"] >= 5.0
     assert med["[F16, F16, F16, F32]"] <= med["Pure F16"] / 50.0
+
+
+@pytest.mark.parametrize("n,cfg", [(4096, "[F16, F16, F16, F32]"), (2048, "Pure F16")])
+def test_inverse_leaf_solve_matches_substitution(tc, oracle, n, cfg):
+    """FP16 leaf solves with m >= 512 run as tcgen05 GEMMs against the leaf's
+    inverse; the backward error stays within 2x of the oracle and of the
+    substitution kernel"""
+    a = oracle.spd_generate(n, 42)
+    if cfg == "Pure F16":
+        a = np.asfortranarray(a * 0.5)  # keep the diagonal inside binary16
+    st_o, det_o, _, rel_o, fl_o = oracle.factor(a, 256, parse_levels(cfg))
+    st1, l1, rel1, fl1 = _run(tc, a, 256, cfg)
+    st2, l2, rel2, fl2 = _run(tc, a, 256, cfg, inverse=False)
+    assert st1.status == st2.status == st_o == "ok"
+    assert fl1.as_tuple() == fl2.as_tuple() == fl_o.as_tuple()
+    assert rel1 <= 2 * rel_o + FLOOR, (rel1, rel_o)
+    assert rel2 <= 2 * rel_o + FLOOR, (rel2, rel_o)
+
+
+@pytest.mark.parametrize("n", [512, 1024])
+def test_singular_diagonal_detail(tc, oracle, n):
+    """an F32 leaf whose diagonal overflows binary16 when a [F16, F32] panel
+    solve reads it (kernels.cpp:78-81): SingularDiagonal with the reference's
+    index, through the substitution kernel (m=256) and the inverse path (m=512)"""
+    a = np.asfortranarray(oracle.spd_generate(n, 3) * 1e10)
+    st, *_ = _run(tc, a, 256, "[F16, F32]")
+    st_o, det_o, *_ = oracle.factor(a, 256, parse_levels("[F16, F32]"))
+    assert st_o == "singular-diagonal"
+    assert st.status == "singular-diagonal"
+    assert st.detail == det_o
+
+
+def test_spd_generate_device_bit_exact(tc, oracle):
+    a = tc.from_device(tc.spd_generate_device(300, 77))
+    assert np.array_equal(a, oracle.spd_generate(300, 77))
