@@ -161,6 +161,21 @@ struct DevProb {
     double alpha, beta;
     int a_kwrap;    // A's K coordinate wraps (inverse solve); 0 = no
     int b_buf;      // B operand buffer (BUF_W16 for inverse solves), -1 = operand level
+    uint32_t check_seq;  // fused require_finite on the stored values (0 = none)
+    int chk_r0, chk_c0;  // origin of the checked block
 };
+
+#ifdef __CUDACC__
+// fused require_finite helpers: the first bad element in column-major order
+__device__ __forceinline__ bool h_bad(__half h) { return (__half_as_ushort(h) & 0x7c00) == 0x7c00; }
+__device__ __forceinline__ void warp_report_min(const DevCtx& c, unsigned long long key) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long x = __shfl_xor_sync(0xffffffffu, key, o);
+        key = x < key ? x : key;
+    }
+    if ((threadIdx.x & 31) == 0 && key != ~0ull) atomicMin(c.status, key);
+}
+#endif
 
 }  // namespace tcb

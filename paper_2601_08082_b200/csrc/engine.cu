@@ -125,6 +125,9 @@ bool Engine::prepare(std::string* err) {
                 d.beta = g.beta;
                 d.a_kwrap = g.a_kwrap;
                 d.b_buf = g.b_buf;
+                d.check_seq = g.check_seq;
+                d.chk_r0 = g.chk_r0;
+                d.chk_c0 = g.chk_c0;
                 dp.push_back(d);
             }
             L.count = int(dp.size());
@@ -166,9 +169,12 @@ void Engine::launch_op(int i, cudaStream_t s) {
         case OP_SHADOW: launch_shadow(ctx_, reinterpret_cast<BlockDesc*>(tab), L.count, L.tiles, op.level, s); break;
         case OP_CHECK: launch_check(ctx_, op.src, r.r0, r.c0, r.m, r.n, op.lower, op.seq, s); break;
         case OP_QUANT: launch_quant(ctx_, op.level, r.r0, r.c0, r.m, r.n, op.slot, op.seq, s); break;
-        case OP_DEQUANT: launch_dequant(ctx_, op.level, r.r0, r.c0, r.m, r.n, op.slot, s); break;
-        case OP_POTRF: launch_potrf_leaf(ctx_, op.level, r.r0, r.m, op.seq, s); break;
-        case OP_TRSM: launch_trsm_leaf(ctx_, op.level, r.r0, r.c0, r.m, r.n, op.lrect.r0, op.seq, s); break;
+        case OP_DEQUANT: launch_dequant(ctx_, op.level, r.r0, r.c0, r.m, r.n, op.slot, op.check_seq, s); break;
+        case OP_POTRF: launch_potrf_leaf(ctx_, op.level, r.r0, r.m, op.seq, op.check_seq, s); break;
+        case OP_TRSM:
+            launch_trsm_leaf(ctx_, op.level, r.r0, r.c0, r.m, r.n, op.lrect.r0, op.seq, op.check_seq, op.chk.r0,
+                             op.chk.c0, s);
+            break;
         case OP_INVERSE: launch_leaf_inverse(ctx_, r.r0, r.m, op.seq, s); break;
         case OP_GEMM:
             if (op.gclass == GC_TC16) launch_gemm_tc(ctx_, tab, L.count, L.tiles, s);
@@ -293,6 +299,20 @@ bool Engine::result(Failure* f, std::string* err) {
     const uint32_t seq = uint32_t(key >> 40);
     const uint64_t local = key & ((1ull << 40) - 1);
     f->seq = seq;
+    // a require_finite point (fused into a producing kernel or standalone)?
+    {
+        const auto& ck = plan.checks;
+        auto it = std::lower_bound(ck.begin(), ck.end(), seq,
+                                   [](const CheckRec& r, uint32_t s) { return r.seq < s; });
+        if (it != ck.end() && it->seq == seq) {
+            f->status = 2;
+            f->block = it->rect;
+            f->elem_row = it->rect.r0 + int(local & 0xFFFFF);
+            f->elem_col = it->rect.c0 + int(local >> 20);
+            f->diagonal = it->diagonal;
+            return true;
+        }
+    }
     const int oi = seq < seq_op_.size() ? seq_op_[seq] : -1;
     if (oi < 0) {
         if (err) *err = "corrupt status word";

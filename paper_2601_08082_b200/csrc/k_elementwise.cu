@@ -201,17 +201,27 @@ __global__ void __launch_bounds__(256) k_quant2(DevCtx c, int lv, int r0, int c0
     }
 }
 
-__global__ void __launch_bounds__(256) k_dequant(DevCtx c, int lv, int r0, int c0, int m, int n, int slot) {
+// dequantize_block; when alpha != 1 it is the panel's last writer, so the
+// post-dequantize require_finite (tree.cpp:121) is fused here too
+__global__ void __launch_bounds__(256) k_dequant(DevCtx c, int lv, int r0, int c0, int m, int n, int slot,
+                                                 uint32_t chk_seq) {
     const double alpha = slot_alpha(c, lv, slot);
     if (alpha == 1.0) return;  // tree.cpp:98
     const int j = blockIdx.x * 256 + threadIdx.x;
-    if (j >= n) return;
-    for (int ii = 0; ii < 16; ++ii) {
-        const int i = blockIdx.y * 16 + ii;
-        if (i >= m) break;
-        const long long off = (long long)(r0 + i) * c.ldw + c0 + j;
-        store_level(c, lv, off, load_level(c, lv, off) * alpha);
-    }
+    unsigned long long bad = ~0ull;
+    if (j < n)
+        for (int ii = 0; ii < 16; ++ii) {
+            const int i = blockIdx.y * 16 + ii;
+            if (i >= m) break;
+            const long long off = (long long)(r0 + i) * c.ldw + c0 + j;
+            const double v = load_level(c, lv, off) * alpha;
+            store_level(c, lv, off, v);
+            if (!isfinite(round_level(lv, v))) {
+                const unsigned long long k = fail_key(chk_seq, elem_local(i, j));
+                bad = k < bad ? k : bad;
+            }
+        }
+    if (chk_seq) warp_report_min(c, bad);
 }
 
 int tiles_of(int m, int n) { return ((m + TS - 1) / TS) * ((n + TS - 1) / TS); }
@@ -297,9 +307,10 @@ void launch_quant(const DevCtx& c, int lv, int r0, int c0, int m, int n, int slo
     k_quant1<<<t, 256, 0, s>>>(c, lv, r0, c0, m, n, slot, seq);
     k_quant2<<<t, 256, 0, s>>>(c, lv, r0, c0, m, n, slot);
 }
-void launch_dequant(const DevCtx& c, int lv, int r0, int c0, int m, int n, int slot, cudaStream_t s) {
+void launch_dequant(const DevCtx& c, int lv, int r0, int c0, int m, int n, int slot, uint32_t chk_seq,
+                    cudaStream_t s) {
     dim3 g((n + 255) / 256, (m + 15) / 16);
-    k_dequant<<<g, 256, 0, s>>>(c, lv, r0, c0, m, n, slot);
+    k_dequant<<<g, 256, 0, s>>>(c, lv, r0, c0, m, n, slot, chk_seq);
 }
 
 }  // namespace tcb

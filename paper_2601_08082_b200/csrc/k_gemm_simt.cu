@@ -26,8 +26,9 @@ __device__ __forceinline__ int find_prob(const DevProb* p, int np, int tile) {
     return lo;
 }
 
-// epilogue of dot_update for an FP32 accumulator (exec level F16 / F32)
-__device__ __forceinline__ void epi_store_f(const DevCtx& c, const DevProb& p, long long off, float s) {
+// epilogue of dot_update for an FP32 accumulator (exec level F16 / F32);
+// returns whether the stored (level-rounded) value is non-finite
+__device__ __forceinline__ bool epi_store_f(const DevCtx& c, const DevProb& p, long long off, float s) {
     float r = p.alpha == -1.0 ? -s : __double2float_rn(p.alpha * double(s));
     if (p.beta != 0.0) {
         const float cv = float(load_level(c, p.exec_level, off));
@@ -35,12 +36,14 @@ __device__ __forceinline__ void epi_store_f(const DevCtx& c, const DevProb& p, l
         r = r + t;
     }
     store_level(c, p.exec_level, off, double(r));
+    return !isfinite(round_level(p.exec_level, double(r)));
 }
 // FP64 accumulator (exec level F64)
-__device__ __forceinline__ void epi_store_d(const DevCtx& c, const DevProb& p, long long off, double s) {
+__device__ __forceinline__ bool epi_store_d(const DevCtx& c, const DevProb& p, long long off, double s) {
     double r = p.alpha * s;
     if (p.beta != 0.0) r = r + p.beta * load_level(c, p.exec_level, off);
     store_level(c, p.exec_level, off, r);
+    return !isfinite(round_level(p.exec_level, r));
 }
 
 template <int OPL, typename Acc>
@@ -88,6 +91,7 @@ __global__ void __launch_bounds__(256) k_gemm_simt(DevCtx c, const DevProb* prob
         }
         __syncthreads();
     }
+    unsigned long long bad = ~0ull;  // fused require_finite (first bad element)
 #pragma unroll
     for (int x = 0; x < 4; ++x)
 #pragma unroll
@@ -96,9 +100,16 @@ __global__ void __launch_bounds__(256) k_gemm_simt(DevCtx c, const DevProb* prob
             if (i >= p.m || j >= p.n) continue;
             if (p.lower && p.c_c0 + j > p.c_r0 + i) continue;
             const long long off = (long long)(p.c_r0 + i) * c.ldw + p.c_c0 + j;
-            if constexpr (sizeof(Acc) == 4) epi_store_f(c, p, off, acc[x][y]);
-            else epi_store_d(c, p, off, acc[x][y]);
+            bool nb;
+            if constexpr (sizeof(Acc) == 4) nb = epi_store_f(c, p, off, acc[x][y]);
+            else nb = epi_store_d(c, p, off, acc[x][y]);
+            if (nb && p.check_seq) {
+                const unsigned long long k =
+                    fail_key(p.check_seq, elem_local(p.c_r0 + i - p.chk_r0, p.c_c0 + j - p.chk_c0));
+                bad = k < bad ? k : bad;
+            }
         }
+    if (p.check_seq) warp_report_min(c, bad);
 }
 
 }  // namespace

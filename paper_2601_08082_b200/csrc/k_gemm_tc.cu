@@ -41,6 +41,8 @@ struct alignas(128) TcProb {
     int exec_level, lower, tile0, tiles_n;
     double alpha, beta;
     int a_kwrap;  // inverse solve: A columns repeat with this period (B = [W_hi | W_lo])
+    uint32_t check_seq;  // fused require_finite (0 = none), element relative to chk origin
+    int chk_r0, chk_c0;
 };
 
 size_t tc_prob_size() { return sizeof(TcProb); }
@@ -279,6 +281,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gemm_tc(DevCtx c, const TcProb*
             const int lvl = p.exec_level;
             // inverse solves carry W scaled by 2^e; undo it exactly here
             const double alpha = p.a_kwrap ? double(c.wscale[p.b_r0]) : p.alpha;
+            // fused require_finite: track the first non-finite stored value
+            const bool chk = p.check_seq != 0;
+            unsigned long long bad = ~0ull;
+            const int iloc = p.c_r0 + i - p.chk_r0;
+            auto note = [&](bool isbad, int j) {
+                if (chk && isbad) {
+                    const unsigned long long k = fail_key(p.check_seq, elem_local(iloc, p.c_c0 + j - p.chk_c0));
+                    bad = k < bad ? k : bad;
+                }
+            };
             for (int cc = 0; cc < BN; cc += 32) {
                 float v[32];
                 __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge first
@@ -306,17 +318,23 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gemm_tc(DevCtx c, const TcProb*
 #pragma unroll
                             for (int e = 0; e < 4; ++e) {
                                 const float2 cf = __half22float2(h[e]);
-                                const float r0 = epi_f(v[8 * g + 2 * e], cf.x, alpha, p.beta);
-                                const float r1 = epi_f(v[8 * g + 2 * e + 1], cf.y, alpha, p.beta);
-                                h[e] = __halves2half2(f2h(r0), f2h(r1));
+                                const __half o0 = f2h(epi_f(v[8 * g + 2 * e], cf.x, alpha, p.beta));
+                                const __half o1 = f2h(epi_f(v[8 * g + 2 * e + 1], cf.y, alpha, p.beta));
+                                note(h_bad(o0), j0 + 8 * g + 2 * e);
+                                note(h_bad(o1), j0 + 8 * g + 2 * e + 1);
+                                h[e] = __halves2half2(o0, o1);
                             }
                             *reinterpret_cast<uint4*>(C + 8 * g) = raw;
                         }
                     } else {
-                        for (int e = 0; e < jmax; ++e) {
-                            const float cv = p.beta != 0.0 ? __half2float(C[e]) : 0.f;
-                            C[e] = f2h(epi_f(v[e], cv, alpha, p.beta));
-                        }
+#pragma unroll
+                        for (int e = 0; e < 32; ++e)
+                            if (e < jmax) {
+                                const float cv = p.beta != 0.0 ? __half2float(C[e]) : 0.f;
+                                const __half o = f2h(epi_f(v[e], cv, alpha, p.beta));
+                                note(h_bad(o), j0 + e);
+                                C[e] = o;
+                            }
                     }
                 } else {
                     float* C = c.b32 + rowoff + j0;
@@ -329,16 +347,26 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gemm_tc(DevCtx c, const TcProb*
                             cv.y = epi_f(v[4 * g + 1], cv.y, alpha, p.beta);
                             cv.z = epi_f(v[4 * g + 2], cv.z, alpha, p.beta);
                             cv.w = epi_f(v[4 * g + 3], cv.w, alpha, p.beta);
+                            note(!isfinite(cv.x), j0 + 4 * g);
+                            note(!isfinite(cv.y), j0 + 4 * g + 1);
+                            note(!isfinite(cv.z), j0 + 4 * g + 2);
+                            note(!isfinite(cv.w), j0 + 4 * g + 3);
                             *reinterpret_cast<float4*>(C + 4 * g) = cv;
                         }
                     } else {
-                        for (int e = 0; e < jmax; ++e) {
-                            const float cv = p.beta != 0.0 ? C[e] : 0.f;
-                            C[e] = epi_f(v[e], cv, alpha, p.beta);
-                        }
+#pragma unroll
+                        for (int e = 0; e < 32; ++e)
+                            if (e < jmax) {
+                                const float cv = p.beta != 0.0 ? C[e] : 0.f;
+                                const float o = epi_f(v[e], cv, alpha, p.beta);
+                                note(!isfinite(o), j0 + e);
+                                C[e] = o;
+                            }
                     }
                 }
             }
+            __syncwarp();
+            if (chk) warp_report_min(c, bad);
             if (++as == 2) {
                 as = 0;
                 aphase ^= 1;
@@ -410,6 +438,9 @@ int tc_build_probs(const DevCtx& c, const std::vector<DevProb>& probs, std::vect
         if (!make_map(&p.tb, w ? c.w16 : c.b16, w ? kW16Ld : c.ldw, d.b_r0 + d.n, d.b_c0 + d.k, BN, err))
             return -1;
         p.a_kwrap = d.a_kwrap;
+        p.check_seq = d.check_seq;
+        p.chk_r0 = d.chk_r0;
+        p.chk_c0 = d.chk_c0;
         p.m = d.m;
         p.n = d.n;
         p.k = d.k;

@@ -51,7 +51,8 @@ struct LeafAcc {
 };
 
 template <int L, bool SMEM>
-__global__ void __launch_bounds__(POTRF_THREADS) k_potrf_leaf(DevCtx c, int r0, int n, uint32_t seq) {
+__global__ void __launch_bounds__(POTRF_THREADS) k_potrf_leaf(DevCtx c, int r0, int n, uint32_t seq,
+                                                              uint32_t chk_seq) {
     using T = typename LvT<L>::T;
     using Acc = typename LvT<L>::Acc;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -65,7 +66,22 @@ __global__ void __launch_bounds__(POTRF_THREADS) k_potrf_leaf(DevCtx c, int r0, 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int NW = POTRF_THREADS / 32;
 
-    if constexpr (SMEM) {
+    // leaf require_finite (tree.cpp:107-108) fused into the load: the first
+    // non-finite element of the lower triangle in column-major order
+    if (chk_seq) {
+        unsigned long long bad = ~0ull;
+        for (int i = warp; i < n; i += NW)
+            for (int j = lane; j <= i; j += 32) {
+                const Acc v = Acc(to_d(g[(long long)i * c.ldw + j]));
+                if constexpr (SMEM) S[(i * (i + 1)) / 2 + j] = v;
+                if (!isfinite(v)) {
+                    const unsigned long long k = fail_key(chk_seq, elem_local(i, j));
+                    bad = k < bad ? k : bad;
+                }
+            }
+        warp_report_min(c, bad);
+        __syncthreads();
+    } else if constexpr (SMEM) {
         for (int i = warp; i < n; i += NW)
             for (int j = lane; j <= i; j += 32) S[(i * (i + 1)) / 2 + j] = Acc(to_d(g[(long long)i * c.ldw + j]));
         __syncthreads();
@@ -177,23 +193,45 @@ __global__ void __launch_bounds__(POTRF_THREADS) k_potrf_leaf(DevCtx c, int r0, 
 }
 
 // trsm_leaf: B (m x n at (br0, bc0)) <- B * L^-T, L the n x n square at lr0
-template <int L>
+// The CTA's 32 rows of B are staged in shared memory (BS) so the
+// finished-column sums read them at smem latency; the in-chunk substitution
+// is right-looking (each new x immediately updates the later partial sums),
+// which leaves one short dependent chain per column.  Fused require_finite
+// (tree.cpp:121) on the values written, relative to the panel origin.
+template <int L, bool BS>
 __global__ void __launch_bounds__(128) k_trsm_leaf(DevCtx c, int br0, int bc0, int m, int n, int lr0,
-                                                  uint32_t seq) {
+                                                  uint32_t seq, uint32_t chk_seq, int chk_r0, int chk_c0) {
     using T = typename LvT<L>::T;
     using Acc = typename LvT<L>::Acc;
     constexpr int TSL = 128;  // staged slice of finished columns
     __shared__ Acc Lc[TSL][PW + 1];
     __shared__ Acc D[PW][PW + 1];
+    extern __shared__ __align__(16) unsigned char trsm_smem[];
+    Acc* Bs = reinterpret_cast<Acc*>(trsm_smem);  // [TRSM_ROWS][n + 1]
+    const int ldb = n + 1;
     const T* Lg = lvbuf<L>(c) + (long long)lr0 * c.ldw + lr0;
     T* Bg = lvbuf<L>(c) + (long long)br0 * c.ldw + bc0;
     // a quad of threads per row: the finished-column sums are split over the
     // quad (t = q, q+4, ...) and reduced with shuffles; the in-chunk
     // substitution is run redundantly by the quad, quad lane 0 stores
     const int q = threadIdx.x & 3;
-    const int i = blockIdx.x * TRSM_ROWS + (threadIdx.x >> 2);
+    const int r = threadIdx.x >> 2;
+    const int i0 = blockIdx.x * TRSM_ROWS;
+    const int i = i0 + r;
     const bool live = i < m;
     T* row = Bg + (long long)(live ? i : 0) * c.ldw;
+    if constexpr (BS) {
+        const int rows = min(TRSM_ROWS, m - i0);
+        for (int rr = threadIdx.x >> 5; rr < rows; rr += 4)
+            for (int t = threadIdx.x & 31; t < n; t += 32)
+                Bs[rr * ldb + t] = Acc(to_d(Bg[(long long)(i0 + rr) * c.ldw + t]));
+        __syncthreads();
+    }
+    auto getx = [&](int t) -> Acc {
+        if constexpr (BS) return Bs[r * ldb + t];
+        else return Acc(to_d(row[t]));
+    };
+    unsigned long long bad = ~0ull;
 
     for (int J = 0; J < n; J += PW) {
         const int w = min(PW, n - J);
@@ -210,7 +248,7 @@ __global__ void __launch_bounds__(128) k_trsm_leaf(DevCtx c, int br0, int bc0, i
             __syncthreads();
             if (live)
                 for (int tt = q; tt < tw; tt += 4) {
-                    const Acc xv = Acc(to_d(row[t0 + tt]));
+                    const Acc xv = getx(t0 + tt);
 #pragma unroll
                     for (int jj = 0; jj < PW; ++jj) acc[jj] = fma(xv, Lc[tt][jj], acc[jj]);
                 }
@@ -239,20 +277,36 @@ __global__ void __launch_bounds__(128) k_trsm_leaf(DevCtx c, int br0, int bc0, i
 #pragma unroll
             for (int jj = 0; jj < PW; ++jj) {
                 if (jj < w) {
-                    Acc s = acc[jj];
-#pragma unroll
-                    for (int tt = 0; tt < jj; ++tt) s = fma(x[tt], D[tt][jj], s);
-                    const Acc v = rnd<L>(Acc(to_d(row[J + jj])) - s);
+                    const Acc v = rnd<L>(getx(J + jj) - acc[jj]);  // rn_level(rn_acc(c - s))
                     x[jj] = rnd<L>(v / D[jj][jj]);
+#pragma unroll
+                    for (int j2 = jj + 1; j2 < PW; ++j2) acc[j2] = fma(x[jj], D[jj][j2], acc[j2]);
+                    if (chk_seq && !isfinite(x[jj])) {
+                        const unsigned long long k =
+                            fail_key(chk_seq, elem_local(br0 + i - chk_r0, bc0 + J + jj - chk_c0));
+                        bad = k < bad ? k : bad;
+                    }
                 }
             }
         }
-        __syncwarp();  // every quad lane has read row[J..J+w) before lane 0 stores
+        __syncwarp();  // every quad lane has read its row's [J, J+w) before lane 0 stores
         if (live && q == 0)
 #pragma unroll
             for (int jj = 0; jj < PW; ++jj)
-                if (jj < w) row[J + jj] = from_double<T>(double(x[jj]));
+                if (jj < w) {
+                    if constexpr (BS) Bs[r * ldb + J + jj] = x[jj];
+                    else row[J + jj] = from_double<T>(double(x[jj]));
+                }
+        __syncwarp();
     }
+    if constexpr (BS) {
+        __syncthreads();
+        const int rows = min(TRSM_ROWS, m - i0);
+        for (int rr = threadIdx.x >> 5; rr < rows; rr += 4)
+            for (int t = threadIdx.x & 31; t < n; t += 32)
+                Bg[(long long)(i0 + rr) * c.ldw + t] = from_double<T>(double(Bs[rr * ldb + t]));
+    }
+    if (chk_seq) warp_report_min(c, bad);
 }
 
 // W = inv(rn16(L)) for one leaf (L the F16-level copy: the leaf itself or its
@@ -311,8 +365,8 @@ __global__ void __launch_bounds__(128) k_leaf_inverse(DevCtx c, int r0, int n, u
     // per-leaf scale: all CTAs of the leaf must agree, so it is derived from
     // the diagonal (|W(t,t)| = 1/|L(t,t)| dominates a diagonally dominant
     // leaf) of the whole leaf, not from this CTA's columns
-    float dmax = 0.f;
-    for (int j = lane; j < n; j += 32) dmax = fmaxf(dmax, fabsf(1.0f / Ls[(j * (j + 1)) / 2 + j]));
+    float dmax = 0.f;  // from global: this CTA only staged rows/cols >= c0
+    for (int j = lane; j < n; j += 32) dmax = fmaxf(dmax, fabsf(1.0f / __half2float(g[(long long)j * c.ldw + j])));
 #pragma unroll
     for (int o = 16; o; o >>= 1) dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
     int e = 0;
@@ -335,10 +389,10 @@ __global__ void __launch_bounds__(128) k_leaf_inverse(DevCtx c, int r0, int n, u
 size_t inverse_smem(int n) { return (size_t(n) * (n + 1) / 2 + size_t(INV_COLS) * n) * sizeof(float); }
 
 template <int L, bool SMEM>
-void potrf_launch(const DevCtx& c, int r0, int n, uint32_t seq, cudaStream_t s) {
+void potrf_launch(const DevCtx& c, int r0, int n, uint32_t seq, uint32_t chk, cudaStream_t s) {
     using Acc = typename LvT<L>::Acc;
     const size_t smem = potrf_smem<Acc>(n, SMEM);
-    k_potrf_leaf<L, SMEM><<<1, POTRF_THREADS, smem, s>>>(c, r0, n, seq);
+    k_potrf_leaf<L, SMEM><<<1, POTRF_THREADS, smem, s>>>(c, r0, n, seq, chk);
 }
 
 }  // namespace
@@ -347,8 +401,11 @@ void launch_leaf_inverse(const DevCtx& c, int r0, int n, uint32_t seq, cudaStrea
     k_leaf_inverse<<<(n + INV_COLS - 1) / INV_COLS, 128, inverse_smem(n), s>>>(c, r0, n, seq);
 }
 
+void init_trsm_attributes();
+
 void init_leaf_attributes() {
     const int cap = 227 * 1024;
+    init_trsm_attributes();
     cudaFuncSetAttribute(k_leaf_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
     cudaFuncSetAttribute(k_potrf_leaf<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
     cudaFuncSetAttribute(k_potrf_leaf<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
@@ -360,7 +417,7 @@ void init_leaf_attributes() {
 
 constexpr size_t kLeafSmemCap = 220 * 1024;
 
-void launch_potrf_leaf(const DevCtx& c, int lv, int r0, int n, uint32_t seq, cudaStream_t s) {
+void launch_potrf_leaf(const DevCtx& c, int lv, int r0, int n, uint32_t seq, uint32_t chk, cudaStream_t s) {
     const bool d = lv == LV_F64;
     const bool fits = (d ? potrf_smem<double>(n, true) : potrf_smem<float>(n, true)) <= kLeafSmemCap;
     const bool pfits = (d ? potrf_smem<double>(n, false) : potrf_smem<float>(n, false)) <= kLeafSmemCap;
@@ -370,20 +427,39 @@ void launch_potrf_leaf(const DevCtx& c, int lv, int r0, int n, uint32_t seq, cud
         return;
     }
     switch (lv) {
-        case LV_F16: fits ? potrf_launch<0, true>(c, r0, n, seq, s) : potrf_launch<0, false>(c, r0, n, seq, s); break;
-        case LV_F32: fits ? potrf_launch<1, true>(c, r0, n, seq, s) : potrf_launch<1, false>(c, r0, n, seq, s); break;
-        default: fits ? potrf_launch<2, true>(c, r0, n, seq, s) : potrf_launch<2, false>(c, r0, n, seq, s); break;
+        case LV_F16: fits ? potrf_launch<0, true>(c, r0, n, seq, chk, s) : potrf_launch<0, false>(c, r0, n, seq, chk, s); break;
+        case LV_F32: fits ? potrf_launch<1, true>(c, r0, n, seq, chk, s) : potrf_launch<1, false>(c, r0, n, seq, chk, s); break;
+        default: fits ? potrf_launch<2, true>(c, r0, n, seq, chk, s) : potrf_launch<2, false>(c, r0, n, seq, chk, s); break;
     }
 }
 
-void launch_trsm_leaf(const DevCtx& c, int lv, int br0, int bc0, int m, int n, int lr0, uint32_t seq,
-                      cudaStream_t s) {
+constexpr size_t kTrsmRowsSmemCap = 100 * 1024;
+
+template <int L>
+void trsm_launch(const DevCtx& c, int br0, int bc0, int m, int n, int lr0, uint32_t seq, uint32_t chk_seq,
+                 int chk_r0, int chk_c0, cudaStream_t s) {
+    using Acc = typename LvT<L>::Acc;
     const int grid = (m + TRSM_ROWS - 1) / TRSM_ROWS;
-    if (grid == 0) return;
+    const size_t rows_smem = size_t(TRSM_ROWS) * (n + 1) * sizeof(Acc);
+    if (rows_smem <= kTrsmRowsSmemCap)
+        k_trsm_leaf<L, true><<<grid, 128, rows_smem, s>>>(c, br0, bc0, m, n, lr0, seq, chk_seq, chk_r0, chk_c0);
+    else
+        k_trsm_leaf<L, false><<<grid, 128, 0, s>>>(c, br0, bc0, m, n, lr0, seq, chk_seq, chk_r0, chk_c0);
+}
+
+void init_trsm_attributes() {
+    cudaFuncSetAttribute(k_trsm_leaf<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrsmRowsSmemCap);
+    cudaFuncSetAttribute(k_trsm_leaf<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrsmRowsSmemCap);
+    cudaFuncSetAttribute(k_trsm_leaf<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrsmRowsSmemCap);
+}
+
+void launch_trsm_leaf(const DevCtx& c, int lv, int br0, int bc0, int m, int n, int lr0, uint32_t seq,
+                      uint32_t chk_seq, int chk_r0, int chk_c0, cudaStream_t s) {
+    if (m <= 0) return;
     switch (lv) {
-        case LV_F16: k_trsm_leaf<0><<<grid, 128, 0, s>>>(c, br0, bc0, m, n, lr0, seq); break;
-        case LV_F32: k_trsm_leaf<1><<<grid, 128, 0, s>>>(c, br0, bc0, m, n, lr0, seq); break;
-        default: k_trsm_leaf<2><<<grid, 128, 0, s>>>(c, br0, bc0, m, n, lr0, seq); break;
+        case LV_F16: trsm_launch<0>(c, br0, bc0, m, n, lr0, seq, chk_seq, chk_r0, chk_c0, s); break;
+        case LV_F32: trsm_launch<1>(c, br0, bc0, m, n, lr0, seq, chk_seq, chk_r0, chk_c0, s); break;
+        default: trsm_launch<2>(c, br0, bc0, m, n, lr0, seq, chk_seq, chk_r0, chk_c0, s); break;
     }
 }
 

@@ -25,7 +25,8 @@ void launch_check(const DevCtx& c, int lv, int r0, int c0, int m, int n, int low
                   cudaStream_t s);
 void launch_quant(const DevCtx& c, int lv, int r0, int c0, int m, int n, int slot, uint32_t seq,
                   cudaStream_t s);
-void launch_dequant(const DevCtx& c, int lv, int r0, int c0, int m, int n, int slot, cudaStream_t s);
+void launch_dequant(const DevCtx& c, int lv, int r0, int c0, int m, int n, int slot, uint32_t chk_seq,
+                    cudaStream_t s);
 
 // spd_generate symmetrization of raw draws (k_elementwise.cu)
 void launch_symmetrize(double* a, long long lda, int n, cudaStream_t s);
@@ -35,9 +36,9 @@ void init_leaf_attributes();
 void init_tc_attributes();
 
 // leaves (k_leaf.cu)
-void launch_potrf_leaf(const DevCtx& c, int lv, int r0, int n, uint32_t seq, cudaStream_t s);
+void launch_potrf_leaf(const DevCtx& c, int lv, int r0, int n, uint32_t seq, uint32_t chk_seq, cudaStream_t s);
 void launch_trsm_leaf(const DevCtx& c, int lv, int br0, int bc0, int m, int n, int lr0, uint32_t seq,
-                      cudaStream_t s);
+                      uint32_t chk_seq, int chk_r0, int chk_c0, cudaStream_t s);
 void launch_leaf_inverse(const DevCtx& c, int r0, int n, uint32_t seq, cudaStream_t s);
 
 // grouped GEMM (k_gemm_simt.cu / k_gemm_tc.cu)

@@ -303,11 +303,19 @@ void Plan::emit_potrf(int node) {
         chk.lower = 1;
         chk.diagonal = 1;
         chk.seq = next_seq();
-        push(std::move(chk));
+        checks.push_back({chk.seq, chk.rect, 1});
+        // the leaf's require_finite (tree.cpp:108) runs inside the POTRF
+        // kernel, which loads the lower triangle anyway
+        const uint32_t chk_seq = chk.seq;
+        if (!opt.fuse_checks) push(std::move(chk));
         Op op;
         op.type = OP_POTRF;
         op.level = nd.level;
         op.rect = blocks[nd.block].rect;
+        if (opt.fuse_checks) {
+            op.check_seq = chk_seq;
+            op.chk = op.rect;
+        }
         op.seq = next_seq();
         const uint64_t n = uint64_t(nd.n);
         add_flops(op.seq, nd.level, K_POTRF, n * (n + 1) * (2 * n + 1) / 6);
@@ -327,33 +335,81 @@ void Plan::emit_potrf(int node) {
         q.rect = blk.rect;
         q.slot = slot;
         q.seq = next_seq();  // the require_finite that precedes quantize
+        checks.push_back({q.seq, blk.rect, 0});
         push(std::move(q));
     } else {
-        Op chk;
-        chk.type = OP_CHECK;
-        chk.level = p;
-        chk.src = p;
-        chk.rect = blk.rect;
-        chk.seq = next_seq();
-        push(std::move(chk));
+        const uint32_t seq = next_seq();
+        checks.push_back({seq, blk.rect, 0});
+        // require_finite before quantize (tree.cpp:114): a non-spine panel's
+        // last writer is the SYRK update of its nearest ancestor, which wrote
+        // the whole block -- its epilogue checks what it stores
+        int last = -1;
+        if (opt.fuse_checks)
+            for (int i = int(probs.size()) - 1; i >= 0; --i) {
+                const GemmProb& g = probs[i];
+                if (g.c_r0 == blk.rect.r0 && g.c_c0 == blk.rect.c0 && g.m == blk.rect.m && g.n == blk.rect.n &&
+                    g.ref_kernel == K_GEMM && g.exec_level == p) {
+                    last = i;
+                    break;
+                }
+            }
+        if (last >= 0) {
+            probs[last].check_seq = seq;
+            probs[last].chk_r0 = blk.rect.r0;
+            probs[last].chk_c0 = blk.rect.c0;
+        } else {
+            Op chk;
+            chk.type = OP_CHECK;
+            chk.level = p;
+            chk.src = p;
+            chk.rect = blk.rect;
+            chk.seq = seq;
+            push(std::move(chk));
+        }
     }
     ensure_shadows(nd.d1, p);
+    const int op0 = int(ops.size()), pr0 = int(probs.size());
     emit_trsm(blk.rect, p, nd.d1);
+    const int op1 = int(ops.size()), pr1 = int(probs.size());
+    int dq_op = -1;
     if (blk.spine_quant) {
         Op dq;
         dq.type = OP_DEQUANT;
         dq.level = p;
         dq.rect = blk.rect;
         dq.slot = slot;
-        push(std::move(dq));
+        dq_op = push(std::move(dq));
     }
-    Op chk;
-    chk.type = OP_CHECK;
-    chk.level = p;
-    chk.src = p;
-    chk.rect = blk.rect;
-    chk.seq = next_seq();
-    push(std::move(chk));
+    // require_finite after dequantize (tree.cpp:121): every panel element's
+    // last writer is the leaf solve of its column block (or the dequantize
+    // when alpha != 1), so those kernels check their outputs
+    const uint32_t post = next_seq();
+    checks.push_back({post, blk.rect, 0});
+    if (opt.fuse_checks) {
+        for (int i = op0; i < op1; ++i)
+            if (ops[i].type == OP_TRSM) {
+                ops[i].check_seq = post;
+                ops[i].chk = blk.rect;
+            }
+        for (int i = pr0; i < pr1; ++i)
+            if (probs[i].ref_kernel == K_TRSM) {
+                probs[i].check_seq = post;
+                probs[i].chk_r0 = blk.rect.r0;
+                probs[i].chk_c0 = blk.rect.c0;
+            }
+        if (dq_op >= 0) {
+            ops[dq_op].check_seq = post;
+            ops[dq_op].chk = blk.rect;
+        }
+    } else {
+        Op chk;
+        chk.type = OP_CHECK;
+        chk.level = p;
+        chk.src = p;
+        chk.rect = blk.rect;
+        chk.seq = post;
+        push(std::move(chk));
+    }
     emit_syrk(nd.d2, blk.rect, p);
     emit_potrf(nd.d2);
 }

@@ -72,6 +72,10 @@ struct GemmProb {
     int ref_kernel = K_GEMM;
     int a_kwrap = 0;        // A's K coordinate wraps at this period (inverse solve: hi|lo)
     int b_buf = -1;         // buffer of the B operand (-1: the operand level's)
+    // fused require_finite on the values this call writes (0 = none): the
+    // element position is reported relative to the checked block's origin
+    uint32_t check_seq = 0;
+    int chk_r0 = 0, chk_c0 = 0;
 };
 
 enum OpType : int {
@@ -113,12 +117,25 @@ struct Op {
     int diagonal = 0;     // OP_CHECK: "diagonal" vs "off-diagonal" wording
     int slot = -1;        // OP_QUANT / OP_DEQUANT: alpha slot
     uint32_t seq = 0;     // status sequence number (0 = op never fails)
+    // fused require_finite: POTRF leaf entry check (lower triangle of rect),
+    // TRSM / DEQUANT: post-dequantize check of the panel at chk (origin)
+    uint32_t check_seq = 0;
+    Rect chk;
     int gclass = GC_TC16; // OP_GEMM
     int prob_begin = 0, prob_end = 0;  // OP_GEMM: range in Plan::probs
     std::vector<int> blocks;           // OP_IMPORT / EXPORT / SHADOW
     std::vector<Access> acc;
     std::vector<int> deps;
     double flops = 0;      // algorithmic flops executed (for per-op timing)
+};
+
+// a require_finite point of the reference (tree.cpp:108, 114, 121): a
+// failure key with this seq is a NumericalBreakdown in `rect`, element
+// position relative to its origin
+struct CheckRec {
+    uint32_t seq;
+    Rect rect;
+    int diagonal;
 };
 
 struct FlopRec {
@@ -130,6 +147,7 @@ struct FlopRec {
 struct PlanOptions {
     bool use_tc = true;      // FP16-operand GEMMs on tcgen05
     bool inverse_trsm = true; // FP16 leaf solves with m >= kInvMinRows as tcgen05 GEMMs
+    bool fuse_checks = true;  // require_finite inside the producing kernels
 };
 
 struct Plan {
@@ -143,6 +161,7 @@ struct Plan {
     std::vector<GemmProb> probs;
     std::vector<Op> ops;
     std::vector<FlopRec> flops;  // in seq order
+    std::vector<CheckRec> checks;  // in seq order
     int n_alpha_slots = 0;
     uint32_t n_seq = 0;
     bool needs_buf[3] = {false, false, false};
