@@ -23,7 +23,8 @@ namespace tcb {
 namespace {
 
 constexpr int PW = 32;  // panel width
-constexpr int TRSM_ROWS = 32;  // rows per trsm CTA (4 threads per row)
+constexpr int TRSM_TPR = 8;                    // threads per row of B
+constexpr int TRSM_ROWS = 128 / TRSM_TPR;      // rows per trsm CTA
 constexpr int POTRF_THREADS = 512;
 constexpr int KT = 16;  // potrf phase (a): finished columns staged per step
 
@@ -138,49 +139,59 @@ __global__ void __launch_bounds__(POTRF_THREADS) k_potrf_leaf(DevCtx c, int r0, 
         }
         __syncthreads();
         // (b1) diagonal block by warp 0: lane l owns row J + l
+        // Right-looking inside the block: a[] holds c - (sums so far) in Acc,
+        // never rounded to the level until the column is complete, so the
+        // arithmetic is the reference's (FP32/FP64 accumulation, one final
+        // rn_level) with the sum reordered; each column costs one short
+        // dependent chain, the updates are independent FMAs.
         if (warp == 0) {
-            Acc x[PW];
+            Acc a[PW];
             const bool live = lane < w;
 #pragma unroll
-            for (int tt = 0; tt < PW; ++tt) x[tt] = (live && tt <= lane && tt < w) ? A.get(J + lane, J + tt) : Acc(0);
+            for (int tt = 0; tt < PW; ++tt)
+                a[tt] = (live && tt <= lane && tt < w) ? A.get(J + lane, J + tt) - P[lane * PW + tt] : Acc(0);
 #pragma unroll
             for (int jj = 0; jj < PW; ++jj) {
                 if (jj < w) {
-                    Acc s = live ? P[lane * PW + jj] : Acc(0);
-#pragma unroll
-                    for (int tt = 0; tt < jj; ++tt) s = fma(x[tt], __shfl_sync(0xffffffffu, x[tt], jj), s);
-                    const Acc v = rnd<L>(x[jj] - s);  // rn_level(rn_acc(c - s))
+                    const Acc v = rnd<L>(a[jj]);  // rn_level(rn_acc(c - s))
                     const Acc piv = __shfl_sync(0xffffffffu, v, jj);
                     if (lane == 0 && !(isfinite(piv) && piv > Acc(0)))
                         report(c, seq, uint64_t(J + jj));
                     const Acc d = rnd<L>(sqrt(piv));
-                    if (lane == jj) x[jj] = d;
-                    else if (lane > jj) x[jj] = rnd<L>(v / d);
+                    const Acc lij = lane == jj ? d : rnd<L>(v / d);
+                    if (lane >= jj) a[jj] = lij;
+#pragma unroll
+                    for (int j2 = jj + 1; j2 < PW; ++j2) {
+                        const Acc lj2 = __shfl_sync(0xffffffffu, a[jj], j2);  // L(J+j2, J+jj)
+                        if (lane > jj) a[j2] = fma(-lij, lj2, a[j2]);
+                    }
                 }
             }
             if (live)
 #pragma unroll
                 for (int tt = 0; tt < PW; ++tt)
-                    if (tt <= lane && tt < w) A.set(J + lane, J + tt, x[tt]);
+                    if (tt <= lane && tt < w) A.set(J + lane, J + tt, a[tt]);
         }
         __syncthreads();
-        // (b2) rows below the diagonal block, one thread per row
+        // (b2) rows below the diagonal block, one thread per row, right-looking
         for (int r = PW + tid; r < R; r += POTRF_THREADS) {
             const int i = J + r;
-            Acc x[PW];
+            Acc a[PW];
+#pragma unroll
+            for (int jj = 0; jj < PW; ++jj) a[jj] = jj < w ? A.get(i, J + jj) - P[r * PW + jj] : Acc(0);
 #pragma unroll
             for (int jj = 0; jj < PW; ++jj) {
                 if (jj < w) {
-                    Acc s = P[r * PW + jj];
+                    const Acc x = rnd<L>(rnd<L>(a[jj]) / A.get(J + jj, J + jj));
+                    a[jj] = x;
 #pragma unroll
-                    for (int tt = 0; tt < jj; ++tt) s = fma(x[tt], A.get(J + jj, J + tt), s);
-                    const Acc v = rnd<L>(A.get(i, J + jj) - s);
-                    x[jj] = rnd<L>(v / A.get(J + jj, J + jj));
+                    for (int j2 = jj + 1; j2 < PW; ++j2)
+                        if (j2 < w) a[j2] = fma(-x, A.get(J + j2, J + jj), a[j2]);
                 }
             }
 #pragma unroll
             for (int jj = 0; jj < PW; ++jj)
-                if (jj < w) A.set(i, J + jj, x[jj]);
+                if (jj < w) A.set(i, J + jj, a[jj]);
         }
         __syncthreads();
     }
@@ -204,8 +215,8 @@ __global__ void __launch_bounds__(128) k_trsm_leaf(DevCtx c, int br0, int bc0, i
     using T = typename LvT<L>::T;
     using Acc = typename LvT<L>::Acc;
     constexpr int TSL = 128;  // staged slice of finished columns
-    __shared__ Acc Lc[TSL][PW + 1];
-    __shared__ Acc D[PW][PW + 1];
+    __shared__ __align__(16) Acc Lc[TSL][PW + 4];  // 16-byte rows: vector broadcast reads
+    __shared__ __align__(16) Acc D[PW][PW + 4];
     extern __shared__ __align__(16) unsigned char trsm_smem[];
     Acc* Bs = reinterpret_cast<Acc*>(trsm_smem);  // [TRSM_ROWS][n + 1]
     const int ldb = n + 1;
@@ -214,8 +225,8 @@ __global__ void __launch_bounds__(128) k_trsm_leaf(DevCtx c, int br0, int bc0, i
     // a quad of threads per row: the finished-column sums are split over the
     // quad (t = q, q+4, ...) and reduced with shuffles; the in-chunk
     // substitution is run redundantly by the quad, quad lane 0 stores
-    const int q = threadIdx.x & 3;
-    const int r = threadIdx.x >> 2;
+    const int q = threadIdx.x % TRSM_TPR;
+    const int r = threadIdx.x / TRSM_TPR;
     const int i0 = blockIdx.x * TRSM_ROWS;
     const int i = i0 + r;
     const bool live = i < m;
@@ -247,7 +258,7 @@ __global__ void __launch_bounds__(128) k_trsm_leaf(DevCtx c, int br0, int bc0, i
             }
             __syncthreads();
             if (live)
-                for (int tt = q; tt < tw; tt += 4) {
+                for (int tt = q; tt < tw; tt += TRSM_TPR) {
                     const Acc xv = getx(t0 + tt);
 #pragma unroll
                     for (int jj = 0; jj < PW; ++jj) acc[jj] = fma(xv, Lc[tt][jj], acc[jj]);
@@ -255,8 +266,7 @@ __global__ void __launch_bounds__(128) k_trsm_leaf(DevCtx c, int br0, int bc0, i
         }
 #pragma unroll
         for (int jj = 0; jj < PW; ++jj) {
-            acc[jj] += __shfl_xor_sync(0xffffffffu, acc[jj], 1);
-            acc[jj] += __shfl_xor_sync(0xffffffffu, acc[jj], 2);
+            for (int o = 1; o < TRSM_TPR; o <<= 1) acc[jj] += __shfl_xor_sync(0xffffffffu, acc[jj], o);
         }
         __syncthreads();
         for (int e = threadIdx.x; e < PW * PW; e += 128) {
