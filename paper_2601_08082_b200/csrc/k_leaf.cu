@@ -25,7 +25,7 @@ namespace {
 constexpr int PW = 32;  // panel width
 constexpr int TRSM_TPR = 8;                    // threads per row of B
 constexpr int TRSM_ROWS = 128 / TRSM_TPR;      // rows per trsm CTA
-constexpr int POTRF_THREADS = 512;
+constexpr int POTRF_THREADS = 256;
 constexpr int KT = 16;  // potrf phase (a): finished columns staged per step
 
 template <typename Acc>
@@ -52,7 +52,7 @@ struct LeafAcc {
 };
 
 template <int L, bool SMEM>
-__global__ void __launch_bounds__(POTRF_THREADS) k_potrf_leaf(DevCtx c, int r0, int n, uint32_t seq,
+__global__ void __launch_bounds__(POTRF_THREADS, 1) k_potrf_leaf(DevCtx c, int r0, int n, uint32_t seq,
                                                               uint32_t chk_seq) {
     using T = typename LvT<L>::T;
     using Acc = typename LvT<L>::Acc;
@@ -139,21 +139,24 @@ __global__ void __launch_bounds__(POTRF_THREADS) k_potrf_leaf(DevCtx c, int r0, 
         }
         __syncthreads();
         // (b1) diagonal block by warp 0: lane l owns row J + l
-        // Right-looking inside the block: a[] holds c - (sums so far) in Acc,
-        // never rounded to the level until the column is complete, so the
-        // arithmetic is the reference's (FP32/FP64 accumulation, one final
-        // rn_level) with the sum reordered; each column costs one short
-        // dependent chain, the updates are independent FMAs.
+        // Right-looking schedule, reference order: s[] accumulates the dot
+        // product sum_t L(i,t) L(j,t) in increasing t exactly as the left-
+        // looking reference does (kernels.cpp:28-32), and c - s is formed
+        // once per element (kernels.cpp:33-37).  Subtracting products from c
+        // directly would round relative to the large diagonal.  Each column
+        // costs one short dependent chain; the s updates are independent.
         if (warp == 0) {
-            Acc a[PW];
+            Acc a[PW], s[PW];
             const bool live = lane < w;
 #pragma unroll
-            for (int tt = 0; tt < PW; ++tt)
-                a[tt] = (live && tt <= lane && tt < w) ? A.get(J + lane, J + tt) - P[lane * PW + tt] : Acc(0);
+            for (int tt = 0; tt < PW; ++tt) {
+                a[tt] = (live && tt <= lane && tt < w) ? A.get(J + lane, J + tt) : Acc(0);
+                s[tt] = (live && tt <= lane && tt < w) ? P[lane * PW + tt] : Acc(0);
+            }
 #pragma unroll
             for (int jj = 0; jj < PW; ++jj) {
                 if (jj < w) {
-                    const Acc v = rnd<L>(a[jj]);  // rn_level(rn_acc(c - s))
+                    const Acc v = rnd<L>(a[jj] - s[jj]);  // rn_level(rn_acc(c - s))
                     const Acc piv = __shfl_sync(0xffffffffu, v, jj);
                     if (lane == 0 && !(isfinite(piv) && piv > Acc(0)))
                         report(c, seq, uint64_t(J + jj));
@@ -163,7 +166,7 @@ __global__ void __launch_bounds__(POTRF_THREADS) k_potrf_leaf(DevCtx c, int r0, 
 #pragma unroll
                     for (int j2 = jj + 1; j2 < PW; ++j2) {
                         const Acc lj2 = __shfl_sync(0xffffffffu, a[jj], j2);  // L(J+j2, J+jj)
-                        if (lane > jj) a[j2] = fma(-lij, lj2, a[j2]);
+                        s[j2] = fma(lij, lj2, s[j2]);
                     }
                 }
             }
@@ -173,25 +176,22 @@ __global__ void __launch_bounds__(POTRF_THREADS) k_potrf_leaf(DevCtx c, int r0, 
                     if (tt <= lane && tt < w) A.set(J + lane, J + tt, a[tt]);
         }
         __syncthreads();
-        // (b2) rows below the diagonal block, one thread per row, right-looking
+        // (b2) rows below the diagonal block, one thread per row, same scheme
         for (int r = PW + tid; r < R; r += POTRF_THREADS) {
             const int i = J + r;
-            Acc a[PW];
+            Acc s[PW];
 #pragma unroll
-            for (int jj = 0; jj < PW; ++jj) a[jj] = jj < w ? A.get(i, J + jj) - P[r * PW + jj] : Acc(0);
+            for (int jj = 0; jj < PW; ++jj) s[jj] = jj < w ? P[r * PW + jj] : Acc(0);
 #pragma unroll
             for (int jj = 0; jj < PW; ++jj) {
                 if (jj < w) {
-                    const Acc x = rnd<L>(rnd<L>(a[jj]) / A.get(J + jj, J + jj));
-                    a[jj] = x;
+                    const Acc x = rnd<L>(rnd<L>(A.get(i, J + jj) - s[jj]) / A.get(J + jj, J + jj));
+                    A.set(i, J + jj, x);
 #pragma unroll
                     for (int j2 = jj + 1; j2 < PW; ++j2)
-                        if (j2 < w) a[j2] = fma(-x, A.get(J + j2, J + jj), a[j2]);
+                        if (j2 < w) s[j2] = fma(x, A.get(J + j2, J + jj), s[j2]);
                 }
             }
-#pragma unroll
-            for (int jj = 0; jj < PW; ++jj)
-                if (jj < w) A.set(i, J + jj, a[jj]);
         }
         __syncthreads();
     }
