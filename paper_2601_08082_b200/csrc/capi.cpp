@@ -439,3 +439,11 @@ int tc_solve_residual_device(int n, const double* dA, int lda, const double* dX,
 }
 
 }  // extern "C"
+
+namespace tcb {
+void leaf_debug_clocks(long long* out, bool reset);
+}
+extern "C" int tc_debug_leaf_clocks(long long* out4, int reset) {
+    tcb::leaf_debug_clocks(out4, reset != 0);
+    return TC_OK;
+}

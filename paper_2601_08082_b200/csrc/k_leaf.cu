@@ -23,6 +23,7 @@ namespace tcb {
 namespace {
 
 constexpr int PW = 32;  // panel width
+__device__ long long g_leaf_clk[8];  // debug: cycles per potrf phase (a, b1, b2), count
 constexpr int TRSM_TPR = 8;                    // threads per row of B
 constexpr int TRSM_ROWS = 128 / TRSM_TPR;      // rows per trsm CTA
 constexpr int POTRF_THREADS = 256;
@@ -30,7 +31,7 @@ constexpr int KT = 16;  // potrf phase (a): finished columns staged per step
 
 template <typename Acc>
 constexpr size_t potrf_smem(int n, bool smem) {
-    return (size_t(n) * PW + size_t(KT) * (n + 4) + size_t(KT) * (PW + 4) +
+    return (size_t(n) * PW + size_t(KT) * (n + 4) + size_t(KT) * (PW + 4) + size_t(PW) * (PW + 4) +
             (smem ? size_t(n) * (n + 1) / 2 : 0)) * sizeof(Acc);
 }
 
@@ -51,6 +52,72 @@ struct LeafAcc {
     }
 };
 
+// (b1) factor the diagonal block at (J, J) on one warp, lane l = row J + l.
+// a[] holds c, s[] the running dot product in the reference's order
+// (kernels.cpp:28-32); c - s is formed once per element (kernels.cpp:33-37)
+// -- subtracting products from c directly would round relative to the
+// large diagonal.  Each solved column is broadcast through Dt (also kept for
+// the rows below: Dt[jj][j2] = L(J+j2, J+jj)).
+template <int L, bool FULL, typename Acc, typename AccT>
+__device__ __forceinline__ void diag_block(const AccT& A, const Acc* P, Acc* Dt, int J, int w, int lane,
+                                           const DevCtx& c, uint32_t seq) {
+    Acc a[PW], s[PW];
+    const bool live = lane < w;
+#pragma unroll
+    for (int tt = 0; tt < PW; ++tt) {
+        const bool in = live && tt <= lane && (FULL || tt < w);
+        a[tt] = in ? A.get(J + lane, J + tt) : Acc(0);
+        s[tt] = in ? P[lane * PW + tt] : Acc(0);
+    }
+#pragma unroll
+    for (int jj = 0; jj < PW; ++jj) {
+        if (FULL || jj < w) {
+            const Acc v = rnd<L>(a[jj] - s[jj]);  // rn_level(rn_acc(c - s))
+            const Acc piv = __shfl_sync(0xffffffffu, v, jj);
+            if (lane == 0 && !(isfinite(piv) && piv > Acc(0))) report(c, seq, uint64_t(J + jj));
+            const Acc d = rnd<L>(sqrt(piv));
+            const Acc lij = lane == jj ? d : rnd<L>(v / d);
+            a[jj] = lij;
+            Acc* col = Dt + jj * (PW + 4);
+            col[lane] = lane >= jj ? lij : Acc(0);
+            __syncwarp();
+#pragma unroll
+            for (int j2 = jj + 1; j2 < PW; ++j2) s[j2] = fma(lij, col[j2], s[j2]);
+        }
+    }
+    if (live)
+#pragma unroll
+        for (int tt = 0; tt < PW; ++tt)
+            if (tt <= lane && (FULL || tt < w)) A.set(J + lane, J + tt, a[tt]);
+}
+
+// (b2) rows J+PW .. J+R-1 against the factored diagonal block: one thread
+// per row, right-looking over the block's columns with the same separate
+// running sum; the block comes from Dt (vector broadcast reads).
+template <int L, bool FULL, typename Acc, typename AccT>
+__device__ __forceinline__ void below_rows(const AccT& A, const Acc* P, const Acc* Dt, int J, int R, int w,
+                                           int tid) {
+    for (int r = PW + tid; r < R; r += POTRF_THREADS) {
+        const int i = J + r;
+        Acc s[PW];
+#pragma unroll
+        for (int jj = 0; jj < PW; ++jj) s[jj] = (FULL || jj < w) ? P[r * PW + jj] : Acc(0);
+#pragma unroll
+        for (int jj = 0; jj < PW; ++jj) {
+            if (FULL || jj < w) {
+                // compiler fence: keep the block's loads inside their
+                // iteration (hoisting all 496 would explode register use)
+                asm volatile("" ::: "memory");
+                const Acc* col = Dt + jj * (PW + 4);
+                const Acc x = rnd<L>(rnd<L>(A.get(i, J + jj) - s[jj]) / col[jj]);
+                A.set(i, J + jj, x);
+#pragma unroll
+                for (int j2 = jj + 1; j2 < PW; ++j2) s[j2] = fma(x, col[j2], s[j2]);
+            }
+        }
+    }
+}
+
 template <int L, bool SMEM>
 __global__ void __launch_bounds__(POTRF_THREADS, 1) k_potrf_leaf(DevCtx c, int r0, int n, uint32_t seq,
                                                               uint32_t chk_seq) {
@@ -61,7 +128,8 @@ __global__ void __launch_bounds__(POTRF_THREADS, 1) k_potrf_leaf(DevCtx c, int r
     Acc* P = reinterpret_cast<Acc*>(smem_raw);    // [n][PW] partial sums
     Acc* As = P + size_t(n) * PW;                 // [KT][ldS]  A(J+r, t0+tt) transposed
     Acc* Bs = As + size_t(KT) * ldS;              // [KT][PW+4] A(J+jj, t0+tt)
-    Acc* S = Bs + size_t(KT) * (PW + 4);          // packed lower triangle (SMEM)
+    Acc* Dt = Bs + size_t(KT) * (PW + 4);         // [PW][PW+4] Dt[jj][j2] = L(J+j2, J+jj)
+    Acc* S = Dt + size_t(PW) * (PW + 4);          // packed lower triangle (SMEM)
     T* g = lvbuf<L>(c) + (long long)r0 * c.ldw + r0;
     LeafAcc<L, SMEM> A{S, g, c.ldw};
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -88,6 +156,8 @@ __global__ void __launch_bounds__(POTRF_THREADS, 1) k_potrf_leaf(DevCtx c, int r
         __syncthreads();
     }
 
+    long long t_ph = clock64();
+    long long* clk = g_leaf_clk;
     for (int J = 0; J < n; J += PW) {
         const int w = min(PW, n - J);
         const int R = n - J;  // rows of this panel
@@ -138,64 +208,25 @@ __global__ void __launch_bounds__(POTRF_THREADS, 1) k_potrf_leaf(DevCtx c, int r
                 }
         }
         __syncthreads();
-        // (b1) diagonal block by warp 0: lane l owns row J + l
-        // Right-looking schedule, reference order: s[] accumulates the dot
-        // product sum_t L(i,t) L(j,t) in increasing t exactly as the left-
-        // looking reference does (kernels.cpp:28-32), and c - s is formed
-        // once per element (kernels.cpp:33-37).  Subtracting products from c
-        // directly would round relative to the large diagonal.  Each column
-        // costs one short dependent chain; the s updates are independent.
-        if (warp == 0) {
-            Acc a[PW], s[PW];
-            const bool live = lane < w;
-#pragma unroll
-            for (int tt = 0; tt < PW; ++tt) {
-                a[tt] = (live && tt <= lane && tt < w) ? A.get(J + lane, J + tt) : Acc(0);
-                s[tt] = (live && tt <= lane && tt < w) ? P[lane * PW + tt] : Acc(0);
-            }
-#pragma unroll
-            for (int jj = 0; jj < PW; ++jj) {
-                if (jj < w) {
-                    const Acc v = rnd<L>(a[jj] - s[jj]);  // rn_level(rn_acc(c - s))
-                    const Acc piv = __shfl_sync(0xffffffffu, v, jj);
-                    if (lane == 0 && !(isfinite(piv) && piv > Acc(0)))
-                        report(c, seq, uint64_t(J + jj));
-                    const Acc d = rnd<L>(sqrt(piv));
-                    const Acc lij = lane == jj ? d : rnd<L>(v / d);
-                    if (lane >= jj) a[jj] = lij;
-#pragma unroll
-                    for (int j2 = jj + 1; j2 < PW; ++j2) {
-                        const Acc lj2 = __shfl_sync(0xffffffffu, a[jj], j2);  // L(J+j2, J+jj)
-                        s[j2] = fma(lij, lj2, s[j2]);
-                    }
-                }
-            }
-            if (live)
-#pragma unroll
-                for (int tt = 0; tt < PW; ++tt)
-                    if (tt <= lane && tt < w) A.set(J + lane, J + tt, a[tt]);
+        if (threadIdx.x == 0) { const long long t = clock64(); clk[0] += t - t_ph; t_ph = t; }
+        // (b1) diagonal block by warp 0 (lane l owns row J + l), then (b2)
+        // the rows below, one thread per row.  Right-looking schedule in the
+        // reference's summation order (see diag_block / below_rows).
+        if (w == PW) {
+            if (warp == 0) diag_block<L, true>(A, P, Dt, J, w, lane, c, seq);
+            __syncthreads();
+            if (threadIdx.x == 0) { const long long t = clock64(); clk[1] += t - t_ph; t_ph = t; }
+            below_rows<L, true>(A, P, Dt, J, R, w, tid);
+        } else {
+            if (warp == 0) diag_block<L, false>(A, P, Dt, J, w, lane, c, seq);
+            __syncthreads();
+            if (threadIdx.x == 0) { const long long t = clock64(); clk[1] += t - t_ph; t_ph = t; }
+            below_rows<L, false>(A, P, Dt, J, R, w, tid);
         }
         __syncthreads();
-        // (b2) rows below the diagonal block, one thread per row, same scheme
-        for (int r = PW + tid; r < R; r += POTRF_THREADS) {
-            const int i = J + r;
-            Acc s[PW];
-#pragma unroll
-            for (int jj = 0; jj < PW; ++jj) s[jj] = jj < w ? P[r * PW + jj] : Acc(0);
-#pragma unroll
-            for (int jj = 0; jj < PW; ++jj) {
-                if (jj < w) {
-                    const Acc x = rnd<L>(rnd<L>(A.get(i, J + jj) - s[jj]) / A.get(J + jj, J + jj));
-                    A.set(i, J + jj, x);
-#pragma unroll
-                    for (int j2 = jj + 1; j2 < PW; ++j2)
-                        if (j2 < w) s[j2] = fma(x, A.get(J + j2, J + jj), s[j2]);
-                }
-            }
-        }
-        __syncthreads();
+        if (threadIdx.x == 0) { const long long t = clock64(); clk[2] += t - t_ph; t_ph = t; }
     }
-
+    if (threadIdx.x == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&clk[3]), 1ull);
     if constexpr (SMEM) {
         for (int i = warp; i < n; i += NW)
             for (int j = lane; j <= i; j += 32)
@@ -244,6 +275,7 @@ __global__ void __launch_bounds__(128) k_trsm_leaf(DevCtx c, int br0, int bc0, i
     };
     unsigned long long bad = ~0ull;
 
+    long long t_tr = clock64();
     for (int J = 0; J < n; J += PW) {
         const int w = min(PW, n - J);
         Acc acc[PW];
@@ -282,11 +314,13 @@ __global__ void __launch_bounds__(128) k_trsm_leaf(DevCtx c, int br0, int bc0, i
                     break;
                 }
             }
+        if (threadIdx.x == 0 && blockIdx.x == 0) { const long long t = clock64(); g_leaf_clk[4] += t - t_tr; t_tr = t; }
         Acc x[PW];
         if (live) {
 #pragma unroll
             for (int jj = 0; jj < PW; ++jj) {
                 if (jj < w) {
+                    asm volatile("" ::: "memory");  // keep D loads in their iteration
                     const Acc v = rnd<L>(getx(J + jj) - acc[jj]);  // rn_level(rn_acc(c - s))
                     x[jj] = rnd<L>(v / D[jj][jj]);
 #pragma unroll
@@ -308,6 +342,7 @@ __global__ void __launch_bounds__(128) k_trsm_leaf(DevCtx c, int br0, int bc0, i
                     else row[J + jj] = from_double<T>(double(x[jj]));
                 }
         __syncwarp();
+        if (threadIdx.x == 0 && blockIdx.x == 0) { const long long t = clock64(); g_leaf_clk[5] += t - t_tr; t_tr = t; }
     }
     if constexpr (BS) {
         __syncthreads();
@@ -316,6 +351,7 @@ __global__ void __launch_bounds__(128) k_trsm_leaf(DevCtx c, int br0, int bc0, i
             for (int t = threadIdx.x & 31; t < n; t += 32)
                 Bg[(long long)(i0 + rr) * c.ldw + t] = from_double<T>(double(Bs[rr * ldb + t]));
     }
+    if (threadIdx.x == 0 && blockIdx.x == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&g_leaf_clk[7]), 1ull);
     if (chk_seq) warp_report_min(c, bad);
 }
 
@@ -415,6 +451,7 @@ void init_trsm_attributes();
 
 void init_leaf_attributes() {
     const int cap = 227 * 1024;
+    init_leaf_cm_attributes();
     init_trsm_attributes();
     cudaFuncSetAttribute(k_leaf_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
     cudaFuncSetAttribute(k_potrf_leaf<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
@@ -428,6 +465,7 @@ void init_leaf_attributes() {
 constexpr size_t kLeafSmemCap = 220 * 1024;
 
 void launch_potrf_leaf(const DevCtx& c, int lv, int r0, int n, uint32_t seq, uint32_t chk, cudaStream_t s) {
+    if (leaf_cm_ok(lv, n)) return launch_potrf_cm(c, lv, r0, n, seq, chk, s);
     const bool d = lv == LV_F64;
     const bool fits = (d ? potrf_smem<double>(n, true) : potrf_smem<float>(n, true)) <= kLeafSmemCap;
     const bool pfits = (d ? potrf_smem<double>(n, false) : potrf_smem<float>(n, false)) <= kLeafSmemCap;
@@ -466,6 +504,7 @@ void init_trsm_attributes() {
 void launch_trsm_leaf(const DevCtx& c, int lv, int br0, int bc0, int m, int n, int lr0, uint32_t seq,
                       uint32_t chk_seq, int chk_r0, int chk_c0, cudaStream_t s) {
     if (m <= 0) return;
+    if (leaf_cm_ok(lv, n)) return launch_trsm_cm(c, lv, br0, bc0, m, n, lr0, seq, chk_seq, chk_r0, chk_c0, s);
     switch (lv) {
         case LV_F16: trsm_launch<0>(c, br0, bc0, m, n, lr0, seq, chk_seq, chk_r0, chk_c0, s); break;
         case LV_F32: trsm_launch<1>(c, br0, bc0, m, n, lr0, seq, chk_seq, chk_r0, chk_c0, s); break;
@@ -473,4 +512,15 @@ void launch_trsm_leaf(const DevCtx& c, int lv, int br0, int bc0, int m, int n, i
     }
 }
 
+}  // namespace tcb
+
+namespace tcb {
+// debug: accumulated potrf-leaf phase cycles since the last call (a, b1, b2, launches)
+void leaf_debug_clocks(long long* out, bool reset) {
+    cudaMemcpyFromSymbol(out, g_leaf_clk, sizeof(long long) * 8);
+    if (reset) {
+        long long z[8] = {0};
+        cudaMemcpyToSymbol(g_leaf_clk, z, sizeof(z));
+    }
+}
 }  // namespace tcb

@@ -39,6 +39,12 @@ void init_tc_attributes();
 void launch_potrf_leaf(const DevCtx& c, int lv, int r0, int n, uint32_t seq, uint32_t chk_seq, cudaStream_t s);
 void launch_trsm_leaf(const DevCtx& c, int lv, int br0, int bc0, int m, int n, int lr0, uint32_t seq,
                       uint32_t chk_seq, int chk_r0, int chk_c0, cudaStream_t s);
+// latency-optimised F16/F32 leaves, n % 32 == 0, n <= 256 (k_leaf_cm.cu)
+bool leaf_cm_ok(int lv, int n);
+void init_leaf_cm_attributes();
+void launch_potrf_cm(const DevCtx& c, int lv, int r0, int n, uint32_t seq, uint32_t chk, cudaStream_t s);
+void launch_trsm_cm(const DevCtx& c, int lv, int br0, int bc0, int m, int n, int lr0, uint32_t seq,
+                    uint32_t chk_seq, int chk_r0, int chk_c0, cudaStream_t s);
 void launch_leaf_inverse(const DevCtx& c, int r0, int n, uint32_t seq, cudaStream_t s);
 
 // grouped GEMM (k_gemm_simt.cu / k_gemm_tc.cu)
