@@ -59,8 +59,13 @@ __device__ void cm_load(float* S, const T* g, long long ld, int n, float* tiles,
         int I = 0;
         while ((I + 1) * (I + 2) / 2 <= k) ++I;
         const int J = k - I * (I + 1) / 2;
-        for (int rr = 0; rr < 32; ++rr) tile[rr * 33 + lane] = to_f(g[(long long)(I * 32 + rr) * ld + J * 32 + lane]);
+        float v[32];  // 32 independent loads in flight per lane
+#pragma unroll
+        for (int rr = 0; rr < 32; ++rr) v[rr] = to_f(g[(long long)(I * 32 + rr) * ld + J * 32 + lane]);
+#pragma unroll
+        for (int rr = 0; rr < 32; ++rr) tile[rr * 33 + lane] = v[rr];
         __syncwarp();
+#pragma unroll 8
         for (int cc = 0; cc < 32; ++cc) {
             const int t = J * 32 + cc, r = I * 32 + lane;
             if (r >= t) S[cm_off(t, n) + r] = tile[lane * 33 + cc];
@@ -82,6 +87,7 @@ __device__ void cm_store(const float* S, T* g, long long ld, int n, float* tiles
             tile[lane * 33 + cc] = r >= t ? S[cm_off(t, n) + r] : 0.f;
         }
         __syncwarp();
+#pragma unroll
         for (int rr = 0; rr < 32; ++rr) {
             const int r = I * 32 + rr, t = J * 32 + lane;
             if (r >= t) g[(long long)r * ld + t] = from_float<T>(tile[rr * 33 + lane]);
@@ -247,8 +253,14 @@ __global__ void __launch_bounds__(TR_THREADS, 1) k_trsm_cm(DevCtx c, int br0, in
     const int rows = min(TR_ROWS, m - i0);
 
     cm_load(S, Lg, c.ldw, n, tiles, warp, TR_THREADS / 32, lane);
-    for (int rr = warp; rr < rows; rr += TR_THREADS / 32)
-        for (int t = lane; t < n; t += 32) Bs[rr * ldb + t] = to_f(Bg[(long long)(i0 + rr) * c.ldw + t]);
+    for (int rr = warp; rr < rows; rr += TR_THREADS / 32) {
+        float v[8];  // n <= 256: one row in 8 independent loads per lane
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = lane + 32 * k < n ? to_f(Bg[(long long)(i0 + rr) * c.ldw + lane + 32 * k]) : 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (lane + 32 * k < n) Bs[rr * ldb + lane + 32 * k] = v[k];
+    }
     __syncthreads();
     for (int j = tid; j < n; j += TR_THREADS) rd[j] = 1.0f / S[cm_off(j, n) + j];
     if (blockIdx.x == 0 && tid == 0)  // singular diagonal (kernels.cpp:78-81), first column
