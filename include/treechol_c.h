@@ -110,6 +110,9 @@ int tc_plan_profile(tc_plan* plan, const double* dA_in, int lda_in, double* dL_o
  * FP16, 1..5 SIMT classes, -1 otherwise), level, algorithmic flops, rect */
 int tc_plan_op_info(const tc_plan* plan, int i, int* type, int* gclass, int* level,
                     double* flops, int* rect4);
+/* dependencies of op i (indices of earlier ops); returns their count
+ * (entries beyond cap are not written), -1 on a bad index */
+int tc_plan_op_deps(const tc_plan* plan, int i, int* deps, int cap);
 /* flops of the last run as SolveOptions::flops would hold them: the full
  * plan on success, the calls completed before the failure otherwise */
 int tc_plan_run_flops(const tc_plan* plan, tc_flops* out);
@@ -138,9 +141,40 @@ int tc_spd_generate_device(int n, uint64_t seed, double* dA, int lda, void* stre
  * only lower triangles are read; NaN if any lower entry is non-finite. */
 int tc_factorization_error_device(int n, const double* dA, int lda, const double* dL,
                                   int ldl, double* out, void* stream);
+/* the same metric on host buffers (staged through device memory) */
+int tc_factorization_error_host(int n, const double* A, int lda, const double* L, int ldl, double* out);
 /* ||b - A x||_2 / (||A||_F ||x||_2 + ||b||_2) with A symmetric (lower read) */
 int tc_solve_residual_device(int n, const double* dA, int lda, const double* dX,
                              const double* dB, double* out, void* stream);
+
+/* ---- standalone block operations (kernels.hpp:20-40, tree.hpp:47-51) ---
+ * The reference's kernel-level API on column-major doubles, executed on the
+ * device with the reference's scalar operation order (bit-identical).  Not
+ * used by the factorization path.  `acc` is the accumulator level of Half
+ * GEMM-style sums (KernelContext::half_accumulator; ignored at F32/F64).
+ * *_device: device pointers, enqueued on `stream`.  *_host: host pointers;
+ * the call stages the block through device memory and synchronizes.
+ * Failures: *fail_index = the block-local index (pivot / diagonal entry),
+ * status TC_NOT_POSITIVE_DEFINITE / TC_SINGULAR_DIAGONAL. */
+
+/* round_matrix (kernels.cpp:9-16); lower != 0: lower triangle only
+ * (round_lower, tree.cpp:33-40) */
+int tc_round_host(int m, int n, double* A, int lda, int level, int lower);
+/* quantize_block (tree.cpp:80-95): returns alpha in *alpha */
+int tc_quantize_host(int m, int n, double* B, int ldb, int level, double* alpha);
+/* dequantize_block (tree.cpp:97-104) */
+int tc_dequantize_host(int m, int n, double* B, int ldb, int level, double alpha);
+/* potrf_leaf (kernels.cpp:42-69) on the n x n lower triangle */
+int tc_potrf_leaf_host(int n, double* A, int lda, int level, int acc, int* fail_index);
+/* trsm_leaf (kernels.cpp:71-92): B (m x n) <- B L^-T, L n x n */
+int tc_trsm_leaf_host(int m, int n, double* B, int ldb, const double* L, int ldl, int level, int acc,
+                      int* fail_index);
+/* gemm_mixed (kernels.cpp:114-132): C (m x n) <- beta C + alpha A B^T, k
+ * columns; lower != 0: syrk_leaf (kernels.cpp:94-112), m == n, B may be A */
+int tc_gemm_mixed_host(int m, int n, int k, double* C, int ldc, const double* A, int lda, const double* B, int ldb,
+                       double alpha, double beta, int level, int acc, int lower);
+int tc_gemm_mixed_device(int m, int n, int k, double* dC, int ldc, const double* dA, int lda, const double* dB,
+                         int ldb, double alpha, double beta, int level, int acc, int lower, void* stream);
 
 /* ---- misc --------------------------------------------------------------- */
 

@@ -113,6 +113,7 @@ def _load():
         "tc_plan_stats": (I, [P, PI, PI, PI]),
         "tc_plan_set_option": (I, [P, C.c_char_p, I]),
         "tc_plan_op_info": (I, [P, I, PI, PI, PI, C.POINTER(D), PI]),
+        "tc_plan_op_deps": (I, [P, I, PI, I]),
         "tc_potrf_device": (I, [P, P, I, P, I, P, C.POINTER(_Info)]),
         "tc_potrf_host": (I, [P, P, I, C.POINTER(_Info)]),
         "tc_plan_profile": (I, [P, P, I, P, I, P, C.POINTER(C.c_float), I]),
@@ -366,6 +367,17 @@ class Plan:
         _raise(_lib.tc_plan_op_info(self._h, i, C.byref(t), C.byref(g), C.byref(lv), C.byref(fl), r))
         return {"type": OP_TYPES[t.value], "gclass": GEMM_CLASSES[g.value] if g.value >= 0 else None,
                 "level": lv.value, "flops": fl.value, "rect": tuple(r)}
+
+    def op_deps(self, i: int):
+        cap = 64
+        while True:
+            arr = (C.c_int * cap)()
+            k = _lib.tc_plan_op_deps(self._h, i, arr, cap)
+            if k < 0:
+                raise InvalidArgument("bad op index")
+            if k <= cap:
+                return list(arr[:k])
+            cap = k
 
     def _status(self, code: int, info: _Info) -> FactorStatus:
         if code in (TC_OK, TC_NPD, TC_BREAKDOWN, TC_SINGULAR):

@@ -95,6 +95,10 @@ void flops_out(const uint64_t L[3], const uint64_t K[4], const uint64_t C[4], tc
 
 }  // namespace
 
+namespace tcb {
+void set_last_error(const std::string& msg) { g_err = msg; }
+}  // namespace tcb
+
 extern "C" {
 
 const char* tc_last_error(void) { return g_err.c_str(); }
@@ -235,6 +239,14 @@ int tc_plan_op_info(const tc_plan* plan, int i, int* type, int* gclass, int* lev
         rect4[3] = op.rect.n;
     }
     return TC_OK;
+}
+
+int tc_plan_op_deps(const tc_plan* plan, int i, int* deps, int cap) {
+    if (!plan || i < 0 || i >= int(plan->eng->plan.ops.size())) return -1;
+    const Op& op = plan->eng->plan.ops[i];
+    const int k = int(op.deps.size());
+    for (int j = 0; j < k && j < cap; ++j) deps[j] = op.deps[j];
+    return k;
 }
 
 int tc_potrf_device(tc_plan* plan, const double* dA_in, int lda_in, double* dL_out, int lda_out, void* stream,
@@ -405,6 +417,27 @@ int tc_factorization_error_device(int n, const double* dA, int lda, const double
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "factorization_error");
     return TC_OK;
+}
+
+int tc_factorization_error_host(int n, const double* A, int lda, const double* L, int ldl, double* out) {
+    if (!A || !L || !out || n < 1 || lda < n || ldl < n) return fail(TC_INVALID_ARGUMENT, "bad arguments");
+    if (!tc_device_available()) return fail(TC_NO_DEVICE, "no CUDA device (there is no CPU fallback)");
+    double* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, sizeof(double) * 2 * size_t(n) * size_t(n));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+    double* dL = d + size_t(n) * size_t(n);
+    e = cudaMemcpy2D(d, sizeof(double) * size_t(n), A, sizeof(double) * size_t(lda), sizeof(double) * size_t(n),
+                     size_t(n), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+        e = cudaMemcpy2D(dL, sizeof(double) * size_t(n), L, sizeof(double) * size_t(ldl), sizeof(double) * size_t(n),
+                         size_t(n), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        cudaFree(d);
+        return cuda_fail(e, "H2D");
+    }
+    const int st = tc_factorization_error_device(n, d, n, dL, n, out, nullptr);
+    cudaFree(d);
+    return st;
 }
 
 int tc_potrs_device(int n, const double* dL, int ldl, double* dB, int ldb, int nrhs, void* stream) {

@@ -62,6 +62,17 @@ int tc_build_probs(const DevCtx& c, const std::vector<DevProb>& probs, std::vect
 void launch_gemm_tc(const DevCtx& c, const void* d_probs, int nprob, int tiles, cudaStream_t s);
 bool tc_supported();
 
+// standalone block operations on column-major doubles (k_blockops.cu)
+void bo_round(double* a, long long lda, int m, int n, int lv, int lower, cudaStream_t s);
+void bo_quantize(double* a, long long lda, int m, int n, int lv, unsigned long long* d_amax, double* d_alpha,
+                 cudaStream_t s);
+void bo_dequantize(double* a, long long lda, int m, int n, int lv, double alpha, cudaStream_t s);
+void bo_gemm(double* c, long long ldc, const double* a, long long lda, const double* b, long long ldb, int m, int n,
+             int k, double alpha, double beta, int lv, int acc, int lower, cudaStream_t s);
+void bo_potrf(double* a, long long lda, int n, int lv, int acc, int* d_status, cudaStream_t s);
+void bo_trsm(double* b, long long ldb, const double* l, long long ldl, int m, int n, int lv, int acc, int* d_status,
+             cudaStream_t s);
+
 // verification (k_verify.cu)
 void launch_fact_error(int n, const double* dA, long long lda, const double* dL, long long ldl,
                        double* d_partials, int* d_nonfinite, int tiles_per_side, cudaStream_t s);
