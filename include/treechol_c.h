@@ -86,7 +86,8 @@ int tc_plan_flops(const tc_plan* plan, tc_flops* out);
 /* plan statistics: number of device ops / kernel launches per factorization */
 int tc_plan_stats(const tc_plan* plan, int* n_ops, int* n_launches, int* n_gemm_problems);
 /* execution knobs: use_graph (default 1), n_streams (default 6),
- * use_tc (default 1: tcgen05 for FP16-operand GEMMs; 0 = SIMT path) */
+ * use_tc (default 1: tcgen05 for FP16-operand GEMMs; 0 = SIMT path),
+ * use_tc32 (default 1: three-pass TF32 tcgen05 for FP32 x FP32 GEMMs) */
 int tc_plan_set_option(tc_plan* plan, const char* key, int value);
 
 /* ---- factorization (tree_potrf, tree.cpp:106-125) ---------------------- */
@@ -175,6 +176,15 @@ int tc_gemm_mixed_host(int m, int n, int k, double* C, int ldc, const double* A,
                        double alpha, double beta, int level, int acc, int lower);
 int tc_gemm_mixed_device(int m, int n, int k, double* dC, int ldc, const double* dA, int lda, const double* dB,
                          int ldb, double alpha, double beta, int level, int acc, int lower, void* stream);
+
+/* ---- development ------------------------------------------------------- */
+
+/* one launch of the grouped GEMM of class gclass (0 tcgen05 FP16, 6 tcgen05
+ * three-pass TF32, 1..5 SIMT) on scratch buffers: C (m x n) -= A (m x k) B^T
+ * (n x k), exec level exec_level, optional lower mask (SYRK leaf) and beta;
+ * *avg_us = mean device time of `iters` back-to-back launches */
+int tc_debug_gemm(int gclass, int m, int n, int k, int lower, double beta, int exec_level, int iters,
+                  float* avg_us);
 
 /* ---- misc --------------------------------------------------------------- */
 

@@ -42,7 +42,7 @@ KERNEL_NAMES = ("POTRF-leaf", "TRSM-leaf", "SYRK-leaf", "GEMM")  # flops.cpp:5-1
 TC_OK, TC_NPD, TC_BREAKDOWN, TC_SINGULAR, TC_INVALID, TC_SYNTAX, TC_VALIDATION, TC_CUDA, TC_NO_DEVICE = range(9)
 
 OP_TYPES = ("import", "export", "check", "quant", "dequant", "shadow", "potrf", "trsm", "gemm", "inverse")
-GEMM_CLASSES = ("tc16", "simt_f16", "simt_f32", "simt_f16d", "simt_f32d", "simt_f64")
+GEMM_CLASSES = ("tc16", "simt_f16", "simt_f32", "simt_f16d", "simt_f32d", "simt_f64", "tc32")
 
 
 # ---------------------------------------------------------------- errors.hpp
@@ -124,6 +124,7 @@ def _load():
         "tc_spd_generate_device": (I, [I, U64, P, I, P]),
         "tc_factorization_error_device": (I, [I, P, I, P, I, C.POINTER(D), P]),
         "tc_solve_residual_device": (I, [I, P, I, P, P, C.POINTER(D), P]),
+        "tc_debug_gemm": (I, [I, I, I, I, I, D, I, I, C.POINTER(C.c_float)]),
         "tc_last_error": (C.c_char_p, []),
         "tc_device_available": (I, []),
         "tc_version": (C.c_char_p, []),
@@ -321,7 +322,7 @@ class Plan:
     (tree.hpp:42-66).  Device workspace is allocated on the first factor."""
 
     def __init__(self, n: int, b: int, config, quantize: bool = True, leaf_size: int = 0, use_tc: bool = True,
-                 use_graph: bool = True, n_streams: int = 0):
+                 use_graph: bool = True, n_streams: int = 0, use_tc32: bool = True):
         self.cfg = _cfg(config)
         self.n, self.b, self.quantize = int(n), int(b), bool(quantize)
         arr = (C.c_int * len(self.cfg.levels))(*self.cfg.levels)
@@ -331,6 +332,8 @@ class Plan:
         self._h = h
         if not use_tc:
             self.set_option("use_tc", 0)
+        if not use_tc32:
+            self.set_option("use_tc32", 0)
         if not use_graph:
             self.set_option("use_graph", 0)
         if n_streams:
@@ -465,6 +468,15 @@ def potrs_device(l_dev, b_dev, n: int | None = None, stream=None):
     b2 = b_dev if b_dev.dim() == 2 else b_dev.view(1, -1)
     _raise(_lib.tc_potrs_device(n, _ptr(l_dev), ldl, _ptr(b2), b2.shape[1], b2.shape[0], _stream_ptr(stream)))
     return b_dev
+
+
+def debug_gemm(gclass: str, m: int, n: int, k: int, lower: bool = False, beta: float = 1.0, exec_level: int = 0,
+               iters: int = 20) -> float:
+    """development: mean device microseconds of one grouped-GEMM launch"""
+    out = C.c_float()
+    _raise(_lib.tc_debug_gemm(GEMM_CLASSES.index(gclass), m, n, k, int(lower), float(beta), exec_level, iters,
+                              C.byref(out)))
+    return out.value
 
 
 def solve_residual_device(a_dev, x_dev, b_dev, n: int | None = None, stream=None) -> float:

@@ -207,10 +207,13 @@ int tc_plan_set_option(tc_plan* plan, const char* key, int value) {
         e.n_streams = value < 1 ? 1 : value;
         return TC_OK;
     }
-    if (k == "use_tc" || k == "inverse_trsm" || k == "fuse_checks") {
+    if (k == "use_tc" || k == "use_tc32" || k == "inverse_trsm" || k == "fuse_checks") {
         if (e.ready()) return fail(TC_INVALID_ARGUMENT, k + " must be set before the first run");
         PlanOptions po = e.plan.opt;
-        bool& field = k == "use_tc" ? po.use_tc : k == "inverse_trsm" ? po.inverse_trsm : po.fuse_checks;
+        bool& field = k == "use_tc"       ? po.use_tc
+                      : k == "use_tc32"   ? po.use_tc32
+                      : k == "inverse_trsm" ? po.inverse_trsm
+                                          : po.fuse_checks;
         if (bool(value) == field) return TC_OK;
         field = value != 0;
         Plan p = Plan::make(e.plan.n, e.plan.b, e.plan.levels, e.plan.quantize, e.plan.leaf_size, po);

@@ -1,0 +1,97 @@
+// capi_debug.cpp -- development entry points (declared in treechol_c.h under
+// "development"): one grouped-GEMM launch of a given operand class on scratch
+// buffers, timed with CUDA events, for kernel tuning and single-kernel ncu
+// captures.  Not used by the factorization path.
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/treechol_c.h"
+#include "launch.hpp"
+#include "plan.hpp"
+
+using namespace tcb;
+
+namespace tcb {
+void set_last_error(const std::string& msg);  // capi.cpp
+}
+
+extern "C" int tc_debug_gemm(int gclass, int m, int n, int k, int lower, double beta, int exec_level, int iters,
+                             float* avg_us) {
+    if (m < 1 || n < 1 || k < 1 || iters < 1 || !avg_us) return TC_INVALID_ARGUMENT;
+    const long long rows = (long long)m + n + k;
+    const long long ldw = ((k + n + 63) / 64) * 64;  // A at cols [0,k), C at cols [k, k+n)
+    DevCtx c{};
+    c.ldw = ldw;
+    void* buf = nullptr;
+    unsigned long long* words = nullptr;
+    const size_t elems = size_t(rows) * size_t(ldw);
+    if (cudaMalloc(&buf, elems * (2 + 4)) != cudaSuccess) return TC_CUDA_ERROR;
+    cudaMalloc(&words, 64);
+    cudaMemset(buf, 0, elems * 6);
+    cudaMemset(words, 0xFF, 8);
+    c.b16 = static_cast<__half*>(buf);
+    c.b32 = reinterpret_cast<float*>(c.b16 + elems);
+    c.status = words;
+    init_tc_attributes();
+    DevProb d{};
+    d.m = m;
+    d.n = n;
+    d.k = k;
+    d.a_r0 = n;  // A rows [n, n+m), B rows [0, n), both at cols [0, k)
+    d.a_c0 = 0;
+    d.b_r0 = 0;
+    d.b_c0 = 0;
+    d.c_r0 = n;
+    d.c_c0 = k;
+    if (lower) {  // syrk leaf: C square on the diagonal (rows and cols [k, k+m))
+        d.b_r0 = n;
+        d.c_r0 = k;
+        d.c_c0 = k;
+    }
+    d.exec_level = exec_level;
+    d.lower = lower;
+    d.alpha = -1.0;
+    d.beta = beta;
+    d.b_buf = -1;
+    std::vector<DevProb> v{d};
+    std::vector<unsigned char> host;
+    int tiles = 0;
+    const bool tc = gclass == GC_TC16 || gclass == GC_TC32;
+    std::string err;
+    if (tc) tiles = tc_build_probs(c, gclass == GC_TC32 ? KIND_TF32X3 : KIND_F16, v, host, &err);
+    else {
+        tiles = simt_tiles(v);
+        host.assign(reinterpret_cast<unsigned char*>(v.data()), reinterpret_cast<unsigned char*>(v.data() + 1));
+    }
+    void* dprob = nullptr;
+    cudaMalloc(&dprob, host.size());
+    cudaMemcpy(dprob, host.data(), host.size(), cudaMemcpyHostToDevice);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    auto launch = [&] {
+        if (tc) launch_gemm_tc(c, gclass == GC_TC32 ? KIND_TF32X3 : KIND_F16, dprob, 1, tiles, nullptr);
+        else launch_gemm_simt(c, gclass, static_cast<DevProb*>(dprob), 1, tiles, nullptr);
+    };
+    launch();  // warm
+    cudaEventRecord(e0);
+    for (int i = 0; i < iters; ++i) launch();
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    *avg_us = ms * 1000.f / float(iters);
+    const cudaError_t e = cudaGetLastError();
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(dprob);
+    cudaFree(words);
+    cudaFree(buf);
+    if (e != cudaSuccess) {
+        set_last_error(cudaGetErrorString(e));
+        return TC_CUDA_ERROR;
+    }
+    return TC_OK;
+}

@@ -131,9 +131,9 @@ bool Engine::prepare(std::string* err) {
                 dp.push_back(d);
             }
             L.count = int(dp.size());
-            if (op.gclass == GC_TC16) {
+            if (op.gclass == GC_TC16 || op.gclass == GC_TC32) {
                 std::vector<unsigned char> tp;
-                L.tiles = tc_build_probs(ctx_, dp, tp, err);
+                L.tiles = tc_build_probs(ctx_, op.gclass == GC_TC32 ? KIND_TF32X3 : KIND_F16, dp, tp, err);
                 if (L.tiles < 0) return false;
                 L.offset = append(tp.data(), tp.size());
             } else {
@@ -177,7 +177,8 @@ void Engine::launch_op(int i, cudaStream_t s) {
             break;
         case OP_INVERSE: launch_leaf_inverse(ctx_, r.r0, r.m, op.seq, s); break;
         case OP_GEMM:
-            if (op.gclass == GC_TC16) launch_gemm_tc(ctx_, tab, L.count, L.tiles, s);
+            if (op.gclass == GC_TC16) launch_gemm_tc(ctx_, KIND_F16, tab, L.count, L.tiles, s);
+            else if (op.gclass == GC_TC32) launch_gemm_tc(ctx_, KIND_TF32X3, tab, L.count, L.tiles, s);
             else launch_gemm_simt(ctx_, op.gclass, reinterpret_cast<DevProb*>(tab), L.count, L.tiles, s);
             break;
     }

@@ -1,27 +1,42 @@
-// k_gemm_tc.cu -- grouped FP16 GEMM on the 5th-generation tensor cores.
+// k_gemm_tc.cu -- grouped GEMM on the 5th-generation tensor cores.
 //
 //   C(i,j) <- rn_exec( rn_f32(alpha*s) + rn_f32(beta*C(i,j)) ),
-//   s = sum_t A(i,t) * B(j,t)   (FP16 operands, exact products, FP32 sums)
+//   s = sum_t A(i,t) * B(j,t)   (FP32 sums in TMEM)
 //
-// This is gemm_mixed / syrk_leaf (kernels.cpp:94-132) for every call whose
-// operands are FP16-valued: exec level F16 (82% of the flops at N=65536
-// [F16,F16,F16,F32]) and F32 exec on FP16 panels (16.4%) -- the products of
-// two binary16 values are exact in binary32, so the reference's
-// rn_f32(a*b) is the identity and an FP32 tensor-core accumulator implements
-// the same arithmetic model (SURVEY headline fact 3).
+// This is gemm_mixed / syrk_leaf (kernels.cpp:94-132) for two operand
+// classes, one template:
 //
-// Structure (one persistent CTA per SM, 192 threads, warp-specialised):
-//   warp 0      TMA producer: 128x64 A and 256x64 B tiles, SWIZZLE_128B,
-//               4-stage smem ring guarded by full/empty mbarriers
+//  KIND_F16   FP16-valued operands, tcgen05 kind::f16 -- exec level F16 (82%
+//             of the flops at N=65536 [F16,F16,F16,F32]) and F32 exec on FP16
+//             panels (16.4%): products of two binary16 values are exact in
+//             binary32, so the reference's rn_f32(a*b) is the identity and an
+//             FP32 accumulator implements the same arithmetic model (SURVEY
+//             headline fact 3).
+//  KIND_TF32X3  FP32 x FP32 operands (F32 exec, 1.6%): each operand is split
+//             x = hi + lo with hi = x truncated to TF32 (exact) and lo = x - hi
+//             (exact in FP32), and s = sum lo_a*hi_b + hi_a*lo_b + hi_a*hi_b
+//             on kind::tf32 -- ~22 significant bits per operand, FP32 sums
+//             (the reference rounds each product to FP32, kernels.cpp:29-30).
+//             The split runs in shared memory between the TMA load and the
+//             MMA (converter warps), so the operands are read from HBM once.
+//
+// Structure (one persistent CTA per SM, warp-specialised):
+//   warp 0      TMA producer: 128x(128 B) A and BNx(128 B) B tiles, SWIZZLE_128B,
+//               STAGES-deep smem ring guarded by full/empty mbarriers
 //   warp 1      TMEM allocator + MMA issuer: one elected lane issues
-//               tcgen05.mma.cta_group::1.kind::f16 (M=128, N=256, K=16) into
-//               a double-buffered FP32 accumulator (2 x 256 TMEM columns)
-//   warps 2-5   epilogue: tcgen05.ld 32x32b -> registers -> rounding to the
-//               destination level -> global (row-major C)
+//               tcgen05.mma.cta_group::1 (M=128, N=BN) into a double-buffered
+//               FP32 accumulator (2 x BN TMEM columns)
+//   warps 2-9   epilogue, two warps per TMEM lane quarter (one per column
+//               half): C prefetched one 32-column chunk ahead, tcgen05.ld
+//               32x32b -> registers -> dot_update tail -> rounding to the
+//               destination level -> global (row-major C); fused
+//               require_finite as one OR per element, located only on failure
+//   warps 10-13 (TF32X3 only) hi/lo split of each stage, then a
+//               fence.proxy.async so the tensor core sees the generic writes
 // A problem list (one tree_syrk = all its output blocks, or one trsm GEMM)
-// is flattened into 128x256 tiles; each problem has its own pair of TMA
+// is flattened into 128xBN tiles; each problem has its own pair of TMA
 // descriptors whose extents end at the problem's edge, so partial tiles are
-// zero-filled by the TMA unit and K need not be a multiple of 64.
+// zero-filled by the TMA unit and K need not be a multiple of the k-block.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -49,17 +64,35 @@ size_t tc_prob_size() { return sizeof(TcProb); }
 
 namespace {
 
-constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
-constexpr int A_BYTES = BM * BK * 2;  // 16 KB
-constexpr int B_BYTES = BN * BK * 2;  // 32 KB
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-constexpr int NTHREADS = 192;
-constexpr uint32_t TMEM_COLS = 512;  // 2 accumulators x 256 columns
+constexpr int BM = 128;
 
-// instruction descriptor, kind::f16: D=F32 (bits 4-5 = 1), A=B=F16 (0),
-// both K-major, N>>3 at bits 17-22, M>>4 at bits 24-28
-constexpr uint32_t IDESC = (1u << 4) | (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+// per operand kind: tile width, k-block (one 128-byte swizzled row), ring
+// depth, threads, TMEM columns and the instruction descriptor
+//   idesc: D=F32 (bits 4-5 = 1), A/B format at bits 7-9 / 10-12 (F16 = 0,
+//   TF32 = 2), both K-major, N>>3 at bits 17-22, M>>4 at bits 24-28
+template <int KIND> struct Cfg;
+template <> struct Cfg<KIND_F16> {
+    static constexpr int BN = 256, ESZ = 2, BK = 64, STAGES = 4, NTHREADS = 320, PASSES = 1;
+    static constexpr uint32_t FMT = 0;
+};
+template <> struct Cfg<KIND_TF32X3> {
+    static constexpr int BN = 128, ESZ = 4, BK = 32, STAGES = 3, NTHREADS = 448, PASSES = 3;
+    static constexpr uint32_t FMT = 2;
+};
+template <int KIND> struct Geo {
+    using C = Cfg<KIND>;
+    static constexpr int BN = C::BN, BK = C::BK, STAGES = C::STAGES;
+    static constexpr int A_BYTES = BM * 128;  // one 128-byte row per tile row
+    static constexpr int B_BYTES = BN * 128;
+    static constexpr int TILE_BYTES = A_BYTES + B_BYTES;  // TMA bytes per stage
+    // TF32X3 keeps a lo copy of both tiles next to the (hi) TMA tiles
+    static constexpr int STAGE_BYTES = TILE_BYTES * (C::PASSES > 1 ? 2 : 1);
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr uint32_t TMEM_COLS = 2 * BN;  // two accumulators
+    static constexpr uint32_t IDESC = (1u << 4) | (C::FMT << 7) | (C::FMT << 10) | (uint32_t(BN >> 3) << 17) |
+                                      (uint32_t(BM >> 4) << 24);
+    static_assert(STAGES * STAGE_BYTES + 2048 <= 227 * 1024, "shared memory");
+};
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -107,14 +140,24 @@ __device__ __forceinline__ uint64_t sdesc(const void* p) {
     return ((a >> 4) & 0x3FFFull) | (1ull << 16) | (uint64_t(1024 >> 4) << 32) | (1ull << 46) | (2ull << 61);
 }
 
-__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accum) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "setp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
-        "}\n" ::"r"(tmem_d),
-        "l"(da), "l"(db), "r"(IDESC), "r"(accum));
+template <int KIND>
+__device__ __forceinline__ void mma_issue(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accum) {
+    if constexpr (KIND == KIND_F16)
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "setp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+            "}\n" ::"r"(tmem_d),
+            "l"(da), "l"(db), "r"(Geo<KIND>::IDESC), "r"(accum));
+    else
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "setp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+            "}\n" ::"r"(tmem_d),
+            "l"(da), "l"(db), "r"(Geo<KIND>::IDESC), "r"(accum));
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
@@ -151,6 +194,7 @@ __device__ __forceinline__ int find_tc_prob(const TcProb* p, int np, int tile) {
 
 // tile -> (problem, tm, tn); false for a lower problem's tile strictly above
 // the diagonal (nothing to write).  Every role evaluates the same predicate.
+template <int BN>
 __device__ __forceinline__ bool tile_coords(const TcProb* probs, int np, int t, int& pi, int& tm, int& tn) {
     pi = find_tc_prob(probs, np, t);
     const TcProb& p = probs[pi];
@@ -160,23 +204,82 @@ __device__ __forceinline__ bool tile_coords(const TcProb* probs, int np, int t, 
     return !(p.lower && p.c_c0 + tn * BN > p.c_r0 + tm * BM + BM - 1);
 }
 
-__device__ __forceinline__ float epi_f(float s, float cv, double alpha, double beta) {
-    float r = alpha == -1.0 ? -s : __double2float_rn(alpha * double(s));
-    if (beta != 0.0) r = r + (beta == 1.0 ? cv : __double2float_rn(beta * double(cv)));
-    return r;
+// dot_update's tail (kernels.cpp:33-37) for an FP32 accumulator s:
+// r = rn_f32(alpha*s); if beta != 0: r = rn_f32(r + rn_f32(beta*c)).  The
+// fast form covers alpha = +-2^e (alpha*s exact in FP32 exactly when it is
+// in double, then rounded once) and beta in {0, 1}; the rest goes through
+// double like the reference.
+struct Epi {
+    bool fast;
+    float af;
+    double alpha, beta;
+    __device__ __forceinline__ float operator()(float s, float cv) const {
+        if (fast) return beta != 0.0 ? af * s + cv : af * s;
+        float r = __double2float_rn(alpha * double(s));
+        if (beta != 0.0) r = r + (beta == 1.0 ? cv : __double2float_rn(beta * double(cv)));
+        return r;
+    }
+};
+__device__ __forceinline__ bool pow2_or_one(double a) {
+    const unsigned long long b = __double_as_longlong(a) & 0x7fffffffffffffffull;
+    const int e = int(b >> 52);
+    return (b & 0xfffffffffffffull) == 0 && e > 1023 - 100 && e < 1023 + 100;
 }
 
-__global__ void __launch_bounds__(NTHREADS, 1) k_gemm_tc(DevCtx c, const TcProb* __restrict__ probs, int np,
-                                                        int tiles) {
+// one 32-column chunk of C for one row: 32 halves (4 x uint4) or 32 floats
+// (8 x float4); prefetched a chunk ahead of its use
+struct CChunk {
+    uint4 r[8];
+};
+__device__ __forceinline__ void load_chunk(CChunk& ch, const void* p, bool f16) {
+    const uint4* q = static_cast<const uint4*>(p);
+#pragma unroll
+    for (int g = 0; g < 8; ++g)
+        if (!f16 || g < 4) ch.r[g] = __ldcg(q + g);
+}
+
+// hi/lo split of one staged tile pair for the three-pass TF32 product:
+// hi = x with the 13 low mantissa bits cleared (exactly TF32), lo = x - hi
+// (exact).  Elementwise, so the TMA swizzle is preserved.  128 threads.
+__device__ __forceinline__ void split_tf32(unsigned char* hi, unsigned char* lo, int bytes, int t) {
+    float4* h = reinterpret_cast<float4*>(hi);
+    float4* l = reinterpret_cast<float4*>(lo);
+    const int n4 = bytes / 16;
+#pragma unroll 4
+    for (int e = t; e < n4; e += 128) {
+        float4 x = h[e], y;
+        float* xs = reinterpret_cast<float*>(&x);
+        float* ys = reinterpret_cast<float*>(&y);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const float hv = __uint_as_float(__float_as_uint(xs[q]) & 0xFFFFE000u);
+            ys[q] = xs[q] - hv;
+            xs[q] = hv;
+        }
+        h[e] = x;
+        l[e] = y;
+    }
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(Cfg<KIND>::NTHREADS, 1) k_gemm_tc(DevCtx c, const TcProb* __restrict__ probs,
+                                                                    int np, int tiles) {
+    using G = Geo<KIND>;
+    constexpr int BN = G::BN, STAGES = G::STAGES;
+    constexpr bool SPLIT = Cfg<KIND>::PASSES > 1;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-byte alignment for SWIZZLE_128B
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                            ~uintptr_t(1023));
-    unsigned char* sA = smem;
-    unsigned char* sB = smem + STAGES * A_BYTES;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+    // stage s: A (hi) | B (hi) [| A lo | B lo]
+    auto sA = [&](int s) { return smem + s * G::STAGE_BYTES; };
+    auto sB = [&](int s) { return smem + s * G::STAGE_BYTES + G::A_BYTES; };
+    auto sAl = [&](int s) { return smem + s * G::STAGE_BYTES + G::TILE_BYTES; };
+    auto sBl = [&](int s) { return smem + s * G::STAGE_BYTES + G::TILE_BYTES + G::A_BYTES; };
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * G::STAGE_BYTES);
     uint64_t* empty = full + STAGES;
-    uint64_t* tfull = empty + STAGES;
+    uint64_t* split = empty + STAGES;  // TF32X3: hi/lo ready
+    uint64_t* tfull = split + STAGES;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -186,16 +289,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gemm_tc(DevCtx c, const TcProb*
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
+            mbar_init(&split[s], 4);
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&tfull[s], 1);
-            mbar_init(&tempty[s], 4);
+            mbar_init(&tempty[s], 8);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(TMEM_COLS));
+                     "r"(G::TMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tc_fence_before();
@@ -210,17 +314,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gemm_tc(DevCtx c, const TcProb*
             uint32_t phase = 0;
             for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
                 int pi, tm, tn;
-                if (!tile_coords(probs, np, t, pi, tm, tn)) continue;
+                if (!tile_coords<BN>(probs, np, t, pi, tm, tn)) continue;
                 const TcProb* p = probs + pi;
                 prefetch_map(&p->ta);
                 prefetch_map(&p->tb);
-                const int nk = (p->k + BK - 1) / BK;
+                const int nk = (p->k + G::BK - 1) / G::BK;
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_expect_tx(&full[stage], STAGE_BYTES);
-                    const int ka = p->a_kwrap ? (kb * BK) % p->a_kwrap : kb * BK;
-                    tma_load_2d(sA + stage * A_BYTES, &p->ta, &full[stage], p->a_c0 + ka, p->a_r0 + tm * BM);
-                    tma_load_2d(sB + stage * B_BYTES, &p->tb, &full[stage], p->b_c0 + kb * BK, p->b_r0 + tn * BN);
+                    mbar_expect_tx(&full[stage], G::TILE_BYTES);
+                    const int ka = p->a_kwrap ? (kb * G::BK) % p->a_kwrap : kb * G::BK;
+                    tma_load_2d(sA(stage), &p->ta, &full[stage], p->a_c0 + ka, p->a_r0 + tm * BM);
+                    tma_load_2d(sB(stage), &p->tb, &full[stage], p->b_c0 + kb * G::BK, p->b_r0 + tn * BN);
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
@@ -236,20 +340,32 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gemm_tc(DevCtx c, const TcProb*
         uint32_t aphase = 0;
         for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
             int pi, tm, tn;
-            if (!tile_coords(probs, np, t, pi, tm, tn)) continue;
-            const int nk = (probs[pi].k + BK - 1) / BK;
+            if (!tile_coords<BN>(probs, np, t, pi, tm, tn)) continue;
+            const int nk = (probs[pi].k + G::BK - 1) / G::BK;
             mbar_wait(&tempty[as], aphase ^ 1);
             tc_fence_after();
             const uint32_t dcol = tmem + uint32_t(as * BN);
             for (int kb = 0; kb < nk; ++kb) {
-                mbar_wait(&full[stage], phase);
+                mbar_wait(SPLIT ? &split[stage] : &full[stage], phase);
                 tc_fence_after();
                 if (lane == 0) {
-                    const uint64_t da = sdesc(sA + stage * A_BYTES);
-                    const uint64_t db = sdesc(sB + stage * B_BYTES);
+                    const uint64_t da = sdesc(sA(stage));
+                    const uint64_t db = sdesc(sB(stage));
+                    // 4 MMAs per 128-byte k-block: +32 bytes (2 in the >>4
+                    // address field) per K=16 (f16) / K=8 (tf32) step
 #pragma unroll
-                    for (int k = 0; k < BK / 16; ++k)  // +32 bytes per K=16 step inside the swizzled row
-                        mma_f16(dcol, da + uint64_t(2 * k), db + uint64_t(2 * k), (kb | k) != 0);
+                    for (int k = 0; k < 4; ++k) {
+                        const uint64_t o = uint64_t(2 * k);
+                        if constexpr (SPLIT) {
+                            // small terms first: lo*hi + hi*lo + hi*hi
+                            const uint64_t dal = sdesc(sAl(stage)), dbl = sdesc(sBl(stage));
+                            mma_issue<KIND>(dcol, dal + o, db + o, (kb | k) != 0);
+                            mma_issue<KIND>(dcol, da + o, dbl + o, 1);
+                            mma_issue<KIND>(dcol, da + o, db + o, 1);
+                        } else {
+                            mma_issue<KIND>(dcol, da + o, db + o, (kb | k) != 0);
+                        }
+                    }
                     mma_commit(&empty[stage]);
                     if (kb == nk - 1) mma_commit(&tfull[as]);
                 }
@@ -264,109 +380,159 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gemm_tc(DevCtx c, const TcProb*
                 aphase ^= 1;
             }
         }
+    } else if (warp >= 10) {
+        // ---------------- hi/lo split (TF32X3) ----------------
+        if constexpr (SPLIT) {
+            const int t128 = threadIdx.x - 10 * 32;
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+                int pi, tm, tn;
+                if (!tile_coords<BN>(probs, np, t, pi, tm, tn)) continue;
+                const int nk = (probs[pi].k + G::BK - 1) / G::BK;
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    split_tf32(sA(stage), sAl(stage), G::A_BYTES, t128);
+                    split_tf32(sB(stage), sBl(stage), G::B_BYTES, t128);
+                    // generic-proxy smem writes -> visible to the tensor core
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&split[stage]);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
     } else {
-        // ---------------- epilogue (warps 2..5) ----------------
-        const int q = warp & 3;  // TMEM lane quarter this warp may access
+        // ---------------- epilogue (warps 2..9) ----------------
+        const int q = warp & 3;             // TMEM lane quarter this warp may access
+        const int half = (warp - 2) >> 2;   // column half of the tile
+        constexpr int HW = BN / 2;          // columns per epilogue warp
         int as = 0;
         uint32_t aphase = 0;
         for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
             int pi, tm, tn;
-            if (!tile_coords(probs, np, t, pi, tm, tn)) continue;
+            if (!tile_coords<BN>(probs, np, t, pi, tm, tn)) continue;
             const TcProb& p = probs[pi];
-            mbar_wait(&tfull[as], aphase);
-            tc_fence_after();
             const int i = tm * BM + q * 32 + lane;  // row of C inside the problem
             const bool row_ok = i < p.m;
+            const bool f16 = p.exec_level == LV_F16;
             const long long rowoff = (long long)(p.c_r0 + (row_ok ? i : 0)) * c.ldw + p.c_c0;
-            const int lvl = p.exec_level;
+            Epi epi;
             // inverse solves carry W scaled by 2^e; undo it exactly here
-            const double alpha = p.a_kwrap ? double(c.wscale[p.b_r0]) : p.alpha;
-            // fused require_finite: track the first non-finite stored value
-            const bool chk = p.check_seq != 0;
-            unsigned long long bad = ~0ull;
-            const int iloc = p.c_r0 + i - p.chk_r0;
-            auto note = [&](bool isbad, int j) {
-                if (chk && isbad) {
-                    const unsigned long long k = fail_key(p.check_seq, elem_local(iloc, p.c_c0 + j - p.chk_c0));
-                    bad = k < bad ? k : bad;
-                }
+            epi.alpha = p.a_kwrap ? double(c.wscale[p.b_r0]) : p.alpha;
+            epi.beta = p.beta;
+            epi.fast = pow2_or_one(epi.alpha) && (p.beta == 0.0 || p.beta == 1.0);
+            epi.af = float(epi.alpha);
+            const bool has_c = p.beta != 0.0;
+            // columns [jlo, jhi) of this row are written (bounds, lower mask)
+            const int jbase = tn * BN + half * HW;
+            int jhi = min(p.n, jbase + HW);
+            if (p.lower) jhi = min(jhi, (p.c_r0 + i) - p.c_c0 + 1);
+            const int nch = row_ok && jhi > jbase ? (jhi - jbase + 31) >> 5 : 0;  // live chunks
+            auto cptr = [&](int j0) -> const void* {
+                return f16 ? static_cast<const void*>(c.b16 + rowoff + j0) : static_cast<const void*>(c.b32 + rowoff + j0);
             };
-            for (int cc = 0; cc < BN; cc += 32) {
+            auto full_chunk = [&](int j0) {
+                return j0 + 32 <= jhi && ((reinterpret_cast<uintptr_t>(cptr(j0)) & 15) == 0);
+            };
+            // C of the first chunk does not depend on the accumulator: load it
+            // before waiting for the MMA
+            CChunk cur, nxt;
+            if (has_c && nch > 0 && full_chunk(jbase)) load_chunk(cur, cptr(jbase), f16);
+            mbar_wait(&tfull[as], aphase);
+            tc_fence_after();
+            uint32_t anybad = 0;
+            int badj = -1;
+            for (int cc = 0; cc < HW; cc += 32) {
                 float v[32];
                 __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge first
-                tmem_ld32(tmem + (uint32_t(q * 32) << 16) + uint32_t(as * BN + cc), v);
-                if (cc == BN - 32) {
+                tmem_ld32(tmem + (uint32_t(q * 32) << 16) + uint32_t(as * BN + half * HW + cc), v);
+                if (cc == HW - 32) {
                     // accumulator drained: hand it back to the MMA warp
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&tempty[as]);
                 }
-                const int j0 = tn * BN + cc;
-                if (!row_ok || j0 >= p.n) continue;
-                // columns allowed in this chunk: bounds and the lower mask
-                int jmax = min(32, p.n - j0);
-                if (p.lower) jmax = min(jmax, (p.c_r0 + i) - (p.c_c0 + j0) + 1);
-                if (jmax <= 0) continue;
-                if (lvl == LV_F16) {
-                    __half* C = c.b16 + rowoff + j0;
-                    const bool vec = jmax == 32 && ((reinterpret_cast<uintptr_t>(C) & 15) == 0);
-                    if (vec) {
+                const int ch = cc >> 5;
+                if (ch >= nch) continue;
+                const int j0 = jbase + cc;
+                if (has_c && ch + 1 < nch && full_chunk(j0 + 32)) load_chunk(nxt, cptr(j0 + 32), f16);
+                uint32_t bad = 0;
+                if (full_chunk(j0)) {
+                    if (f16) {
+                        uint4* C = reinterpret_cast<uint4*>(c.b16 + rowoff + j0);
 #pragma unroll
                         for (int g = 0; g < 4; ++g) {
-                            uint4 raw = p.beta != 0.0 ? *reinterpret_cast<const uint4*>(C + 8 * g) : make_uint4(0, 0, 0, 0);
-                            __half2* h = reinterpret_cast<__half2*>(&raw);
+                            uint4 raw = has_c ? cur.r[g] : make_uint4(0, 0, 0, 0);
+                            uint32_t* w = reinterpret_cast<uint32_t*>(&raw);
 #pragma unroll
                             for (int e = 0; e < 4; ++e) {
-                                const float2 cf = __half22float2(h[e]);
-                                const __half o0 = f2h(epi_f(v[8 * g + 2 * e], cf.x, alpha, p.beta));
-                                const __half o1 = f2h(epi_f(v[8 * g + 2 * e + 1], cf.y, alpha, p.beta));
-                                note(h_bad(o0), j0 + 8 * g + 2 * e);
-                                note(h_bad(o1), j0 + 8 * g + 2 * e + 1);
-                                h[e] = __halves2half2(o0, o1);
+                                const float2 cf = __half22float2(*reinterpret_cast<__half2*>(&w[e]));
+                                const __half2 o = __floats2half2_rn(epi(v[8 * g + 2 * e], cf.x),
+                                                                    epi(v[8 * g + 2 * e + 1], cf.y));
+                                w[e] = *reinterpret_cast<const uint32_t*>(&o);
+                                bad |= ((w[e] & 0x7c00u) == 0x7c00u) | ((w[e] & 0x7c000000u) == 0x7c000000u);
                             }
-                            *reinterpret_cast<uint4*>(C + 8 * g) = raw;
+                            C[g] = raw;
                         }
                     } else {
-#pragma unroll
-                        for (int e = 0; e < 32; ++e)
-                            if (e < jmax) {
-                                const float cv = p.beta != 0.0 ? __half2float(C[e]) : 0.f;
-                                const __half o = f2h(epi_f(v[e], cv, alpha, p.beta));
-                                note(h_bad(o), j0 + e);
-                                C[e] = o;
-                            }
-                    }
-                } else {
-                    float* C = c.b32 + rowoff + j0;
-                    const bool vec = jmax == 32 && ((reinterpret_cast<uintptr_t>(C) & 15) == 0);
-                    if (vec) {
+                        float4* C = reinterpret_cast<float4*>(c.b32 + rowoff + j0);
 #pragma unroll
                         for (int g = 0; g < 8; ++g) {
-                            float4 cv = p.beta != 0.0 ? *reinterpret_cast<const float4*>(C + 4 * g) : make_float4(0, 0, 0, 0);
-                            cv.x = epi_f(v[4 * g + 0], cv.x, alpha, p.beta);
-                            cv.y = epi_f(v[4 * g + 1], cv.y, alpha, p.beta);
-                            cv.z = epi_f(v[4 * g + 2], cv.z, alpha, p.beta);
-                            cv.w = epi_f(v[4 * g + 3], cv.w, alpha, p.beta);
-                            note(!isfinite(cv.x), j0 + 4 * g);
-                            note(!isfinite(cv.y), j0 + 4 * g + 1);
-                            note(!isfinite(cv.z), j0 + 4 * g + 2);
-                            note(!isfinite(cv.w), j0 + 4 * g + 3);
-                            *reinterpret_cast<float4*>(C + 4 * g) = cv;
+                            float4 cv = has_c ? *reinterpret_cast<const float4*>(&cur.r[g]) : make_float4(0, 0, 0, 0);
+                            cv.x = epi(v[4 * g + 0], cv.x);
+                            cv.y = epi(v[4 * g + 1], cv.y);
+                            cv.z = epi(v[4 * g + 2], cv.z);
+                            cv.w = epi(v[4 * g + 3], cv.w);
+                            bad |= ((__float_as_uint(cv.x) & 0x7f800000u) == 0x7f800000u) |
+                                   ((__float_as_uint(cv.y) & 0x7f800000u) == 0x7f800000u) |
+                                   ((__float_as_uint(cv.z) & 0x7f800000u) == 0x7f800000u) |
+                                   ((__float_as_uint(cv.w) & 0x7f800000u) == 0x7f800000u);
+                            C[g] = cv;
                         }
-                    } else {
+                    }
+                } else {
+                    // ragged / unaligned chunk: element by element
+                    const int jm = min(32, jhi - j0);
 #pragma unroll
-                        for (int e = 0; e < 32; ++e)
-                            if (e < jmax) {
-                                const float cv = p.beta != 0.0 ? C[e] : 0.f;
-                                const float o = epi_f(v[e], cv, alpha, p.beta);
-                                note(!isfinite(o), j0 + e);
-                                C[e] = o;
+                    for (int e = 0; e < 32; ++e)
+                        if (e < jm) {
+                            if (f16) {
+                                __half* C = c.b16 + rowoff + j0 + e;
+                                const __half o = f2h(epi(v[e], has_c ? __half2float(*C) : 0.f));
+                                bad |= h_bad(o);
+                                *C = o;
+                            } else {
+                                float* C = c.b32 + rowoff + j0 + e;
+                                const float o = epi(v[e], has_c ? *C : 0.f);
+                                bad |= !isfinite(o);
+                                *C = o;
                             }
+                        }
+                }
+                if (bad && badj < 0) {
+                    // locate the first non-finite value of this chunk (rare path)
+                    const int jm = min(32, jhi - j0);
+                    for (int e = 0; e < jm && badj < 0; ++e) {
+                        const bool b = f16 ? h_bad(c.b16[rowoff + j0 + e]) : !isfinite(c.b32[rowoff + j0 + e]);
+                        if (b) badj = j0 + e;
                     }
                 }
+                anybad |= bad;
+                cur = nxt;
             }
-            __syncwarp();
-            if (chk) warp_report_min(c, bad);
+            if (p.check_seq != 0) {
+                // fused require_finite: first bad element in column-major order
+                unsigned long long key = ~0ull;
+                if (badj >= 0)
+                    key = fail_key(p.check_seq, elem_local(p.c_r0 + i - p.chk_r0, p.c_c0 + badj - p.chk_c0));
+                __syncwarp();
+                warp_report_min(c, key);
+            }
+            (void)anybad;
             if (++as == 2) {
                 as = 0;
                 aphase ^= 1;
@@ -376,7 +542,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gemm_tc(DevCtx c, const TcProb*
 
     tc_fence_before();
     __syncthreads();
-    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(G::TMEM_COLS));
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
@@ -392,20 +559,22 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
-bool make_map(CUtensorMap* m, const __half* base, long long ldw, int rows_end, int cols_end, int box_rows,
+// 2-D map over a row-major buffer, k-block wide (one 128-byte row) boxes
+bool make_map(CUtensorMap* m, const void* base, bool f32, long long ldw, int rows_end, int cols_end, int box_rows,
               std::string* err) {
     auto enc = get_encode();
     if (!enc) {
         if (err) *err = "cuTensorMapEncodeTiled unavailable";
         return false;
     }
+    const int esz = f32 ? 4 : 2;
     cuuint64_t dims[2] = {cuuint64_t(cols_end), cuuint64_t(rows_end)};
-    cuuint64_t strides[1] = {cuuint64_t(ldw) * 2};
-    cuuint32_t box[2] = {cuuint32_t(BK), cuuint32_t(box_rows)};
+    cuuint64_t strides[1] = {cuuint64_t(ldw) * esz};
+    cuuint32_t box[2] = {cuuint32_t(128 / esz), cuuint32_t(box_rows)};
     cuuint32_t estr[2] = {1, 1};
-    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half*>(base), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult r = enc(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
+                     const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
         if (err) *err = "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")";
         return false;
@@ -423,19 +592,23 @@ bool tc_supported() {
     return major == 10 && minor == 0 && get_encode() != nullptr;
 }
 
-int tc_build_probs(const DevCtx& c, const std::vector<DevProb>& probs, std::vector<unsigned char>& out,
+int tc_build_probs(const DevCtx& c, int kind, const std::vector<DevProb>& probs, std::vector<unsigned char>& out,
                    std::string* err) {
     out.assign(probs.size() * sizeof(TcProb), 0);
     TcProb* tp = reinterpret_cast<TcProb*>(out.data());
+    const bool f32 = kind == KIND_TF32X3;
+    const int BN = f32 ? Cfg<KIND_TF32X3>::BN : Cfg<KIND_F16>::BN;
+    const void* obuf = f32 ? static_cast<const void*>(c.b32) : static_cast<const void*>(c.b16);
     int tiles = 0;
     for (size_t i = 0; i < probs.size(); ++i) {
         const DevProb& d = probs[i];
         TcProb& p = tp[i];
         // A extent ends at the problem's K edge (an inverse solve's A is the
         // n-wide leaf column block read twice: its extent is n, period a_kwrap)
-        if (!make_map(&p.ta, c.b16, c.ldw, d.a_r0 + d.m, d.a_c0 + (d.a_kwrap ? d.n : d.k), BM, err)) return -1;
+        if (!make_map(&p.ta, obuf, f32, c.ldw, d.a_r0 + d.m, d.a_c0 + (d.a_kwrap ? d.n : d.k), BM, err)) return -1;
         const bool w = d.b_buf == BUF_W16;
-        if (!make_map(&p.tb, w ? c.w16 : c.b16, w ? kW16Ld : c.ldw, d.b_r0 + d.n, d.b_c0 + d.k, BN, err))
+        if (!make_map(&p.tb, w ? static_cast<const void*>(c.w16) : obuf, f32 && !w, w ? kW16Ld : c.ldw, d.b_r0 + d.n,
+                      d.b_c0 + d.k, BN, err))
             return -1;
         p.a_kwrap = d.a_kwrap;
         p.check_seq = d.check_seq;
@@ -467,13 +640,20 @@ void init_tc_attributes() {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaFuncSetAttribute(k_gemm_tc<KIND_F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo<KIND_F16>::SMEM_BYTES);
+    cudaFuncSetAttribute(k_gemm_tc<KIND_TF32X3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Geo<KIND_TF32X3>::SMEM_BYTES);
 }
 
-void launch_gemm_tc(const DevCtx& c, const void* d_probs, int nprob, int tiles, cudaStream_t s) {
+void launch_gemm_tc(const DevCtx& c, int kind, const void* d_probs, int nprob, int tiles, cudaStream_t s) {
     if (tiles <= 0) return;
     const int grid = tiles < g_sms ? tiles : g_sms;
-    k_gemm_tc<<<grid, NTHREADS, SMEM_BYTES, s>>>(c, static_cast<const TcProb*>(d_probs), nprob, tiles);
+    const TcProb* p = static_cast<const TcProb*>(d_probs);
+    if (kind == KIND_TF32X3)
+        k_gemm_tc<KIND_TF32X3><<<grid, Cfg<KIND_TF32X3>::NTHREADS, Geo<KIND_TF32X3>::SMEM_BYTES, s>>>(c, p, nprob,
+                                                                                                    tiles);
+    else
+        k_gemm_tc<KIND_F16><<<grid, Cfg<KIND_F16>::NTHREADS, Geo<KIND_F16>::SMEM_BYTES, s>>>(c, p, nprob, tiles);
 }
 
 }  // namespace tcb

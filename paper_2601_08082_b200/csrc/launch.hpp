@@ -57,9 +57,11 @@ void launch_gemm_simt(const DevCtx& c, int gclass, const DevProb* d_probs, int n
 struct TcProb;  // defined in k_gemm_tc.cu (holds TMA descriptors)
 size_t tc_prob_size();
 // fills host-side TcProb records (tensor maps over the F16 buffer)
-int tc_build_probs(const DevCtx& c, const std::vector<DevProb>& probs, std::vector<unsigned char>& out,
+// operand kinds of the tensor-core GEMM (k_gemm_tc.cu)
+enum { KIND_F16 = 0, KIND_TF32X3 = 1 };
+int tc_build_probs(const DevCtx& c, int kind, const std::vector<DevProb>& probs, std::vector<unsigned char>& out,
                    std::string* err);
-void launch_gemm_tc(const DevCtx& c, const void* d_probs, int nprob, int tiles, cudaStream_t s);
+void launch_gemm_tc(const DevCtx& c, int kind, const void* d_probs, int nprob, int tiles, cudaStream_t s);
 bool tc_supported();
 
 // standalone block operations on column-major doubles (k_blockops.cu)

@@ -67,7 +67,12 @@ int Plan::gemm_class(int op_level, int exec_level, const GemmProb* g) const {
         const bool aligned = !g || (g->a_c0 % 8 == 0 && g->b_c0 % 8 == 0 && g->k % 8 == 0);
         return (opt.use_tc && aligned) ? GC_TC16 : GC_SIMT_F16;
     }
-    if (op_level == LV_F32) return exec_level == LV_F64 ? GC_SIMT_F32D : GC_SIMT_F32;
+    if (op_level == LV_F32) {
+        if (exec_level == LV_F64) return GC_SIMT_F32D;
+        // TMA: 16-byte aligned rows (column offsets multiples of 4 floats)
+        const bool aligned = !g || (g->a_c0 % 4 == 0 && g->b_c0 % 4 == 0 && g->k % 4 == 0);
+        return (opt.use_tc && opt.use_tc32 && aligned) ? GC_TC32 : GC_SIMT_F32;
+    }
     return GC_SIMT_F64;
 }
 

@@ -99,6 +99,7 @@ enum GemmClass : int {
     GC_SIMT_F16D = 3, // FP16 operands, FP64 accumulate (F64 exec)
     GC_SIMT_F32D = 4, // FP32 operands, FP64 accumulate
     GC_SIMT_F64 = 5,  // FP64 operands, FP64 accumulate
+    GC_TC32 = 6,      // FP32 operands, three-pass TF32 split on tcgen05, FP32 accumulate (exec F32)
 };
 
 struct Access {
@@ -146,6 +147,7 @@ struct FlopRec {
 
 struct PlanOptions {
     bool use_tc = true;      // FP16-operand GEMMs on tcgen05
+    bool use_tc32 = true;    // FP32 x FP32 GEMMs on tcgen05 (three-pass TF32)
     bool inverse_trsm = true; // FP16 leaf solves with m >= kInvMinRows as tcgen05 GEMMs
     bool fuse_checks = true;  // require_finite inside the producing kernels
 };
