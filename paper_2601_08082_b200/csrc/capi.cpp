@@ -479,6 +479,13 @@ int tc_solve_residual_device(int n, const double* dA, int lda, const double* dX,
 namespace tcb {
 void leaf_debug_clocks(long long* out, bool reset);
 }
+namespace tcb {
+void potrf_debug_clocks(long long* out, bool reset);
+}
+extern "C" int tc_debug_potrf_clocks(long long* out8, int reset) {
+    tcb::potrf_debug_clocks(out8, reset != 0);
+    return TC_OK;
+}
 extern "C" int tc_debug_leaf_clocks(long long* out4, int reset) {
     tcb::leaf_debug_clocks(out4, reset != 0);
     return TC_OK;

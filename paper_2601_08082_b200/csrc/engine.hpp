@@ -68,6 +68,7 @@ class Engine {
     void* d_bufs_ = nullptr;
     unsigned long long* d_words_ = nullptr;  // status + alpha slots
     void* d_w16_ = nullptr;                  // leaf inverses + scales
+    void* d_w32_ = nullptr;                  // FP32 leaf inverses
     unsigned char* d_arena_ = nullptr;
     std::vector<OpLaunch> launch_;
     std::vector<cudaStream_t> streams_;

@@ -606,10 +606,12 @@ int tc_build_probs(const DevCtx& c, int kind, const std::vector<DevProb>& probs,
         // A extent ends at the problem's K edge (an inverse solve's A is the
         // n-wide leaf column block read twice: its extent is n, period a_kwrap)
         if (!make_map(&p.ta, obuf, f32, c.ldw, d.a_r0 + d.m, d.a_c0 + (d.a_kwrap ? d.n : d.k), BM, err)) return -1;
-        const bool w = d.b_buf == BUF_W16;
-        if (!make_map(&p.tb, w ? static_cast<const void*>(c.w16) : obuf, f32 && !w, w ? kW16Ld : c.ldw, d.b_r0 + d.n,
-                      d.b_c0 + d.k, BN, err))
-            return -1;
+        const void* bbuf = d.b_buf == BUF_W16 ? static_cast<const void*>(c.w16)
+                           : d.b_buf == BUF_W32 ? static_cast<const void*>(c.w32)
+                                                : obuf;
+        const long long bld = d.b_buf == BUF_W16 ? kW16Ld : d.b_buf == BUF_W32 ? kW32Ld : c.ldw;
+        const bool bf32 = d.b_buf == BUF_W32 || (f32 && d.b_buf != BUF_W16);
+        if (!make_map(&p.tb, bbuf, bf32, bld, d.b_r0 + d.n, d.b_c0 + d.k, BN, err)) return -1;
         p.a_kwrap = d.a_kwrap;
         p.check_seq = d.check_seq;
         p.chk_r0 = d.chk_r0;

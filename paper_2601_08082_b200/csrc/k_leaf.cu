@@ -452,6 +452,8 @@ void init_trsm_attributes();
 void init_leaf_attributes() {
     const int cap = 227 * 1024;
     init_leaf_cm_attributes();
+    init_potrf_v2_attributes();
+    init_inv2_attributes();
     init_trsm_attributes();
     cudaFuncSetAttribute(k_leaf_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
     cudaFuncSetAttribute(k_potrf_leaf<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
@@ -465,6 +467,7 @@ void init_leaf_attributes() {
 constexpr size_t kLeafSmemCap = 220 * 1024;
 
 void launch_potrf_leaf(const DevCtx& c, int lv, int r0, int n, uint32_t seq, uint32_t chk, cudaStream_t s) {
+    if (potrf_v2_ok(lv, n)) return launch_potrf_v2(c, lv, r0, n, seq, chk, s);
     if (leaf_cm_ok(lv, n)) return launch_potrf_cm(c, lv, r0, n, seq, chk, s);
     const bool d = lv == LV_F64;
     const bool fits = (d ? potrf_smem<double>(n, true) : potrf_smem<float>(n, true)) <= kLeafSmemCap;

@@ -28,6 +28,9 @@ void launch_quant(const DevCtx& c, int lv, int r0, int c0, int m, int n, int slo
 void launch_dequant(const DevCtx& c, int lv, int r0, int c0, int m, int n, int slot, uint32_t chk_seq,
                     cudaStream_t s);
 
+// spin until *host_flag (mapped pinned memory) becomes non-zero (profiling)
+void launch_gate(volatile int* host_flag, cudaStream_t s);
+
 // spd_generate symmetrization of raw draws (k_elementwise.cu)
 void launch_symmetrize(double* a, long long lda, int n, cudaStream_t s);
 
@@ -46,6 +49,14 @@ void launch_potrf_cm(const DevCtx& c, int lv, int r0, int n, uint32_t seq, uint3
 void launch_trsm_cm(const DevCtx& c, int lv, int br0, int bc0, int m, int n, int lr0, uint32_t seq,
                     uint32_t chk_seq, int chk_r0, int chk_c0, cudaStream_t s);
 void launch_leaf_inverse(const DevCtx& c, int r0, int n, uint32_t seq, cudaStream_t s);
+// leaf inverse W = inv(L), n % 32 == 0, n <= 256: mode 0 -> W16 pair, 1 -> W32 (k_inverse.cu)
+bool inv2_ok(int n);
+void init_inv2_attributes();
+void launch_leaf_inv2(const DevCtx& c, int mode, int r0, int n, uint32_t seq, cudaStream_t s);
+// 512-thread F16/F32 leaf POTRF, n % 32 == 0, n <= 256 (k_potrf.cu)
+bool potrf_v2_ok(int lv, int n);
+void init_potrf_v2_attributes();
+void launch_potrf_v2(const DevCtx& c, int lv, int r0, int n, uint32_t seq, uint32_t chk, cudaStream_t s);
 
 // grouped GEMM (k_gemm_simt.cu / k_gemm_tc.cu)
 // problems must already be in device memory with tile0 / tiles_n filled by

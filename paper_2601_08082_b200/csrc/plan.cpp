@@ -128,13 +128,18 @@ void Plan::emit_trsm(Rect B, int p, int lnode) {
         // large FP16 leaf solve on the tensor cores: X = rn16(B (W_hi + W_lo)^T)
         // with W = inv(rn16(L)) from the leaf's inverse op.  Rows are
         // independent, so the tile owning a row block reads and overwrites it.
-        const bool inv = opt.use_tc && opt.inverse_trsm && p == LV_F16 && L.leaf && L.n <= kW16Lo &&
-                         B.m >= kInvMinRows && B.c0 % 8 == 0 && L.r0 % 8 == 0;
-        if (inv) {
+        // (F16: X = rn16(B (W_hi + W_lo)^T), W = inv(rn16(L)) as an FP16 pair;
+        //  F32: X = rn32(B W^T) on the three-pass TF32 kernel, W = inv(L))
+        const bool inv16 = opt.use_tc && opt.inverse_trsm && p == LV_F16 && L.leaf && L.n <= kW16Lo &&
+                           B.m >= kInvMinRows && B.c0 % 8 == 0 && L.r0 % 8 == 0;
+        const bool inv32 = opt.use_tc && opt.use_tc32 && opt.inverse_trsm && p == LV_F32 && L.leaf &&
+                           L.n <= kW32Ld && L.n % 32 == 0 && B.c0 % 4 == 0 && L.r0 % 4 == 0;
+        if (inv16 || inv32) {
             const int lb = nodes[lnode].block;
-            if (!has_inverse[lb]) {
-                has_inverse[lb] = 1;
-                needs_w16 = true;
+            const uint8_t bit = inv16 ? 1 : 2;
+            if (!(has_inverse[lb] & bit)) {
+                has_inverse[lb] |= bit;
+                (inv16 ? needs_w16 : needs_w32) = true;
                 Op iv;
                 iv.type = OP_INVERSE;
                 iv.level = p;
@@ -145,13 +150,13 @@ void Plan::emit_trsm(Rect B, int p, int lnode) {
             GemmProb g;
             g.m = B.m;
             g.n = L.n;
-            g.k = 2 * kW16Lo;
+            g.k = inv16 ? 2 * kW16Lo : L.n;
             g.a_r0 = B.r0;
             g.a_c0 = B.c0;
-            g.a_kwrap = kW16Lo;
+            g.a_kwrap = inv16 ? kW16Lo : 0;
             g.b_r0 = L.r0;
             g.b_c0 = 0;
-            g.b_buf = BUF_W16;
+            g.b_buf = inv16 ? BUF_W16 : BUF_W32;
             g.c_r0 = B.r0;
             g.c_c0 = B.c0;
             g.exec_level = p;
@@ -162,7 +167,7 @@ void Plan::emit_trsm(Rect B, int p, int lnode) {
             Op op;
             op.type = OP_GEMM;
             op.level = p;
-            op.gclass = GC_TC16;
+            op.gclass = inv16 ? GC_TC16 : GC_TC32;
             op.prob_begin = int(probs.size());
             probs.push_back(g);
             op.prob_end = int(probs.size());
@@ -459,7 +464,8 @@ void Plan::finalize_accesses() {
                 break;
             case OP_INVERSE:
                 op.acc.push_back({op.level, op.rect, false});
-                op.acc.push_back({BUF_W16, {op.rect.r0, 0, op.rect.m, kW16Ld}, true});
+                if (op.level == LV_F16) op.acc.push_back({BUF_W16, {op.rect.r0, 0, op.rect.m, kW16Ld}, true});
+                else op.acc.push_back({BUF_W32, {op.rect.r0, 0, op.rect.m, kW32Ld}, true});
                 break;
             case OP_TRSM:
                 op.acc.push_back({op.level, op.rect, true});

@@ -22,13 +22,17 @@
 namespace tcb {
 
 enum Level : int { LV_F16 = 0, LV_F32 = 1, LV_F64 = 2 };
-enum Buf : int { BUF_F16 = 0, BUF_F32 = 1, BUF_F64 = 2, BUF_USER = 3, BUF_ALPHA = 4, BUF_W16 = 5, BUF_COUNT = 6 };
+enum Buf : int { BUF_F16 = 0, BUF_F32 = 1, BUF_F64 = 2, BUF_USER = 3, BUF_ALPHA = 4, BUF_W16 = 5, BUF_W32 = 6,
+                 BUF_COUNT = 7 };
 
 // inverse-based FP16 leaf solves: W = inv(rn16(L_leaf)) as an FP16 hi/lo pair
 // in the W16 workspace (row r0+j of a leaf at columns [0,n) hi, [256, 256+n) lo)
 constexpr int kW16Ld = 512;
 constexpr int kW16Lo = 256;
-constexpr int kInvMinRows = 512;  // below this the substitution kernel is used
+constexpr int kInvMinRows = 512;  // below this the substitution kernel is used (F16)
+// FP32 leaf inverses W = inv(L) (row r0+i of a leaf, columns [0, n)), for
+// inverse-based FP32 leaf solves on the three-pass TF32 tensor-core GEMM
+constexpr int kW32Ld = 256;
 enum RefKernel : int { K_POTRF = 0, K_TRSM = 1, K_SYRK = 2, K_GEMM = 3 };
 
 struct Rect {
@@ -168,6 +172,7 @@ struct Plan {
     uint32_t n_seq = 0;
     bool needs_buf[3] = {false, false, false};
     bool needs_w16 = false;
+    bool needs_w32 = false;
 
     // build + plan (throws std::invalid_argument on bad input)
     static Plan make(int n, int b, const std::vector<int>& levels, bool quantize,
@@ -185,7 +190,7 @@ struct Plan {
 
    private:
     std::vector<std::vector<uint8_t>> has_shadow;  // [block][level]
-    std::vector<uint8_t> has_inverse;              // [block] W16 ready
+    std::vector<uint8_t> has_inverse;              // [block] bit 0: W16 ready, bit 1: W32 ready
     int build_node(int r0, int n, int depth);
     void emit_potrf(int node);
     void emit_trsm(Rect brect, int p, int lnode);
