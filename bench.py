@@ -272,8 +272,10 @@ def run_ours(args):
             t = torch.tensor([e2e_s], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_s = float(t.item())
-        h2d = n * n * 8
-        d2h = sum((n - j0) * min(256, n - j0) for j0 in range(0, n, 256)) * 8
+        # lower triangle in leaf-column strips (the diagonal leaf squares whole),
+        # both directions (Engine::enqueue_host)
+        h2d = sum((n - j0) * min(b, n - j0) for j0 in range(0, n, b)) * 8
+        d2h = h2d
         e2e = {"value": ws * args.e2e_steps * flops / e2e_s / 1e12, "unit": "TFLOP/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
                "note": "each step re-factors the previous step's in-place output (SPD lower triangle)"}

@@ -99,8 +99,11 @@ int tc_plan_set_option(tc_plan* plan, const char* key, int value);
  * info == NULL it only enqueues (read the outcome with tc_plan_status). */
 int tc_potrf_device(tc_plan* plan, const double* dA_in, int lda_in, double* dL_out,
                     int lda_out, void* stream, tc_info* info);
-/* Host buffers: H2D copy, device factorization, D2H of the lower triangle,
- * in place on A (exactly the reference's TileView contract). */
+/* Host buffers, in place on A (the reference's TileView contract): the lower
+ * triangle is copied to the device in leaf-column strips, factored, and every
+ * block is copied back as soon as it is final, so the copies overlap the
+ * factorization (one captured graph per (A, lda) when A is pinned).  The
+ * strict upper triangle is returned bit-for-bit unchanged. */
 int tc_potrf_host(tc_plan* plan, double* A, int lda, tc_info* info);
 /* Serialized, eagerly launched run with a CUDA event after every op:
  * op_ms[i] = device time of op i (cap entries).  For roofline accounting. */

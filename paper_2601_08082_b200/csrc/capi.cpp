@@ -23,10 +23,6 @@ struct tc_plan {
     std::unique_ptr<Engine> eng;
     Failure last;
     bool have_result = false;
-    double* d_host_stage = nullptr;  // device copy used by tc_potrf_host
-    ~tc_plan() {
-        if (d_host_stage) cudaFree(d_host_stage);
-    }
 };
 
 namespace {
@@ -293,29 +289,14 @@ int tc_potrf_host(tc_plan* plan, double* A, int lda, tc_info* info) {
     const int n = plan->eng->plan.n;
     if (lda < n) return fail(TC_INVALID_ARGUMENT, "leading dimension < n");
     if (!tc_device_available()) return fail(TC_NO_DEVICE, "no CUDA device (there is no CPU fallback)");
-    cudaError_t e;
-    if (!plan->d_host_stage) {
-        e = cudaMalloc(&plan->d_host_stage, sizeof(double) * size_t(n) * size_t(n));
-        if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
-    }
-    cudaStream_t s = nullptr;
-    e = cudaMemcpy2DAsync(plan->d_host_stage, sizeof(double) * size_t(n), A, sizeof(double) * size_t(lda),
-                          sizeof(double) * size_t(n), size_t(n), cudaMemcpyHostToDevice, s);
-    if (e != cudaSuccess) return cuda_fail(e, "H2D");
+    std::string err;
+    plan->have_result = false;
+    // copies of the caller's lower triangle overlap the factorization
+    // (Engine::enqueue_host); the strict upper triangle comes back bit-for-bit
+    // unchanged (only the diagonal leaf squares carry upper elements along)
+    if (!plan->eng->enqueue_host(A, lda, nullptr, &err)) return fail(TC_CUDA_ERROR, err);
     tc_info local;
-    int st = tc_potrf_device(plan, plan->d_host_stage, n, plan->d_host_stage, n, s, &local);
-    if (st == TC_CUDA_ERROR || st == TC_NO_DEVICE || st == TC_INVALID_ARGUMENT) return st;
-    // lower triangle back (upper columns untouched on both sides)
-    for (int j0 = 0; j0 < n; j0 += 256) {
-        const int w = std::min(256, n - j0);
-        // rows j0..n-1 of columns j0..j0+w-1: a trapezoid covering the lower part
-        e = cudaMemcpy2DAsync(A + size_t(j0) * lda + j0, sizeof(double) * size_t(lda),
-                              plan->d_host_stage + size_t(j0) * n + j0, sizeof(double) * size_t(n),
-                              sizeof(double) * size_t(n - j0), size_t(w), cudaMemcpyDeviceToHost, s);
-        if (e != cudaSuccess) return cuda_fail(e, "D2H");
-    }
-    e = cudaStreamSynchronize(s);
-    if (e != cudaSuccess) return cuda_fail(e, "sync");
+    const int st = tc_plan_status(plan, &local);
     if (info) *info = local;
     return st;
 }

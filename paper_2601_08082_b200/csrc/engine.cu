@@ -28,6 +28,13 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 Engine::~Engine() {
     if (gexec_) cudaGraphExecDestroy(gexec_);
     if (graph_) cudaGraphDestroy(graph_);
+    if (hexec_) cudaGraphExecDestroy(hexec_);
+    if (hgraph_) cudaGraphDestroy(hgraph_);
+    for (auto e : ev_h2d_) cudaEventDestroy(e);
+    for (auto e : ev_d2h_) cudaEventDestroy(e);
+    if (cs_h2d_) cudaStreamDestroy(cs_h2d_);
+    if (cs_d2h_) cudaStreamDestroy(cs_d2h_);
+    if (d_stage_) cudaFree(d_stage_);
     for (auto e : events_) cudaEventDestroy(e);
     if (fork_) cudaEventDestroy(fork_);
     for (auto s : streams_) cudaStreamDestroy(s);
@@ -200,9 +207,14 @@ void Engine::reset_words(cudaStream_t s) {
 }
 
 // enqueue every op on the stream pool (works eagerly or under capture)
-bool Engine::enqueue_ops(cudaStream_t origin, std::string* err) {
+bool Engine::enqueue_ops(cudaStream_t origin, std::string* err, const HostIO* io) {
     const int N = int(plan.ops.size());
-    const int S = std::max(1, n_streams);
+    // compute streams 0..C-1, then one stream for the imports and one for the
+    // exports: a transfer-side op never sits in front of unrelated compute
+    // (in-order streams would otherwise turn a wait for the caller's data
+    // into a wait for everything queued behind it)
+    const int C = std::max(1, n_streams);
+    const int S = C + 2, SI = C, SE = C + 1;
     if (int(streams_.size()) < S) {
         for (int s = int(streams_.size()); s < S; ++s) {
             cudaStream_t st;
@@ -218,30 +230,30 @@ bool Engine::enqueue_ops(cudaStream_t origin, std::string* err) {
         }
     }
     if (!fork_) TC_TRY(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming));
-    // stream assignment: continue a dep's stream when that dep is its tail
+    // stream assignment: continue a dep's compute stream when that dep is its tail
     std::vector<int> sid(N, 0), tail(S, -1), last_use(S, -1);
     std::vector<char> need_ev(N, 0);
     std::vector<std::vector<int>> waits(N);
     for (int i = 0; i < N; ++i) {
-        int pick = -1;
-        for (int d : plan.ops[i].deps)
-            if (tail[sid[d]] == d) {
-                pick = sid[d];
-                break;
-            }
+        const OpType ty = plan.ops[i].type;
+        int pick = ty == OP_IMPORT ? SI : ty == OP_EXPORT ? SE : -1;
+        if (pick < 0) {
+            for (int d : plan.ops[i].deps)
+                if (sid[d] < C && tail[sid[d]] == d) {
+                    pick = sid[d];
+                    break;
+                }
+        }
         if (pick < 0) {
             pick = 0;
-            for (int s = 1; s < S; ++s)
+            for (int s = 1; s < C; ++s)
                 if (last_use[s] < last_use[pick]) pick = s;
         }
         sid[i] = pick;
         for (int d : plan.ops[i].deps)
-            if (sid[d] != pick || tail[pick] != d) {
-                // same-stream deps are ordered already unless another op intervened (still ordered)
-                if (sid[d] != pick) {
-                    waits[i].push_back(d);
-                    need_ev[d] = 1;
-                }
+            if (sid[d] != pick) {  // same-stream deps are ordered already
+                waits[i].push_back(d);
+                need_ev[d] = 1;
             }
         tail[pick] = i;
         last_use[pick] = i;
@@ -249,15 +261,50 @@ bool Engine::enqueue_ops(cudaStream_t origin, std::string* err) {
     reset_words(origin);
     TC_TRY(cudaEventRecord(fork_, origin));
     for (int s = 0; s < S; ++s) TC_TRY(cudaStreamWaitEvent(streams_[s], fork_, 0));
+    const int n = plan.n;
+    const size_t esz = sizeof(double);
+    if (io) {
+        // H2D of every block in the order the recursion first needs them
+        // (the diagonal leaf squares whole, so their upper halves come back
+        // unchanged with the per-block D2H)
+        TC_TRY(cudaStreamWaitEvent(cs_h2d_, fork_, 0));
+        TC_TRY(cudaStreamWaitEvent(cs_d2h_, fork_, 0));
+        for (int b : plan.block_order) {
+            const Rect& r = plan.blocks[b].rect;
+            TC_TRY(cudaMemcpy2DAsync(d_stage_ + size_t(r.c0) * n + r.r0, esz * n, io->host + size_t(r.c0) * io->lda + r.r0,
+                                     esz * io->lda, esz * size_t(r.m), size_t(r.n), cudaMemcpyHostToDevice, cs_h2d_));
+            TC_TRY(cudaEventRecord(ev_h2d_[b], cs_h2d_));
+        }
+    }
+    int n_d2h = 0;
     for (int i = 0; i < N; ++i) {
         cudaStream_t st = streams_[sid[i]];
         for (int d : waits[i]) TC_TRY(cudaStreamWaitEvent(st, events_[d], 0));
+        const Op& op = plan.ops[i];
+        if (io && (op.type == OP_IMPORT || op.type == OP_QUANT))  // the caller's doubles have arrived
+            for (int b : op.blocks) TC_TRY(cudaStreamWaitEvent(st, ev_h2d_[b], 0));
         launch_op(i, st);
         if (need_ev[i]) TC_TRY(cudaEventRecord(events_[i], st));
+        if (io && op.type == OP_EXPORT) {
+            // this block is final: copy it back while the rest computes
+            cudaEvent_t e = ev_d2h_[n_d2h++];
+            TC_TRY(cudaEventRecord(e, st));
+            TC_TRY(cudaStreamWaitEvent(cs_d2h_, e, 0));
+            const Rect& r = op.rect;
+            TC_TRY(cudaMemcpy2DAsync(io->host + size_t(r.c0) * io->lda + r.r0, esz * io->lda,
+                                     d_stage_ + size_t(r.c0) * n + r.r0, esz * n, esz * size_t(r.m), size_t(r.n),
+                                     cudaMemcpyDeviceToHost, cs_d2h_));
+        }
     }
     for (int s = 0; s < S; ++s) {
         TC_TRY(cudaEventRecord(events_[N + s], streams_[s]));
         TC_TRY(cudaStreamWaitEvent(origin, events_[N + s], 0));
+    }
+    if (io) {
+        TC_TRY(cudaEventRecord(ev_d2h_[n_d2h], cs_d2h_));
+        TC_TRY(cudaStreamWaitEvent(origin, ev_d2h_[n_d2h], 0));
+        TC_TRY(cudaEventRecord(ev_d2h_[n_d2h + 1], cs_h2d_));
+        TC_TRY(cudaStreamWaitEvent(origin, ev_d2h_[n_d2h + 1], 0));
     }
     TC_TRY(cudaGetLastError());
     return true;
@@ -295,6 +342,64 @@ bool Engine::enqueue(const double* a_in, long long lda_in, double* l_out, long l
         TC_TRY(cudaGraphLaunch(gexec_, stream));
     } else {
         if (!enqueue_ops(stream, err)) return false;
+    }
+    last_stream_ = stream;
+    return true;
+}
+
+bool Engine::enqueue_host(double* host, long long lda, cudaStream_t stream, std::string* err) {
+    if (!prepare(err)) return false;
+    const int n = plan.n;
+    if (!d_stage_) {
+        TC_TRY(cudaMalloc(&d_stage_, sizeof(double) * size_t(n) * size_t(n)));
+        TC_TRY(cudaStreamCreateWithFlags(&cs_h2d_, cudaStreamNonBlocking));
+        TC_TRY(cudaStreamCreateWithFlags(&cs_d2h_, cudaStreamNonBlocking));
+        ev_h2d_.resize(plan.blocks.size());
+        for (auto& e : ev_h2d_) TC_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        int n_exp = 0;
+        for (const Op& op : plan.ops) n_exp += op.type == OP_EXPORT;
+        ev_d2h_.resize(size_t(n_exp) + 2);
+        for (auto& e : ev_d2h_) TC_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    static int ring = 0;
+    RunArgs* slot = h_ra_ + (ring++ % kRaRing);
+    slot->a_in = d_stage_;
+    slot->l_out = d_stage_;
+    slot->lda_in = n;
+    slot->lda_out = n;
+    TC_TRY(cudaMemcpyAsync(d_ra_, slot, sizeof(RunArgs), cudaMemcpyHostToDevice, stream));
+    HostIO io{host, lda};
+    cudaPointerAttributes pa{};
+    const bool pinned = cudaPointerGetAttributes(&pa, host) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    if (use_graph && pinned) {
+        if (!hexec_ || hkey_ != host || hkey_lda_ != lda) {
+            if (hexec_) cudaGraphExecDestroy(hexec_);
+            if (hgraph_) cudaGraphDestroy(hgraph_);
+            hexec_ = nullptr;
+            hgraph_ = nullptr;
+            cudaStream_t cap;
+            TC_TRY(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+            TC_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+            std::string e2;
+            const bool ok = enqueue_ops(cap, &e2, &io);
+            cudaGraph_t g = nullptr;
+            const cudaError_t ce = cudaStreamEndCapture(cap, &g);
+            cudaStreamDestroy(cap);
+            if (!ok) {
+                if (err) *err = e2;
+                if (g) cudaGraphDestroy(g);
+                return false;
+            }
+            TC_TRY(ce);
+            hgraph_ = g;
+            TC_TRY(cudaGraphInstantiate(&hexec_, hgraph_, 0));
+            hkey_ = host;
+            hkey_lda_ = lda;
+        }
+        TC_TRY(cudaGraphLaunch(hexec_, stream));
+    } else {
+        if (!enqueue_ops(stream, err, &io)) return false;
     }
     last_stream_ = stream;
     return true;

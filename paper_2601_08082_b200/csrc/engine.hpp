@@ -47,6 +47,12 @@ class Engine {
     // enqueue one factorization (import .. export) on `stream`
     bool enqueue(const double* a_in, long long lda_in, double* l_out, long long lda_out, cudaStream_t stream,
                  std::string* err);
+    // host buffers (the TileView contract): H2D of the lower triangle in
+    // leaf-column strips, the factorization on a device staging copy, and a
+    // D2H of every block as soon as it is exported -- copies overlap the
+    // compute.  Captured into its own graph per (host pointer, lda) when the
+    // buffer is pinned; eager otherwise.
+    bool enqueue_host(double* host, long long lda, cudaStream_t stream, std::string* err);
     // wait for the last enqueue and decode the status word
     bool result(Failure* f, std::string* err);
     // serialized eager run with an event after every op (per-op timing)
@@ -79,9 +85,23 @@ class Engine {
     cudaGraphExec_t gexec_ = nullptr;
     std::vector<int> seq_op_;  // seq -> op index
 
+    // host pipeline state
+    struct HostIO {
+        double* host;
+        long long lda;
+    };
+    double* d_stage_ = nullptr;
+    cudaStream_t cs_h2d_ = nullptr, cs_d2h_ = nullptr;
+    std::vector<cudaEvent_t> ev_h2d_;     // per block: H2D done
+    std::vector<cudaEvent_t> ev_d2h_;     // per export: D2H done (joined at the end)
+    cudaGraph_t hgraph_ = nullptr;
+    cudaGraphExec_t hexec_ = nullptr;
+    const double* hkey_ = nullptr;
+    long long hkey_lda_ = 0;
+
     void launch_op(int i, cudaStream_t s);
     void reset_words(cudaStream_t s);
-    bool enqueue_ops(cudaStream_t origin, std::string* err);
+    bool enqueue_ops(cudaStream_t origin, std::string* err, const HostIO* io = nullptr);
 };
 
 }  // namespace tcb

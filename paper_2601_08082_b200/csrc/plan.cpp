@@ -343,6 +343,7 @@ void Plan::emit_potrf(int node) {
         q.type = OP_QUANT;
         q.level = p;
         q.rect = blk.rect;
+        q.blocks.push_back(nd.block);
         q.slot = slot;
         q.seq = next_seq();  // the require_finite that precedes quantize
         checks.push_back({q.seq, blk.rect, 0});
@@ -429,17 +430,20 @@ void Plan::emit_potrf(int node) {
 // ---------------------------------------------------------------------------
 
 void Plan::finalize_accesses() {
-    const Rect whole{0, 0, n, n};
     for (Op& op : ops) {
         op.acc.clear();
         switch (op.type) {
             case OP_IMPORT:
-                op.acc.push_back({BUF_USER, whole, false});
-                for (int blk : op.blocks) op.acc.push_back({blocks[blk].level, blocks[blk].rect, true});
+                for (int blk : op.blocks) {
+                    op.acc.push_back({BUF_USER, blocks[blk].rect, false});
+                    op.acc.push_back({blocks[blk].level, blocks[blk].rect, true});
+                }
                 break;
             case OP_EXPORT:
-                op.acc.push_back({BUF_USER, whole, true});
-                for (int blk : op.blocks) op.acc.push_back({blocks[blk].level, blocks[blk].rect, false});
+                for (int blk : op.blocks) {
+                    op.acc.push_back({BUF_USER, blocks[blk].rect, true});
+                    op.acc.push_back({blocks[blk].level, blocks[blk].rect, false});
+                }
                 break;
             case OP_CHECK:
                 op.acc.push_back({op.src, op.rect, false});
@@ -563,18 +567,48 @@ Plan Plan::make(int n, int b, const std::vector<int>& levels, bool quantize, int
     P.has_inverse.assign(P.blocks.size(), 0);
     for (const Block& blk : P.blocks) P.needs_buf[blk.level] = true;
 
-    Op imp;
-    imp.type = OP_IMPORT;
-    for (int i = 0; i < int(P.blocks.size()); ++i)
-        if (!P.blocks[i].spine_quant) imp.blocks.push_back(i);
-    imp.rect = {0, 0, n, n};
-    P.push(std::move(imp));
+    // one import / export op per storage block, in the order the recursion
+    // first touches / finalizes them (depth first: diag1, the off-diagonal,
+    // diag2): a block is imported right before its first use and exported as
+    // soon as it is final, so with host buffers the copies overlap the
+    // factorization in that order (Engine::enqueue_host)
+    std::vector<int> order;
+    {
+        std::vector<int> stack{0};
+        while (!stack.empty()) {
+            const int id = stack.back();
+            stack.pop_back();
+            if (id < 0) {  // marker: emit the split's off-diagonal block
+                order.push_back(P.nodes[-id - 1].block);
+                continue;
+            }
+            const Node& nd = P.nodes[id];
+            if (nd.leaf) {
+                order.push_back(nd.block);
+                continue;
+            }
+            stack.push_back(nd.d2);
+            stack.push_back(-id - 1);
+            stack.push_back(nd.d1);
+        }
+    }
+    P.block_order = order;
+    for (int i : order)
+        if (!P.blocks[i].spine_quant) {
+            Op imp;
+            imp.type = OP_IMPORT;
+            imp.blocks.push_back(i);
+            imp.rect = P.blocks[i].rect;
+            P.push(std::move(imp));
+        }
     P.emit_potrf(0);
-    Op exp;
-    exp.type = OP_EXPORT;
-    for (int i = 0; i < int(P.blocks.size()); ++i) exp.blocks.push_back(i);
-    exp.rect = {0, 0, n, n};
-    P.push(std::move(exp));
+    for (int i : order) {
+        Op exp;
+        exp.type = OP_EXPORT;
+        exp.blocks.push_back(i);
+        exp.rect = P.blocks[i].rect;
+        P.push(std::move(exp));
+    }
     P.finalize_accesses();
     P.build_deps();
     return P;

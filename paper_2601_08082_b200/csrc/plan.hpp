@@ -168,6 +168,7 @@ struct Plan {
     std::vector<Op> ops;
     std::vector<FlopRec> flops;  // in seq order
     std::vector<CheckRec> checks;  // in seq order
+    std::vector<int> block_order;  // depth-first (first use / finalization) order
     int n_alpha_slots = 0;
     uint32_t n_seq = 0;
     bool needs_buf[3] = {false, false, false};
