@@ -259,7 +259,7 @@ def run_ours(args):
         host = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
         host.copy_(a)
         hnp = host.numpy().T  # Fortran view of the column-major bytes
-        del l
+        l = None
         torch.cuda.empty_cache()
         plan.factor_host(hnp)  # warm (allocates the staging buffer)
         barrier()
@@ -280,6 +280,31 @@ def run_ours(args):
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
                "note": "each step re-factors the previous step's in-place output (SPD lower triangle)"}
 
+    # C4: a batch of independent N=16384 systems (POTRF + POTRS), sharded
+    # across the ranks with no data-path collective
+    # release the C3 plan (level buffers, staging copy) and matrices first
+    import gc
+    plan = a = l = host = hnp = None
+    gc.collect()
+    torch.cuda.empty_cache()
+    c4 = None
+    if args.c4_count > 0:
+        from paper_2601_08082_b200.batch import run_batch_on_rank
+        if ws > 1:
+            dist.barrier()
+        local, tot, fl = run_batch_on_rank(args.c4_count, args.c4_n, b, CFG, seed0=1000, concurrency=args.c4_conc,
+                                           world=ws, rank=rank)
+        c4 = {"workload": f"C4: {args.c4_count} x N={args.c4_n} b={b} {CFG} POTRF+POTRS (1 RHS), sharded over "
+                          f"{ws} rank(s), {args.c4_conc} plans per GPU",
+              "value": tot.systems * fl / (tot.device_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+              "solves_per_s": tot.systems / (tot.device_ms * 1e-3), "systems": tot.systems, "failed": tot.failed,
+              "ms_max_over_ranks": tot.device_ms, "worst_solve_residual": tot.worst_residual,
+              "data": "device-generated SPD of spd_generate's distribution (not the mt19937_64 stream)"}
+
+    variants = None
+    if args.variants and rank == 0:
+        variants = run_variants(args, tc, torch)
+
     cpu = None
     if rank == 0 and ws == 1 and args.cpu_n > 0:
         cpu = cpu_baseline_sample(args)
@@ -295,12 +320,48 @@ def run_ours(args):
                            "l2": "inputs (34 GB) larger than L2; no flush needed"},
                 "status": st.status, "rel_error": rel, "digits": -math.log10(rel) if rel > 0 else None,
                 "clocks": clk.summary(), "gpu_launches": stats["launches"] * args.steps,
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "c4": c4, "variants": variants,
                 "breakdown_ms_serialized": {k: round(v[0], 3) for k, v in sorted(by_type.items(),
                                                                                   key=lambda kv: -kv[1][0])}}
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
+
+
+def run_variants(args, tc, torch):
+    """accuracy / speed bounds through the same kernels (north_star): Pure F16
+    and the mixed tree on A * 2^-1 (Pure F16 overflows the N=65536 diagonal,
+    n + r > 65504; the power-of-two scaling is exact), and
+    Pure F64 on A."""
+    n, b = args.n, args.b
+    out = {}
+    for name, cfg, scale in (("mixed_half_scaled", CFG, 0.5), ("pure_f16_half_scaled", "Pure F16", 0.5),
+                             ("pure_f64", "Pure F64", 1.0)):
+        a = tc.spd_generate_device(n, SEED)
+        if scale != 1.0:
+            a.mul_(scale)
+        l = torch.empty_like(a)
+        plan = tc.Plan(n, b, cfg, True)
+        st = plan.factor_device(a, l)
+        reps = 1 if cfg == "Pure F64" else 3
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        ev0.record()
+        for _ in range(reps):
+            plan.factor_device(a, l, sync=False)
+        ev1.record()
+        torch.cuda.synchronize()
+        ms = ev0.elapsed_time(ev1) / reps
+        st = plan.status()
+        rel = tc.factorization_error_device(a, l) if st.status == "ok" else float("nan")
+        out[name] = {"config": cfg, "input_scale": scale, "status": st.status, "ms": ms,
+                     "tflops": potrf_flops(n) / (ms * 1e-3) / 1e12, "rel_error": rel}
+        del a, l, plan
+        torch.cuda.empty_cache()
+    m, h = out["mixed_half_scaled"], out["pure_f16_half_scaled"]
+    out["mixed_vs_pure_f16_throughput"] = h["ms"] / m["ms"]
+    out["pure_f16_vs_mixed_error"] = h["rel_error"] / m["rel_error"] if m["rel_error"] > 0 else None
+    return out
 
 
 def main():
@@ -314,6 +375,11 @@ def main():
     ap.add_argument("--e2e-steps", dest="e2e_steps", type=int, default=2)
     ap.add_argument("--cpu-n", dest="cpu_n", type=int, default=1536)
     ap.add_argument("--ref-n", dest="ref_n", type=int, default=1536)
+    ap.add_argument("--c4-count", dest="c4_count", type=int, default=64)
+    ap.add_argument("--c4-n", dest="c4_n", type=int, default=16384)
+    ap.add_argument("--c4-conc", dest="c4_conc", type=int, default=4)
+    ap.add_argument("--variants", action="store_true",
+                    help="also time Pure F16 / Pure F64 trees (bounds) at N; slow (F64 runs on SIMT)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -133,6 +133,23 @@ int tc_info_message(const tc_plan* plan, const tc_info* info, char* buf, int buf
 int tc_potrs_device(int n, const double* dL, int ldl, double* dB, int ldb, int nrhs,
                     void* stream);
 
+/* ---- batched POTRF + POTRS (BASELINE config C4) ------------------------ */
+
+/* A batch driver for independent order-n systems with one precision tree:
+ * `concurrency` plans (own workspace, graph and stream each) run systems
+ * side by side on the current device. */
+typedef struct tc_batch tc_batch;
+int tc_batch_create(int n, int b, const int* levels, int nlevels, int quantize, int concurrency,
+                    tc_batch** out);
+void tc_batch_destroy(tc_batch* batch);
+/* Factors dA[k] in place (device, column-major, lda) for k < count and, if
+ * dB && dB[k], solves A X = B for its nrhs right-hand sides (dB[k], ldb,
+ * overwritten by X).  status[k] = tc_status of system k; index[k] (optional)
+ * = its failing row.  Returns TC_OK, the first failing status, or an
+ * argument / device error. */
+int tc_batch_run(tc_batch* batch, int count, double* const* dA, int lda, double* const* dB, int ldb,
+                 int nrhs, int* status, int* index);
+
 /* ---- analysis (analysis.cpp) ------------------------------------------- */
 
 /* spd_generate(n, seed) into a host column-major buffer (lda >= n);

@@ -125,6 +125,9 @@ def _load():
         "tc_factorization_error_device": (I, [I, P, I, P, I, C.POINTER(D), P]),
         "tc_solve_residual_device": (I, [I, P, I, P, P, C.POINTER(D), P]),
         "tc_debug_gemm": (I, [I, I, I, I, I, D, I, I, C.POINTER(C.c_float)]),
+        "tc_batch_create": (I, [I, I, PI, I, I, I, C.POINTER(P)]),
+        "tc_batch_destroy": (None, [P]),
+        "tc_batch_run": (I, [P, I, C.POINTER(P), I, C.POINTER(P), I, I, PI, PI]),
         "tc_last_error": (C.c_char_p, []),
         "tc_device_available": (I, []),
         "tc_version": (C.c_char_p, []),
@@ -424,6 +427,45 @@ class Plan:
         _raise(_lib.tc_plan_profile(self._h, _ptr(a_in), _check_dev(a_in, self.n, "a_in"), _ptr(l_out),
                                     _check_dev(l_out, self.n, "l_out"), _stream_ptr(stream), out, n_ops))
         return list(out)
+
+
+class Batch:
+    """Batched tree_potrf + POTRS of independent systems on one device
+    (tc_batch_*; BASELINE config C4).  `concurrency` plans run side by side."""
+
+    def __init__(self, n: int, b: int, config, quantize: bool = True, concurrency: int = 4):
+        self.cfg = _cfg(config)
+        self.n = int(n)
+        arr = (C.c_int * len(self.cfg.levels))(*self.cfg.levels)
+        h = C.c_void_p()
+        _raise(_lib.tc_batch_create(self.n, int(b), arr, len(self.cfg.levels), int(bool(quantize)), int(concurrency),
+                                    C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib is not None:
+            _lib.tc_batch_destroy(h)
+            self._h = None
+
+    def run(self, a_list, b_list=None):
+        """factor every a_list[k] in place (device column-major tensors, see
+        to_device) and solve with b_list[k] (device tensors (nrhs, n)) if
+        given; returns the per-system status names"""
+        k = len(a_list)
+        lda = _check_dev(a_list[0], self.n, "A") if k else self.n
+        pa = (C.c_void_p * k)(*[_ptr(a) for a in a_list])
+        pb, ldb, nrhs = None, self.n, 1
+        if b_list is not None:
+            b2 = [x if x.dim() == 2 else x.view(1, -1) for x in b_list]
+            ldb, nrhs = b2[0].shape[1], b2[0].shape[0]
+            pb = (C.c_void_p * k)(*[_ptr(x) for x in b2])
+        st = (C.c_int * max(k, 1))()
+        idx = (C.c_int * max(k, 1))()
+        code = _lib.tc_batch_run(self._h, k, pa, lda, pb, ldb, nrhs, st, idx)
+        if code not in (TC_OK, TC_NPD, TC_BREAKDOWN, TC_SINGULAR):
+            _raise(code)
+        return [_STATUS_NAMES[st[i]] for i in range(k)]
 
 
 # ---------------------------------------------------------------- analysis.hpp

@@ -1,0 +1,124 @@
+// capi_batch.cpp -- batched POTRF + POTRS of independent SPD systems on one
+// device (BASELINE config C4: 64 x N=16384).
+//
+// One system's factorization is critical-path bound at these sizes (the
+// leaf chain leaves most SMs idle), so `concurrency` independent plans --
+// each its own workspace, CUDA graph and stream -- run systems side by side,
+// round robin.  Per system: tree_potrf (the plan's graph; the caller's
+// pointers go through RunArgs), a copy of its status word, then the forward
+// and backward substitution of its right-hand sides on the same stream.
+// Multi-GPU sharding of a batch is done by the caller (one process per GPU,
+// no data-path collective: paper_2601_08082_b200/batch.py).
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/treechol_c.h"
+#include "engine.hpp"
+#include "launch.hpp"
+#include "plan.hpp"
+
+using namespace tcb;
+
+namespace tcb {
+void set_last_error(const std::string& msg);  // capi.cpp
+}
+
+struct tc_batch {
+    std::vector<std::unique_ptr<Engine>> eng;
+    std::vector<cudaStream_t> streams;
+    unsigned long long* h_status = nullptr;  // pinned, one word per system
+    int cap = 0;
+    ~tc_batch() {
+        for (auto s : streams) cudaStreamDestroy(s);
+        if (h_status) cudaFreeHost(h_status);
+    }
+};
+
+namespace {
+int bfail(int code, const std::string& m) {
+    set_last_error(m);
+    return code;
+}
+}  // namespace
+
+extern "C" {
+
+int tc_batch_create(int n, int b, const int* levels, int nlevels, int quantize, int concurrency, tc_batch** out) {
+    if (!out || !levels || nlevels < 1 || n < 1 || b < 1 || concurrency < 1)
+        return bfail(TC_INVALID_ARGUMENT, "bad arguments");
+    *out = nullptr;
+    try {
+        auto* bt = new tc_batch;
+        for (int i = 0; i < concurrency; ++i) {
+            PlanOptions po;
+            bt->eng.push_back(std::make_unique<Engine>(
+                Plan::make(n, b, std::vector<int>(levels, levels + nlevels), quantize != 0, 0, po)));
+        }
+        *out = bt;
+        return TC_OK;
+    } catch (const std::exception& e) {
+        return bfail(TC_INVALID_ARGUMENT, e.what());
+    }
+}
+
+void tc_batch_destroy(tc_batch* bt) { delete bt; }
+
+int tc_batch_run(tc_batch* bt, int count, double* const* dA, int lda, double* const* dB, int ldb, int nrhs,
+                 int* status, int* index) {
+    if (!bt || count < 0 || (count > 0 && (!dA || !status))) return bfail(TC_INVALID_ARGUMENT, "bad arguments");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
+        cudaGetLastError();
+        return bfail(TC_NO_DEVICE, "no CUDA device (there is no CPU fallback)");
+    }
+    const int n = bt->eng[0]->plan.n;
+    if (lda < n || (dB && (ldb < n || nrhs < 1))) return bfail(TC_INVALID_ARGUMENT, "bad leading dimensions");
+    const int C = int(bt->eng.size());
+    std::string err;
+    while (int(bt->streams.size()) < C) {
+        cudaStream_t s;
+        if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return bfail(TC_CUDA_ERROR, "stream");
+        bt->streams.push_back(s);
+    }
+    if (bt->cap < count) {
+        if (bt->h_status) cudaFreeHost(bt->h_status);
+        bt->h_status = nullptr;
+        if (cudaMallocHost(&bt->h_status, sizeof(unsigned long long) * size_t(count)) != cudaSuccess)
+            return bfail(TC_CUDA_ERROR, "cudaMallocHost");
+        bt->cap = count;
+    }
+    for (int k = 0; k < count; ++k) {
+        const int e = k % C;
+        Engine& eng = *bt->eng[size_t(e)];
+        cudaStream_t s = bt->streams[size_t(e)];
+        if (!eng.enqueue(dA[k], lda, dA[k], lda, s, &err)) return bfail(TC_CUDA_ERROR, err);
+        if (!eng.copy_status(bt->h_status + k, s, &err)) return bfail(TC_CUDA_ERROR, err);
+        if (dB && dB[k]) {
+            // POTRS on the factor just written
+            const int nb = (n + 63) / 64;
+            int* d_cnt = nullptr;
+            if (cudaMallocAsync(&d_cnt, sizeof(int) * size_t(nb + 1) * size_t(nrhs), s) != cudaSuccess)
+                return bfail(TC_CUDA_ERROR, "cudaMallocAsync");
+            launch_potrs(n, dA[k], lda, dB[k], ldb, nrhs, d_cnt, nullptr, s);
+            cudaFreeAsync(d_cnt, s);
+        }
+    }
+    for (auto s : bt->streams)
+        if (cudaStreamSynchronize(s) != cudaSuccess) return bfail(TC_CUDA_ERROR, "batch synchronize");
+    const cudaError_t ce = cudaGetLastError();
+    if (ce != cudaSuccess) return bfail(TC_CUDA_ERROR, cudaGetErrorString(ce));
+    int worst = TC_OK;
+    for (int k = 0; k < count; ++k) {
+        Failure f;
+        if (!bt->eng[size_t(k % C)]->decode(bt->h_status[k], &f, &err)) return bfail(TC_CUDA_ERROR, err);
+        status[k] = f.status;
+        if (index) index[k] = f.status == TC_NUMERICAL_BREAKDOWN ? f.elem_row : f.index;
+        if (f.status && worst == TC_OK) worst = f.status;
+    }
+    return worst;
+}
+
+}  // extern "C"

@@ -31,6 +31,7 @@ Engine::~Engine() {
     if (hexec_) cudaGraphExecDestroy(hexec_);
     if (hgraph_) cudaGraphDestroy(hgraph_);
     for (auto e : ev_h2d_) cudaEventDestroy(e);
+    for (auto e : ra_ev_) cudaEventDestroy(e);
     for (auto e : ev_d2h_) cudaEventDestroy(e);
     if (cs_h2d_) cudaStreamDestroy(cs_h2d_);
     if (cs_d2h_) cudaStreamDestroy(cs_d2h_);
@@ -310,16 +311,36 @@ bool Engine::enqueue_ops(cudaStream_t origin, std::string* err, const HostIO* io
     return true;
 }
 
+// a pinned RunArgs slot whose previous H2D copy has executed (the copies
+// read the host slot asynchronously, in stream order)
+RunArgs* Engine::next_args(std::string* err) {
+    const int k = ra_next_++ % kRaRing;
+    if (ra_ev_.empty()) {
+        ra_ev_.resize(kRaRing);
+        for (auto& e : ra_ev_)
+            if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+                if (err) *err = "cudaEventCreate";
+                return nullptr;
+            }
+    }
+    if (cudaEventSynchronize(ra_ev_[size_t(k)]) != cudaSuccess) {
+        if (err) *err = "cudaEventSynchronize";
+        return nullptr;
+    }
+    return h_ra_ + k;
+}
+
 bool Engine::enqueue(const double* a_in, long long lda_in, double* l_out, long long lda_out, cudaStream_t stream,
                      std::string* err) {
     if (!prepare(err)) return false;
-    static int ring = 0;
-    RunArgs* slot = h_ra_ + (ring++ % kRaRing);
+    RunArgs* slot = next_args(err);
+    if (!slot) return false;
     slot->a_in = a_in;
     slot->l_out = l_out;
     slot->lda_in = lda_in;
     slot->lda_out = lda_out;
     TC_TRY(cudaMemcpyAsync(d_ra_, slot, sizeof(RunArgs), cudaMemcpyHostToDevice, stream));
+    TC_TRY(cudaEventRecord(ra_ev_[size_t(slot - h_ra_)], stream));
     if (use_graph) {
         if (!gexec_) {
             cudaStream_t cap;
@@ -361,13 +382,14 @@ bool Engine::enqueue_host(double* host, long long lda, cudaStream_t stream, std:
         ev_d2h_.resize(size_t(n_exp) + 2);
         for (auto& e : ev_d2h_) TC_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
-    static int ring = 0;
-    RunArgs* slot = h_ra_ + (ring++ % kRaRing);
+    RunArgs* slot = next_args(err);
+    if (!slot) return false;
     slot->a_in = d_stage_;
     slot->l_out = d_stage_;
     slot->lda_in = n;
     slot->lda_out = n;
     TC_TRY(cudaMemcpyAsync(d_ra_, slot, sizeof(RunArgs), cudaMemcpyHostToDevice, stream));
+    TC_TRY(cudaEventRecord(ra_ev_[size_t(slot - h_ra_)], stream));
     HostIO io{host, lda};
     cudaPointerAttributes pa{};
     const bool pinned = cudaPointerGetAttributes(&pa, host) == cudaSuccess && pa.type == cudaMemoryTypeHost;
@@ -408,8 +430,16 @@ bool Engine::enqueue_host(double* host, long long lda, cudaStream_t stream, std:
 bool Engine::result(Failure* f, std::string* err) {
     TC_TRY(cudaMemcpyAsync(h_status_, d_words_, sizeof(unsigned long long), cudaMemcpyDeviceToHost, last_stream_));
     TC_TRY(cudaStreamSynchronize(last_stream_));
+    return decode(*h_status_, f, err);
+}
+
+bool Engine::copy_status(unsigned long long* host_slot, cudaStream_t s, std::string* err) {
+    TC_TRY(cudaMemcpyAsync(host_slot, d_words_, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    return true;
+}
+
+bool Engine::decode(unsigned long long key, Failure* f, std::string* err) const {
     *f = Failure{};
-    const unsigned long long key = *h_status_;
     if (key == ~0ull) return true;
     const uint32_t seq = uint32_t(key >> 40);
     const uint64_t local = key & ((1ull << 40) - 1);
@@ -465,7 +495,8 @@ bool Engine::result(Failure* f, std::string* err) {
 bool Engine::profile(const double* a_in, long long lda_in, double* l_out, long long lda_out, cudaStream_t stream,
                      std::vector<float>& op_ms, std::string* err) {
     if (!prepare(err)) return false;
-    RunArgs* slot = h_ra_;
+    RunArgs* slot = next_args(err);
+    if (!slot) return false;
     slot->a_in = a_in;
     slot->l_out = l_out;
     slot->lda_in = lda_in;

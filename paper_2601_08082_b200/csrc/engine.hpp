@@ -55,6 +55,10 @@ class Engine {
     bool enqueue_host(double* host, long long lda, cudaStream_t stream, std::string* err);
     // wait for the last enqueue and decode the status word
     bool result(Failure* f, std::string* err);
+    // enqueue a copy of the status word of the run just enqueued on `s`
+    // into host memory (batched drivers), and decode such a copy
+    bool copy_status(unsigned long long* host_slot, cudaStream_t s, std::string* err);
+    bool decode(unsigned long long key, Failure* f, std::string* err) const;
     // serialized eager run with an event after every op (per-op timing)
     bool profile(const double* a_in, long long lda_in, double* l_out, long long lda_out, cudaStream_t stream,
                  std::vector<float>& op_ms, std::string* err);
@@ -98,6 +102,10 @@ class Engine {
     cudaGraphExec_t hexec_ = nullptr;
     const double* hkey_ = nullptr;
     long long hkey_lda_ = 0;
+
+    std::vector<cudaEvent_t> ra_ev_;  // per RunArgs slot: its H2D copy was issued
+    int ra_next_ = 0;
+    RunArgs* next_args(std::string* err);
 
     void launch_op(int i, cudaStream_t s);
     void reset_words(cudaStream_t s);

@@ -1,0 +1,96 @@
+"""Batched POTRF + POTRS (BASELINE config C4) and its multi-GPU sharding.
+
+CPU: the shard partition and the cross-rank reduction on a world_size-2
+gloo group (the N>1 host path; there is no data-path collective to test).
+GPU: a batch through tc_batch_run against the oracle (status, backward
+error, solve residual), including a failing system in the middle of a batch.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from paper_2601_08082_b200.batch import ShardResult, reduce_results, shard
+
+
+def test_shard_partition_properties():
+    for count in (0, 1, 7, 64, 65):
+        for world in (1, 2, 3, 4, 8):
+            parts = [list(shard(count, world, r)) for r in range(world)]
+            flat = [k for p in parts for k in p]
+            assert flat == list(range(count))
+            sizes = [len(p) for p in parts]
+            assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(ValueError):
+        shard(4, 2, 2)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    mine = shard(64, world, rank)
+    local = ShardResult(len(mine), rank, 10.0 + rank, 1e-15 * (rank + 1))
+    tot = reduce_results(local)
+    q.put((rank, list(mine)[:1], tot.systems, tot.failed, tot.device_ms, tot.worst_residual))
+    dist.destroy_process_group()
+
+
+def test_sharded_reduction_gloo_world2():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    out = sorted(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    assert out[0][1] == [0] and out[1][1] == [32]
+    for _, _, systems, failed, ms, res in out:
+        assert systems == 64 and failed == 1 and ms == 11.0 and res == pytest.approx(2e-15)
+
+
+@pytest.mark.gpu
+def test_batch_matches_oracle(tc, oracle):
+    import torch
+    from pyoracle import parse_levels
+    n, b, cfg = 512, 64, "[F16, F16, F32]"
+    seeds = [3, 4, 5, 6, 7]
+    mats = [oracle.spd_generate(n, s) for s in seeds]
+    mats[2] = mats[2].copy(order="F")
+    mats[2][100, 100] = -1.0  # indefinite: NotPositiveDefinite at row 100 (oracle decides)
+    a_dev = [tc.to_device(m) for m in mats]
+    a0 = [x.clone() for x in a_dev]
+    rhs = [torch.from_numpy(m.sum(axis=1)).reshape(1, n).to("cuda") for m in mats]
+    rhs0 = [x.clone() for x in rhs]
+    batch = tc.Batch(n, b, cfg, True, concurrency=2)
+    st = batch.run(a_dev, rhs)
+    for k, m in enumerate(mats):
+        st_o, det_o, _, rel_o, _ = oracle.factor(m, b, parse_levels(cfg))
+        assert st[k] == st_o, (k, st[k], st_o, det_o)
+        if st_o == "ok":
+            rel = tc.factorization_error_device(a0[k], a_dev[k])
+            assert rel <= 2 * rel_o, (k, rel, rel_o)
+            res = tc.solve_residual_device(a0[k], rhs[k][0].contiguous(), rhs0[k][0].contiguous())
+            assert res < 1e-5, (k, res)
+
+
+@pytest.mark.gpu
+def test_batch_rank_driver_single_gpu(tc):
+    from paper_2601_08082_b200.batch import run_batch_on_rank
+    local, tot, flops = run_batch_on_rank(4, 1024, 128, "[F16, F16, F16, F32]", seed0=11, concurrency=2,
+                                          in_flight=4)
+    assert local.systems == 4 and tot.failed == 0
+    assert tot.worst_residual < 1e-5 and flops > 0 and tot.device_ms > 0
