@@ -199,8 +199,16 @@ __device__ __forceinline__ bool tile_coords(const TcProb* probs, int np, int t, 
     pi = find_tc_prob(probs, np, t);
     const TcProb& p = probs[pi];
     const int lt = t - p.tile0;
-    tm = lt / p.tiles_n;
-    tn = lt % p.tiles_n;
+    // grouped raster: bands of GROUP tile rows, column-major inside a band,
+    // so the CTAs resident at once share a few A and B panels per k-block
+    // (L2 reuse; a plain row-major order streams ~tiles_n B panels from DRAM)
+    constexpr int GROUP = 16;
+    const int tiles_m = (p.m + BM - 1) / BM;
+    const int band = GROUP * p.tiles_n;
+    const int g = lt / band, r = lt - g * band;
+    const int rows = min(GROUP, tiles_m - g * GROUP);
+    tm = g * GROUP + r % rows;
+    tn = r / rows;
     return !(p.lower && p.c_c0 + tn * BN > p.c_r0 + tm * BM + BM - 1);
 }
 
