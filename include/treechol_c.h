@@ -109,6 +109,10 @@ int tc_potrf_host(tc_plan* plan, double* A, int lda, tc_info* info);
  * op_ms[i] = device time of op i (cap entries).  For roofline accounting. */
 int tc_plan_profile(tc_plan* plan, const double* dA_in, int lda_in, double* dL_out,
                     int lda_out, void* stream, float* op_ms, int cap);
+/* Eager multi-stream run with timing events around every op: t_start[i],
+ * t_end[i] = ms from the run's start (the concurrency timeline). */
+int tc_plan_timeline(tc_plan* plan, const double* dA_in, int lda_in, double* dL_out, int lda_out,
+                     void* stream, float* t_start, float* t_end, int cap);
 /* op i of the plan: type (0 import, 1 export, 2 check, 3 quant, 4 dequant,
  * 5 shadow, 6 potrf leaf, 7 trsm leaf, 8 gemm), gemm class (0 = tcgen05
  * FP16, 1..5 SIMT classes, -1 otherwise), level, algorithmic flops, rect */

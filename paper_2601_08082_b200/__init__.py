@@ -118,6 +118,7 @@ def _load():
         "tc_potrf_host": (I, [P, P, I, C.POINTER(_Info)]),
         "tc_plan_profile": (I, [P, P, I, P, I, P, C.POINTER(C.c_float), I]),
         "tc_plan_status": (I, [P, C.POINTER(_Info)]),
+        "tc_plan_timeline": (I, [P, P, I, P, I, P, C.POINTER(C.c_float), C.POINTER(C.c_float), I]),
         "tc_info_message": (I, [P, C.POINTER(_Info), C.c_char_p, I]),
         "tc_potrs_device": (I, [I, P, I, P, I, I, P]),
         "tc_spd_generate_host": (I, [I, U64, P, I]),
@@ -419,6 +420,14 @@ class Plan:
         info = _Info()
         code = _lib.tc_potrf_host(self._h, a.ctypes.data, a.shape[0], C.byref(info))
         return self._status(code, info)
+
+    def timeline(self, a_in, l_out, stream=None):
+        """eager multi-stream run; per-op (start, end) ms from the start"""
+        n_ops = self.stats()["ops"]
+        t0, t1 = (C.c_float * n_ops)(), (C.c_float * n_ops)()
+        _raise(_lib.tc_plan_timeline(self._h, _ptr(a_in), _check_dev(a_in, self.n, "a_in"), _ptr(l_out),
+                                     _check_dev(l_out, self.n, "l_out"), _stream_ptr(stream), t0, t1, n_ops))
+        return list(t0), list(t1)
 
     def profile(self, a_in, l_out, stream=None):
         """serialized eager run; per-op device milliseconds"""

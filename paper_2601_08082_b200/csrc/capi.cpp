@@ -198,6 +198,11 @@ int tc_plan_set_option(tc_plan* plan, const char* key, int value) {
         e.use_graph = value != 0;
         return TC_OK;
     }
+    if (k == "bulk_tiles_per_cta" || k == "bulk_max_ctas") {
+        if (e.ready() && e.use_graph) return fail(TC_INVALID_ARGUMENT, k + " must be set before the first run");
+        (k == "bulk_tiles_per_cta" ? e.bulk_tiles_per_cta : e.bulk_max_ctas) = value < 0 ? 0 : value;
+        return TC_OK;
+    }
     if (k == "n_streams") {
         if (e.ready()) return fail(TC_INVALID_ARGUMENT, "n_streams must be set before the first run");
         e.n_streams = value < 1 ? 1 : value;
@@ -212,6 +217,18 @@ int tc_plan_set_option(tc_plan* plan, const char* key, int value) {
                                           : po.fuse_checks;
         if (bool(value) == field) return TC_OK;
         field = value != 0;
+        Plan p = Plan::make(e.plan.n, e.plan.b, e.plan.levels, e.plan.quantize, e.plan.leaf_size, po);
+        const bool g = e.use_graph;
+        const int s = e.n_streams;
+        plan->eng = std::make_unique<Engine>(std::move(p));
+        plan->eng->use_graph = g;
+        plan->eng->n_streams = s;
+        return TC_OK;
+    }
+    if (k == "syrk_split_min") {
+        if (e.ready()) return fail(TC_INVALID_ARGUMENT, k + " must be set before the first run");
+        PlanOptions po = e.plan.opt;
+        po.syrk_split_min = value < 1 ? (1 << 30) : value;
         Plan p = Plan::make(e.plan.n, e.plan.b, e.plan.levels, e.plan.quantize, e.plan.leaf_size, po);
         const bool g = e.use_graph;
         const int s = e.n_streams;
@@ -299,6 +316,20 @@ int tc_potrf_host(tc_plan* plan, double* A, int lda, tc_info* info) {
     const int st = tc_plan_status(plan, &local);
     if (info) *info = local;
     return st;
+}
+
+int tc_plan_timeline(tc_plan* plan, const double* dA_in, int lda_in, double* dL_out, int lda_out, void* stream,
+                     float* t_start, float* t_end, int cap) {
+    if (!plan || !dA_in || !dL_out || !t_start || !t_end) return fail(TC_INVALID_ARGUMENT, "null argument");
+    std::vector<float> a, b;
+    std::string err;
+    if (!plan->eng->timeline(dA_in, lda_in, dL_out, lda_out, static_cast<cudaStream_t>(stream), a, b, &err))
+        return fail(TC_CUDA_ERROR, err);
+    for (int i = 0; i < cap && i < int(a.size()); ++i) {
+        t_start[i] = a[i];
+        t_end[i] = b[i];
+    }
+    return TC_OK;
 }
 
 int tc_plan_profile(tc_plan* plan, const double* dA_in, int lda_in, double* dL_out, int lda_out, void* stream,

@@ -76,9 +76,27 @@ extern "C" int tc_debug_gemm(int gclass, int m, int n, int k, int lower, double 
         else launch_gemm_simt(c, gclass, static_cast<DevProb*>(dprob), 1, tiles, nullptr);
     };
     launch();  // warm
-    cudaEventRecord(e0);
-    for (int i = 0; i < iters; ++i) launch();
-    cudaEventRecord(e1);
+    // back-to-back launches captured in a graph: device time per launch
+    // without host launch gaps
+    cudaStream_t cs;
+    cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ge = nullptr;
+    cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+    for (int i = 0; i < iters; ++i) {
+        if (tc) launch_gemm_tc(c, gclass == GC_TC32 ? KIND_TF32X3 : KIND_F16, dprob, 1, tiles, cs);
+        else launch_gemm_simt(c, gclass, static_cast<DevProb*>(dprob), 1, tiles, cs);
+    }
+    cudaStreamEndCapture(cs, &g);
+    cudaGraphInstantiate(&ge, g, 0);
+    cudaGraphLaunch(ge, cs);
+    cudaStreamSynchronize(cs);
+    cudaEventRecord(e0, cs);
+    cudaGraphLaunch(ge, cs);
+    cudaEventRecord(e1, cs);
+    cudaGraphExecDestroy(ge);
+    cudaGraphDestroy(g);
+    cudaStreamDestroy(cs);
     cudaEventSynchronize(e1);
     float ms = 0;
     cudaEventElapsedTime(&ms, e0, e1);

@@ -2,7 +2,9 @@
 #include "engine.hpp"
 
 #include <algorithm>
+#include <chrono>
 #include <cstring>
+#include <thread>
 
 #include "launch.hpp"
 
@@ -194,8 +196,9 @@ void Engine::launch_op(int i, cudaStream_t s) {
             else launch_leaf_inverse(ctx_, r.r0, r.m, op.seq, s);
             break;
         case OP_GEMM:
-            if (op.gclass == GC_TC16) launch_gemm_tc(ctx_, KIND_F16, tab, L.count, L.tiles, s);
-            else if (op.gclass == GC_TC32) launch_gemm_tc(ctx_, KIND_TF32X3, tab, L.count, L.tiles, s);
+            if (op.gclass == GC_TC16 || op.gclass == GC_TC32)
+                launch_gemm_tc(ctx_, op.gclass == GC_TC32 ? KIND_TF32X3 : KIND_F16, tab, L.count, L.tiles, s,
+                               op.bulk ? bulk_max_ctas : 0, op.bulk ? bulk_tiles_per_cta : 0);
             else launch_gemm_simt(ctx_, op.gclass, reinterpret_cast<DevProb*>(tab), L.count, L.tiles, s);
             break;
     }
@@ -208,18 +211,26 @@ void Engine::reset_words(cudaStream_t s) {
 }
 
 // enqueue every op on the stream pool (works eagerly or under capture)
-bool Engine::enqueue_ops(cudaStream_t origin, std::string* err, const HostIO* io) {
+bool Engine::enqueue_ops(cudaStream_t origin, std::string* err, const HostIO* io, std::vector<cudaEvent_t>* tl) {
     const int N = int(plan.ops.size());
     // compute streams 0..C-1, then one stream for the imports and one for the
     // exports: a transfer-side op never sits in front of unrelated compute
     // (in-order streams would otherwise turn a wait for the caller's data
     // into a wait for everything queued behind it)
-    const int C = std::max(1, n_streams);
+    const int C = std::max(2, n_streams);
+    // compute streams: [0, CH) high priority -- the leaf chain, TRSMs, checks,
+    // quantization (the factorization's critical path) -- and [CH, C) low
+    // priority -- the trailing SYRK updates, whose CTAs yield SMs to the
+    // chain as they finish tiles
+    const int CH = C / 2;
     const int S = C + 2, SI = C, SE = C + 1;
     if (int(streams_.size()) < S) {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);  // hi = greatest priority (numerically lowest)
         for (int s = int(streams_.size()); s < S; ++s) {
             cudaStream_t st;
-            TC_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+            const int prio = s < CH ? hi : lo;
+            TC_TRY(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, prio));
             streams_.push_back(st);
         }
     }
@@ -231,27 +242,30 @@ bool Engine::enqueue_ops(cudaStream_t origin, std::string* err, const HostIO* io
         }
     }
     if (!fork_) TC_TRY(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming));
-    // stream assignment: continue a dep's compute stream when that dep is its tail
+    // stream assignment: continue a dep's stream of the same class when that
+    // dep is its tail, else the least recently used stream of the class
     std::vector<int> sid(N, 0), tail(S, -1), last_use(S, -1);
     std::vector<char> need_ev(N, 0);
     std::vector<std::vector<int>> waits(N);
     for (int i = 0; i < N; ++i) {
-        const OpType ty = plan.ops[i].type;
+        const Op& op = plan.ops[i];
+        const OpType ty = op.type;
+        const int b0 = op.bulk ? CH : 0, b1 = op.bulk ? C : CH;
         int pick = ty == OP_IMPORT ? SI : ty == OP_EXPORT ? SE : -1;
         if (pick < 0) {
-            for (int d : plan.ops[i].deps)
-                if (sid[d] < C && tail[sid[d]] == d) {
+            for (int d : op.deps)
+                if (sid[d] >= b0 && sid[d] < b1 && tail[sid[d]] == d) {
                     pick = sid[d];
                     break;
                 }
         }
         if (pick < 0) {
-            pick = 0;
-            for (int s = 1; s < C; ++s)
+            pick = b0;
+            for (int s = b0 + 1; s < b1; ++s)
                 if (last_use[s] < last_use[pick]) pick = s;
         }
         sid[i] = pick;
-        for (int d : plan.ops[i].deps)
+        for (int d : op.deps)
             if (sid[d] != pick) {  // same-stream deps are ordered already
                 waits[i].push_back(d);
                 need_ev[d] = 1;
@@ -284,7 +298,9 @@ bool Engine::enqueue_ops(cudaStream_t origin, std::string* err, const HostIO* io
         const Op& op = plan.ops[i];
         if (io && (op.type == OP_IMPORT || op.type == OP_QUANT))  // the caller's doubles have arrived
             for (int b : op.blocks) TC_TRY(cudaStreamWaitEvent(st, ev_h2d_[b], 0));
+        if (tl) TC_TRY(cudaEventRecord((*tl)[2 * i], st));
         launch_op(i, st);
+        if (tl) TC_TRY(cudaEventRecord((*tl)[2 * i + 1], st));
         if (need_ev[i]) TC_TRY(cudaEventRecord(events_[i], st));
         if (io && op.type == OP_EXPORT) {
             // this block is final: copy it back while the rest computes
@@ -489,6 +505,52 @@ bool Engine::decode(unsigned long long key, Failure* f, std::string* err) const 
             if (err) *err = "status from an op that cannot fail";
             return false;
     }
+    return true;
+}
+
+bool Engine::timeline(const double* a_in, long long lda_in, double* l_out, long long lda_out, cudaStream_t stream,
+                      std::vector<float>& t0, std::vector<float>& t1, std::string* err) {
+    if (!prepare(err)) return false;
+    RunArgs* slot = next_args(err);
+    if (!slot) return false;
+    slot->a_in = a_in;
+    slot->l_out = l_out;
+    slot->lda_in = lda_in;
+    slot->lda_out = lda_out;
+    TC_TRY(cudaMemcpyAsync(d_ra_, slot, sizeof(RunArgs), cudaMemcpyHostToDevice, stream));
+    TC_TRY(cudaEventRecord(ra_ev_[size_t(slot - h_ra_)], stream));
+    const int N = int(plan.ops.size());
+    std::vector<cudaEvent_t> tl(2 * size_t(N));
+    for (auto& e : tl) TC_TRY(cudaEventCreate(&e));
+    int* flag = nullptr;
+    TC_TRY(cudaHostAlloc(&flag, sizeof(int), cudaHostAllocMapped));
+    *reinterpret_cast<volatile int*>(flag) = 0;
+    int* dflag = nullptr;
+    TC_TRY(cudaHostGetDevicePointer(&dflag, flag, 0));
+    launch_gate(dflag, stream);  // hold the device until most of the work is queued
+    cudaEvent_t origin_ev;
+    TC_TRY(cudaEventCreate(&origin_ev));
+    TC_TRY(cudaEventRecord(origin_ev, stream));
+    std::thread release([flag] {
+        std::this_thread::sleep_for(std::chrono::milliseconds(300));
+        __sync_synchronize();
+        *reinterpret_cast<volatile int*>(flag) = 1;
+    });
+    const bool ok = enqueue_ops(stream, err, nullptr, &tl);
+    release.join();
+    if (!ok) return false;
+    TC_TRY(cudaStreamSynchronize(stream));
+    TC_TRY(cudaDeviceSynchronize());
+    t0.assign(N, 0.f);
+    t1.assign(N, 0.f);
+    for (int i = 0; i < N; ++i) {
+        cudaEventElapsedTime(&t0[i], origin_ev, tl[2 * i]);
+        cudaEventElapsedTime(&t1[i], origin_ev, tl[2 * i + 1]);
+    }
+    for (auto& e : tl) cudaEventDestroy(e);
+    cudaEventDestroy(origin_ev);
+    cudaFreeHost(flag);
+    last_stream_ = stream;
     return true;
 }
 

@@ -43,6 +43,8 @@ class Engine {
     Plan plan;
     bool use_graph = true;
     int n_streams = 6;
+    int bulk_tiles_per_cta = 0;  // trailing-update GEMMs: 0 persistent, else tiles per CTA
+    int bulk_max_ctas = 0;       // persistent trailing-update GEMMs: CTA cap (0 = one per SM)
 
     // enqueue one factorization (import .. export) on `stream`
     bool enqueue(const double* a_in, long long lda_in, double* l_out, long long lda_out, cudaStream_t stream,
@@ -109,7 +111,14 @@ class Engine {
 
     void launch_op(int i, cudaStream_t s);
     void reset_words(cudaStream_t s);
-    bool enqueue_ops(cudaStream_t origin, std::string* err, const HostIO* io = nullptr);
+    bool enqueue_ops(cudaStream_t origin, std::string* err, const HostIO* io = nullptr,
+                     std::vector<cudaEvent_t>* tl = nullptr);
+
+   public:
+    // eager multi-stream run with a timing event before and after every op:
+    // start/end (ms from the first op's start) -- the concurrency timeline
+    bool timeline(const double* a_in, long long lda_in, double* l_out, long long lda_out, cudaStream_t stream,
+                  std::vector<float>& t0, std::vector<float>& t1, std::string* err);
 };
 
 }  // namespace tcb

@@ -655,9 +655,16 @@ void init_tc_attributes() {
                          Geo<KIND_TF32X3>::SMEM_BYTES);
 }
 
-void launch_gemm_tc(const DevCtx& c, int kind, const void* d_probs, int nprob, int tiles, cudaStream_t s) {
+void launch_gemm_tc(const DevCtx& c, int kind, const void* d_probs, int nprob, int tiles, cudaStream_t s,
+                    int max_ctas, int tiles_per_cta) {
     if (tiles <= 0) return;
-    const int grid = tiles < g_sms ? tiles : g_sms;
+    // persistent (tiles_per_cta = 0: one CTA per SM) or a bounded number of
+    // tiles per CTA, so SMs free up between tiles and work on higher-priority
+    // streams is not locked out; max_ctas caps the CTAs resident at once
+    int grid = tiles_per_cta > 0 ? (tiles + tiles_per_cta - 1) / tiles_per_cta : g_sms;
+    if (grid < g_sms && tiles_per_cta > 0) grid = g_sms;
+    if (max_ctas > 0 && grid > max_ctas && tiles_per_cta == 0) grid = max_ctas;
+    if (grid > tiles) grid = tiles;
     const TcProb* p = static_cast<const TcProb*>(d_probs);
     if (kind == KIND_TF32X3)
         k_gemm_tc<KIND_TF32X3><<<grid, Cfg<KIND_TF32X3>::NTHREADS, Geo<KIND_TF32X3>::SMEM_BYTES, s>>>(c, p, nprob,

@@ -72,7 +72,8 @@ size_t tc_prob_size();
 enum { KIND_F16 = 0, KIND_TF32X3 = 1 };
 int tc_build_probs(const DevCtx& c, int kind, const std::vector<DevProb>& probs, std::vector<unsigned char>& out,
                    std::string* err);
-void launch_gemm_tc(const DevCtx& c, int kind, const void* d_probs, int nprob, int tiles, cudaStream_t s);
+void launch_gemm_tc(const DevCtx& c, int kind, const void* d_probs, int nprob, int tiles, cudaStream_t s,
+                    int max_ctas = 0, int tiles_per_cta = 0);
 bool tc_supported();
 
 // standalone block operations on column-major doubles (k_blockops.cu)

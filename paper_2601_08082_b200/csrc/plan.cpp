@@ -227,6 +227,29 @@ void Plan::emit_trsm(Rect B, int p, int lnode) {
 // into one launch per operand class.
 // ---------------------------------------------------------------------------
 
+// the off-diagonal update C21 -= A2 A1^T of one tree_syrk split, at the
+// destination's level (tree.cpp:149)
+GemmProb Plan::syrk_offdiag(int cnode, Rect A) {
+    const Node& C = nodes[cnode];
+    const int n1 = C.n1;
+    const Rect off = blocks[C.block].rect;
+    GemmProb g;
+    g.m = off.m;
+    g.n = off.n;
+    g.k = A.n;
+    g.a_r0 = A.r0 + n1;
+    g.a_c0 = A.c0;
+    g.b_r0 = A.r0;
+    g.b_c0 = A.c0;
+    g.c_r0 = off.r0;
+    g.c_c0 = off.c0;
+    g.exec_level = C.level;
+    g.seq = next_seq();
+    g.ref_kernel = K_GEMM;
+    add_flops(g.seq, C.level, K_GEMM, 2ull * uint64_t(g.m) * uint64_t(g.n) * uint64_t(g.k));
+    return g;
+}
+
 void Plan::collect_syrk(int cnode, Rect A, int p, std::vector<GemmProb>& out) {
     const Node& C = nodes[cnode];
     if (C.leaf) {
@@ -249,33 +272,16 @@ void Plan::collect_syrk(int cnode, Rect A, int p, std::vector<GemmProb>& out) {
         return;
     }
     const int n1 = C.n1;
-    const int d1 = C.d1, d2 = C.d2, lvl = C.level;
-    const Rect off = blocks[C.block].rect;
+    const int d1 = C.d1, d2 = C.d2;
     Rect A1{A.r0, A.c0, n1, A.n};
     Rect A2{A.r0 + n1, A.c0, A.m - n1, A.n};
     collect_syrk(d1, A1, p, out);
-    GemmProb g;
-    g.m = off.m;
-    g.n = off.n;
-    g.k = A.n;
-    g.a_r0 = A2.r0;
-    g.a_c0 = A2.c0;
-    g.b_r0 = A1.r0;
-    g.b_c0 = A1.c0;
-    g.c_r0 = off.r0;
-    g.c_c0 = off.c0;
-    g.exec_level = lvl;
-    g.seq = next_seq();
-    g.ref_kernel = K_GEMM;
-    add_flops(g.seq, lvl, K_GEMM, 2ull * uint64_t(g.m) * uint64_t(g.n) * uint64_t(g.k));
-    out.push_back(g);
+    out.push_back(syrk_offdiag(cnode, A));
     collect_syrk(d2, A2, p, out);
 }
 
-void Plan::emit_syrk(int cnode, Rect A, int p) {
-    std::vector<GemmProb> all;
-    collect_syrk(cnode, A, p, all);
-    // one launch per class, classes in order of first appearance
+// one launch per operand class, classes in order of first appearance
+void Plan::push_gemm_group(const std::vector<GemmProb>& all, int p) {
     std::vector<int> classes;
     for (const auto& g : all) {
         const int c = gemm_class(p, g.exec_level, &g);
@@ -294,8 +300,29 @@ void Plan::emit_syrk(int cnode, Rect A, int p) {
                 op.flops += double(g.lower ? 2.0 * g.m * g.n * g.k / 2.0 : 2.0 * g.m * g.n * g.k);
             }
         op.prob_end = int(probs.size());
+        op.bulk = 1;
         push(std::move(op));
     }
+}
+
+// A large tree_syrk is emitted as separate launches for its diag1 part, its
+// off-diagonal GEMM and its diag2 part (recursively, down to
+// opt.syrk_split_min): the recursion that follows (tree_potrf(diag2) ->
+// tree_potrf(diag2.diag1) -> ...) then starts as soon as the region it reads
+// is updated, while the rest of the update runs beside it (lookahead).  The
+// sequence numbers keep the reference's order either way.
+void Plan::emit_syrk(int cnode, Rect A, int p) {
+    const Node& C = nodes[cnode];
+    if (!C.leaf && C.n >= opt.syrk_split_min) {
+        const int n1 = C.n1, d1 = C.d1, d2 = C.d2;
+        emit_syrk(d1, Rect{A.r0, A.c0, n1, A.n}, p);
+        push_gemm_group({syrk_offdiag(cnode, A)}, p);
+        emit_syrk(d2, Rect{A.r0 + n1, A.c0, A.m - n1, A.n}, p);
+        return;
+    }
+    std::vector<GemmProb> all;
+    collect_syrk(cnode, A, p, all);
+    push_gemm_group(all, p);
 }
 
 // ---------------------------------------------------------------------------

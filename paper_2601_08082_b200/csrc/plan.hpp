@@ -132,6 +132,7 @@ struct Op {
     std::vector<Access> acc;
     std::vector<int> deps;
     double flops = 0;      // algorithmic flops executed (for per-op timing)
+    int bulk = 0;          // 1: trailing (SYRK) update, off the factorization's critical chain
 };
 
 // a require_finite point of the reference (tree.cpp:108, 114, 121): a
@@ -154,6 +155,7 @@ struct PlanOptions {
     bool use_tc32 = true;    // FP32 x FP32 GEMMs on tcgen05 (three-pass TF32)
     bool inverse_trsm = true; // FP16 leaf solves with m >= kInvMinRows as tcgen05 GEMMs
     bool fuse_checks = true;  // require_finite inside the producing kernels
+    int syrk_split_min = 2048; // tree_syrk nodes at least this large launch per region (lookahead)
 };
 
 struct Plan {
@@ -197,6 +199,8 @@ struct Plan {
     void emit_trsm(Rect brect, int p, int lnode);
     void emit_syrk(int cnode, Rect arect, int p);
     void collect_syrk(int cnode, Rect arect, int p, std::vector<GemmProb>& out);
+    GemmProb syrk_offdiag(int cnode, Rect arect);
+    void push_gemm_group(const std::vector<GemmProb>& all, int p);
     void ensure_shadows(int node, int p);
     int push(Op op);
     uint32_t next_seq() { return ++n_seq; }

@@ -25,8 +25,12 @@ def main():
     ap.add_argument("--ncu-pick", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="one serialized run (for ncu)")
     ap.add_argument("--json", default="")
+    ap.add_argument("--opt", action="append", default=[], help="plan option key=value (repeatable)")
     args = ap.parse_args()
     plan = tc.Plan(args.n, args.b, args.cfg)
+    for kv in args.opt:
+        k, v = kv.split("=")
+        plan.set_option(k, int(v))
     nops = plan.stats()["ops"]
     infos = [plan.op_info(i) for i in range(nops)]
     if args.ncu_pick:
