@@ -198,6 +198,11 @@ int tc_plan_set_option(tc_plan* plan, const char* key, int value) {
         e.use_graph = value != 0;
         return TC_OK;
     }
+    if (k == "dag_graph") {
+        if (e.ready() && e.use_graph) return fail(TC_INVALID_ARGUMENT, k + " must be set before the first run");
+        e.dag_graph = value != 0;
+        return TC_OK;
+    }
     if (k == "bulk_tiles_per_cta" || k == "bulk_max_ctas") {
         if (e.ready() && e.use_graph) return fail(TC_INVALID_ARGUMENT, k + " must be set before the first run");
         (k == "bulk_tiles_per_cta" ? e.bulk_tiles_per_cta : e.bulk_max_ctas) = value < 0 ? 0 : value;

@@ -358,6 +358,10 @@ bool Engine::enqueue(const double* a_in, long long lda_in, double* l_out, long l
     TC_TRY(cudaMemcpyAsync(d_ra_, slot, sizeof(RunArgs), cudaMemcpyHostToDevice, stream));
     TC_TRY(cudaEventRecord(ra_ev_[size_t(slot - h_ra_)], stream));
     if (use_graph) {
+        if (!gexec_ && dag_graph) {
+            if (!build_dag_graph(&graph_, nullptr, err)) return false;
+            TC_TRY(cudaGraphInstantiate(&gexec_, graph_, 0));
+        }
         if (!gexec_) {
             cudaStream_t cap;
             TC_TRY(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
@@ -381,6 +385,97 @@ bool Engine::enqueue(const double* a_in, long long lda_in, double* l_out, long l
         if (!enqueue_ops(stream, err)) return false;
     }
     last_stream_ = stream;
+    return true;
+}
+
+bool Engine::build_dag_graph(cudaGraph_t* out, const HostIO* io, std::string* err) {
+    *out = nullptr;
+    const int N = int(plan.ops.size());
+    cudaGraph_t g = nullptr;
+    TC_TRY(cudaGraphCreate(&g, 0));
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaStream_t cap_hi = nullptr, cap_lo = nullptr;
+    TC_TRY(cudaStreamCreateWithPriority(&cap_hi, cudaStreamNonBlocking, hi));
+    TC_TRY(cudaStreamCreateWithPriority(&cap_lo, cudaStreamNonBlocking, lo));
+    bool ok = true;
+    std::string e2;
+    // capture fn on stream s into a child graph and add it with deps
+    auto add = [&](cudaStream_t s, const std::vector<cudaGraphNode_t>& deps, auto&& fn,
+                   cudaGraphNode_t* node) -> bool {
+        cudaGraph_t child = nullptr;
+        if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return false;
+        fn(s);
+        if (cudaStreamEndCapture(s, &child) != cudaSuccess || !child) return false;
+        // the scheduling priority of the capture stream, made explicit on
+        // every kernel node: the chain's CTAs go first when SMs free up
+        size_t nn = 0;
+        cudaGraphGetNodes(child, nullptr, &nn);
+        std::vector<cudaGraphNode_t> kids(nn);
+        if (nn) cudaGraphGetNodes(child, kids.data(), &nn);
+        for (cudaGraphNode_t k : kids) {
+            cudaGraphNodeType ty;
+            if (cudaGraphNodeGetType(k, &ty) == cudaSuccess && ty == cudaGraphNodeTypeKernel) {
+                cudaKernelNodeAttrValue v{};
+                v.priority = s == cap_hi ? hi : lo;
+                cudaGraphKernelNodeSetAttribute(k, cudaKernelNodeAttributePriority, &v);
+            }
+        }
+        cudaGetLastError();
+        const cudaError_t e =
+            cudaGraphAddChildGraphNode(node, g, deps.empty() ? nullptr : deps.data(), deps.size(), child);
+        cudaGraphDestroy(child);
+        return e == cudaSuccess;
+    };
+    cudaGraphNode_t root = nullptr;
+    ok = add(cap_hi, {}, [&](cudaStream_t s) { reset_words(s); }, &root);
+    // host IO: H2D per block (chained, depth-first order) and D2H per export
+    std::vector<cudaGraphNode_t> h2d(plan.blocks.size(), nullptr);
+    const int n = plan.n;
+    const size_t esz = sizeof(double);
+    if (ok && io) {
+        cudaGraphNode_t prev = root;
+        for (int b : plan.block_order) {
+            const Rect& r = plan.blocks[b].rect;
+            ok = add(cap_lo, {prev}, [&](cudaStream_t s) {
+                     cudaMemcpy2DAsync(d_stage_ + size_t(r.c0) * n + r.r0, esz * n,
+                                       io->host + size_t(r.c0) * io->lda + r.r0, esz * io->lda, esz * size_t(r.m),
+                                       size_t(r.n), cudaMemcpyHostToDevice, s);
+                 }, &h2d[size_t(b)]);
+            if (!ok) break;
+            prev = h2d[size_t(b)];
+        }
+    }
+    std::vector<cudaGraphNode_t> node(size_t(N), nullptr);
+    cudaGraphNode_t prev_d2h = root;
+    for (int i = 0; ok && i < N; ++i) {
+        const Op& op = plan.ops[i];
+        std::vector<cudaGraphNode_t> deps;
+        for (int d : op.deps) deps.push_back(node[size_t(d)]);
+        if (io && (op.type == OP_IMPORT || op.type == OP_QUANT))
+            for (int b : op.blocks) deps.push_back(h2d[size_t(b)]);
+        if (deps.empty()) deps.push_back(root);
+        ok = add(op.bulk ? cap_lo : cap_hi, deps, [&](cudaStream_t s) { launch_op(i, s); }, &node[size_t(i)]);
+        if (ok && io && op.type == OP_EXPORT) {
+            const Rect& r = op.rect;
+            cudaGraphNode_t d2h = nullptr;
+            ok = add(cap_lo, {node[size_t(i)], prev_d2h}, [&](cudaStream_t s) {
+                     cudaMemcpy2DAsync(io->host + size_t(r.c0) * io->lda + r.r0, esz * io->lda,
+                                       d_stage_ + size_t(r.c0) * n + r.r0, esz * n, esz * size_t(r.m), size_t(r.n),
+                                       cudaMemcpyDeviceToHost, s);
+                 }, &d2h);
+            prev_d2h = d2h;
+        }
+    }
+    cudaStreamDestroy(cap_hi);
+    cudaStreamDestroy(cap_lo);
+    if (!ok) {
+        cudaGetLastError();
+        cudaGraphDestroy(g);
+        if (err) *err = "building the DAG graph failed";
+        return false;
+    }
+    *out = g;
     return true;
 }
 
@@ -416,20 +511,24 @@ bool Engine::enqueue_host(double* host, long long lda, cudaStream_t stream, std:
             if (hgraph_) cudaGraphDestroy(hgraph_);
             hexec_ = nullptr;
             hgraph_ = nullptr;
-            cudaStream_t cap;
-            TC_TRY(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
-            TC_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
-            std::string e2;
-            const bool ok = enqueue_ops(cap, &e2, &io);
             cudaGraph_t g = nullptr;
-            const cudaError_t ce = cudaStreamEndCapture(cap, &g);
-            cudaStreamDestroy(cap);
-            if (!ok) {
-                if (err) *err = e2;
-                if (g) cudaGraphDestroy(g);
-                return false;
+            if (dag_graph) {
+                if (!build_dag_graph(&g, &io, err)) return false;
+            } else {
+                cudaStream_t cap;
+                TC_TRY(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+                TC_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+                std::string e2;
+                const bool ok = enqueue_ops(cap, &e2, &io);
+                const cudaError_t ce = cudaStreamEndCapture(cap, &g);
+                cudaStreamDestroy(cap);
+                if (!ok) {
+                    if (err) *err = e2;
+                    if (g) cudaGraphDestroy(g);
+                    return false;
+                }
+                TC_TRY(ce);
             }
-            TC_TRY(ce);
             hgraph_ = g;
             TC_TRY(cudaGraphInstantiate(&hexec_, hgraph_, 0));
             hkey_ = host;

@@ -45,6 +45,7 @@ class Engine {
     int n_streams = 6;
     int bulk_tiles_per_cta = 0;  // trailing-update GEMMs: 0 persistent, else tiles per CTA
     int bulk_max_ctas = 0;       // persistent trailing-update GEMMs: CTA cap (0 = one per SM)
+    bool dag_graph = true;       // explicit DAG graph (else: captured multi-stream enqueue)
 
     // enqueue one factorization (import .. export) on `stream`
     bool enqueue(const double* a_in, long long lda_in, double* l_out, long long lda_out, cudaStream_t stream,
@@ -113,6 +114,10 @@ class Engine {
     void reset_words(cudaStream_t s);
     bool enqueue_ops(cudaStream_t origin, std::string* err, const HostIO* io = nullptr,
                      std::vector<cudaEvent_t>* tl = nullptr);
+    // the op DAG as an explicit CUDA graph: one child-graph node per op (its
+    // launch captured alone), edges = the plan's dependencies only -- no
+    // stream-order edges between independent ops
+    bool build_dag_graph(cudaGraph_t* out, const HostIO* io, std::string* err);
 
    public:
     // eager multi-stream run with a timing event before and after every op:

@@ -250,3 +250,35 @@ def test_singular_diagonal_detail(tc, oracle, n):
 def test_spd_generate_device_bit_exact(tc, oracle):
     a = tc.from_device(tc.spd_generate_device(300, 77))
     assert np.array_equal(a, oracle.spd_generate(300, 77))
+
+
+def test_c2_matches_reference_golden(tc):
+    """BASELINE config C2 (N=8192, b=256, [F16, F32, F64], seed 42) against
+    tests/golden/c2.json: the oracle's outcome (1.8759406e-06), equal to the
+    compiled reference's (1.875941e-06)."""
+    import json
+    import os
+    import torch
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "c2.json")))
+    a = tc.spd_generate_device(g["n"], g["seed"])
+    l = torch.empty_like(a)
+    plan = tc.Plan(g["n"], g["b"], g["config"])
+    st = plan.factor_device(a, l)
+    assert st.status == g["status"] == "ok"
+    assert list(plan.run_flops().as_tuple()) == g["flops"]
+    rel = tc.factorization_error_device(a, l)
+    assert rel <= 2 * g["rel_error"], (rel, g["rel_error"])
+
+
+def test_c1_ten_seed_median_within_2x(tc, oracle):
+    """C1 (N=1024, b=128, [F16, F64]) over seeds 0-9: the median
+    backward error within 2x of the reference's median."""
+    rel_g, rel_o = [], []
+    for seed in range(10):
+        a = oracle.spd_generate(1024, seed)
+        st_o, _, _, r_o, _ = oracle.factor(a, 128, parse_levels("[F16, F64]"))
+        st, _, r, _ = _run(tc, a, 128, "[F16, F64]")
+        assert st.status == st_o == "ok"
+        rel_g.append(r)
+        rel_o.append(r_o)
+    assert np.median(rel_g) <= 2 * np.median(rel_o), (np.median(rel_g), np.median(rel_o))
