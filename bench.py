@@ -377,7 +377,7 @@ def main():
     ap.add_argument("--ref-n", dest="ref_n", type=int, default=1536)
     ap.add_argument("--c4-count", dest="c4_count", type=int, default=64)
     ap.add_argument("--c4-n", dest="c4_n", type=int, default=16384)
-    ap.add_argument("--c4-conc", dest="c4_conc", type=int, default=4)
+    ap.add_argument("--c4-conc", dest="c4_conc", type=int, default=8)
     ap.add_argument("--variants", action="store_true",
                     help="also time Pure F16 / Pure F64 trees (bounds) at N; slow (F64 runs on SIMT)")
     args = ap.parse_args()

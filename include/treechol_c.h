@@ -146,6 +146,9 @@ typedef struct tc_batch tc_batch;
 int tc_batch_create(int n, int b, const int* levels, int nlevels, int quantize, int concurrency,
                     tc_batch** out);
 void tc_batch_destroy(tc_batch* batch);
+/* execution knobs of every plan of the batch (bulk_tiles_per_cta, dag_graph,
+ * use_graph; see tc_plan_set_option), before the first run */
+int tc_batch_set_option(tc_batch* batch, const char* key, int value);
 /* Factors dA[k] in place (device, column-major, lda) for k < count and, if
  * dB && dB[k], solves A X = B for its nrhs right-hand sides (dB[k], ldb,
  * overwritten by X).  status[k] = tc_status of system k; index[k] (optional)

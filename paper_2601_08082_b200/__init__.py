@@ -128,6 +128,7 @@ def _load():
         "tc_debug_gemm": (I, [I, I, I, I, I, D, I, I, C.POINTER(C.c_float)]),
         "tc_batch_create": (I, [I, I, PI, I, I, I, C.POINTER(P)]),
         "tc_batch_destroy": (None, [P]),
+        "tc_batch_set_option": (I, [P, C.c_char_p, I]),
         "tc_batch_run": (I, [P, I, C.POINTER(P), I, C.POINTER(P), I, I, PI, PI]),
         "tc_last_error": (C.c_char_p, []),
         "tc_device_available": (I, []),
@@ -456,6 +457,9 @@ class Batch:
         if h and _lib is not None:
             _lib.tc_batch_destroy(h)
             self._h = None
+
+    def set_option(self, key: str, value: int):
+        _raise(_lib.tc_batch_set_option(self._h, key.encode(), int(value)))
 
     def run(self, a_list, b_list=None):
         """factor every a_list[k] in place (device column-major tensors, see

@@ -60,14 +60,19 @@ def synthetic_spd_device(n: int, seed: int, device="cuda"):
     return a
 
 
-def run_batch_on_rank(count: int, n: int, b: int, config, seed0: int = 0, nrhs: int = 1, concurrency: int = 4,
-                      world: int = 1, rank: int = 0, group=None, check: int = 1, in_flight: int = 8):
+def run_batch_on_rank(count: int, n: int, b: int, config, seed0: int = 0, nrhs: int = 1, concurrency: int = 8,
+                      world: int = 1, rank: int = 0, group=None, check: int = 1, in_flight: int = 16):
     """factor + solve this rank's share of a batch of `count` systems (seeds
     seed0 + k).  Returns (local ShardResult, reduced ShardResult, flops)."""
     import torch
     import paper_2601_08082_b200 as tc
     mine = shard(count, world, rank)
     batch = tc.Batch(n, b, config, True, concurrency)
+    # warm-up (untimed): builds every plan's workspace and CUDA graph
+    warm = [synthetic_spd_device(n, seed0 + 10 ** 6 + k) for k in range(concurrency)]
+    batch.run(warm)
+    del warm
+    torch.cuda.synchronize()
     failed, worst, dev_ms = 0, 0.0, 0.0
     ks = list(mine)
     for c0 in range(0, len(ks), in_flight):

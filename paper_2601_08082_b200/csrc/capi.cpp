@@ -465,11 +465,13 @@ int tc_potrs_device(int n, const double* dL, int ldl, double* dB, int ldb, int n
     if (!tc_device_available()) return fail(TC_NO_DEVICE, "no CUDA device");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int nb = (n + 63) / 64;
-    int* d_cnt = nullptr;
-    cudaError_t e = cudaMallocAsync(&d_cnt, sizeof(int) * size_t(nb + 1) * size_t(nrhs), s);
+    double* d_work = nullptr;
+    cudaError_t e = cudaMallocAsync(&d_work, sizeof(double) * potrs_work_doubles(n, nrhs) +
+                                                 sizeof(int) * size_t(nb + 1) * size_t(nrhs), s);
     if (e != cudaSuccess) return cuda_fail(e, "alloc");
-    launch_potrs(n, dL, ldl, dB, ldb, nrhs, d_cnt, nullptr, s);
-    cudaFreeAsync(d_cnt, s);
+    int* d_cnt = reinterpret_cast<int*>(d_work + potrs_work_doubles(n, nrhs));
+    launch_potrs(n, dL, ldl, dB, ldb, nrhs, d_cnt, d_work, s);
+    cudaFreeAsync(d_work, s);
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "potrs");
     return TC_OK;

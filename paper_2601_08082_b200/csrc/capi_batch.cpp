@@ -66,6 +66,19 @@ int tc_batch_create(int n, int b, const int* levels, int nlevels, int quantize, 
 
 void tc_batch_destroy(tc_batch* bt) { delete bt; }
 
+int tc_batch_set_option(tc_batch* bt, const char* key, int value) {
+    if (!bt || !key) return bfail(TC_INVALID_ARGUMENT, "null argument");
+    const std::string k = key;
+    for (auto& e : bt->eng) {
+        if (e->ready()) return bfail(TC_INVALID_ARGUMENT, k + " must be set before the first run");
+        if (k == "bulk_tiles_per_cta") e->bulk_tiles_per_cta = value < 0 ? 0 : value;
+        else if (k == "dag_graph") e->dag_graph = value != 0;
+        else if (k == "use_graph") e->use_graph = value != 0;
+        else return bfail(TC_INVALID_ARGUMENT, "unknown option '" + k + "'");
+    }
+    return TC_OK;
+}
+
 int tc_batch_run(tc_batch* bt, int count, double* const* dA, int lda, double* const* dB, int ldb, int nrhs,
                  int* status, int* index) {
     if (!bt || count < 0 || (count > 0 && (!dA || !status))) return bfail(TC_INVALID_ARGUMENT, "bad arguments");
@@ -99,11 +112,14 @@ int tc_batch_run(tc_batch* bt, int count, double* const* dA, int lda, double* co
         if (dB && dB[k]) {
             // POTRS on the factor just written
             const int nb = (n + 63) / 64;
-            int* d_cnt = nullptr;
-            if (cudaMallocAsync(&d_cnt, sizeof(int) * size_t(nb + 1) * size_t(nrhs), s) != cudaSuccess)
+            double* d_work = nullptr;
+            if (cudaMallocAsync(&d_work, sizeof(double) * potrs_work_doubles(n, nrhs) +
+                                             sizeof(int) * size_t(nb + 1) * size_t(nrhs),
+                                s) != cudaSuccess)
                 return bfail(TC_CUDA_ERROR, "cudaMallocAsync");
-            launch_potrs(n, dA[k], lda, dB[k], ldb, nrhs, d_cnt, nullptr, s);
-            cudaFreeAsync(d_cnt, s);
+            launch_potrs(n, dA[k], lda, dB[k], ldb, nrhs,
+                         reinterpret_cast<int*>(d_work + potrs_work_doubles(n, nrhs)), d_work, s);
+            cudaFreeAsync(d_work, s);
         }
     }
     for (auto s : bt->streams)

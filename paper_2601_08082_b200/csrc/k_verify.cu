@@ -130,126 +130,131 @@ __device__ __forceinline__ void st_release(int* p, int v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// forward: y = L^-1 b, in place on b.  counters: [0] ticket, [1..nb] flags
+// diagonal-block inverses W_I = inv(L(I,I)) (64 x 64, row-major at W + I*64*64),
+// one CTA per block, one thread per column (independent forward
+// substitutions): they take the 64-step dependent solve off the block chain
+// of the substitutions below
+__global__ void __launch_bounds__(VT) k_potrs_diaginv(int n, const double* __restrict__ Lm, long long ldl,
+                                                     double* __restrict__ W) {
+    __shared__ double Ls[VT][VT + 1];
+    const int I = blockIdx.x, i0 = I * VT, rows = min(VT, n - i0), t = threadIdx.x;
+    for (int c = 0; c < VT; ++c) Ls[t][c] = (t < rows && c < rows && t >= c) ? Lm[(long long)(i0 + c) * ldl + i0 + t] : 0.0;
+    __syncthreads();
+    double* Wi = W + size_t(I) * VT * VT;
+    double w[VT];
+#pragma unroll
+    for (int i = 0; i < VT; ++i) {
+        double s = (i == t) ? 1.0 : 0.0;
+#pragma unroll
+        for (int k = 0; k < i; ++k) s = fma(-Ls[i][k], w[k], s);
+        w[i] = (i >= t && i < rows) ? s / Ls[i][i] : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < VT; ++i) Wi[i * VT + t] = w[i];
+}
+
+// forward: y = L^-1 b, in place on b.  counters: [0] ticket, [1..nb] flags.
+// Block I (64 rows) claims a ticket, accumulates L(I,J) y_J for every
+// finished J < I as their flags appear (coalesced column reads of L), then
+// y_I = W_I (b_I - sum) -- a 64x64 product, no dependent chain.
 __global__ void __launch_bounds__(256) k_potrs_fwd(int n, const double* __restrict__ Lm, long long ldl, double* B,
-                                                   long long ldb, int* counters) {
+                                                   long long ldb, int* counters, const double* __restrict__ W) {
     const int nb = (n + VT - 1) / VT;
     int* cnt = counters + blockIdx.y * (nb + 1);
     double* y = B + blockIdx.y * ldb;
     __shared__ int sI;
     __shared__ double part[4][VT];
-    __shared__ double yb[VT];
+    __shared__ double rhs[VT];
     if (threadIdx.x == 0) sI = atomicAdd(cnt, 1);
     __syncthreads();
     const int I = sI;
     const int i0 = I * VT;
+    const int rows = min(VT, n - i0);
     const int r = threadIdx.x & 63, q = threadIdx.x >> 6;
     const int gi = i0 + r;
+    // this block's W row segment does not depend on the chain: load it first
+    const double* Wi = W + size_t(I) * VT * VT;
+    double wv[16];
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) wv[kk] = Wi[r * VT + q * 16 + kk];
     double acc = 0.0;
     for (int J = 0; J < I; ++J) {
+        // L(I, J) is read before waiting for y_J (off the chain)
+        const int k0 = J * VT + q * 16;
+        double lv[16];
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) lv[kk] = gi < n ? Lm[(long long)(k0 + kk) * ldl + gi] : 0.0;
         if (threadIdx.x == 0)
             while (ld_acquire(cnt + 1 + J) == 0) {
             }
         __syncthreads();
-        const int k0 = J * VT + q * 16;
-        if (gi < n)
-#pragma unroll 4
-            for (int kk = 0; kk < 16; ++kk) {
-                const int k = k0 + kk;
-                acc = fma(Lm[(long long)k * ldl + gi], __ldcg(y + k), acc);
-            }
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) acc = fma(lv[kk], __ldcg(y + k0 + kk), acc);
     }
     part[q][r] = acc;
     __syncthreads();
-    if (threadIdx.x < 32) {
-        // diagonal block solve by one warp: lane l owns rows l and l + 32
-        double v[2];
-        for (int h = 0; h < 2; ++h) {
-            const int rr = threadIdx.x + 32 * h, g = i0 + rr;
-            v[h] = g < n ? y[g] - (part[0][rr] + part[1][rr] + part[2][rr] + part[3][rr]) : 0.0;
-        }
-        const int rows = min(VT, n - i0);
-        for (int k = 0; k < rows; ++k) {
-            const int owner = k & 31, h = k >> 5;
-            double xk = __shfl_sync(0xffffffffu, h ? v[1] : v[0], owner);
-            xk = xk / Lm[(long long)(i0 + k) * ldl + i0 + k];
-            if (threadIdx.x == owner) {
-                if (h) v[1] = xk;
-                else v[0] = xk;
-            }
-            for (int hh = 0; hh < 2; ++hh) {
-                const int rr = threadIdx.x + 32 * hh;
-                if (rr > k && rr < rows) v[hh] -= Lm[(long long)(i0 + k) * ldl + i0 + rr] * xk;
-            }
-        }
-        for (int h = 0; h < 2; ++h) {
-            const int rr = threadIdx.x + 32 * h;
-            if (rr < rows) y[i0 + rr] = v[h];
-        }
-        __threadfence();
-        __syncwarp();
-        if (threadIdx.x == 0) st_release(cnt + 1 + I, 1);
-    }
+    if (threadIdx.x < VT) rhs[r] = r < rows ? y[gi] - (part[0][r] + part[1][r] + part[2][r] + part[3][r]) : 0.0;
+    __syncthreads();
+    // y_I = W_I rhs: 4 partial dot products per row
+    double s = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) s = fma(wv[kk], rhs[q * 16 + kk], s);
+    part[q][r] = s;
+    __syncthreads();
+    if (threadIdx.x < VT && r < rows) y[gi] = part[0][r] + part[1][r] + part[2][r] + part[3][r];
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) st_release(cnt + 1 + I, 1);
 }
 
-// backward: x = L^-T y, in place, blocks in reverse order
+// backward: x = L^-T y, in place, blocks in reverse order; x_I = W_I^T (y_I - sum)
 __global__ void __launch_bounds__(256) k_potrs_bwd(int n, const double* __restrict__ Lm, long long ldl, double* B,
-                                                   long long ldb, int* counters) {
+                                                   long long ldb, int* counters, const double* __restrict__ W) {
     const int nb = (n + VT - 1) / VT;
     int* cnt = counters + blockIdx.y * (nb + 1);
     double* y = B + blockIdx.y * ldb;
     __shared__ int sI;
     __shared__ double part[4][VT];
+    __shared__ double rhs[VT];
     if (threadIdx.x == 0) sI = nb - 1 - atomicAdd(cnt, 1);
     __syncthreads();
     const int I = sI;
     const int i0 = I * VT;
+    const int rows = min(VT, n - i0);
     const int r = threadIdx.x & 63, q = threadIdx.x >> 6;
     const int gi = i0 + r;  // x_gi needs sum_{k > block} L(k, gi) x_k
+    const double* Wi = W + size_t(I) * VT * VT;
+    double wv[16];
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) wv[kk] = Wi[(q * 16 + kk) * VT + r];
     double acc = 0.0;
     for (int J = nb - 1; J > I; --J) {
+        const int k0 = J * VT + q * 16;
+        double lv[16];
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) lv[kk] = (gi < n && k0 + kk < n) ? Lm[(long long)gi * ldl + k0 + kk] : 0.0;
         if (threadIdx.x == 0)
             while (ld_acquire(cnt + 1 + J) == 0) {
             }
         __syncthreads();
-        const int k0 = J * VT + q * 16;
-        if (gi < n)
-            for (int kk = 0; kk < 16; ++kk) {
-                const int k = k0 + kk;
-                if (k < n) acc = fma(Lm[(long long)gi * ldl + k], __ldcg(y + k), acc);
-            }
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk)
+            if (k0 + kk < n) acc = fma(lv[kk], __ldcg(y + k0 + kk), acc);
     }
     part[q][r] = acc;
     __syncthreads();
-    if (threadIdx.x < 32) {
-        double v[2];
-        const int rows = min(VT, n - i0);
-        for (int h = 0; h < 2; ++h) {
-            const int rr = threadIdx.x + 32 * h, g = i0 + rr;
-            v[h] = rr < rows ? y[g] - (part[0][rr] + part[1][rr] + part[2][rr] + part[3][rr]) : 0.0;
-        }
-        for (int k = rows - 1; k >= 0; --k) {
-            const int owner = k & 31, h = k >> 5;
-            double xk = __shfl_sync(0xffffffffu, h ? v[1] : v[0], owner);
-            xk = xk / Lm[(long long)(i0 + k) * ldl + i0 + k];
-            if (threadIdx.x == owner) {
-                if (h) v[1] = xk;
-                else v[0] = xk;
-            }
-            for (int hh = 0; hh < 2; ++hh) {
-                const int rr = threadIdx.x + 32 * hh;
-                // row rr < k of L^T: x_rr -= L(k, rr) x_k
-                if (rr < k) v[hh] -= Lm[(long long)(i0 + rr) * ldl + i0 + k] * xk;
-            }
-        }
-        for (int h = 0; h < 2; ++h) {
-            const int rr = threadIdx.x + 32 * h;
-            if (rr < rows) y[i0 + rr] = v[h];
-        }
-        __threadfence();
-        __syncwarp();
-        if (threadIdx.x == 0) st_release(cnt + 1 + I, 1);
-    }
+    if (threadIdx.x < VT) rhs[r] = r < rows ? y[gi] - (part[0][r] + part[1][r] + part[2][r] + part[3][r]) : 0.0;
+    __syncthreads();
+    // x_I = W_I^T rhs
+    double s = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) s = fma(wv[kk], rhs[q * 16 + kk], s);
+    part[q][r] = s;
+    __syncthreads();
+    if (threadIdx.x < VT && r < rows) y[gi] = part[0][r] + part[1][r] + part[2][r] + part[3][r];
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) st_release(cnt + 1 + I, 1);
 }
 
 // ---------------------------------------------------------------- residual
@@ -325,16 +330,17 @@ void launch_fact_error(int n, const double* dA, long long lda, const double* dL,
     k_fact_error_final<<<1, 256, 0, s>>>(d_partials, tiles, d_nonfinite, d_partials + 2 * size_t(tiles));
 }
 
-size_t potrs_work_doubles(int n, int nrhs) { return 0; }
+size_t potrs_work_doubles(int n, int nrhs) { return size_t((n + VT - 1) / VT) * VT * VT; }
 
 void launch_potrs(int n, const double* dL, long long ldl, double* dB, long long ldb, int nrhs, int* d_counters,
-                  double*, cudaStream_t s) {
+                  double* d_work, cudaStream_t s) {
     const int nb = (n + VT - 1) / VT;
     const size_t cbytes = sizeof(int) * size_t(nb + 1) * size_t(nrhs);
+    k_potrs_diaginv<<<nb, VT, 0, s>>>(n, dL, ldl, d_work);
     cudaMemsetAsync(d_counters, 0, cbytes, s);
-    k_potrs_fwd<<<dim3(nb, nrhs), 256, 0, s>>>(n, dL, ldl, dB, ldb, d_counters);
+    k_potrs_fwd<<<dim3(nb, nrhs), 256, 0, s>>>(n, dL, ldl, dB, ldb, d_counters, d_work);
     cudaMemsetAsync(d_counters, 0, cbytes, s);
-    k_potrs_bwd<<<dim3(nb, nrhs), 256, 0, s>>>(n, dL, ldl, dB, ldb, d_counters);
+    k_potrs_bwd<<<dim3(nb, nrhs), 256, 0, s>>>(n, dL, ldl, dB, ldb, d_counters, d_work);
 }
 
 int residual_partials(int n) { return (n + VT - 1) / VT; }

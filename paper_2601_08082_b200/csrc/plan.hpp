@@ -155,7 +155,7 @@ struct PlanOptions {
     bool use_tc32 = true;    // FP32 x FP32 GEMMs on tcgen05 (three-pass TF32)
     bool inverse_trsm = true; // FP16 leaf solves with m >= kInvMinRows as tcgen05 GEMMs
     bool fuse_checks = true;  // require_finite inside the producing kernels
-    int syrk_split_min = 1024; // tree_syrk nodes at least this large launch per region (lookahead)
+    int syrk_split_min = 1 << 30; // tree_syrk nodes at least this large launch per region (lookahead; off by default: it shortens the critical path but adds launches, a net loss for batches)
 };
 
 struct Plan {
