@@ -103,24 +103,29 @@ int tc_batch_run(tc_batch* bt, int count, double* const* dA, int lda, double* co
             return bfail(TC_CUDA_ERROR, "cudaMallocHost");
         bt->cap = count;
     }
+    // all factorizations first, then the solves: the substitutions are
+    // block chains that keep their CTAs resident while they wait, so mixing
+    // them into the factorizations would take SMs from the concurrent plans
     for (int k = 0; k < count; ++k) {
         const int e = k % C;
         Engine& eng = *bt->eng[size_t(e)];
         cudaStream_t s = bt->streams[size_t(e)];
         if (!eng.enqueue(dA[k], lda, dA[k], lda, s, &err)) return bfail(TC_CUDA_ERROR, err);
         if (!eng.copy_status(bt->h_status + k, s, &err)) return bfail(TC_CUDA_ERROR, err);
-        if (dB && dB[k]) {
-            // POTRS on the factor just written
-            const int nb = (n + 63) / 64;
-            double* d_work = nullptr;
-            if (cudaMallocAsync(&d_work, sizeof(double) * potrs_work_doubles(n, nrhs) +
-                                             sizeof(int) * size_t(nb + 1) * size_t(nrhs),
-                                s) != cudaSuccess)
-                return bfail(TC_CUDA_ERROR, "cudaMallocAsync");
-            launch_potrs(n, dA[k], lda, dB[k], ldb, nrhs,
-                         reinterpret_cast<int*>(d_work + potrs_work_doubles(n, nrhs)), d_work, s);
-            cudaFreeAsync(d_work, s);
-        }
+    }
+    for (int k = 0; dB && k < count; ++k) {
+        if (!dB[k]) continue;
+        cudaStream_t s = bt->streams[size_t(k % C)];
+        // POTRS on the factor just written
+        const int nb = (n + 63) / 64;
+        double* d_work = nullptr;
+        if (cudaMallocAsync(&d_work, sizeof(double) * potrs_work_doubles(n, nrhs) +
+                                         sizeof(int) * size_t(nb + 1) * size_t(nrhs),
+                            s) != cudaSuccess)
+            return bfail(TC_CUDA_ERROR, "cudaMallocAsync");
+        launch_potrs(n, dA[k], lda, dB[k], ldb, nrhs, reinterpret_cast<int*>(d_work + potrs_work_doubles(n, nrhs)),
+                     d_work, s);
+        cudaFreeAsync(d_work, s);
     }
     for (auto s : bt->streams)
         if (cudaStreamSynchronize(s) != cudaSuccess) return bfail(TC_CUDA_ERROR, "batch synchronize");
