@@ -130,6 +130,12 @@ def _load():
         "tc_batch_destroy": (None, [P]),
         "tc_batch_set_option": (I, [P, C.c_char_p, I]),
         "tc_batch_run": (I, [P, I, C.POINTER(P), I, C.POINTER(P), I, I, PI, PI]),
+        "tc_round_host": (I, [I, I, P, I, I, I]),
+        "tc_quantize_host": (I, [I, I, P, I, I, C.POINTER(D)]),
+        "tc_dequantize_host": (I, [I, I, P, I, I, D]),
+        "tc_potrf_leaf_host": (I, [I, P, I, I, I, PI]),
+        "tc_trsm_leaf_host": (I, [I, I, P, I, P, I, I, I, PI]),
+        "tc_gemm_mixed_host": (I, [I, I, I, P, I, P, I, P, I, D, D, I, I, I]),
         "tc_last_error": (C.c_char_p, []),
         "tc_device_available": (I, []),
         "tc_version": (C.c_char_p, []),
@@ -479,6 +485,74 @@ class Batch:
         if code not in (TC_OK, TC_NPD, TC_BREAKDOWN, TC_SINGULAR):
             _raise(code)
         return [_STATUS_NAMES[st[i]] for i in range(k)]
+
+
+# ---------------------------------------------------------------- kernels.hpp / tree.hpp block ops
+# The reference's kernel-level API on host Fortran float64 arrays, executed
+# on the device in the reference's scalar operation order (k_blockops.cu).
+
+def _fortran(x, what):
+    if not (isinstance(x, np.ndarray) and x.dtype == np.float64 and x.flags.f_contiguous):
+        raise InvalidArgument(f"{what} must be a Fortran-ordered float64 array")
+    return x
+
+
+def round_matrix(tile: np.ndarray, level: int, lower: bool = False):
+    """kernels.cpp:9-16 (round_lower of tree.cpp:33-40 with lower=True)"""
+    t = _fortran(tile, "tile")
+    _raise(_lib.tc_round_host(t.shape[0], t.shape[1], t.ctypes.data, t.shape[0], level, int(lower)))
+
+
+def quantize_block(b: np.ndarray, target: int) -> float:
+    """tree.cpp:80-95; returns alpha"""
+    t = _fortran(b, "b")
+    al = C.c_double()
+    _raise(_lib.tc_quantize_host(t.shape[0], t.shape[1], t.ctypes.data, t.shape[0], target, C.byref(al)))
+    return al.value
+
+
+def dequantize_block(b: np.ndarray, alpha: float, level: int):
+    """tree.cpp:97-104"""
+    t = _fortran(b, "b")
+    _raise(_lib.tc_dequantize_host(t.shape[0], t.shape[1], t.ctypes.data, t.shape[0], level, float(alpha)))
+
+
+def potrf_leaf(a: np.ndarray, level: int, acc: int = SINGLE):
+    """kernels.cpp:42-69 in place; NotPositiveDefinite(local index)"""
+    t = _fortran(a, "a")
+    bad = C.c_int(-1)
+    code = _lib.tc_potrf_leaf_host(t.shape[0], t.ctypes.data, t.shape[0], level, acc, C.byref(bad))
+    if code == TC_NPD:
+        raise NotPositiveDefinite(bad.value)
+    _raise(code)
+
+
+def trsm_leaf(b: np.ndarray, l: np.ndarray, level: int, acc: int = SINGLE):
+    """kernels.cpp:71-92: B <- B L^-T in place; SingularDiagonal(local index)"""
+    tb, tl = _fortran(b, "b"), _fortran(l, "l")
+    bad = C.c_int(-1)
+    code = _lib.tc_trsm_leaf_host(tb.shape[0], tb.shape[1], tb.ctypes.data, tb.shape[0], tl.ctypes.data,
+                                  tl.shape[0], level, acc, C.byref(bad))
+    if code == TC_SINGULAR:
+        raise SingularDiagonal(bad.value)
+    _raise(code)
+
+
+def gemm_mixed(c: np.ndarray, a: np.ndarray, b: np.ndarray, alpha: float, beta: float, level: int,
+               acc: int = SINGLE):
+    """kernels.cpp:114-132: C <- beta C + alpha A B^T in place"""
+    tc_, ta, tb = _fortran(c, "c"), _fortran(a, "a"), _fortran(b, "b")
+    _raise(_lib.tc_gemm_mixed_host(tc_.shape[0], tc_.shape[1], ta.shape[1], tc_.ctypes.data, tc_.shape[0],
+                                   ta.ctypes.data, ta.shape[0], tb.ctypes.data, tb.shape[0], float(alpha),
+                                   float(beta), level, acc, 0))
+
+
+def syrk_leaf(c: np.ndarray, a: np.ndarray, alpha: float, beta: float, level: int, acc: int = SINGLE):
+    """kernels.cpp:94-112: lower(C) <- beta C + alpha A A^T in place"""
+    tc_, ta = _fortran(c, "c"), _fortran(a, "a")
+    _raise(_lib.tc_gemm_mixed_host(tc_.shape[0], tc_.shape[0], ta.shape[1], tc_.ctypes.data, tc_.shape[0],
+                                   ta.ctypes.data, ta.shape[0], ta.ctypes.data, ta.shape[0], float(alpha),
+                                   float(beta), level, acc, 1))
 
 
 # ---------------------------------------------------------------- analysis.hpp
