@@ -244,9 +244,16 @@ def run_ours(args):
             tc_ms += t
             tc_fl += info["flops"]
     achieved = tc_fl / (tc_ms * 1e-3) / 1e12 if tc_ms else 0.0
+    # DRAM traffic per launch of the same kernel, from the committed ncu
+    # launch list of this command (profiles/ncu_traffic.json)
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
     roofline = {"bound": "tensor", "kernel": "k_gemm_tc (tcgen05 kind::f16, FP32 accumulate)",
                 "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
-                "frac": achieved / peaks["bf16_tflops"], "traffic": None,
+                "frac": achieved / peaks["bf16_tflops"], "traffic": traffic, "traffic_unit": "bytes/launch (ncu)",
                 "peak_kind": f"{peak_kind} bf16 burst (MEASURED_PEAKS.json)",
                 "share_of_step": tc_ms / tot_ms if tot_ms else None,
                 "launches": by_type.get("gemm/tc16", [0, 0, 0])[2]}

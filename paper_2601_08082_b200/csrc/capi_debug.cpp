@@ -27,12 +27,13 @@ extern "C" int tc_debug_gemm(int gclass, int m, int n, int k, int lower, double 
     void* buf = nullptr;
     unsigned long long* words = nullptr;
     const size_t elems = size_t(rows) * size_t(ldw);
-    if (cudaMalloc(&buf, elems * (2 + 4)) != cudaSuccess) return TC_CUDA_ERROR;
+    if (cudaMalloc(&buf, elems * (2 + 4 + 8)) != cudaSuccess) return TC_CUDA_ERROR;
     cudaMalloc(&words, 64);
-    cudaMemset(buf, 0, elems * 6);
+    cudaMemset(buf, 0, elems * 14);
     cudaMemset(words, 0xFF, 8);
     c.b16 = static_cast<__half*>(buf);
     c.b32 = reinterpret_cast<float*>(c.b16 + elems);
+    c.b64 = reinterpret_cast<double*>(c.b32 + elems);
     c.status = words;
     init_tc_attributes();
     DevProb d{};

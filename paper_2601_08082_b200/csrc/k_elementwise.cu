@@ -18,9 +18,10 @@ namespace {
 
 constexpr int TS = 32;  // tile side
 
-__global__ void __launch_bounds__(256) k_import(DevCtx c, const BlockDesc* blocks, int nb) {
+// grid-stride over 32x32 tiles (a few thousand CTAs, not one per tile)
+__global__ void __launch_bounds__(256) k_import(DevCtx c, const BlockDesc* blocks, int nb, int tiles) {
     __shared__ double tile[TS][TS + 1];
-    const int t = blockIdx.x;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
     const BlockDesc bd = blocks[find_block(blocks, nb, t)];
     const int lt = t - bd.tile0;
     const int i0 = (lt / bd.tiles_n) * TS, j0 = (lt % bd.tiles_n) * TS;
@@ -44,11 +45,13 @@ __global__ void __launch_bounds__(256) k_import(DevCtx c, const BlockDesc* block
             store_level(c, bd.level, (long long)(bd.r0 + i) * c.ldw + bd.c0 + j, v);
         }
     }
+    __syncthreads();
+    }
 }
 
-__global__ void __launch_bounds__(256) k_export(DevCtx c, const BlockDesc* blocks, int nb) {
+__global__ void __launch_bounds__(256) k_export(DevCtx c, const BlockDesc* blocks, int nb, int tiles) {
     __shared__ double tile[TS][TS + 1];
-    const int t = blockIdx.x;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
     const BlockDesc bd = blocks[find_block(blocks, nb, t)];
     const int lt = t - bd.tile0;
     const int i0 = (lt / bd.tiles_n) * TS, j0 = (lt % bd.tiles_n) * TS;
@@ -69,11 +72,13 @@ __global__ void __launch_bounds__(256) k_export(DevCtx c, const BlockDesc* block
         if (i < bd.m && j < bd.n && !(bd.lower && j > i))
             l[(long long)(bd.c0 + j) * ldl + bd.r0 + i] = tile[tx][ty + r];
     }
+    __syncthreads();
+    }
 }
 
 // shadow: blocks carry their source level; target is `p`
-__global__ void __launch_bounds__(256) k_shadow(DevCtx c, const BlockDesc* blocks, int nb, int p) {
-    const int t = blockIdx.x;
+__global__ void __launch_bounds__(256) k_shadow(DevCtx c, const BlockDesc* blocks, int nb, int p, int tiles) {
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
     const BlockDesc bd = blocks[find_block(blocks, nb, t)];
     const int lt = t - bd.tile0;
     const int i0 = (lt / bd.tiles_n) * TS, j0 = (lt % bd.tiles_n) * TS;
@@ -87,6 +92,7 @@ __global__ void __launch_bounds__(256) k_shadow(DevCtx c, const BlockDesc* block
             if (bd.lower && j > i) v = 0.0;
             store_level(c, p, off, v);
         }
+    }
     }
 }
 
@@ -123,25 +129,36 @@ __global__ void __launch_bounds__(256) k_quant1(DevCtx c, int lv, int r0, int c0
     __shared__ double tile[TS][TS + 1];
     __shared__ unsigned long long smax[8], skey[8];
     const int tiles_n = (n + TS - 1) / TS;
-    const int i0 = (blockIdx.x / tiles_n) * TS, j0 = (blockIdx.x % tiles_n) * TS;
+    const int tiles = tiles_n * ((m + TS - 1) / TS);
     const double* a = c.ra->a_in;
     const long long lda = c.ra->lda_in;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     unsigned long long mx = 0, key = ~0ull;
+    // grid-stride over 32x32 tiles; one reduction per CTA at the end
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int i0 = (t / tiles_n) * TS, j0 = (t % tiles_n) * TS;
 #pragma unroll
-    for (int r = 0; r < TS; r += 8) {
-        const int i = i0 + tx, j = j0 + ty + r;
-        double v = 0.0;
-        if (i < m && j < n) {
-            v = a[(long long)(c0 + j) * lda + r0 + i];
-            if (!isfinite(v)) {
-                const unsigned long long k = fail_key(seq, elem_local(i, j));
-                key = k < key ? k : key;
+        for (int r = 0; r < TS; r += 8) {
+            const int i = i0 + tx, j = j0 + ty + r;
+            double v = 0.0;
+            if (i < m && j < n) {
+                v = a[(long long)(c0 + j) * lda + r0 + i];
+                if (!isfinite(v)) {
+                    const unsigned long long k = fail_key(seq, elem_local(i, j));
+                    key = k < key ? k : key;
+                }
+                const unsigned long long bits = __double_as_longlong(fabs(v));
+                mx = bits > mx ? bits : mx;
             }
-            const unsigned long long bits = __double_as_longlong(fabs(v));
-            mx = bits > mx ? bits : mx;
+            tile[ty + r][tx] = v;
         }
-        tile[ty + r][tx] = v;
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < TS; r += 8) {
+            const int i = i0 + ty + r, j = j0 + tx;
+            if (i < m && j < n) store_level(c, lv, (long long)(r0 + i) * c.ldw + c0 + j, tile[tx][ty + r]);
+        }
+        __syncthreads();
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
@@ -164,11 +181,6 @@ __global__ void __launch_bounds__(256) k_quant1(DevCtx c, int lv, int r0, int c0
         if (M) atomicMax(c.alpha_bits + slot, M);
         if (K != ~0ull) atomicMin(c.status, K);
     }
-#pragma unroll
-    for (int r = 0; r < TS; r += 8) {
-        const int i = i0 + ty + r, j = j0 + tx;
-        if (i < m && j < n) store_level(c, lv, (long long)(r0 + i) * c.ldw + c0 + j, tile[tx][ty + r]);
-    }
 }
 
 __device__ __forceinline__ double slot_alpha(const DevCtx& c, int lv, int slot) {
@@ -184,20 +196,24 @@ __global__ void __launch_bounds__(256) k_quant2(DevCtx c, int lv, int r0, int c0
     if (alpha == 1.0) return;
     __shared__ double tile[TS][TS + 1];
     const int tiles_n = (n + TS - 1) / TS;
-    const int i0 = (blockIdx.x / tiles_n) * TS, j0 = (blockIdx.x % tiles_n) * TS;
+    const int tiles = tiles_n * ((m + TS - 1) / TS);
     const double* a = c.ra->a_in;
     const long long lda = c.ra->lda_in;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int i0 = (t / tiles_n) * TS, j0 = (t % tiles_n) * TS;
 #pragma unroll
-    for (int r = 0; r < TS; r += 8) {
-        const int i = i0 + tx, j = j0 + ty + r;
-        tile[ty + r][tx] = (i < m && j < n) ? a[(long long)(c0 + j) * lda + r0 + i] : 0.0;
-    }
-    __syncthreads();
+        for (int r = 0; r < TS; r += 8) {
+            const int i = i0 + tx, j = j0 + ty + r;
+            tile[ty + r][tx] = (i < m && j < n) ? a[(long long)(c0 + j) * lda + r0 + i] : 0.0;
+        }
+        __syncthreads();
 #pragma unroll
-    for (int r = 0; r < TS; r += 8) {
-        const int i = i0 + ty + r, j = j0 + tx;
-        if (i < m && j < n) store_level(c, lv, (long long)(r0 + i) * c.ldw + c0 + j, tile[tx][ty + r] / alpha);
+        for (int r = 0; r < TS; r += 8) {
+            const int i = i0 + ty + r, j = j0 + tx;
+            if (i < m && j < n) store_level(c, lv, (long long)(r0 + i) * c.ldw + c0 + j, tile[tx][ty + r] / alpha);
+        }
+        __syncthreads();
     }
 }
 
@@ -287,14 +303,15 @@ int make_block_table(const std::vector<BlockDescHost>& in, std::vector<BlockDesc
     return tiles;
 }
 
+static int tile_grid(int tiles) { return tiles < 148 * 8 ? tiles : 148 * 8; }
 void launch_import(const DevCtx& c, const BlockDesc* d_blocks, int nb, int tiles, cudaStream_t s) {
-    if (tiles > 0) k_import<<<tiles, 256, 0, s>>>(c, d_blocks, nb);
+    if (tiles > 0) k_import<<<tile_grid(tiles), 256, 0, s>>>(c, d_blocks, nb, tiles);
 }
 void launch_export(const DevCtx& c, const BlockDesc* d_blocks, int nb, int tiles, cudaStream_t s) {
-    if (tiles > 0) k_export<<<tiles, 256, 0, s>>>(c, d_blocks, nb);
+    if (tiles > 0) k_export<<<tile_grid(tiles), 256, 0, s>>>(c, d_blocks, nb, tiles);
 }
 void launch_shadow(const DevCtx& c, const BlockDesc* d_blocks, int nb, int tiles, int p, cudaStream_t s) {
-    if (tiles > 0) k_shadow<<<tiles, 256, 0, s>>>(c, d_blocks, nb, p);
+    if (tiles > 0) k_shadow<<<tile_grid(tiles), 256, 0, s>>>(c, d_blocks, nb, p, tiles);
 }
 void launch_check(const DevCtx& c, int lv, int r0, int c0, int m, int n, int lower, uint32_t seq,
                   cudaStream_t s) {
@@ -304,8 +321,9 @@ void launch_check(const DevCtx& c, int lv, int r0, int c0, int m, int n, int low
 void launch_quant(const DevCtx& c, int lv, int r0, int c0, int m, int n, int slot, uint32_t seq,
                   cudaStream_t s) {
     const int t = tiles_of(m, n);
-    k_quant1<<<t, 256, 0, s>>>(c, lv, r0, c0, m, n, slot, seq);
-    k_quant2<<<t, 256, 0, s>>>(c, lv, r0, c0, m, n, slot);
+    const int g = t < 148 * 8 ? t : 148 * 8;
+    k_quant1<<<g, 256, 0, s>>>(c, lv, r0, c0, m, n, slot, seq);
+    k_quant2<<<g, 256, 0, s>>>(c, lv, r0, c0, m, n, slot);
 }
 void launch_dequant(const DevCtx& c, int lv, int r0, int c0, int m, int n, int slot, uint32_t chk_seq,
                     cudaStream_t s) {

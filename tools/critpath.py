@@ -34,11 +34,12 @@ def main():
     nops = plan.stats()["ops"]
     infos = [plan.op_info(i) for i in range(nops)]
     if args.ncu_pick:
-        # launch order of the serialized profile run == op order; quant = 2 launches
+        # launch order of the serialized profile run == op order; the index
+        # counts every k_gemm_tc launch (both operand kinds match the name)
         best, best_i, idx = -1.0, -1, 0
         for i, inf in enumerate(infos):
-            if inf["type"] == "gemm" and inf["gclass"] == "tc16":
-                if inf["flops"] > best:
+            if inf["type"] == "gemm" and inf["gclass"] in ("tc16", "tc32"):
+                if inf["gclass"] == "tc16" and inf["flops"] > best:
                     best, best_i = inf["flops"], idx
                 idx += 1
         print(best_i)

@@ -13,7 +13,9 @@ SHAPES = [  # (m, n, k, lower, beta, exec)
 for cls in sys.argv[1:] or ["tc16", "tc32", "simt_f32"]:
     for (m, n, k, lo, beta, ex) in SHAPES:
         if cls != "tc16" and ex == 0:
-            ex = 1
+            ex = 2 if cls == "simt_f64" else 1
+        if cls == "simt_f64":
+            ex = 2
         if cls != "tc16" and m * n * k > 2 ** 36:
             continue
         us = tc.debug_gemm(cls, m, n, k, bool(lo), beta, ex, iters=10)
