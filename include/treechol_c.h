@@ -137,6 +137,33 @@ int tc_info_message(const tc_plan* plan, const tc_info* info, char* buf, int buf
 int tc_potrs_device(int n, const double* dL, int ldl, double* dB, int ldb, int nrhs,
                     void* stream);
 
+/* ---- distributed single factorization (BASELINE config C5) ------------- */
+
+/* The two pieces a rank runs for the top split of an order-N factorization
+ * (n1 = N/2, n2 = N - n1) besides whole factorizations; levels are the big
+ * tree's (the split's subtrees sit at depth 1, its panel at depth 0).
+ * tc_plan_create_trsm: the caller's buffer (device, column-major doubles,
+ *   lda >= n1 + m) holds the factored L11 in rows [0, n1) and a row block of
+ *   A21 in rows [n1, n1 + m); the run quantizes the block with the alpha of
+ *   tc_plan_set_external_absmax (the max |A21| over ALL ranks' rows),
+ *   solves it against L11 (tree_trsm, tree.cpp:127-138), dequantizes and
+ *   writes it back in place (rows [n1, n1 + m) only).
+ * tc_plan_create_syrk_rows: the buffer (lda >= 2 n2) holds A22 in rows
+ *   [0, n2) (columns [0, n2)) and the solved A21 in rows [n2, 2 n2)
+ *   (columns [0, n1)); the run applies tree_syrk(A22, A21) (tree.cpp:
+ *   140-152) to A22's rows [row_lo, row_hi) and writes those rows back.
+ * Both run through tc_potrf_device like a factorization plan.  Row blocks
+ * of a GEMM are independent, so the distributed factor equals the
+ * single-device one bit for bit (tests/test_distributed.py). */
+int tc_plan_create_trsm(int n1, int m, int b, const int* levels, int nlevels, int leaf_size, tc_plan** out);
+int tc_plan_create_syrk_rows(int n2, int k, int b, const int* levels, int nlevels, int row_lo, int row_hi,
+                             tc_plan** out);
+int tc_plan_set_external_absmax(tc_plan* plan, double absmax);
+/* storage extent (rows, cols) a plan's caller buffer must cover */
+int tc_plan_extent(const tc_plan* plan, int* rows, int* cols);
+/* max |A(i,j)| over an m x n device block (NaN skipped, like quantize_block) */
+int tc_absmax_device(int m, int n, const double* dA, int lda, double* out, void* stream);
+
 /* ---- batched POTRF + POTRS (BASELINE config C4) ------------------------ */
 
 /* A batch driver for independent order-n systems with one precision tree:

@@ -126,6 +126,11 @@ def _load():
         "tc_factorization_error_device": (I, [I, P, I, P, I, C.POINTER(D), P]),
         "tc_solve_residual_device": (I, [I, P, I, P, P, C.POINTER(D), P]),
         "tc_debug_gemm": (I, [I, I, I, I, I, D, I, I, C.POINTER(C.c_float)]),
+        "tc_plan_create_trsm": (I, [I, I, I, PI, I, I, C.POINTER(P)]),
+        "tc_plan_create_syrk_rows": (I, [I, I, I, PI, I, I, I, C.POINTER(P)]),
+        "tc_plan_set_external_absmax": (I, [P, D]),
+        "tc_plan_extent": (I, [P, PI, PI]),
+        "tc_absmax_device": (I, [I, I, P, I, C.POINTER(D), P]),
         "tc_batch_create": (I, [I, I, PI, I, I, I, C.POINTER(P)]),
         "tc_batch_destroy": (None, [P]),
         "tc_batch_set_option": (I, [P, C.c_char_p, I]),
@@ -356,6 +361,39 @@ class Plan:
             _lib.tc_plan_destroy(h)
             self._h = None
 
+    @classmethod
+    def _wrap(cls, h, n, b, config, rows):
+        self = cls.__new__(cls)
+        self.cfg = _cfg(config)
+        self.n, self.b, self.quantize = int(rows), int(b), True
+        self._h = h
+        return self
+
+    @classmethod
+    def panel_trsm(cls, n1: int, m: int, b: int, config, leaf_size: int = 0) -> "Plan":
+        """distributed C5 piece: rows [0, n1) = factored L11, rows [n1, n1+m)
+        = a row block of A21 to quantize (external alpha) and solve
+        (tc_plan_create_trsm)"""
+        cfg = _cfg(config)
+        arr = (C.c_int * len(cfg.levels))(*cfg.levels)
+        h = C.c_void_p()
+        _raise(_lib.tc_plan_create_trsm(n1, m, b, arr, len(cfg.levels), leaf_size, C.byref(h)))
+        return cls._wrap(h, n1, b, cfg, n1 + m)
+
+    @classmethod
+    def panel_syrk_rows(cls, n2: int, k: int, b: int, config, row_lo: int, row_hi: int) -> "Plan":
+        """distributed C5 piece: rows [0, n2) = A22, rows [n2, 2 n2) = the
+        solved A21; tree_syrk on A22's rows [row_lo, row_hi)
+        (tc_plan_create_syrk_rows)"""
+        cfg = _cfg(config)
+        arr = (C.c_int * len(cfg.levels))(*cfg.levels)
+        h = C.c_void_p()
+        _raise(_lib.tc_plan_create_syrk_rows(n2, k, b, arr, len(cfg.levels), row_lo, row_hi, C.byref(h)))
+        return cls._wrap(h, n2, b, cfg, 2 * n2)
+
+    def set_external_absmax(self, amax: float):
+        _raise(_lib.tc_plan_set_external_absmax(self._h, float(amax)))
+
     def set_option(self, key: str, value: int):
         _raise(_lib.tc_plan_set_option(self._h, key.encode(), int(value)))
 
@@ -561,6 +599,14 @@ def spd_generate(n: int, seed: int) -> np.ndarray:
     a = np.empty((n, n), dtype=np.float64, order="F")
     _raise(_lib.tc_spd_generate_host(n, C.c_uint64(seed), a.ctypes.data, n))
     return a
+
+
+def absmax_device(a_dev, m: int, n: int, stream=None) -> float:
+    """max |A(i,j)| over the m x n column-major device block (NaN skipped)"""
+    out = C.c_double()
+    lda = a_dev.shape[1] if a_dev.dim() == 2 else m
+    _raise(_lib.tc_absmax_device(m, n, _ptr(a_dev), lda, C.byref(out), _stream_ptr(stream)))
+    return out.value
 
 
 def spd_generate_device(n: int, seed: int, device="cuda"):

@@ -262,6 +262,69 @@ int tc_plan_op_info(const tc_plan* plan, int i, int* type, int* gclass, int* lev
     return TC_OK;
 }
 
+int tc_plan_create_trsm(int n1, int m, int b, const int* levels, int nlevels, int leaf_size, tc_plan** out) {
+    if (!out || !levels_ok(levels, nlevels)) return fail(TC_INVALID_ARGUMENT, "bad arguments");
+    *out = nullptr;
+    try {
+        Plan p = Plan::make_trsm(n1, m, b, std::vector<int>(levels, levels + nlevels), leaf_size, PlanOptions{});
+        auto* h = new tc_plan;
+        h->eng = std::make_unique<Engine>(std::move(p));
+        *out = h;
+        return TC_OK;
+    } catch (const std::exception& e) {
+        return fail(TC_INVALID_ARGUMENT, e.what());
+    }
+}
+
+int tc_plan_create_syrk_rows(int n2, int k, int b, const int* levels, int nlevels, int row_lo, int row_hi,
+                             tc_plan** out) {
+    if (!out || !levels_ok(levels, nlevels)) return fail(TC_INVALID_ARGUMENT, "bad arguments");
+    *out = nullptr;
+    try {
+        Plan p = Plan::make_syrk_rows(n2, k, b, std::vector<int>(levels, levels + nlevels), row_lo, row_hi,
+                                      PlanOptions{});
+        auto* h = new tc_plan;
+        h->eng = std::make_unique<Engine>(std::move(p));
+        *out = h;
+        return TC_OK;
+    } catch (const std::exception& e) {
+        return fail(TC_INVALID_ARGUMENT, e.what());
+    }
+}
+
+int tc_plan_set_external_absmax(tc_plan* plan, double absmax) {
+    if (!plan) return fail(TC_INVALID_ARGUMENT, "null plan");
+    std::string err;
+    if (!plan->eng->set_external_absmax(absmax, &err)) return fail(TC_INVALID_ARGUMENT, err);
+    return TC_OK;
+}
+
+int tc_plan_extent(const tc_plan* plan, int* rows, int* cols) {
+    if (!plan) return fail(TC_INVALID_ARGUMENT, "null plan");
+    if (rows) *rows = plan->eng->plan.rows;
+    if (cols) *cols = plan->eng->plan.cols;
+    return TC_OK;
+}
+
+int tc_absmax_device(int m, int n, const double* dA, int lda, double* out, void* stream) {
+    if (!dA || !out || m < 0 || n < 0 || lda < m) return fail(TC_INVALID_ARGUMENT, "bad arguments");
+    if (!tc_device_available()) return fail(TC_NO_DEVICE, "no CUDA device (there is no CPU fallback)");
+    *out = 0.0;
+    if (m == 0 || n == 0) return TC_OK;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    unsigned long long* d = nullptr;
+    cudaError_t e = cudaMallocAsync(&d, sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return cuda_fail(e, "alloc");
+    bo_absmax(dA, lda, m, n, d, s);
+    unsigned long long bits = 0;
+    e = cudaMemcpyAsync(&bits, d, sizeof bits, cudaMemcpyDeviceToHost, s);
+    cudaFreeAsync(d, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, "absmax");
+    std::memcpy(out, &bits, sizeof bits);
+    return TC_OK;
+}
+
 int tc_plan_op_deps(const tc_plan* plan, int i, int* deps, int cap) {
     if (!plan || i < 0 || i >= int(plan->eng->plan.ops.size())) return -1;
     const Op& op = plan->eng->plan.ops[i];
@@ -273,8 +336,8 @@ int tc_plan_op_deps(const tc_plan* plan, int i, int* deps, int cap) {
 int tc_potrf_device(tc_plan* plan, const double* dA_in, int lda_in, double* dL_out, int lda_out, void* stream,
                     tc_info* info) {
     if (!plan || !dA_in || !dL_out) return fail(TC_INVALID_ARGUMENT, "null argument");
-    const int n = plan->eng->plan.n;
-    if (lda_in < n || lda_out < n) return fail(TC_INVALID_ARGUMENT, "leading dimension < n");
+    const int n = plan->eng->plan.rows > 0 ? plan->eng->plan.rows : plan->eng->plan.n;
+    if (lda_in < n || lda_out < n) return fail(TC_INVALID_ARGUMENT, "leading dimension < rows");
     if (!tc_device_available()) return fail(TC_NO_DEVICE, "no CUDA device (there is no CPU fallback)");
     std::string err;
     plan->have_result = false;

@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstring>
 #include <thread>
 
@@ -49,6 +50,7 @@ Engine::~Engine() {
     if (d_ra_) cudaFree(d_ra_);
     if (h_ra_) cudaFreeHost(h_ra_);
     if (h_status_) cudaFreeHost(h_status_);
+    if (h_ext_) cudaFreeHost(h_ext_);
 }
 
 int Engine::launches_per_run() const {
@@ -62,8 +64,9 @@ bool Engine::prepare(std::string* err) {
     TC_TRY(cudaGetDevice(&device_));
     init_leaf_attributes();
     init_tc_attributes();
-    const int n = plan.n;
-    const long long ldw = (long long)align_up(size_t(n), 64);
+    // level buffers: rows x ldw (n x n for a factorization plan)
+    const int n = plan.rows > 0 ? plan.rows : plan.n;
+    const long long ldw = (long long)align_up(size_t(plan.cols > 0 ? plan.cols : plan.n), 64);
     ctx_.ldw = ldw;
     // level buffers: one allocation, 256-byte aligned sub-buffers
     size_t sz[3] = {0, 0, 0}, off[3] = {0, 0, 0}, total = 0;
@@ -208,6 +211,25 @@ void Engine::reset_words(cudaStream_t s) {
     cudaMemsetAsync(d_words_, 0xFF, sizeof(unsigned long long), s);
     if (plan.n_alpha_slots > 0)
         cudaMemsetAsync(d_words_ + 1, 0, sizeof(unsigned long long) * size_t(plan.n_alpha_slots), s);
+    // an externally reduced max|B| (distributed panel): the slot starts at
+    // it, so the local atomicMax leaves it unchanged and the quantize uses
+    // the global alpha (read from pinned memory when the copy executes)
+    if (plan.ext_alpha_slot >= 0 && h_ext_)
+        cudaMemcpyAsync(d_words_ + 1 + plan.ext_alpha_slot, h_ext_, sizeof(unsigned long long),
+                        cudaMemcpyHostToDevice, s);
+}
+
+bool Engine::set_external_absmax(double amax, std::string* err) {
+    if (plan.ext_alpha_slot < 0) {
+        if (err) *err = "plan has no external alpha slot";
+        return false;
+    }
+    if (!h_ext_) TC_TRY(cudaMallocHost(&h_ext_, sizeof(unsigned long long)));
+    const double a = std::fabs(amax);
+    unsigned long long bits;
+    std::memcpy(&bits, &a, sizeof bits);
+    *h_ext_ = (a != a) ? 0ull : bits;  // NaN skipped like the local max
+    return true;
 }
 
 // enqueue every op on the stream pool (works eagerly or under capture)

@@ -69,6 +69,8 @@ class Engine {
     int launches_per_run() const;
 
     bool ready() const { return ready_; }
+    // distributed panel plans: the all-reduced max|B| of the panel rows
+    bool set_external_absmax(double amax, std::string* err);
     bool prepare(std::string* err);
 
    private:
@@ -78,6 +80,7 @@ class Engine {
     RunArgs* d_ra_ = nullptr;
     RunArgs* h_ra_ = nullptr;
     unsigned long long* h_status_ = nullptr;
+    unsigned long long* h_ext_ = nullptr;     // pinned: external max|B| bits
     void* d_bufs_ = nullptr;
     unsigned long long* d_words_ = nullptr;  // status + alpha slots
     void* d_w16_ = nullptr;                  // leaf inverses + scales

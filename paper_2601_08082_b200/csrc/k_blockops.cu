@@ -174,6 +174,11 @@ void bo_quantize(double* a, long long lda, int m, int n, int lv, unsigned long l
     k_bo_scale<<<grid_for((long long)m * n, 256), 256, 0, s>>>(a, lda, m, n, lv, 0, d_amax, 1.0, d_alpha);
 }
 
+void bo_absmax(const double* a, long long lda, int m, int n, unsigned long long* d_amax, cudaStream_t s) {
+    cudaMemsetAsync(d_amax, 0, sizeof(unsigned long long), s);
+    k_bo_absmax<<<grid_for((long long)m * n, 256), 256, 0, s>>>(a, lda, m, n, d_amax);
+}
+
 void bo_dequantize(double* a, long long lda, int m, int n, int lv, double alpha, cudaStream_t s) {
     k_bo_scale<<<grid_for((long long)m * n, 256), 256, 0, s>>>(a, lda, m, n, lv, 1, nullptr, alpha, nullptr);
 }

@@ -80,6 +80,7 @@ bool tc_supported();
 void bo_round(double* a, long long lda, int m, int n, int lv, int lower, cudaStream_t s);
 void bo_quantize(double* a, long long lda, int m, int n, int lv, unsigned long long* d_amax, double* d_alpha,
                  cudaStream_t s);
+void bo_absmax(const double* a, long long lda, int m, int n, unsigned long long* d_amax, cudaStream_t s);
 void bo_dequantize(double* a, long long lda, int m, int n, int lv, double alpha, cudaStream_t s);
 void bo_gemm(double* c, long long ldc, const double* a, long long lda, const double* b, long long ldb, int m, int n,
              int k, double alpha, double beta, int lv, int acc, int lower, cudaStream_t s);

@@ -329,48 +329,21 @@ void Plan::emit_syrk(int cnode, Rect A, int p) {
 // tree_potrf (tree.cpp:106-125)
 // ---------------------------------------------------------------------------
 
-void Plan::emit_potrf(int node) {
-    const Node nd = nodes[node];
-    if (nd.leaf) {
-        Op chk;
-        chk.type = OP_CHECK;
-        chk.level = nd.level;
-        chk.src = nd.level;
-        chk.rect = blocks[nd.block].rect;
-        chk.lower = 1;
-        chk.diagonal = 1;
-        chk.seq = next_seq();
-        checks.push_back({chk.seq, chk.rect, 1});
-        // the leaf's require_finite (tree.cpp:108) runs inside the POTRF
-        // kernel, which loads the lower triangle anyway
-        const uint32_t chk_seq = chk.seq;
-        if (!opt.fuse_checks) push(std::move(chk));
-        Op op;
-        op.type = OP_POTRF;
-        op.level = nd.level;
-        op.rect = blocks[nd.block].rect;
-        if (opt.fuse_checks) {
-            op.check_seq = chk_seq;
-            op.chk = op.rect;
-        }
-        op.seq = next_seq();
-        const uint64_t n = uint64_t(nd.n);
-        add_flops(op.seq, nd.level, K_POTRF, n * (n + 1) * (2 * n + 1) / 6);
-        op.flops = double(n) * n * n / 3.0;
-        push(std::move(op));
-        return;
-    }
-    emit_potrf(nd.d1);
-    const Block blk = blocks[nd.block];
+// the off-diagonal panel of a split (tree.cpp:113-121): require_finite,
+// quantize (spine panels; ext_slot >= 0: an alpha slot already allocated,
+// e.g. filled from outside by a distributed driver), tree_trsm against the
+// factored diag1 tree rooted at lnode, dequantize, require_finite
+void Plan::emit_panel(int bi, int lnode, int ext_slot) {
+    const Block blk = blocks[bi];
     const int p = blk.level;
     int slot = -1;
     if (blk.spine_quant) {
-        slot = n_alpha_slots++;
+        slot = ext_slot >= 0 ? ext_slot : n_alpha_slots++;
         Op q;
         q.type = OP_QUANT;
         q.level = p;
         q.rect = blk.rect;
-        q.blocks.push_back(nd.block);
+        q.blocks.push_back(bi);
         q.slot = slot;
         q.seq = next_seq();  // the require_finite that precedes quantize
         checks.push_back({q.seq, blk.rect, 0});
@@ -405,9 +378,9 @@ void Plan::emit_potrf(int node) {
             push(std::move(chk));
         }
     }
-    ensure_shadows(nd.d1, p);
+    ensure_shadows(lnode, p);
     const int op0 = int(ops.size()), pr0 = int(probs.size());
-    emit_trsm(blk.rect, p, nd.d1);
+    emit_trsm(blk.rect, p, lnode);
     const int op1 = int(ops.size()), pr1 = int(probs.size());
     int dq_op = -1;
     if (blk.spine_quant) {
@@ -448,6 +421,43 @@ void Plan::emit_potrf(int node) {
         chk.seq = post;
         push(std::move(chk));
     }
+}
+
+void Plan::emit_potrf(int node) {
+    const Node nd = nodes[node];
+    if (nd.leaf) {
+        Op chk;
+        chk.type = OP_CHECK;
+        chk.level = nd.level;
+        chk.src = nd.level;
+        chk.rect = blocks[nd.block].rect;
+        chk.lower = 1;
+        chk.diagonal = 1;
+        chk.seq = next_seq();
+        checks.push_back({chk.seq, chk.rect, 1});
+        // the leaf's require_finite (tree.cpp:108) runs inside the POTRF
+        // kernel, which loads the lower triangle anyway
+        const uint32_t chk_seq = chk.seq;
+        if (!opt.fuse_checks) push(std::move(chk));
+        Op op;
+        op.type = OP_POTRF;
+        op.level = nd.level;
+        op.rect = blocks[nd.block].rect;
+        if (opt.fuse_checks) {
+            op.check_seq = chk_seq;
+            op.chk = op.rect;
+        }
+        op.seq = next_seq();
+        const uint64_t n = uint64_t(nd.n);
+        add_flops(op.seq, nd.level, K_POTRF, n * (n + 1) * (2 * n + 1) / 6);
+        op.flops = double(n) * n * n / 3.0;
+        push(std::move(op));
+        return;
+    }
+    emit_potrf(nd.d1);
+    const Block blk = blocks[nd.block];
+    const int p = blk.level;
+    emit_panel(nd.block, nd.d1, -1);
     emit_syrk(nd.d2, blk.rect, p);
     emit_potrf(nd.d2);
 }
@@ -573,6 +583,7 @@ Plan Plan::make(int n, int b, const std::vector<int>& levels, bool quantize, int
         if (l < LV_F16 || l > LV_F64) throw std::invalid_argument("precision level out of range");
     Plan P;
     P.n = n;
+    P.rows = P.cols = n;
     P.b = b;
     P.leaf_size = leaf_size > 0 ? leaf_size : b;
     P.levels = levels;
@@ -704,6 +715,165 @@ struct Counter {
     }
 };
 }  // namespace
+
+// depth-first block order of the subtree at `root` (first use / finalization)
+static std::vector<int> dfs_blocks(const Plan& P, int root) {
+    std::vector<int> order, stack{root};
+    while (!stack.empty()) {
+        const int id = stack.back();
+        stack.pop_back();
+        if (id < 0) {
+            order.push_back(P.nodes[-id - 1].block);
+            continue;
+        }
+        const Node& nd = P.nodes[id];
+        if (nd.leaf) {
+            order.push_back(nd.block);
+            continue;
+        }
+        stack.push_back(nd.d2);
+        stack.push_back(-id - 1);
+        stack.push_back(nd.d1);
+    }
+    return order;
+}
+
+static void check_args(int b, const std::vector<int>& levels) {
+    if (b < 1) throw std::invalid_argument("leaf size must be >= 1");
+    if (levels.empty()) throw std::invalid_argument("empty precision config");
+    for (int l : levels)
+        if (l < LV_F16 || l > LV_F64) throw std::invalid_argument("precision level out of range");
+}
+
+Plan Plan::make_trsm(int n1, int m, int b, const std::vector<int>& levels, int leaf_size, const PlanOptions& opt) {
+    check_args(b, levels);
+    if (n1 < 1 || m < 1) throw std::invalid_argument("panel TRSM needs n1, m >= 1");
+    Plan P;
+    P.n = n1;
+    P.rows = n1 + m;
+    P.cols = n1;
+    P.b = b;
+    P.leaf_size = leaf_size > 0 ? leaf_size : b;
+    P.levels = levels;
+    P.quantize = true;
+    P.opt = opt;
+    P.build_node(0, n1, 1);  // L11 = the big tree's diag1
+    Block pb;
+    pb.rect = {n1, 0, m, n1};
+    pb.level = P.at_depth(0);
+    pb.spine_quant = pb.level != LV_F64;  // the top panel: quantized from the caller's doubles
+    const int pbi = int(P.blocks.size());
+    P.blocks.push_back(pb);
+    P.has_shadow.assign(P.blocks.size(), std::vector<uint8_t>(3, 0));
+    P.has_inverse.assign(P.blocks.size(), 0);
+    for (const Block& blk : P.blocks) P.needs_buf[blk.level] = true;
+    P.block_order = dfs_blocks(P, 0);
+    P.block_order.push_back(pbi);
+    for (int i : P.block_order)
+        if (!P.blocks[i].spine_quant) {
+            Op imp;
+            imp.type = OP_IMPORT;
+            imp.blocks.push_back(i);
+            imp.rect = P.blocks[i].rect;
+            P.push(std::move(imp));
+        }
+    int slot = -1;
+    if (pb.spine_quant) {
+        slot = P.n_alpha_slots++;
+        P.ext_alpha_slot = slot;
+    }
+    P.emit_panel(pbi, 0, slot);
+    Op exp;
+    exp.type = OP_EXPORT;
+    exp.blocks.push_back(pbi);
+    exp.rect = pb.rect;
+    P.push(std::move(exp));
+    P.finalize_accesses();
+    P.build_deps();
+    return P;
+}
+
+Plan Plan::make_syrk_rows(int n2, int k, int b, const std::vector<int>& levels, int row_lo, int row_hi,
+                          const PlanOptions& opt) {
+    check_args(b, levels);
+    if (n2 < 1 || k < 1 || k > n2 || row_lo < 0 || row_hi > n2 || row_lo >= row_hi)
+        throw std::invalid_argument("panel SYRK: bad sizes or row range");
+    Plan P;
+    P.n = n2;
+    P.rows = 2 * n2;
+    P.cols = n2;
+    P.b = b;
+    P.leaf_size = b;
+    P.levels = levels;
+    P.quantize = true;
+    P.opt = opt;
+    P.build_node(0, n2, 1);  // A22 = the big tree's diag2
+    const int ntree = int(P.blocks.size());
+    const int p = P.at_depth(0);
+    // A22's blocks restricted to the rows (a leaf may not straddle a bound)
+    std::vector<int> mine;
+    for (int i = 0; i < ntree; ++i) {
+        const Rect r = P.blocks[i].rect;
+        const int lo = std::max(r.r0, row_lo), hi = std::min(r.r0 + r.m, row_hi);
+        if (lo >= hi) continue;
+        if (P.blocks[i].leaf && (lo != r.r0 || hi != r.r0 + r.m))
+            throw std::invalid_argument("panel SYRK: row range splits a diagonal leaf");
+        Block pb = P.blocks[i];
+        pb.rect = {lo, r.c0, hi - lo, r.n};
+        pb.node = -1;
+        mine.push_back(int(P.blocks.size()));
+        P.blocks.push_back(pb);
+    }
+    Block ab;
+    ab.rect = {n2, 0, n2, k};
+    ab.level = p;
+    const int abi = int(P.blocks.size());
+    P.blocks.push_back(ab);
+    P.has_shadow.assign(P.blocks.size(), std::vector<uint8_t>(3, 0));
+    P.has_inverse.assign(P.blocks.size(), 0);
+    P.needs_buf[p] = true;
+    for (int i : mine) P.needs_buf[P.blocks[i].level] = true;
+    P.block_order = mine;
+    P.block_order.push_back(abi);
+    for (int i : P.block_order) {
+        Op imp;
+        imp.type = OP_IMPORT;
+        imp.blocks.push_back(i);
+        imp.rect = P.blocks[i].rect;
+        P.push(std::move(imp));
+    }
+    // tree_syrk(A22, A21, -1, 1, p) with every problem clipped to the rows
+    std::vector<GemmProb> all, kept;
+    P.collect_syrk(0, ab.rect, p, all);
+    P.flops.clear();
+    for (GemmProb g : all) {
+        const int lo = std::max(g.c_r0, row_lo), hi = std::min(g.c_r0 + g.m, row_hi);
+        if (lo >= hi) continue;
+        const int d = lo - g.c_r0;
+        if (g.lower && (d != 0 || hi - lo != g.m))
+            throw std::invalid_argument("panel SYRK: row range splits a diagonal leaf");
+        g.c_r0 += d;
+        g.a_r0 += d;
+        g.m = hi - lo;
+        // flops of the rows kept (informational: the distributed parts sum
+        // to the reference's totals)
+        const uint64_t f = g.lower ? uint64_t(g.m) * uint64_t(g.m + 1) * uint64_t(g.k)
+                                   : 2ull * uint64_t(g.m) * uint64_t(g.n) * uint64_t(g.k);
+        P.add_flops(g.seq, g.exec_level, g.lower ? K_SYRK : K_GEMM, f);
+        kept.push_back(g);
+    }
+    if (!kept.empty()) P.push_gemm_group(kept, p);
+    for (int i : mine) {
+        Op exp;
+        exp.type = OP_EXPORT;
+        exp.blocks.push_back(i);
+        exp.rect = P.blocks[i].rect;
+        P.push(std::move(exp));
+    }
+    P.finalize_accesses();
+    P.build_deps();
+    return P;
+}
 
 void static_flop_breakdown(int n, int b, const std::vector<int>& levels, uint64_t by_level[3],
                            uint64_t by_kernel[4], uint64_t calls[4]) {

@@ -160,6 +160,10 @@ struct PlanOptions {
 
 struct Plan {
     int n = 0, b = 0, leaf_size = 0;
+    // storage extent of the level buffers (rows x cols); n x n for a
+    // factorization, larger for the distributed panel plans below
+    int rows = 0, cols = 0;
+    int ext_alpha_slot = -1;  // alpha slot filled from outside before every run (distributed TRSM)
     std::vector<int> levels;
     bool quantize = true;
     PlanOptions opt;
@@ -181,6 +185,24 @@ struct Plan {
     static Plan make(int n, int b, const std::vector<int>& levels, bool quantize,
                      int leaf_size, const PlanOptions& opt);
 
+    // Distributed single factorization (BASELINE config C5), the two pieces
+    // a rank runs besides whole factorizations.  Both use the big tree's
+    // levels: the top split's diag1 / diag2 subtrees sit at depth 1, its
+    // off-diagonal panel at depth 0.
+    //  make_trsm: rows [0, n1) hold the factored L11 (tree of order n1),
+    //    rows [n1, n1 + m) a row block of the panel A21; quantize it with an
+    //    external alpha (the all-reduced max over every rank's rows), solve
+    //    against L11 (tree_trsm), dequantize; only the panel is exported.
+    //  make_syrk_rows: rows [0, n2) hold A22 (tree of order n2), rows
+    //    [n2, 2 n2) the solved panel A21 (k = n1 columns, stored values);
+    //    tree_syrk(A22, A21) restricted to output rows [row_lo, row_hi)
+    //    (GEMM rows are independent: the restriction changes no element's
+    //    arithmetic); only those rows of A22 are imported and exported.
+    static Plan make_trsm(int n1, int m, int b, const std::vector<int>& levels, int leaf_size,
+                          const PlanOptions& opt);
+    static Plan make_syrk_rows(int n2, int k, int b, const std::vector<int>& levels, int row_lo, int row_hi,
+                               const PlanOptions& opt);
+
     int at_depth(int d) const { return levels[d < int(levels.size()) ? d : int(levels.size()) - 1]; }
     int leaf_level() const { return levels.back(); }
 
@@ -196,6 +218,7 @@ struct Plan {
     std::vector<uint8_t> has_inverse;              // [block] bit 0: W16 ready, bit 1: W32 ready
     int build_node(int r0, int n, int depth);
     void emit_potrf(int node);
+    void emit_panel(int block, int lnode, int ext_slot);
     void emit_trsm(Rect brect, int p, int lnode);
     void emit_syrk(int cnode, Rect arect, int p);
     void collect_syrk(int cnode, Rect arect, int p, std::vector<GemmProb>& out);
