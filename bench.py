@@ -308,6 +308,30 @@ def run_ours(args):
               "ms_max_over_ranks": tot.device_ms, "worst_solve_residual": tot.worst_residual,
               "data": "device-generated SPD of spd_generate's distribution (not the mt19937_64 stream)"}
 
+    # C5: one factorization split over the ranks (NCCL broadcast of L11,
+    # all-reduce of the panel alpha, all-gather of the solved panel), at the
+    # C3 size so it compares with the single-GPU value above
+    c5 = None
+    if ws > 1 and args.c5_n > 0:
+        from paper_2601_08082_b200.distributed import potrf_top_split, synthetic_pieces
+        a11, a21, a22 = synthetic_pieces(args.c5_n, b, SEED, ws, rank)
+        cache = {}
+        times = []
+        for it in range(3):  # the first call builds the plans
+            res = potrf_top_split(args.c5_n, b, CFG, a11=a11.clone() if a11 is not None else None, a21_rows=a21,
+                                  a22_rows=a22, cache=cache)
+            t = torch.tensor([res.device_ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            times.append(float(t.item()))
+        ms5 = min(times[1:])
+        c5 = {"workload": f"C5-style: one N={args.c5_n} factorization, top TRSM/SYRK row-split over {ws} GPUs, "
+                          f"L11 broadcast + alpha all-reduce + panel all-gather over NCCL",
+              "value": potrf_flops(args.c5_n) / (ms5 * 1e-3) / 1e12, "unit": "TFLOP/s", "ms": ms5,
+              "status": res.status, "scaling": "strong",
+              "data": "device-generated SPD of spd_generate's distribution"}
+        del a11, a21, a22, cache, res
+        torch.cuda.empty_cache()
+
     variants = None
     if args.variants and rank == 0:
         variants = run_variants(args, tc, torch)
@@ -327,7 +351,7 @@ def run_ours(args):
                            "l2": "inputs (34 GB) larger than L2; no flush needed"},
                 "status": st.status, "rel_error": rel, "digits": -math.log10(rel) if rel > 0 else None,
                 "clocks": clk.summary(), "gpu_launches": stats["launches"] * args.steps,
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "c4": c4, "variants": variants,
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "c4": c4, "c5": c5, "variants": variants,
                 "breakdown_ms_serialized": {k: round(v[0], 3) for k, v in sorted(by_type.items(),
                                                                                   key=lambda kv: -kv[1][0])}}
         print(json.dumps(line), flush=True)
@@ -385,6 +409,8 @@ def main():
     ap.add_argument("--c4-count", dest="c4_count", type=int, default=64)
     ap.add_argument("--c4-n", dest="c4_n", type=int, default=16384)
     ap.add_argument("--c4-conc", dest="c4_conc", type=int, default=8)
+    ap.add_argument("--c5-n", dest="c5_n", type=int, default=65536,
+                    help="N of the distributed single factorization run when --gpus > 1 (0: off)")
     ap.add_argument("--variants", action="store_true",
                     help="also time Pure F16 / Pure F64 trees (bounds) at N; slow (F64 runs on SIMT)")
     args = ap.parse_args()

@@ -112,13 +112,15 @@ class _Coll:
 
 
 def potrf_top_split(n: int, b: int, config, a11=None, a21_rows=None, a22_rows=None, group=None,
-                    timed: bool = True) -> DistResult:
+                    cache: dict | None = None) -> DistResult:
     """Distributed tree_potrf of an order-n matrix (quantization on).
 
     Inputs (device float64, column-major): rank 0 passes ``a11`` (n1 x n1,
     factored in place); every rank passes ``a21_rows`` = A21[R_r, :]
     (tensor (n1, m_r)) and ``a22_rows`` = A22[R_r, :] (tensor (n2, m_r)),
     with R_r = row_partition(n2, world, b)[rank].  Returns the factor pieces.
+    ``cache`` (a dict kept by the caller) keeps the plans -- their device
+    workspace and CUDA graphs -- across calls.
     """
     import torch
     import paper_2601_08082_b200 as tc
@@ -133,6 +135,13 @@ def potrf_top_split(n: int, b: int, config, a11=None, a21_rows=None, a22_rows=No
     m = hi - lo
     res = DistResult(rows=(lo, hi))
     sub = shifted_levels(levels)
+    cache = {} if cache is None else cache
+
+    def plan(key, make):
+        if key not in cache:
+            cache[key] = make()
+        return cache[key]
+
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     co.barrier()
     torch.cuda.synchronize()
@@ -141,7 +150,7 @@ def potrf_top_split(n: int, b: int, config, a11=None, a21_rows=None, a22_rows=No
     # 1-2. factor A11 on rank 0, broadcast L11 in the lowest exact format
     l11_t = exact_dtype(max(sub))
     if co.rank == 0:
-        p11 = tc.Plan(n1, b, sub)
+        p11 = plan("p11", lambda: tc.Plan(n1, b, sub))
         st = p11.factor_device(a11)
         if st.status != "ok":
             res.status = st.status
@@ -162,7 +171,7 @@ def potrf_top_split(n: int, b: int, config, a11=None, a21_rows=None, a22_rows=No
         t[:, :n1].copy_(l11_x)
         t[:, n1:].copy_(a21_rows)
         del l11_x
-        pt = tc.Plan.panel_trsm(n1, m, b, cfg)
+        pt = plan("pt", lambda: tc.Plan.panel_trsm(n1, m, b, cfg))
         pt.set_external_absmax(amax)
         st = pt.factor_device(t)
         if st.status != "ok":
@@ -184,7 +193,7 @@ def potrf_top_split(n: int, b: int, config, a11=None, a21_rows=None, a22_rows=No
     del pieces
     if m > 0:
         s[:, lo:hi].copy_(a22_rows)
-        ps = tc.Plan.panel_syrk_rows(n2, n1, b, cfg, lo, hi)
+        ps = plan("ps", lambda: tc.Plan.panel_syrk_rows(n2, n1, b, cfg, lo, hi))
         st = ps.factor_device(s)
         if st.status != "ok":
             res.status = st.status
@@ -198,7 +207,7 @@ def potrf_top_split(n: int, b: int, config, a11=None, a21_rows=None, a22_rows=No
         for (l2, h2), piece in zip(parts, got):
             if h2 > l2:
                 a22[:, l2:h2].copy_(piece)
-        p22 = tc.Plan(n2, b, sub)
+        p22 = plan("p22", lambda: tc.Plan(n2, b, sub))
         st = p22.factor_device(a22)
         if st.status != "ok":
             res.status = st.status
@@ -208,3 +217,23 @@ def potrf_top_split(n: int, b: int, config, a11=None, a21_rows=None, a22_rows=No
     torch.cuda.synchronize()
     res.device_ms = ev0.elapsed_time(ev1)
     return res
+
+
+def synthetic_pieces(n: int, b: int, seed: int, world: int, rank: int):
+    """this rank's inputs of a device-generated SPD matrix of spd_generate's
+    distribution (off-diagonal uniform [0, 1), n on the diagonal; only the
+    lower triangle is read): (a11 on rank 0 else None, a21_rows, a22_rows)"""
+    import torch
+    n1, n2 = n // 2, n - n // 2
+    lo, hi = row_partition(n2, world, b)[rank]
+    g = torch.Generator(device="cuda").manual_seed(int(seed) * 1000 + rank)
+    a11 = None
+    if rank == 0:
+        r = torch.rand((n1, n1), dtype=torch.float64, device="cuda", generator=g)
+        a11 = (r + r.T).mul_(0.5)
+        a11.diagonal().add_(float(n))
+    a21 = torch.rand((n1, hi - lo), dtype=torch.float64, device="cuda", generator=g)
+    a22 = torch.rand((n2, hi - lo), dtype=torch.float64, device="cuda", generator=g)
+    idx = torch.arange(hi - lo, device="cuda")
+    a22[lo + idx, idx] += float(n)
+    return a11, a21, a22
