@@ -192,6 +192,129 @@ __global__ void __launch_bounds__(256) k_gemm_dmma(DevCtx c, const DevProb* prob
     if (p.check_seq) warp_report_min(c, bad);
 }
 
+// Small FP32 x FP32 problems (F32 exec) on the warp-level tensor path:
+// mma.sync m16n8k8 TF32 with a three-pass hi/lo split (hi = x truncated to
+// TF32, lo = x - hi; lo*hi + hi*lo + hi*hi, FP32 accumulate) -- the same
+// arithmetic as the tcgen05 TF32X3 kernel, without its per-launch setup
+// (TMEM allocation, descriptors, pipeline fill), which dominates the
+// 256-wide leaf-level solves and updates on the factorization's chain.
+// Same 64x64 tiles / problem tables as the SIMT kernel; 4 warps of 32x32.
+constexpr int MK = 32, MLD = MK + 4;  // k-slab, padded row (conflict-free fragments)
+
+__device__ __forceinline__ void mma_tf32x(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+__device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
+    hi = __float_as_uint(x) & 0xFFFFE000u;
+    lo = __float_as_uint(x - __uint_as_float(hi));
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int bytes) {
+    const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(bytes) : "memory");
+}
+
+__global__ void __launch_bounds__(128) k_gemm_mma32(DevCtx c, const DevProb* probs, int np) {
+    __shared__ __align__(16) float As[2][BM][MLD];
+    __shared__ __align__(16) float Bs[2][BN][MLD];
+    const DevProb p = probs[find_prob(probs, np, blockIdx.x)];
+    const int lt = blockIdx.x - p.tile0;
+    const int tm = lt / p.tiles_n, tn = lt % p.tiles_n;
+    const int i0 = tm * BM, j0 = tn * BN;
+    if (p.lower && p.c_c0 + j0 > p.c_r0 + i0 + BM - 1) return;  // tile above the diagonal
+    const float* buf = c.b32;
+    // B from the FP32 leaf inverses for inverse-based solves (plan.hpp kW32Ld)
+    const float* bbuf = p.b_buf == BUF_W32 ? c.w32 : c.b32;
+    const long long bld = p.b_buf == BUF_W32 ? kW32Ld : c.ldw;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wm = warp >> 1, wn = warp & 1;  // 2 x 2 warps of 32 x 32
+    const int g = lane >> 2, tq = lane & 3;
+    float acc[2][4][4];
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[x][y][e] = 0.f;
+    // 64 x 32 slabs of A and B, double-buffered with cp.async (zero-filled
+    // outside the problem): the next slab loads while this one multiplies
+    auto load = [&](int k0, int sb) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int e = threadIdx.x + 128 * q;  // 512 x 16 B per operand
+            const int r = e >> 3, kq = (e & 7) * 4;
+            const int kg = k0 + kq;
+            const int kb = min(16, max(0, (p.k - kg) * 4));
+            const int ia = i0 + r, jb = j0 + r;
+            cp_async16(&As[sb][r][kq], buf + (long long)(p.a_r0 + (ia < p.m ? ia : 0)) * c.ldw + p.a_c0 + (kb ? kg : 0),
+                       ia < p.m ? kb : 0);
+            cp_async16(&Bs[sb][r][kq], bbuf + (long long)(p.b_r0 + (jb < p.n ? jb : 0)) * bld + p.b_c0 + (kb ? kg : 0),
+                       jb < p.n ? kb : 0);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    const int ns = (p.k + MK - 1) / MK;
+    load(0, 0);
+    for (int st = 0; st < ns; ++st) {
+        const int sb = st & 1;
+        if (st + 1 < ns) {
+            load((st + 1) * MK, sb ^ 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < MK; kk += 8) {
+            uint32_t ah[2][4], al[2][4];
+#pragma unroll
+            for (int x = 0; x < 2; ++x) {
+                const int rb = wm * 32 + x * 16;
+                split_tf32(As[sb][rb + g][kk + tq], ah[x][0], al[x][0]);
+                split_tf32(As[sb][rb + g + 8][kk + tq], ah[x][1], al[x][1]);
+                split_tf32(As[sb][rb + g][kk + tq + 4], ah[x][2], al[x][2]);
+                split_tf32(As[sb][rb + g + 8][kk + tq + 4], ah[x][3], al[x][3]);
+            }
+#pragma unroll
+            for (int y = 0; y < 4; ++y) {
+                const int cb = wn * 32 + y * 8;
+                uint32_t bh[2], bl[2];
+                split_tf32(Bs[sb][cb + g][kk + tq], bh[0], bl[0]);
+                split_tf32(Bs[sb][cb + g][kk + tq + 4], bh[1], bl[1]);
+#pragma unroll
+                for (int x = 0; x < 2; ++x) {
+                    mma_tf32x(acc[x][y], al[x], bh);
+                    mma_tf32x(acc[x][y], ah[x], bl);
+                    mma_tf32x(acc[x][y], ah[x], bh);
+                }
+            }
+        }
+        __syncthreads();
+    }
+    unsigned long long bad = ~0ull;
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int i = i0 + wm * 32 + x * 16 + g + (e >= 2 ? 8 : 0);
+                const int j = j0 + wn * 32 + y * 8 + 2 * tq + (e & 1);
+                if (i >= p.m || j >= p.n) continue;
+                if (p.lower && p.c_c0 + j > p.c_r0 + i) continue;
+                const long long off = (long long)(p.c_r0 + i) * c.ldw + p.c_c0 + j;
+                if (epi_store_f(c, p, off, acc[x][y][e]) && p.check_seq) {
+                    const unsigned long long k =
+                        fail_key(p.check_seq, elem_local(p.c_r0 + i - p.chk_r0, p.c_c0 + j - p.chk_c0));
+                    bad = k < bad ? k : bad;
+                }
+            }
+    if (p.check_seq) warp_report_min(c, bad);
+}
+
 }  // namespace
 
 int simt_tiles(std::vector<DevProb>& probs) {
@@ -210,6 +333,7 @@ void launch_gemm_simt(const DevCtx& c, int gclass, const DevProb* d_probs, int n
     switch (gclass) {
         case GC_SIMT_F16: k_gemm_simt<0, float><<<tiles, 256, 0, s>>>(c, d_probs, nprob); break;
         case GC_SIMT_F32: k_gemm_simt<1, float><<<tiles, 256, 0, s>>>(c, d_probs, nprob); break;
+        case GC_MMA32: k_gemm_mma32<<<tiles, 128, 0, s>>>(c, d_probs, nprob); break;
         // FP64 accumulation on the FP64 tensor pipe (DMMA)
         case GC_SIMT_F16D: k_gemm_dmma<0><<<tiles, 256, 0, s>>>(c, d_probs, nprob); break;
         case GC_SIMT_F32D: k_gemm_dmma<1><<<tiles, 256, 0, s>>>(c, d_probs, nprob); break;

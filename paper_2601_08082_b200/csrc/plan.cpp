@@ -71,7 +71,10 @@ int Plan::gemm_class(int op_level, int exec_level, const GemmProb* g) const {
         if (exec_level == LV_F64) return GC_SIMT_F32D;
         // TMA: 16-byte aligned rows (column offsets multiples of 4 floats)
         const bool aligned = !g || (g->a_c0 % 4 == 0 && g->b_c0 % 4 == 0 && g->k % 4 == 0);
-        return (opt.use_tc && opt.use_tc32 && aligned) ? GC_TC32 : GC_SIMT_F32;
+        if (!(opt.use_tc && opt.use_tc32)) return GC_SIMT_F32;
+        // small problems: the warp-level path (float4 loads need the same alignment)
+        if (g && aligned && g->b_buf < 0 && double(g->m) * g->n * g->k <= opt.mma32_max) return GC_MMA32;
+        return aligned ? GC_TC32 : GC_SIMT_F32;
     }
     return GC_SIMT_F64;
 }
@@ -167,7 +170,9 @@ void Plan::emit_trsm(Rect B, int p, int lnode) {
             Op op;
             op.type = OP_GEMM;
             op.level = p;
-            op.gclass = inv16 ? GC_TC16 : GC_TC32;
+            op.gclass = inv16                                                        ? GC_TC16
+                        : double(g.m) * g.n * g.k <= opt.mma32_max ? GC_MMA32
+                                                                   : GC_TC32;
             op.prob_begin = int(probs.size());
             probs.push_back(g);
             op.prob_end = int(probs.size());

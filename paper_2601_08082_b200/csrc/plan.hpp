@@ -104,6 +104,7 @@ enum GemmClass : int {
     GC_SIMT_F32D = 4, // FP32 operands, FP64 accumulate
     GC_SIMT_F64 = 5,  // FP64 operands, FP64 accumulate
     GC_TC32 = 6,      // FP32 operands, three-pass TF32 split on tcgen05, FP32 accumulate (exec F32)
+    GC_MMA32 = 7,     // the same arithmetic on mma.sync, for problems too small for tcgen05's setup
 };
 
 struct Access {
@@ -153,6 +154,7 @@ struct FlopRec {
 struct PlanOptions {
     bool use_tc = true;      // FP16-operand GEMMs on tcgen05
     bool use_tc32 = true;    // FP32 x FP32 GEMMs on tcgen05 (three-pass TF32)
+    double mma32_max = 16777216.0;  // m*n*k at or below which they run on mma.sync instead (the 256^3 leaf-level ones)
     bool inverse_trsm = true; // FP16 leaf solves with m >= kInvMinRows as tcgen05 GEMMs
     bool fuse_checks = true;  // require_finite inside the producing kernels
     int syrk_split_min = 1 << 30; // tree_syrk nodes at least this large launch per region (lookahead; off by default: it shortens the critical path but adds launches, a net loss for batches)
