@@ -11,8 +11,10 @@
 //
 // CTA c computes column block c of W by block forward substitution:
 //   W(I,c) = inv(L(I,I)) (delta_Ic - sum_{c<=K<I} L(I,K) W(K,c)),  I >= c
-// -- the 32x32x32 products on all 16 warps, the 32x32 triangular solve on
-// one warp (lane = column, right-looking, reciprocal + Newton correction).
+// -- both products on the warp-level tensor path (mma.sync TF32, three-pass
+// hi/lo split: FP32-accurate); the 32x32 diagonal inverses by one warp each
+// (lane = column, right-looking substitution), the next one computed while
+// the current block's product runs.
 // The first solve's singular-diagonal check (kernels.cpp:79-81) is reported
 // here: the first j with L(j,j) zero or non-finite.
 #include "device.cuh"
@@ -23,6 +25,19 @@ namespace tcb {
 namespace {
 
 constexpr int IT = 512;
+constexpr int WLD = 36, WBS = 32 * WLD;  // W / inverse / partial blocks: row-major, padded rows
+
+__device__ __forceinline__ void mma_tf32_i(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+// x = hi + lo, hi = x truncated to TF32 (exact), lo = x - hi (exact)
+__device__ __forceinline__ void tf32_split(float x, uint32_t& hi, uint32_t& lo) {
+    hi = __float_as_uint(x) & 0xFFFFE000u;
+    lo = __float_as_uint(x - __uint_as_float(hi));
+}
 
 __device__ __forceinline__ int isw(int r, int c) { return (c << 5) + (r ^ ((c & 7) << 2)); }
 
@@ -34,8 +49,10 @@ __global__ void __launch_bounds__(IT, 1) k_leaf_inv2(DevCtx c, int r0, int n, ui
     const int NB = NT - cb;  // row blocks I = cb .. NT-1
     // tiles (I, K), cb <= K <= I, local index (I-cb)(I-cb+1)/2 + (K-cb)
     float* Ls = ism;
-    float* Wb = Ls + ((NB * (NB + 1)) >> 1) * 1024;  // [NB][32][32] row-major W(I, cb)
-    float* Rd = Wb + NB * 1024;                       // [NB*32] reciprocal diagonal
+    float* Wb = Ls + ((NB * (NB + 1)) >> 1) * 1024;  // [NB][32][WLD] row-major W(I, cb)
+    float* Dv = Wb + NB * WBS;                        // [2][32][WLD] inv(L(I,I)), double-buffered
+    float* Pq = Dv + 2 * WBS;                         // [2][32][WLD] K-split partials of the product
+    float* Rd = Pq + 2 * WBS;                         // [NB*32] reciprocal diagonal
     const T* g = lvbuf<MODE == 0 ? 0 : 1>(c) + (long long)r0 * c.ldw + r0;
     const long long ld = c.ldw;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -66,43 +83,92 @@ __global__ void __launch_bounds__(IT, 1) k_leaf_inv2(DevCtx c, int r0, int n, ui
     }
     __syncthreads();
 
+    // inv(L(I,I)) of one diagonal block by one warp: lane = column, right-
+    // looking forward substitution, reciprocal + Newton correction
+    auto diag_inverse = [&](int I, float* D) {
+        const float* Lt = tl(I, I);
+        float x[32];
+#pragma unroll
+        for (int r = 0; r < 32; ++r) x[r] = r == lane ? 1.f : 0.f;
+#pragma unroll
+        for (int r = 0; r < 32; ++r) {
+            const float d = Lt[isw(r, r)], rd = Rd[(I - cb) * 32 + r];
+            const float q = x[r] * rd;
+            x[r] = fmaf(fmaf(-q, d, x[r]), rd, q);
+#pragma unroll
+            for (int k = r + 1; k < 32; ++k) x[k] = fmaf(-Lt[isw(k, r)], x[r], x[k]);
+        }
+#pragma unroll
+        for (int r = 0; r < 32; ++r) D[r * WLD + lane] = x[r];
+    };
+    if (warp == 0) diag_inverse(cb, Dv);
+    __syncthreads();
+
+    const int gq = lane >> 2, tq = lane & 3;
     for (int I = cb; I < NT; ++I) {
-        // rhs = delta - sum_K L(I,K) W(K,cb); thread: rows warp, warp+16; col lane
-        float* Wi = Wb + (I - cb) * 1024;
-        {
-            float s0 = 0.f, s1 = 0.f;
-            for (int K = cb; K < I; ++K) {
+        float* Wi = Wb + (I - cb) * WBS;
+        float* Dc = Dv + ((I - cb) & 1) * WBS;
+        // (1) P = sum_{cb <= K < I} L(I,K) W(K,cb) on the tensor cores: 8
+        //     16x8 output tiles, the K range split over two warp groups
+        if (I > cb) {
+            const int tile = warp & 7, kg = warp >> 3;
+            const int mt = tile >> 2, nb = tile & 3;
+            float acc[4] = {0.f, 0.f, 0.f, 0.f};
+            const int nk = 4 * (I - cb);  // k-steps of 8
+            for (int ks = kg * nk / 2; ks < (kg + 1) * nk / 2; ++ks) {
+                const int K = cb + (ks >> 2), kk = (ks & 3) * 8;
                 const float* Lt = tl(I, K);
-                const float* Wk = Wb + (K - cb) * 1024;
-#pragma unroll 8
-                for (int k = 0; k < 32; ++k) {
-                    const float w = Wk[k * 32 + lane];
-                    s0 = fmaf(Lt[isw(warp, k)], w, s0);
-                    s1 = fmaf(Lt[isw(warp + 16, k)], w, s1);
-                }
+                const float* Wk = Wb + (K - cb) * WBS;
+                const int r = mt * 16 + gq;
+                uint32_t ah[4], al[4], bh[2], bl[2];
+                tf32_split(Lt[isw(r, kk + tq)], ah[0], al[0]);
+                tf32_split(Lt[isw(r + 8, kk + tq)], ah[1], al[1]);
+                tf32_split(Lt[isw(r, kk + tq + 4)], ah[2], al[2]);
+                tf32_split(Lt[isw(r + 8, kk + tq + 4)], ah[3], al[3]);
+                tf32_split(Wk[(kk + tq) * WLD + nb * 8 + gq], bh[0], bl[0]);
+                tf32_split(Wk[(kk + tq + 4) * WLD + nb * 8 + gq], bh[1], bl[1]);
+                mma_tf32_i(acc, al, bh);
+                mma_tf32_i(acc, ah, bl);
+                mma_tf32_i(acc, ah, bh);
             }
-            const float d0 = (I == cb && warp == lane) ? 1.f : 0.f;
-            const float d1 = (I == cb && warp + 16 == lane) ? 1.f : 0.f;
-            Wi[warp * 32 + lane] = d0 - s0;
-            Wi[(warp + 16) * 32 + lane] = d1 - s1;
+            float* P = Pq + kg * WBS;
+            const int r = mt * 16 + gq, col = nb * 8 + 2 * tq;
+            P[r * WLD + col] = acc[0];
+            P[r * WLD + col + 1] = acc[1];
+            P[(r + 8) * WLD + col] = acc[2];
+            P[(r + 8) * WLD + col + 1] = acc[3];
         }
         __syncthreads();
-        if (warp == 0) {
-            // W(I,cb)(:, lane) = inv(L(I,I)) rhs(:, lane), right-looking
-            const float* Lt = tl(I, I);
-            float w[32];
+        // (2) W(I,cb) = inv(L(I,I)) (delta - P) on warps 0-7; warp 8 inverts
+        //     the next diagonal block meanwhile
+        if (warp < 8) {
+            const int mt = warp >> 2, nb = warp & 3;
+            auto rhs = [&](int rr, int cc) {
+                const float dl = (I == cb && rr == cc) ? 1.f : 0.f;
+                return I > cb ? dl - Pq[rr * WLD + cc] - Pq[WBS + rr * WLD + cc] : dl;
+            };
+            float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-            for (int r = 0; r < 32; ++r) w[r] = Wi[r * 32 + lane];
-#pragma unroll
-            for (int r = 0; r < 32; ++r) {
-                const float d = Lt[isw(r, r)], rd = Rd[(I - cb) * 32 + r];
-                const float q = w[r] * rd;
-                w[r] = fmaf(fmaf(-q, d, w[r]), rd, q);
-#pragma unroll
-                for (int k = r + 1; k < 32; ++k) w[k] = fmaf(-Lt[isw(k, r)], w[r], w[k]);
+            for (int kk = 0; kk < 32; kk += 8) {
+                const int r = mt * 16 + gq;
+                uint32_t ah[4], al[4], bh[2], bl[2];
+                tf32_split(Dc[r * WLD + kk + tq], ah[0], al[0]);
+                tf32_split(Dc[(r + 8) * WLD + kk + tq], ah[1], al[1]);
+                tf32_split(Dc[r * WLD + kk + tq + 4], ah[2], al[2]);
+                tf32_split(Dc[(r + 8) * WLD + kk + tq + 4], ah[3], al[3]);
+                tf32_split(rhs(kk + tq, nb * 8 + gq), bh[0], bl[0]);
+                tf32_split(rhs(kk + tq + 4, nb * 8 + gq), bh[1], bl[1]);
+                mma_tf32_i(acc, al, bh);
+                mma_tf32_i(acc, ah, bl);
+                mma_tf32_i(acc, ah, bh);
             }
-#pragma unroll
-            for (int r = 0; r < 32; ++r) Wi[r * 32 + lane] = w[r];
+            const int r = mt * 16 + gq, col = nb * 8 + 2 * tq;
+            Wi[r * WLD + col] = acc[0];
+            Wi[r * WLD + col + 1] = acc[1];
+            Wi[(r + 8) * WLD + col] = acc[2];
+            Wi[(r + 8) * WLD + col + 1] = acc[3];
+        } else if (warp == 8 && I + 1 < NT) {
+            diag_inverse(I + 1, Dv + ((I + 1 - cb) & 1) * WBS);
         }
         __syncthreads();
     }
@@ -120,7 +186,7 @@ __global__ void __launch_bounds__(IT, 1) k_leaf_inv2(DevCtx c, int r0, int n, ui
         __half* W = c.w16 + (long long)r0 * kW16Ld;
         for (int e2 = tid; e2 < n * 32; e2 += IT) {
             const int i = e2 >> 5, j = e2 & 31, t = cb * 32 + j;
-            const float w = (i >= cb * 32) ? Wb[((i >> 5) - cb) * 1024 + (i & 31) * 32 + j] * up : 0.f;
+            const float w = (i >= cb * 32) ? Wb[((i >> 5) - cb) * WBS + (i & 31) * WLD + j] * up : 0.f;
             const float wz = i >= t ? w : 0.f;
             const __half hi = __float2half_rn(wz);
             const __half lo = __float2half_rn(wz - __half2float(hi));
@@ -131,7 +197,7 @@ __global__ void __launch_bounds__(IT, 1) k_leaf_inv2(DevCtx c, int r0, int n, ui
         float* W = c.w32 + (long long)r0 * kW32Ld;
         for (int e2 = tid; e2 < n * 32; e2 += IT) {
             const int i = e2 >> 5, j = e2 & 31, t = cb * 32 + j;
-            const float w = (i >= cb * 32) ? Wb[((i >> 5) - cb) * 1024 + (i & 31) * 32 + j] : 0.f;
+            const float w = (i >= cb * 32) ? Wb[((i >> 5) - cb) * WBS + (i & 31) * WLD + j] : 0.f;
             W[(long long)i * kW32Ld + t] = i >= t ? w : 0.f;
         }
     }
@@ -139,7 +205,7 @@ __global__ void __launch_bounds__(IT, 1) k_leaf_inv2(DevCtx c, int r0, int n, ui
 
 size_t inv2_smem(int n) {
     const int NB = n / 32;
-    return (size_t(NB * (NB + 1) / 2) * 1024 + size_t(NB) * 1024 + size_t(NB) * 32) * sizeof(float);
+    return (size_t(NB * (NB + 1) / 2) * 1024 + size_t(NB + 4) * WBS + size_t(NB) * 32) * sizeof(float);
 }
 
 }  // namespace
