@@ -113,6 +113,17 @@ int tc_plan_profile(tc_plan* plan, const double* dA_in, int lda_in, double* dL_o
  * t_end[i] = ms from the run's start (the concurrency timeline). */
 int tc_plan_timeline(tc_plan* plan, const double* dA_in, int lda_in, double* dL_out, int lda_out,
                      void* stream, float* t_start, float* t_end, int cap);
+/* development: the same for the host entry point (eager, pinned host buffer
+ * factored in place): op start/end plus the completion time of each H2D copy
+ * (block order) and each D2H copy (export order), ms from the first copy */
+int tc_plan_timeline_host(tc_plan* plan, double* host, int lda, void* stream, float* t_start, float* t_end,
+                          int cap_ops, float* t_h2d, int cap_h2d, float* t_d2h, int cap_d2h);
+/* development: one run of the host entry point's own CUDA graph with a
+ * global-timer stamp after every op / H2D / D2H node: completion times in ms
+ * from the graph's root (ops in op order, H2D in block order, D2H in export
+ * order; -1 = not run) */
+int tc_plan_trace_host(tc_plan* plan, double* host, int lda, void* stream, float* t_ops, int cap_ops, float* t_h2d,
+                       int cap_h2d, float* t_d2h, int cap_d2h);
 /* op i of the plan: type (0 import, 1 export, 2 check, 3 quant, 4 dequant,
  * 5 shadow, 6 potrf leaf, 7 trsm leaf, 8 gemm), gemm class (0 = tcgen05
  * FP16, 1..5 SIMT classes, -1 otherwise), level, algorithmic flops, rect */

@@ -119,6 +119,10 @@ def _load():
         "tc_plan_profile": (I, [P, P, I, P, I, P, C.POINTER(C.c_float), I]),
         "tc_plan_status": (I, [P, C.POINTER(_Info)]),
         "tc_plan_timeline": (I, [P, P, I, P, I, P, C.POINTER(C.c_float), C.POINTER(C.c_float), I]),
+        "tc_plan_trace_host": (I, [P, P, I, P, C.POINTER(C.c_float), I, C.POINTER(C.c_float), I,
+                                   C.POINTER(C.c_float), I]),
+        "tc_plan_timeline_host": (I, [P, P, I, P, C.POINTER(C.c_float), C.POINTER(C.c_float), I,
+                                      C.POINTER(C.c_float), I, C.POINTER(C.c_float), I]),
         "tc_info_message": (I, [P, C.POINTER(_Info), C.c_char_p, I]),
         "tc_potrs_device": (I, [I, P, I, P, I, I, P]),
         "tc_spd_generate_host": (I, [I, U64, P, I]),

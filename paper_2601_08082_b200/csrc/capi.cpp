@@ -412,6 +412,35 @@ int tc_plan_timeline(tc_plan* plan, const double* dA_in, int lda_in, double* dL_
     return TC_OK;
 }
 
+int tc_plan_timeline_host(tc_plan* plan, double* host, int lda, void* stream, float* t_start, float* t_end,
+                          int cap_ops, float* t_h2d, int cap_h2d, float* t_d2h, int cap_d2h) {
+    if (!plan || !host || !t_start || !t_end || !t_h2d || !t_d2h) return fail(TC_INVALID_ARGUMENT, "null argument");
+    std::vector<float> a, b, h, d;
+    std::string err;
+    if (!plan->eng->timeline_host(host, lda, static_cast<cudaStream_t>(stream), a, b, h, d, &err))
+        return fail(TC_CUDA_ERROR, err);
+    for (int i = 0; i < cap_ops && i < int(a.size()); ++i) {
+        t_start[i] = a[i];
+        t_end[i] = b[i];
+    }
+    for (int i = 0; i < cap_h2d && i < int(h.size()); ++i) t_h2d[i] = h[i];
+    for (int i = 0; i < cap_d2h && i < int(d.size()); ++i) t_d2h[i] = d[i];
+    return TC_OK;
+}
+
+int tc_plan_trace_host(tc_plan* plan, double* host, int lda, void* stream, float* t_ops, int cap_ops, float* t_h2d,
+                       int cap_h2d, float* t_d2h, int cap_d2h) {
+    if (!plan || !host || !t_ops || !t_h2d || !t_d2h) return fail(TC_INVALID_ARGUMENT, "null argument");
+    std::vector<float> a, h, d;
+    std::string err;
+    if (!plan->eng->trace_host(host, lda, static_cast<cudaStream_t>(stream), a, h, d, &err))
+        return fail(TC_CUDA_ERROR, err);
+    for (int i = 0; i < cap_ops && i < int(a.size()); ++i) t_ops[i] = a[i];
+    for (int i = 0; i < cap_h2d && i < int(h.size()); ++i) t_h2d[i] = h[i];
+    for (int i = 0; i < cap_d2h && i < int(d.size()); ++i) t_d2h[i] = d[i];
+    return TC_OK;
+}
+
 int tc_plan_profile(tc_plan* plan, const double* dA_in, int lda_in, double* dL_out, int lda_out, void* stream,
                     float* op_ms, int cap) {
     if (!plan || !dA_in || !dL_out || !op_ms) return fail(TC_INVALID_ARGUMENT, "null argument");

@@ -24,6 +24,15 @@ constexpr int kRaRing = 16;
         }                                                                   \
     } while (0)
 
+// split a column-major rect into column ranges of at most kChunkBytes (the
+// copy in flight is the longest any other work queued behind it on a shared
+// hardware channel can wait)
+void chunk_rect(const Rect& r, std::vector<Rect>& out) {
+    constexpr double kChunkBytes = 64.0 * 1024 * 1024;
+    const int w = std::max(1, int(kChunkBytes / (8.0 * std::max(1, r.m))));
+    for (int c = 0; c < r.n; c += w) out.push_back({r.r0, r.c0 + c, r.m, std::min(w, r.n - c)});
+}
+
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 }  // namespace
@@ -33,6 +42,9 @@ Engine::~Engine() {
     if (graph_) cudaGraphDestroy(graph_);
     if (hexec_) cudaGraphExecDestroy(hexec_);
     if (hgraph_) cudaGraphDestroy(hgraph_);
+    drop_host_phases();
+    for (auto e : ev_hc_) cudaEventDestroy(e);
+    for (auto e : ev_dc_) cudaEventDestroy(e);
     for (auto e : ev_h2d_) cudaEventDestroy(e);
     for (auto e : ra_ev_) cudaEventDestroy(e);
     for (auto e : ev_d2h_) cudaEventDestroy(e);
@@ -311,6 +323,11 @@ bool Engine::enqueue_ops(cudaStream_t origin, std::string* err, const HostIO* io
             TC_TRY(cudaMemcpy2DAsync(d_stage_ + size_t(r.c0) * n + r.r0, esz * n, io->host + size_t(r.c0) * io->lda + r.r0,
                                      esz * io->lda, esz * size_t(r.m), size_t(r.n), cudaMemcpyHostToDevice, cs_h2d_));
             TC_TRY(cudaEventRecord(ev_h2d_[b], cs_h2d_));
+            if (tl_h2d_) {
+                tl_h2d_->emplace_back();
+                TC_TRY(cudaEventCreate(&tl_h2d_->back()));
+                TC_TRY(cudaEventRecord(tl_h2d_->back(), cs_h2d_));
+            }
         }
     }
     int n_d2h = 0;
@@ -333,6 +350,11 @@ bool Engine::enqueue_ops(cudaStream_t origin, std::string* err, const HostIO* io
             TC_TRY(cudaMemcpy2DAsync(io->host + size_t(r.c0) * io->lda + r.r0, esz * io->lda,
                                      d_stage_ + size_t(r.c0) * n + r.r0, esz * n, esz * size_t(r.m), size_t(r.n),
                                      cudaMemcpyDeviceToHost, cs_d2h_));
+            if (tl_d2h_) {
+                tl_d2h_->emplace_back();
+                TC_TRY(cudaEventCreate(&tl_d2h_->back()));
+                TC_TRY(cudaEventRecord(tl_d2h_->back(), cs_d2h_));
+            }
         }
     }
     for (int s = 0; s < S; ++s) {
@@ -381,7 +403,7 @@ bool Engine::enqueue(const double* a_in, long long lda_in, double* l_out, long l
     TC_TRY(cudaEventRecord(ra_ev_[size_t(slot - h_ra_)], stream));
     if (use_graph) {
         if (!gexec_ && dag_graph) {
-            if (!build_dag_graph(&graph_, nullptr, err)) return false;
+            if (!build_dag_graph(&graph_, -1, err)) return false;
             TC_TRY(cudaGraphInstantiate(&gexec_, graph_, 0));
         }
         if (!gexec_) {
@@ -410,8 +432,11 @@ bool Engine::enqueue(const double* a_in, long long lda_in, double* l_out, long l
     return true;
 }
 
-bool Engine::build_dag_graph(cudaGraph_t* out, const HostIO* io, std::string* err) {
+bool Engine::build_dag_graph(cudaGraph_t* out, int phase, std::string* err) {
     *out = nullptr;
+    // phase >= 0: only the ops of that host-path phase (edges to earlier
+    // phases are satisfied by the launch order); the root only in phase 0
+    auto in = [&](int i) { return phase < 0 || ph_op_[size_t(i)] == phase; };
     const int N = int(plan.ops.size());
     cudaGraph_t g = nullptr;
     TC_TRY(cudaGraphCreate(&g, 0));
@@ -450,45 +475,27 @@ bool Engine::build_dag_graph(cudaGraph_t* out, const HostIO* io, std::string* er
         return e == cudaSuccess;
     };
     cudaGraphNode_t root = nullptr;
-    ok = add(cap_hi, {}, [&](cudaStream_t s) { reset_words(s); }, &root);
-    // host IO: H2D per block (chained, depth-first order) and D2H per export
-    std::vector<cudaGraphNode_t> h2d(plan.blocks.size(), nullptr);
-    const int n = plan.n;
-    const size_t esz = sizeof(double);
-    if (ok && io) {
-        cudaGraphNode_t prev = root;
-        for (int b : plan.block_order) {
-            const Rect& r = plan.blocks[b].rect;
-            ok = add(cap_lo, {prev}, [&](cudaStream_t s) {
-                     cudaMemcpy2DAsync(d_stage_ + size_t(r.c0) * n + r.r0, esz * n,
-                                       io->host + size_t(r.c0) * io->lda + r.r0, esz * io->lda, esz * size_t(r.m),
-                                       size_t(r.n), cudaMemcpyHostToDevice, s);
-                 }, &h2d[size_t(b)]);
-            if (!ok) break;
-            prev = h2d[size_t(b)];
-        }
-    }
+    if (phase <= 0) ok = add(cap_hi, {}, [&](cudaStream_t s) { reset_words(s); }, &root);
+    // trace mode: slot 0 root, 1 + i op i
+    auto stamp = [&](cudaGraphNode_t after, int k) {
+        if (!d_trace_ || !ok || !after) return;
+        cudaGraphNode_t sn = nullptr;
+        unsigned long long* slot = d_trace_ + k;
+        ok = add(cap_lo, {after}, [&](cudaStream_t s) { launch_stamp(slot, s); }, &sn);
+    };
+    stamp(root, 0);
     std::vector<cudaGraphNode_t> node(size_t(N), nullptr);
-    cudaGraphNode_t prev_d2h = root;
     for (int i = 0; ok && i < N; ++i) {
+        if (!in(i)) continue;
         const Op& op = plan.ops[i];
         std::vector<cudaGraphNode_t> deps;
-        for (int d : op.deps) deps.push_back(node[size_t(d)]);
-        if (io && (op.type == OP_IMPORT || op.type == OP_QUANT))
-            for (int b : op.blocks) deps.push_back(h2d[size_t(b)]);
-        if (deps.empty()) deps.push_back(root);
+        for (int d : op.deps)
+            if (in(d)) deps.push_back(node[size_t(d)]);
+        if (deps.empty() && root) deps.push_back(root);
         ok = add(op.bulk ? cap_lo : cap_hi, deps, [&](cudaStream_t s) { launch_op(i, s); }, &node[size_t(i)]);
-        if (ok && io && op.type == OP_EXPORT) {
-            const Rect& r = op.rect;
-            cudaGraphNode_t d2h = nullptr;
-            ok = add(cap_lo, {node[size_t(i)], prev_d2h}, [&](cudaStream_t s) {
-                     cudaMemcpy2DAsync(io->host + size_t(r.c0) * io->lda + r.r0, esz * io->lda,
-                                       d_stage_ + size_t(r.c0) * n + r.r0, esz * n, esz * size_t(r.m), size_t(r.n),
-                                       cudaMemcpyDeviceToHost, s);
-                 }, &d2h);
-            prev_d2h = d2h;
-        }
     }
+    if (d_trace_)
+        for (int i = 0; i < N; ++i) stamp(node[size_t(i)], 1 + i);
     cudaStreamDestroy(cap_hi);
     cudaStreamDestroy(cap_lo);
     if (!ok) {
@@ -501,20 +508,24 @@ bool Engine::build_dag_graph(cudaGraph_t* out, const HostIO* io, std::string* er
     return true;
 }
 
-bool Engine::enqueue_host(double* host, long long lda, cudaStream_t stream, std::string* err) {
-    if (!prepare(err)) return false;
+bool Engine::ensure_stage(std::string* err) {
+    if (d_stage_) return true;
     const int n = plan.n;
-    if (!d_stage_) {
-        TC_TRY(cudaMalloc(&d_stage_, sizeof(double) * size_t(n) * size_t(n)));
-        TC_TRY(cudaStreamCreateWithFlags(&cs_h2d_, cudaStreamNonBlocking));
-        TC_TRY(cudaStreamCreateWithFlags(&cs_d2h_, cudaStreamNonBlocking));
-        ev_h2d_.resize(plan.blocks.size());
-        for (auto& e : ev_h2d_) TC_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        int n_exp = 0;
-        for (const Op& op : plan.ops) n_exp += op.type == OP_EXPORT;
-        ev_d2h_.resize(size_t(n_exp) + 2);
-        for (auto& e : ev_d2h_) TC_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    }
+    TC_TRY(cudaMalloc(&d_stage_, sizeof(double) * size_t(n) * size_t(n)));
+    TC_TRY(cudaStreamCreateWithFlags(&cs_h2d_, cudaStreamNonBlocking));
+    TC_TRY(cudaStreamCreateWithFlags(&cs_d2h_, cudaStreamNonBlocking));
+    ev_h2d_.resize(plan.blocks.size());
+    for (auto& e : ev_h2d_) TC_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    int n_exp = 0;
+    for (const Op& op : plan.ops) n_exp += op.type == OP_EXPORT;
+    ev_d2h_.resize(size_t(n_exp) + 2);
+    for (auto& e : ev_d2h_) TC_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    return true;
+}
+
+bool Engine::enqueue_host(double* host, long long lda, cudaStream_t stream, std::string* err) {
+    if (!prepare(err) || !ensure_stage(err)) return false;
+    const int n = plan.n;
     RunArgs* slot = next_args(err);
     if (!slot) return false;
     slot->a_in = d_stage_;
@@ -527,30 +538,29 @@ bool Engine::enqueue_host(double* host, long long lda, cudaStream_t stream, std:
     cudaPointerAttributes pa{};
     const bool pinned = cudaPointerGetAttributes(&pa, host) == cudaSuccess && pa.type == cudaMemoryTypeHost;
     cudaGetLastError();
-    if (use_graph && pinned) {
+    if (use_graph && pinned && dag_graph) {
+        if (hph_exec_.empty() && !build_host_phases(err)) return false;
+        if (!run_host(io, stream, err)) return false;
+    } else if (use_graph && pinned) {
         if (!hexec_ || hkey_ != host || hkey_lda_ != lda) {
             if (hexec_) cudaGraphExecDestroy(hexec_);
             if (hgraph_) cudaGraphDestroy(hgraph_);
             hexec_ = nullptr;
             hgraph_ = nullptr;
             cudaGraph_t g = nullptr;
-            if (dag_graph) {
-                if (!build_dag_graph(&g, &io, err)) return false;
-            } else {
-                cudaStream_t cap;
-                TC_TRY(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
-                TC_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
-                std::string e2;
-                const bool ok = enqueue_ops(cap, &e2, &io);
-                const cudaError_t ce = cudaStreamEndCapture(cap, &g);
-                cudaStreamDestroy(cap);
-                if (!ok) {
-                    if (err) *err = e2;
-                    if (g) cudaGraphDestroy(g);
-                    return false;
-                }
-                TC_TRY(ce);
+            cudaStream_t cap;
+            TC_TRY(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+            TC_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+            std::string e2;
+            const bool ok = enqueue_ops(cap, &e2, &io);
+            const cudaError_t ce = cudaStreamEndCapture(cap, &g);
+            cudaStreamDestroy(cap);
+            if (!ok) {
+                if (err) *err = e2;
+                if (g) cudaGraphDestroy(g);
+                return false;
             }
+            TC_TRY(ce);
             hgraph_ = g;
             TC_TRY(cudaGraphInstantiate(&hexec_, hgraph_, 0));
             hkey_ = host;
@@ -561,6 +571,168 @@ bool Engine::enqueue_host(double* host, long long lda, cudaStream_t stream, std:
         if (!enqueue_ops(stream, err, &io)) return false;
     }
     last_stream_ = stream;
+    return true;
+}
+
+// host-path phases: op i's phase follows the last H2D it needs (its own
+// block for an import / quant, else the latest of its dependencies), the H2D
+// stream cut into ~kPhases equal byte ranges (empty ranges dropped)
+bool Engine::build_host_phases(std::string* err) {
+    constexpr int kPhases = 16;
+    const int N = int(plan.ops.size()), B = int(plan.block_order.size());
+    std::vector<int> pos(plan.blocks.size(), -1);
+    std::vector<double> cum(size_t(B), 0.0);
+    double tot = 0.0;
+    for (int k = 0; k < B; ++k) {
+        const Rect& r = plan.blocks[size_t(plan.block_order[size_t(k)])].rect;
+        pos[size_t(plan.block_order[size_t(k)])] = k;
+        tot += double(r.m) * double(r.n);
+        cum[size_t(k)] = tot;
+    }
+    std::vector<int> need(size_t(N), -1);
+    for (int i = 0; i < N; ++i) {
+        const Op& op = plan.ops[size_t(i)];
+        int m = -1;
+        for (int d : op.deps) m = std::max(m, need[size_t(d)]);
+        if (op.type == OP_IMPORT || op.type == OP_QUANT)
+            for (int b : op.blocks) m = std::max(m, pos[size_t(b)]);
+        need[size_t(i)] = m;
+    }
+    // raw phase of an H2D position: its byte range; then compact
+    auto raw = [&](int k) { return k < 0 ? 0 : std::min(kPhases - 1, int(cum[size_t(k)] * kPhases / tot)); };
+    std::vector<int> used(kPhases, 0), wait(kPhases, -1);
+    for (int i = 0; i < N; ++i) used[size_t(raw(need[size_t(i)]))] = 1;
+    std::vector<int> remap(kPhases, -1);
+    int P = 0;
+    for (int q = 0; q < kPhases; ++q)
+        if (used[size_t(q)]) remap[size_t(q)] = P++;
+    ph_op_.assign(size_t(N), 0);
+    ph_wait_.assign(size_t(P), -1);
+    for (int i = 0; i < N; ++i) {
+        const int p = remap[size_t(raw(need[size_t(i)]))];
+        ph_op_[size_t(i)] = p;
+        if (need[size_t(i)] >= 0)
+            ph_wait_[size_t(p)] = std::max(ph_wait_[size_t(p)], need[size_t(i)]);
+    }
+    // H2D chunks in block order; a phase needs every chunk up to the last
+    // one of its latest block.  D2H chunks of the exports, ordered by phase
+    hc_rect_.clear();
+    std::vector<int> last_chunk(size_t(B), -1);
+    for (int k = 0; k < B; ++k) {
+        chunk_rect(plan.blocks[size_t(plan.block_order[size_t(k)])].rect, hc_rect_);
+        last_chunk[size_t(k)] = int(hc_rect_.size()) - 1;
+    }
+    ph_need_.assign(size_t(P), -1);
+    for (int p = 0; p < P; ++p)
+        if (ph_wait_[size_t(p)] >= 0) ph_need_[size_t(p)] = last_chunk[size_t(ph_wait_[size_t(p)])];
+    std::vector<std::pair<int, Rect>> dl;
+    for (int i = 0; i < N; ++i)
+        if (plan.ops[size_t(i)].type == OP_EXPORT) {
+            std::vector<Rect> rs;
+            chunk_rect(plan.ops[size_t(i)].rect, rs);
+            for (const Rect& r : rs) dl.push_back({ph_op_[size_t(i)], r});
+        }
+    std::stable_sort(dl.begin(), dl.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+    dc_rect_.clear();
+    dc_phase_.clear();
+    for (auto& x : dl) {
+        dc_phase_.push_back(x.first);
+        dc_rect_.push_back(x.second);
+    }
+    for (int p = 0; p < P; ++p) {
+        cudaGraph_t g = nullptr;
+        if (!build_dag_graph(&g, p, err)) return false;
+        cudaGraphExec_t x = nullptr;
+        const cudaError_t e = cudaGraphInstantiate(&x, g, 0);
+        cudaGraphDestroy(g);
+        TC_TRY(e);
+        hph_exec_.push_back(x);
+        cudaEvent_t ev;
+        TC_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        ev_ph_.push_back(ev);
+    }
+    return true;
+}
+
+void Engine::drop_host_phases() {
+    for (auto x : hph_exec_) cudaGraphExecDestroy(x);
+    for (auto e : ev_ph_) cudaEventDestroy(e);
+    hph_exec_.clear();
+    ev_ph_.clear();
+}
+
+
+// host entry point with the DAG graphs (synchronous): the calling thread
+// feeds the copy engines and launches each phase's graph once the blocks it
+// reads have landed and the previous phase has finished, and copies every
+// exported block back once its phase has finished.  Nothing on the device
+// ever waits on a copy or on a later phase (a waiting stream head would also
+// stall unrelated work sharing its hardware channel); at most kDepth copies
+// per direction are in flight.
+bool Engine::run_host(const HostIO& io, cudaStream_t stream, std::string* err) {
+    constexpr int kDepth = 3;
+    const int n = plan.n, N = int(plan.ops.size());
+    const int P = int(hph_exec_.size()), H = int(hc_rect_.size()), D = int(dc_rect_.size());
+    const size_t esz = sizeof(double);
+    while (int(ev_hc_.size()) < H) {
+        cudaEvent_t e;
+        TC_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        ev_hc_.push_back(e);
+    }
+    while (int(ev_dc_.size()) < D) {
+        cudaEvent_t e;
+        TC_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        ev_dc_.push_back(e);
+    }
+    // earlier work on `stream` (the RunArgs upload, a previous run) first
+    if (!fork_) TC_TRY(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming));
+    TC_TRY(cudaEventRecord(fork_, stream));
+    TC_TRY(cudaEventSynchronize(fork_));
+    auto done = [&](cudaEvent_t e, bool* ok) {
+        const cudaError_t q = cudaEventQuery(e);
+        if (q == cudaSuccess) return true;
+        if (q != cudaErrorNotReady) *ok = false;
+        return false;
+    };
+    int h_iss = 0, h_done = 0, p_iss = 0, p_done = 0, d_iss = 0, d_done = 0;
+    bool ok = true;
+    while (ok && (h_done < H || p_done < P || d_done < D)) {
+        bool moved = false;
+        while (h_done < h_iss && done(ev_hc_[size_t(h_done)], &ok)) ++h_done, moved = true;
+        while (ok && h_iss < H && h_iss - h_done < kDepth) {
+            const Rect& r = hc_rect_[size_t(h_iss)];
+            TC_TRY(cudaMemcpy2DAsync(d_stage_ + size_t(r.c0) * n + r.r0, esz * n,
+                                     io.host + size_t(r.c0) * io.lda + r.r0, esz * io.lda, esz * size_t(r.m),
+                                     size_t(r.n), cudaMemcpyHostToDevice, cs_h2d_));
+            if (d_trace_) launch_stamp(d_trace_ + 1 + N + h_iss, cs_h2d_);
+            TC_TRY(cudaEventRecord(ev_hc_[size_t(h_iss)], cs_h2d_));
+            ++h_iss;
+            moved = true;
+        }
+        while (p_done < p_iss && done(ev_ph_[size_t(p_done)], &ok)) ++p_done, moved = true;
+        if (ok && p_iss < P && p_iss == p_done && h_done > ph_need_[size_t(p_iss)]) {
+            TC_TRY(cudaGraphLaunch(hph_exec_[size_t(p_iss)], stream));
+            TC_TRY(cudaEventRecord(ev_ph_[size_t(p_iss)], stream));
+            ++p_iss;
+            moved = true;
+        }
+        while (d_done < d_iss && done(ev_dc_[size_t(d_done)], &ok)) ++d_done, moved = true;
+        while (ok && d_iss < D && d_iss - d_done < kDepth && p_done > dc_phase_[size_t(d_iss)]) {
+            const Rect& r = dc_rect_[size_t(d_iss)];
+            TC_TRY(cudaMemcpy2DAsync(io.host + size_t(r.c0) * io.lda + r.r0, esz * io.lda,
+                                     d_stage_ + size_t(r.c0) * n + r.r0, esz * n, esz * size_t(r.m), size_t(r.n),
+                                     cudaMemcpyDeviceToHost, cs_d2h_));
+            if (d_trace_) launch_stamp(d_trace_ + 1 + N + H + d_iss, cs_d2h_);
+            TC_TRY(cudaEventRecord(ev_dc_[size_t(d_iss)], cs_d2h_));
+            ++d_iss;
+            moved = true;
+        }
+        if (!moved) std::this_thread::sleep_for(std::chrono::microseconds(20));
+    }
+    if (!ok) {
+        if (err) *err = std::string("host pipeline: ") + cudaGetErrorString(cudaGetLastError());
+        return false;
+    }
     return true;
 }
 
@@ -672,6 +844,106 @@ bool Engine::timeline(const double* a_in, long long lda_in, double* l_out, long 
     cudaEventDestroy(origin_ev);
     cudaFreeHost(flag);
     last_stream_ = stream;
+    return true;
+}
+
+bool Engine::timeline_host(double* host, long long lda, cudaStream_t stream, std::vector<float>& t0,
+                           std::vector<float>& t1, std::vector<float>& th2d, std::vector<float>& td2h,
+                           std::string* err) {
+    if (!prepare(err) || !ensure_stage(err)) return false;
+    const int n = plan.n;
+    RunArgs* slot = next_args(err);
+    if (!slot) return false;
+    slot->a_in = d_stage_;
+    slot->l_out = d_stage_;
+    slot->lda_in = n;
+    slot->lda_out = n;
+    TC_TRY(cudaMemcpyAsync(d_ra_, slot, sizeof(RunArgs), cudaMemcpyHostToDevice, stream));
+    TC_TRY(cudaEventRecord(ra_ev_[size_t(slot - h_ra_)], stream));
+    const int N = int(plan.ops.size());
+    std::vector<cudaEvent_t> tl(2 * size_t(N)), eh, ed;
+    for (auto& e : tl) TC_TRY(cudaEventCreate(&e));
+    int* flag = nullptr;
+    TC_TRY(cudaHostAlloc(&flag, sizeof(int), cudaHostAllocMapped));
+    *reinterpret_cast<volatile int*>(flag) = 0;
+    int* dflag = nullptr;
+    TC_TRY(cudaHostGetDevicePointer(&dflag, flag, 0));
+    launch_gate(dflag, stream);
+    cudaEvent_t origin_ev;
+    TC_TRY(cudaEventCreate(&origin_ev));
+    TC_TRY(cudaEventRecord(origin_ev, stream));
+    std::thread release([flag] {
+        std::this_thread::sleep_for(std::chrono::milliseconds(300));
+        __sync_synchronize();
+        *reinterpret_cast<volatile int*>(flag) = 1;
+    });
+    HostIO io{host, lda};
+    tl_h2d_ = &eh;
+    tl_d2h_ = &ed;
+    const bool ok = enqueue_ops(stream, err, &io, &tl);
+    tl_h2d_ = tl_d2h_ = nullptr;
+    release.join();
+    if (!ok) return false;
+    TC_TRY(cudaStreamSynchronize(stream));
+    TC_TRY(cudaDeviceSynchronize());
+    auto rd = [&](std::vector<cudaEvent_t>& ev, std::vector<float>& out) {
+        out.assign(ev.size(), 0.f);
+        for (size_t i = 0; i < ev.size(); ++i) cudaEventElapsedTime(&out[i], origin_ev, ev[i]);
+        for (auto& e : ev) cudaEventDestroy(e);
+    };
+    t0.assign(N, 0.f);
+    t1.assign(N, 0.f);
+    for (int i = 0; i < N; ++i) {
+        cudaEventElapsedTime(&t0[i], origin_ev, tl[2 * i]);
+        cudaEventElapsedTime(&t1[i], origin_ev, tl[2 * i + 1]);
+    }
+    for (auto& e : tl) cudaEventDestroy(e);
+    rd(eh, th2d);
+    rd(ed, td2h);
+    cudaEventDestroy(origin_ev);
+    cudaFreeHost(flag);
+    return true;
+}
+
+bool Engine::trace_host(double* host, long long lda, cudaStream_t stream, std::vector<float>& top,
+                        std::vector<float>& th2d, std::vector<float>& td2h, std::string* err) {
+    if (!prepare(err) || !ensure_stage(err)) return false;
+    const int N = int(plan.ops.size());
+    std::vector<Rect> hr, dr;  // the copy chunks run_host will issue
+    for (int b : plan.block_order) chunk_rect(plan.blocks[size_t(b)].rect, hr);
+    for (const Op& op : plan.ops)
+        if (op.type == OP_EXPORT) chunk_rect(op.rect, dr);
+    const int B = int(hr.size()), E = int(dr.size());
+    const size_t slots = 1 + size_t(N) + size_t(B) + size_t(E);
+    TC_TRY(cudaMalloc(&d_trace_, slots * sizeof(unsigned long long)));
+    TC_TRY(cudaMemset(d_trace_, 0, slots * sizeof(unsigned long long)));
+    auto drop = [&] {
+        if (hexec_) cudaGraphExecDestroy(hexec_);
+        if (hgraph_) cudaGraphDestroy(hgraph_);
+        hexec_ = nullptr;
+        hgraph_ = nullptr;
+        hkey_ = nullptr;
+        drop_host_phases();
+    };
+    drop();  // rebuild with stamp nodes
+    const bool ok = enqueue_host(host, lda, stream, err);
+    std::vector<unsigned long long> h(slots, 0);
+    bool ok2 = ok && cudaStreamSynchronize(stream) == cudaSuccess &&
+               cudaMemcpy(h.data(), d_trace_, slots * sizeof(unsigned long long), cudaMemcpyDeviceToHost) == cudaSuccess;
+    drop();
+    cudaFree(d_trace_);
+    d_trace_ = nullptr;
+    if (!ok2) {
+        if (err && err->empty()) *err = "trace run failed";
+        return false;
+    }
+    auto ms = [&](size_t k) { return h[k] ? float(double((long long)(h[k] - h[0])) * 1e-6) : -1e9f; };
+    top.assign(N, 0.f);
+    th2d.assign(B, 0.f);
+    td2h.assign(E, 0.f);
+    for (int i = 0; i < N; ++i) top[i] = ms(1 + i);
+    for (int i = 0; i < B; ++i) th2d[i] = ms(1 + N + i);
+    for (int i = 0; i < E; ++i) td2h[i] = ms(1 + N + B + i);
     return true;
 }
 

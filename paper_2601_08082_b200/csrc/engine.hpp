@@ -104,6 +104,14 @@ class Engine {
     cudaStream_t cs_h2d_ = nullptr, cs_d2h_ = nullptr;
     std::vector<cudaEvent_t> ev_h2d_;     // per block: H2D done
     std::vector<cudaEvent_t> ev_d2h_;     // per export: D2H done (joined at the end)
+    std::vector<cudaEvent_t>* tl_h2d_ = nullptr;  // timeline_host: timing events after each copy
+    std::vector<cudaEvent_t>* tl_d2h_ = nullptr;
+    bool ensure_stage(std::string* err);
+    bool run_host(const HostIO& io, cudaStream_t stream, std::string* err);
+    std::vector<Rect> hc_rect_, dc_rect_;      // H2D chunks (block order), D2H chunks (by phase)
+    std::vector<int> dc_phase_, ph_need_;      // phase of each D2H chunk; last H2D chunk a phase reads
+    std::vector<cudaEvent_t> ev_hc_, ev_dc_;   // per chunk: copy done
+    unsigned long long* d_trace_ = nullptr;  // trace_host: stamp slots (null: no stamp nodes)
     cudaGraph_t hgraph_ = nullptr;
     cudaGraphExec_t hexec_ = nullptr;
     const double* hkey_ = nullptr;
@@ -120,13 +128,30 @@ class Engine {
     // the op DAG as an explicit CUDA graph: one child-graph node per op (its
     // launch captured alone), edges = the plan's dependencies only -- no
     // stream-order edges between independent ops
-    bool build_dag_graph(cudaGraph_t* out, const HostIO* io, std::string* err);
+    bool build_dag_graph(cudaGraph_t* out, int phase, std::string* err);
+    // host entry point: one DAG graph per phase of the H2D stream
+    std::vector<cudaGraphExec_t> hph_exec_;
+    std::vector<cudaEvent_t> ev_ph_;
+    std::vector<int> ph_op_, ph_wait_;  // phase of each op; last block (H2D position) a phase reads (-1: none)
+    bool build_host_phases(std::string* err);
+    void drop_host_phases();
 
    public:
     // eager multi-stream run with a timing event before and after every op:
     // start/end (ms from the first op's start) -- the concurrency timeline
     bool timeline(const double* a_in, long long lda_in, double* l_out, long long lda_out, cudaStream_t stream,
                   std::vector<float>& t0, std::vector<float>& t1, std::string* err);
+    // the same for the host entry point (eager): op start/end plus the
+    // completion time of every H2D copy (block order) and D2H copy (export
+    // order), ms from the first H2D's start
+    bool timeline_host(double* host, long long lda, cudaStream_t stream, std::vector<float>& t0,
+                       std::vector<float>& t1, std::vector<float>& th2d, std::vector<float>& td2h, std::string* err);
+    // the host entry point's pipeline itself (DAG graph phases), with a
+    // global-timer stamp after the root, every op and every H2D / D2H copy
+    // chunk: completion times (ms from the root) -- ops in op order, H2D
+    // chunks in issue order, D2H chunks in issue order
+    bool trace_host(double* host, long long lda, cudaStream_t stream, std::vector<float>& top,
+                    std::vector<float>& th2d, std::vector<float>& td2h, std::string* err);
 };
 
 }  // namespace tcb

@@ -345,6 +345,13 @@ __global__ void k_gate(volatile int* flag) {
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     } while (*flag == 0 && t - t0 < 5000000000ull);
 }
+// development trace: the global timer (ns) when this node runs
+__global__ void k_stamp(unsigned long long* out) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    *out = t;
+}
 }  // namespace
 void launch_gate(volatile int* host_flag, cudaStream_t s) { k_gate<<<1, 1, 0, s>>>(host_flag); }
+void launch_stamp(unsigned long long* out, cudaStream_t s) { k_stamp<<<1, 1, 0, s>>>(out); }
 }  // namespace tcb

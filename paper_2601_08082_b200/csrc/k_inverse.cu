@@ -12,9 +12,8 @@
 // CTA c computes column block c of W by block forward substitution:
 //   W(I,c) = inv(L(I,I)) (delta_Ic - sum_{c<=K<I} L(I,K) W(K,c)),  I >= c
 // -- both products on the warp-level tensor path (mma.sync TF32, three-pass
-// hi/lo split: FP32-accurate); the 32x32 diagonal inverses by one warp each
-// (lane = column, right-looking substitution), the next one computed while
-// the current block's product runs.
+// hi/lo split: FP32-accurate); the 32x32 diagonal inverses up front, one
+// warp each (lane = column, right-looking substitution).
 // The first solve's singular-diagonal check (kernels.cpp:79-81) is reported
 // here: the first j with L(j,j) zero or non-finite.
 #include "device.cuh"
@@ -50,8 +49,7 @@ __global__ void __launch_bounds__(IT, 1) k_leaf_inv2(DevCtx c, int r0, int n, ui
     // tiles (I, K), cb <= K <= I, local index (I-cb)(I-cb+1)/2 + (K-cb)
     float* Ls = ism;
     float* Wb = Ls + ((NB * (NB + 1)) >> 1) * 1024;  // [NB][32][WLD] row-major W(I, cb)
-    float* Dv = Wb + NB * WBS;                        // [2][32][WLD] inv(L(I,I)), double-buffered
-    float* Pq = Dv + 2 * WBS;                         // [2][32][WLD] K-split partials of the product
+    float* Pq = Wb + NB * WBS;                        // [2][32][WLD] K-split partials of the product
     float* Rd = Pq + 2 * WBS;                         // [NB*32] reciprocal diagonal
     const T* g = lvbuf<MODE == 0 ? 0 : 1>(c) + (long long)r0 * c.ldw + r0;
     const long long ld = c.ldw;
@@ -83,10 +81,12 @@ __global__ void __launch_bounds__(IT, 1) k_leaf_inv2(DevCtx c, int r0, int n, ui
     }
     __syncthreads();
 
-    // inv(L(I,I)) of one diagonal block by one warp: lane = column, right-
-    // looking forward substitution, reciprocal + Newton correction
-    auto diag_inverse = [&](int I, float* D) {
-        const float* Lt = tl(I, I);
+    // inv(L(I,I)) of every diagonal block, one warp each, in place (the
+    // diagonal tiles are read only as these inverses afterwards): lane =
+    // column, right-looking forward substitution, reciprocal + Newton step
+    if (warp < NB) {
+        const int I = cb + warp;
+        float* Lt = tl(I, I);
         float x[32];
 #pragma unroll
         for (int r = 0; r < 32; ++r) x[r] = r == lane ? 1.f : 0.f;
@@ -98,16 +98,16 @@ __global__ void __launch_bounds__(IT, 1) k_leaf_inv2(DevCtx c, int r0, int n, ui
 #pragma unroll
             for (int k = r + 1; k < 32; ++k) x[k] = fmaf(-Lt[isw(k, r)], x[r], x[k]);
         }
+        __syncwarp();
 #pragma unroll
-        for (int r = 0; r < 32; ++r) D[r * WLD + lane] = x[r];
-    };
-    if (warp == 0) diag_inverse(cb, Dv);
+        for (int r = 0; r < 32; ++r) Lt[isw(r, lane)] = x[r];
+    }
     __syncthreads();
 
     const int gq = lane >> 2, tq = lane & 3;
     for (int I = cb; I < NT; ++I) {
         float* Wi = Wb + (I - cb) * WBS;
-        float* Dc = Dv + ((I - cb) & 1) * WBS;
+        const float* Dc = tl(I, I);  // inv(L(I,I)), tile layout
         // (1) P = sum_{cb <= K < I} L(I,K) W(K,cb) on the tensor cores: 8
         //     16x8 output tiles, the K range split over two warp groups
         if (I > cb) {
@@ -139,8 +139,7 @@ __global__ void __launch_bounds__(IT, 1) k_leaf_inv2(DevCtx c, int r0, int n, ui
             P[(r + 8) * WLD + col + 1] = acc[3];
         }
         __syncthreads();
-        // (2) W(I,cb) = inv(L(I,I)) (delta - P) on warps 0-7; warp 8 inverts
-        //     the next diagonal block meanwhile
+        // (2) W(I,cb) = inv(L(I,I)) (delta - P) on warps 0-7
         if (warp < 8) {
             const int mt = warp >> 2, nb = warp & 3;
             auto rhs = [&](int rr, int cc) {
@@ -152,10 +151,10 @@ __global__ void __launch_bounds__(IT, 1) k_leaf_inv2(DevCtx c, int r0, int n, ui
             for (int kk = 0; kk < 32; kk += 8) {
                 const int r = mt * 16 + gq;
                 uint32_t ah[4], al[4], bh[2], bl[2];
-                tf32_split(Dc[r * WLD + kk + tq], ah[0], al[0]);
-                tf32_split(Dc[(r + 8) * WLD + kk + tq], ah[1], al[1]);
-                tf32_split(Dc[r * WLD + kk + tq + 4], ah[2], al[2]);
-                tf32_split(Dc[(r + 8) * WLD + kk + tq + 4], ah[3], al[3]);
+                tf32_split(Dc[isw(r, kk + tq)], ah[0], al[0]);
+                tf32_split(Dc[isw(r + 8, kk + tq)], ah[1], al[1]);
+                tf32_split(Dc[isw(r, kk + tq + 4)], ah[2], al[2]);
+                tf32_split(Dc[isw(r + 8, kk + tq + 4)], ah[3], al[3]);
                 tf32_split(rhs(kk + tq, nb * 8 + gq), bh[0], bl[0]);
                 tf32_split(rhs(kk + tq + 4, nb * 8 + gq), bh[1], bl[1]);
                 mma_tf32_i(acc, al, bh);
@@ -167,8 +166,6 @@ __global__ void __launch_bounds__(IT, 1) k_leaf_inv2(DevCtx c, int r0, int n, ui
             Wi[r * WLD + col + 1] = acc[1];
             Wi[(r + 8) * WLD + col] = acc[2];
             Wi[(r + 8) * WLD + col + 1] = acc[3];
-        } else if (warp == 8 && I + 1 < NT) {
-            diag_inverse(I + 1, Dv + ((I + 1 - cb) & 1) * WBS);
         }
         __syncthreads();
     }
@@ -205,7 +202,7 @@ __global__ void __launch_bounds__(IT, 1) k_leaf_inv2(DevCtx c, int r0, int n, ui
 
 size_t inv2_smem(int n) {
     const int NB = n / 32;
-    return (size_t(NB * (NB + 1) / 2) * 1024 + size_t(NB + 4) * WBS + size_t(NB) * 32) * sizeof(float);
+    return (size_t(NB * (NB + 1) / 2) * 1024 + size_t(NB + 2) * WBS + size_t(NB) * 32) * sizeof(float);
 }
 
 }  // namespace

@@ -30,6 +30,7 @@ void launch_dequant(const DevCtx& c, int lv, int r0, int c0, int m, int n, int s
 
 // spin until *host_flag (mapped pinned memory) becomes non-zero (profiling)
 void launch_gate(volatile int* host_flag, cudaStream_t s);
+void launch_stamp(unsigned long long* out, cudaStream_t s);
 
 // spd_generate symmetrization of raw draws (k_elementwise.cu)
 void launch_symmetrize(double* a, long long lda, int n, cudaStream_t s);

@@ -194,6 +194,28 @@ def test_host_entry_point_in_place(tc, oracle):
     assert np.array_equal(l[iu], a[iu])
 
 
+@pytest.mark.parametrize("dag", [1, 0])
+def test_host_entry_point_pinned_graph(tc, oracle, dag):
+    """pinned host buffer: the copies overlap the factorization graph (H2D /
+    D2H on the copy streams, event nodes in the graph); repeated calls reuse
+    the graph and must see each call's data"""
+    import torch
+    n = 1024
+    plan = tc.Plan(n, 64, "[F16, F16, F32]")
+    plan.set_option("dag_graph", dag)
+    for seed in (7, 8):
+        a = oracle.spd_generate(n, seed)
+        host = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+        host.numpy().T[:] = a
+        st = plan.factor_host(host.numpy().T)
+        assert st.status == "ok"
+        _, l_dev, _, _ = _run(tc, a, 64, "[F16, F16, F32]")
+        l = host.numpy().T
+        assert np.array_equal(np.tril(l), np.tril(l_dev))
+        iu = np.triu_indices(n, 1)
+        assert np.array_equal(l[iu], a[iu])
+
+
 def test_ladder_ordering_n1024(tc, oracle):
     """criteria 2-3 (acceptance.cpp:103-163) on seeds 0-2 against the
     published medians (proj/test_output.txt:19-24, 34)"""
