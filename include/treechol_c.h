@@ -185,7 +185,9 @@ int tc_batch_create(int n, int b, const int* levels, int nlevels, int quantize, 
                     tc_batch** out);
 void tc_batch_destroy(tc_batch* batch);
 /* execution knobs of every plan of the batch (bulk_tiles_per_cta, dag_graph,
- * use_graph; see tc_plan_set_option), before the first run */
+ * use_graph; see tc_plan_set_option), before the first run; and
+ * "solve_order" (any time): 0 (default) every factorization first, then the
+ * solves; 1 each system's POTRS right behind its factorization */
 int tc_batch_set_option(tc_batch* batch, const char* key, int value);
 /* Factors dA[k] in place (device, column-major, lda) for k < count and, if
  * dB && dB[k], solves A X = B for its nrhs right-hand sides (dB[k], ldb,

@@ -70,8 +70,9 @@ def run_batch_on_rank(count: int, n: int, b: int, config, seed0: int = 0, nrhs: 
     batch = tc.Batch(n, b, config, True, concurrency)
     # warm-up (untimed): builds every plan's workspace and CUDA graph
     warm = [synthetic_spd_device(n, seed0 + 10 ** 6 + k) for k in range(concurrency)]
-    batch.run(warm)
-    del warm
+    wb = [a.sum(dim=0, keepdim=True).repeat(nrhs, 1).contiguous() for a in warm]
+    batch.run(warm, wb)  # the solve path too (its workspace, first kernel loads)
+    del warm, wb
     torch.cuda.synchronize()
     failed, worst, dev_ms = 0, 0.0, 0.0
     ks = list(mine)

@@ -31,8 +31,14 @@ struct tc_batch {
     std::vector<cudaStream_t> streams;
     unsigned long long* h_status = nullptr;  // pinned, one word per system
     int cap = 0;
+    // per stream: POTRS workspace (diagonal-block inverses + ticket / flag
+    // words), allocated once -- reused by that stream's solves in order
+    std::vector<double*> work;
+    size_t work_bytes = 0;
+    int solve_order = 0;  // 0: every factorization, then the solves; 1: interleaved per stream
     ~tc_batch() {
         for (auto s : streams) cudaStreamDestroy(s);
+        for (auto w : work) cudaFree(w);
         if (h_status) cudaFreeHost(h_status);
     }
 };
@@ -69,6 +75,10 @@ void tc_batch_destroy(tc_batch* bt) { delete bt; }
 int tc_batch_set_option(tc_batch* bt, const char* key, int value) {
     if (!bt || !key) return bfail(TC_INVALID_ARGUMENT, "null argument");
     const std::string k = key;
+    if (k == "solve_order") {
+        bt->solve_order = value != 0;
+        return TC_OK;
+    }
     for (auto& e : bt->eng) {
         if (e->ready()) return bfail(TC_INVALID_ARGUMENT, k + " must be set before the first run");
         if (k == "bulk_tiles_per_cta") e->bulk_tiles_per_cta = value < 0 ? 0 : value;
@@ -103,29 +113,46 @@ int tc_batch_run(tc_batch* bt, int count, double* const* dA, int lda, double* co
             return bfail(TC_CUDA_ERROR, "cudaMallocHost");
         bt->cap = count;
     }
-    // all factorizations first, then the solves: the substitutions are
-    // block chains that keep their CTAs resident while they wait, so mixing
-    // them into the factorizations would take SMs from the concurrent plans
-    for (int k = 0; k < count; ++k) {
+    const int nb = (n + 63) / 64;
+    const size_t wbytes = sizeof(double) * potrs_work_doubles(n, nrhs) + sizeof(int) * size_t(nb + 1) * size_t(nrhs);
+    if (dB && (bt->work.size() < size_t(C) || bt->work_bytes < wbytes)) {
+        for (size_t i = 0; i < bt->work.size(); ++i) {
+            cudaStreamSynchronize(bt->streams[i]);
+            cudaFree(bt->work[i]);
+        }
+        bt->work.assign(size_t(C), nullptr);
+        for (auto& w : bt->work)
+            if (cudaMalloc(&w, wbytes) != cudaSuccess) return bfail(TC_CUDA_ERROR, "cudaMalloc (POTRS workspace)");
+        bt->work_bytes = wbytes;
+    }
+    auto factor = [&](int k) {
         const int e = k % C;
         Engine& eng = *bt->eng[size_t(e)];
         cudaStream_t s = bt->streams[size_t(e)];
-        if (!eng.enqueue(dA[k], lda, dA[k], lda, s, &err)) return bfail(TC_CUDA_ERROR, err);
-        if (!eng.copy_status(bt->h_status + k, s, &err)) return bfail(TC_CUDA_ERROR, err);
-    }
-    for (int k = 0; dB && k < count; ++k) {
-        if (!dB[k]) continue;
-        cudaStream_t s = bt->streams[size_t(k % C)];
-        // POTRS on the factor just written
-        const int nb = (n + 63) / 64;
-        double* d_work = nullptr;
-        if (cudaMallocAsync(&d_work, sizeof(double) * potrs_work_doubles(n, nrhs) +
-                                         sizeof(int) * size_t(nb + 1) * size_t(nrhs),
-                            s) != cudaSuccess)
-            return bfail(TC_CUDA_ERROR, "cudaMallocAsync");
+        return eng.enqueue(dA[k], lda, dA[k], lda, s, &err) && eng.copy_status(bt->h_status + k, s, &err);
+    };
+    // POTRS on the factor just written, on the same
+    // stream; a bounded set of persistent CTAs per solve
+    auto solve = [&](int k) {
+        if (!dB || !dB[k]) return;
+        const int e = k % C;
+        double* d_work = bt->work[size_t(e)];
         launch_potrs(n, dA[k], lda, dB[k], ldb, nrhs, reinterpret_cast<int*>(d_work + potrs_work_doubles(n, nrhs)),
-                     d_work, s);
-        cudaFreeAsync(d_work, s);
+                     d_work, bt->streams[size_t(e)], 64);
+    };
+    if (bt->solve_order == 0) {
+        // all factorizations first, then the solves (the solves' waiting
+        // CTAs never sit beside a factorization)
+        for (int k = 0; k < count; ++k)
+            if (!factor(k)) return bfail(TC_CUDA_ERROR, err);
+        for (int k = 0; k < count; ++k) solve(k);
+    } else {
+        // each system's solve right behind its factorization: the solves of
+        // one stream overlap the other streams' factorizations
+        for (int k = 0; k < count; ++k) {
+            if (!factor(k)) return bfail(TC_CUDA_ERROR, err);
+            solve(k);
+        }
     }
     for (auto s : bt->streams)
         if (cudaStreamSynchronize(s) != cudaSuccess) return bfail(TC_CUDA_ERROR, "batch synchronize");

@@ -165,9 +165,11 @@ __global__ void __launch_bounds__(256) k_potrs_fwd(int n, const double* __restri
     __shared__ int sI;
     __shared__ double part[4][VT];
     __shared__ double rhs[VT];
+    for (;;) {  // persistent: claim tickets until every block row is done
     if (threadIdx.x == 0) sI = atomicAdd(cnt, 1);
     __syncthreads();
     const int I = sI;
+    if (I >= nb) break;
     const int i0 = I * VT;
     const int rows = min(VT, n - i0);
     const int r = threadIdx.x & 63, q = threadIdx.x >> 6;
@@ -205,6 +207,7 @@ __global__ void __launch_bounds__(256) k_potrs_fwd(int n, const double* __restri
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) st_release(cnt + 1 + I, 1);
+    }
 }
 
 // backward: x = L^-T y, in place, blocks in reverse order; x_I = W_I^T (y_I - sum)
@@ -216,9 +219,11 @@ __global__ void __launch_bounds__(256) k_potrs_bwd(int n, const double* __restri
     __shared__ int sI;
     __shared__ double part[4][VT];
     __shared__ double rhs[VT];
+    for (;;) {
     if (threadIdx.x == 0) sI = nb - 1 - atomicAdd(cnt, 1);
     __syncthreads();
     const int I = sI;
+    if (I < 0) break;
     const int i0 = I * VT;
     const int rows = min(VT, n - i0);
     const int r = threadIdx.x & 63, q = threadIdx.x >> 6;
@@ -255,6 +260,7 @@ __global__ void __launch_bounds__(256) k_potrs_bwd(int n, const double* __restri
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) st_release(cnt + 1 + I, 1);
+    }
 }
 
 // ---------------------------------------------------------------- residual
@@ -333,14 +339,18 @@ void launch_fact_error(int n, const double* dA, long long lda, const double* dL,
 size_t potrs_work_doubles(int n, int nrhs) { return size_t((n + VT - 1) / VT) * VT * VT; }
 
 void launch_potrs(int n, const double* dL, long long ldl, double* dB, long long ldb, int nrhs, int* d_counters,
-                  double* d_work, cudaStream_t s) {
+                  double* d_work, cudaStream_t s, int max_ctas) {
     const int nb = (n + VT - 1) / VT;
     const size_t cbytes = sizeof(int) * size_t(nb + 1) * size_t(nrhs);
     k_potrs_diaginv<<<nb, VT, 0, s>>>(n, dL, ldl, d_work);
     cudaMemsetAsync(d_counters, 0, cbytes, s);
-    k_potrs_fwd<<<dim3(nb, nrhs), 256, 0, s>>>(n, dL, ldl, dB, ldb, d_counters, d_work);
+    // persistent CTAs claiming block rows by ticket; a batch bounds their
+    // number (max_ctas) so concurrent solves all stay resident instead of
+    // filling the SMs with waiting CTAs
+    const int g = max_ctas > 0 && max_ctas < nb ? max_ctas : nb;
+    k_potrs_fwd<<<dim3(g, nrhs), 256, 0, s>>>(n, dL, ldl, dB, ldb, d_counters, d_work);
     cudaMemsetAsync(d_counters, 0, cbytes, s);
-    k_potrs_bwd<<<dim3(nb, nrhs), 256, 0, s>>>(n, dL, ldl, dB, ldb, d_counters, d_work);
+    k_potrs_bwd<<<dim3(g, nrhs), 256, 0, s>>>(n, dL, ldl, dB, ldb, d_counters, d_work);
 }
 
 int residual_partials(int n) { return (n + VT - 1) / VT; }

@@ -94,7 +94,7 @@ void launch_fact_error(int n, const double* dA, long long lda, const double* dL,
                        double* d_partials, int* d_nonfinite, int tiles_per_side, cudaStream_t s);
 int fact_error_partials(int n, int* tiles_per_side);
 void launch_potrs(int n, const double* dL, long long ldl, double* dB, long long ldb, int nrhs,
-                  int* d_counters, double* d_work, cudaStream_t s);
+                  int* d_counters, double* d_work, cudaStream_t s, int max_ctas = 0);
 size_t potrs_work_doubles(int n, int nrhs);
 void launch_residual(int n, const double* dA, long long lda, const double* dX, const double* dB,
                      double* d_partials, cudaStream_t s);
