@@ -33,13 +33,20 @@ struct tc_batch {
     int cap = 0;
     // per stream: POTRS workspace (diagonal-block inverses + ticket / flag
     // words), allocated once -- reused by that stream's solves in order
-    std::vector<double*> work;
+    std::vector<void*> work;
     size_t work_bytes = 0;
-    int solve_order = 0;  // 0: every factorization, then the solves; 1: interleaved per stream
+    int solve_order = 0;  // 0: every factorization, then all solves in one launch; 1: interleaved per stream
+    void** h_tab = nullptr;  // POTRS pointer tables (L then B), pinned / device
+    void** d_tab = nullptr;
+    int tab_cap = 0;
+    cudaEvent_t join = nullptr;
     ~tc_batch() {
         for (auto s : streams) cudaStreamDestroy(s);
         for (auto w : work) cudaFree(w);
         if (h_status) cudaFreeHost(h_status);
+        if (h_tab) cudaFreeHost(h_tab);
+        if (d_tab) cudaFree(d_tab);
+        if (join) cudaEventDestroy(join);
     }
 };
 
@@ -113,17 +120,27 @@ int tc_batch_run(tc_batch* bt, int count, double* const* dA, int lda, double* co
             return bfail(TC_CUDA_ERROR, "cudaMallocHost");
         bt->cap = count;
     }
-    const int nb = (n + 63) / 64;
-    const size_t wbytes = sizeof(double) * potrs_work_doubles(n, nrhs) + sizeof(int) * size_t(nb + 1) * size_t(nrhs);
-    if (dB && (bt->work.size() < size_t(C) || bt->work_bytes < wbytes)) {
-        for (size_t i = 0; i < bt->work.size(); ++i) {
-            cudaStreamSynchronize(bt->streams[i]);
-            cudaFree(bt->work[i]);
-        }
-        bt->work.assign(size_t(C), nullptr);
+    // solve_order 1: a POTRS workspace per stream; 0: one for the batch
+    const size_t wbytes = bt->solve_order ? potrs_batch_work_bytes(n, 1, nrhs) : potrs_batch_work_bytes(n, count, nrhs);
+    const size_t nwork = bt->solve_order ? size_t(C) : 1;
+    if (dB && (bt->work.size() < nwork || bt->work_bytes < wbytes)) {
+        for (auto s : bt->streams) cudaStreamSynchronize(s);
+        for (auto w : bt->work) cudaFree(w);
+        bt->work.assign(nwork, nullptr);
         for (auto& w : bt->work)
             if (cudaMalloc(&w, wbytes) != cudaSuccess) return bfail(TC_CUDA_ERROR, "cudaMalloc (POTRS workspace)");
         bt->work_bytes = wbytes;
+    }
+    if (dB && bt->tab_cap < count) {
+        for (auto s : bt->streams) cudaStreamSynchronize(s);
+        if (bt->h_tab) cudaFreeHost(bt->h_tab);
+        if (bt->d_tab) cudaFree(bt->d_tab);
+        bt->h_tab = nullptr;
+        bt->d_tab = nullptr;
+        if (cudaMallocHost(&bt->h_tab, 2 * sizeof(void*) * size_t(count)) != cudaSuccess ||
+            cudaMalloc(&bt->d_tab, 2 * sizeof(void*) * size_t(count)) != cudaSuccess)
+            return bfail(TC_CUDA_ERROR, "POTRS pointer tables");
+        bt->tab_cap = count;
     }
     auto factor = [&](int k) {
         const int e = k % C;
@@ -136,16 +153,35 @@ int tc_batch_run(tc_batch* bt, int count, double* const* dA, int lda, double* co
     auto solve = [&](int k) {
         if (!dB || !dB[k]) return;
         const int e = k % C;
-        double* d_work = bt->work[size_t(e)];
-        launch_potrs(n, dA[k], lda, dB[k], ldb, nrhs, reinterpret_cast<int*>(d_work + potrs_work_doubles(n, nrhs)),
-                     d_work, bt->streams[size_t(e)], 64);
+        double* d_work = static_cast<double*>(bt->work[size_t(e)]);
+        launch_potrs(n, dA[k], lda, dB[k], ldb, nrhs, nullptr, d_work, bt->streams[size_t(e)], 64);
     };
     if (bt->solve_order == 0) {
-        // all factorizations first, then the solves (the solves' waiting
-        // CTAs never sit beside a factorization)
+        // all factorizations first, then every solve in one launch sequence
+        // (persistent CTAs over all (block, system) pairs; the waiting CTAs
+        // never sit beside a factorization)
         for (int k = 0; k < count; ++k)
             if (!factor(k)) return bfail(TC_CUDA_ERROR, err);
-        for (int k = 0; k < count; ++k) solve(k);
+        int ns = 0;
+        for (int k = 0; dB && k < count; ++k)
+            if (dB[k]) {
+                bt->h_tab[ns] = dA[k];
+                bt->h_tab[count + ns] = dB[k];
+                ++ns;
+            }
+        if (ns > 0) {
+            cudaStream_t s0 = bt->streams[0];
+            if (!bt->join) cudaEventCreateWithFlags(&bt->join, cudaEventDisableTiming);
+            for (int e = 1; e < C; ++e) {
+                cudaEventRecord(bt->join, bt->streams[size_t(e)]);
+                cudaStreamWaitEvent(s0, bt->join, 0);
+            }
+            // compact the B half right behind the L half
+            for (int i = 0; i < ns; ++i) bt->h_tab[ns + i] = bt->h_tab[count + i];
+            cudaMemcpyAsync(bt->d_tab, bt->h_tab, 2 * sizeof(void*) * size_t(ns), cudaMemcpyHostToDevice, s0);
+            launch_potrs_batch(n, ns, reinterpret_cast<const double* const*>(bt->d_tab), lda,
+                               reinterpret_cast<double* const*>(bt->d_tab + ns), ldb, nrhs, bt->work[0], 148 * 6, s0);
+        }
     } else {
         // each system's solve right behind its factorization: the solves of
         // one stream overlap the other streams' factorizations

@@ -130,17 +130,36 @@ __device__ __forceinline__ void st_release(int* p, int v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// diagonal-block inverses W_I = inv(L(I,I)) (64 x 64, row-major at W + I*64*64),
-// one CTA per block, one thread per column (independent forward
+// The solves of a set of problems (system s, right-hand side r) -- one, or
+// a whole batch in one launch.  System s: factor Ls[s] (ld ldl), right-hand
+// sides Bs[s] + r*ldb; tables null: the single system L0 / B0.
+struct PotrsArgs {
+    int n, nsys, nrhs;
+    const double* const* Ls;
+    double* const* Bs;
+    const double* L0;
+    double* B0;
+    long long ldl, ldb;
+    int* ticket;  // one word per direction: the next (block, problem) pair
+    int* flags;   // [problem][nb]: block done
+    double* W;    // [system][nb][VT][VT] diagonal-block inverses
+};
+__device__ __forceinline__ const double* potrs_L(const PotrsArgs& a, int s) { return a.Ls ? a.Ls[s] : a.L0; }
+__device__ __forceinline__ double* potrs_B(const PotrsArgs& a, int s) { return a.Bs ? a.Bs[s] : a.B0; }
+
+// diagonal-block inverses W_I = inv(L(I,I)) (64 x 64, row-major), one CTA
+// per (block, system), one thread per column (independent forward
 // substitutions): they take the 64-step dependent solve off the block chain
 // of the substitutions below
-__global__ void __launch_bounds__(VT) k_potrs_diaginv(int n, const double* __restrict__ Lm, long long ldl,
-                                                     double* __restrict__ W) {
+__global__ void __launch_bounds__(VT) k_potrs_diaginv(PotrsArgs a) {
     __shared__ double Ls[VT][VT + 1];
-    const int I = blockIdx.x, i0 = I * VT, rows = min(VT, n - i0), t = threadIdx.x;
+    const int n = a.n, nb = (n + VT - 1) / VT;
+    const int I = blockIdx.x, sys = blockIdx.y, i0 = I * VT, rows = min(VT, n - i0), t = threadIdx.x;
+    const double* Lm = potrs_L(a, sys);
+    const long long ldl = a.ldl;
     for (int c = 0; c < VT; ++c) Ls[t][c] = (t < rows && c < rows && t >= c) ? Lm[(long long)(i0 + c) * ldl + i0 + t] : 0.0;
     __syncthreads();
-    double* Wi = W + size_t(I) * VT * VT;
+    double* Wi = a.W + (size_t(sys) * nb + I) * VT * VT;
     double w[VT];
 #pragma unroll
     for (int i = 0; i < VT; ++i) {
@@ -153,113 +172,67 @@ __global__ void __launch_bounds__(VT) k_potrs_diaginv(int n, const double* __res
     for (int i = 0; i < VT; ++i) Wi[i * VT + t] = w[i];
 }
 
-// forward: y = L^-1 b, in place on b.  counters: [0] ticket, [1..nb] flags.
-// Block I (64 rows) claims a ticket, accumulates L(I,J) y_J for every
-// finished J < I as their flags appear (coalesced column reads of L), then
-// y_I = W_I (b_I - sum) -- a 64x64 product, no dependent chain.
-__global__ void __launch_bounds__(256) k_potrs_fwd(int n, const double* __restrict__ Lm, long long ldl, double* B,
-                                                   long long ldb, int* counters, const double* __restrict__ W) {
-    const int nb = (n + VT - 1) / VT;
-    int* cnt = counters + blockIdx.y * (nb + 1);
-    double* y = B + blockIdx.y * ldb;
-    __shared__ int sI;
+// forward y = L^-1 b / backward x = L^-T y, in place.  Persistent CTAs claim
+// tickets t -> (block index t / P, problem t % P): every problem's blocks are
+// claimed in chain order, so a CTA only ever waits on blocks already claimed
+// by running CTAs.  Block I accumulates L(I,J) y_J (forward) or L(J,I) x_J
+// (backward) over the finished J as their flags appear -- the L reads are
+// issued before each wait, off the chain -- then y_I = W_I (b_I - sum) /
+// x_I = W_I^T (y_I - sum): a 64x64 product, no dependent chain.
+template <bool BWD>
+__global__ void __launch_bounds__(256) k_potrs_sweep(PotrsArgs a) {
+    const int n = a.n, nb = (n + VT - 1) / VT, P = a.nsys * a.nrhs;
+    __shared__ int sT;
     __shared__ double part[4][VT];
     __shared__ double rhs[VT];
-    for (;;) {  // persistent: claim tickets until every block row is done
-    if (threadIdx.x == 0) sI = atomicAdd(cnt, 1);
-    __syncthreads();
-    const int I = sI;
-    if (I >= nb) break;
-    const int i0 = I * VT;
-    const int rows = min(VT, n - i0);
     const int r = threadIdx.x & 63, q = threadIdx.x >> 6;
-    const int gi = i0 + r;
-    // this block's W row segment does not depend on the chain: load it first
-    const double* Wi = W + size_t(I) * VT * VT;
-    double wv[16];
-#pragma unroll
-    for (int kk = 0; kk < 16; ++kk) wv[kk] = Wi[r * VT + q * 16 + kk];
-    double acc = 0.0;
-    for (int J = 0; J < I; ++J) {
-        // L(I, J) is read before waiting for y_J (off the chain)
-        const int k0 = J * VT + q * 16;
-        double lv[16];
-#pragma unroll
-        for (int kk = 0; kk < 16; ++kk) lv[kk] = gi < n ? Lm[(long long)(k0 + kk) * ldl + gi] : 0.0;
-        if (threadIdx.x == 0)
-            while (ld_acquire(cnt + 1 + J) == 0) {
-            }
-        __syncthreads();
-#pragma unroll
-        for (int kk = 0; kk < 16; ++kk) acc = fma(lv[kk], __ldcg(y + k0 + kk), acc);
-    }
-    part[q][r] = acc;
-    __syncthreads();
-    if (threadIdx.x < VT) rhs[r] = r < rows ? y[gi] - (part[0][r] + part[1][r] + part[2][r] + part[3][r]) : 0.0;
-    __syncthreads();
-    // y_I = W_I rhs: 4 partial dot products per row
-    double s = 0.0;
-#pragma unroll
-    for (int kk = 0; kk < 16; ++kk) s = fma(wv[kk], rhs[q * 16 + kk], s);
-    part[q][r] = s;
-    __syncthreads();
-    if (threadIdx.x < VT && r < rows) y[gi] = part[0][r] + part[1][r] + part[2][r] + part[3][r];
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) st_release(cnt + 1 + I, 1);
-    }
-}
-
-// backward: x = L^-T y, in place, blocks in reverse order; x_I = W_I^T (y_I - sum)
-__global__ void __launch_bounds__(256) k_potrs_bwd(int n, const double* __restrict__ Lm, long long ldl, double* B,
-                                                   long long ldb, int* counters, const double* __restrict__ W) {
-    const int nb = (n + VT - 1) / VT;
-    int* cnt = counters + blockIdx.y * (nb + 1);
-    double* y = B + blockIdx.y * ldb;
-    __shared__ int sI;
-    __shared__ double part[4][VT];
-    __shared__ double rhs[VT];
+    const long long ldl = a.ldl;
     for (;;) {
-    if (threadIdx.x == 0) sI = nb - 1 - atomicAdd(cnt, 1);
-    __syncthreads();
-    const int I = sI;
-    if (I < 0) break;
-    const int i0 = I * VT;
-    const int rows = min(VT, n - i0);
-    const int r = threadIdx.x & 63, q = threadIdx.x >> 6;
-    const int gi = i0 + r;  // x_gi needs sum_{k > block} L(k, gi) x_k
-    const double* Wi = W + size_t(I) * VT * VT;
-    double wv[16];
-#pragma unroll
-    for (int kk = 0; kk < 16; ++kk) wv[kk] = Wi[(q * 16 + kk) * VT + r];
-    double acc = 0.0;
-    for (int J = nb - 1; J > I; --J) {
-        const int k0 = J * VT + q * 16;
-        double lv[16];
-#pragma unroll
-        for (int kk = 0; kk < 16; ++kk) lv[kk] = (gi < n && k0 + kk < n) ? Lm[(long long)gi * ldl + k0 + kk] : 0.0;
-        if (threadIdx.x == 0)
-            while (ld_acquire(cnt + 1 + J) == 0) {
-            }
+        if (threadIdx.x == 0) sT = atomicAdd(a.ticket, 1);
         __syncthreads();
+        const int t = sT;
+        if (t >= nb * P) break;
+        const int p = t % P, sys = p / a.nrhs, rr = p % a.nrhs;
+        const int I = BWD ? nb - 1 - t / P : t / P;
+        const double* Lm = potrs_L(a, sys);
+        double* y = potrs_B(a, sys) + rr * a.ldb;
+        int* fl = a.flags + size_t(p) * nb;
+        const int i0 = I * VT, rows = min(VT, n - i0), gi = i0 + r;
+        // this block's W segment does not depend on the chain: load it first
+        const double* Wi = a.W + (size_t(sys) * nb + I) * VT * VT;
+        double wv[16];
 #pragma unroll
-        for (int kk = 0; kk < 16; ++kk)
-            if (k0 + kk < n) acc = fma(lv[kk], __ldcg(y + k0 + kk), acc);
-    }
-    part[q][r] = acc;
-    __syncthreads();
-    if (threadIdx.x < VT) rhs[r] = r < rows ? y[gi] - (part[0][r] + part[1][r] + part[2][r] + part[3][r]) : 0.0;
-    __syncthreads();
-    // x_I = W_I^T rhs
-    double s = 0.0;
+        for (int kk = 0; kk < 16; ++kk) wv[kk] = BWD ? Wi[(q * 16 + kk) * VT + r] : Wi[r * VT + q * 16 + kk];
+        double acc = 0.0;
+        for (int step = 0; step < (BWD ? nb - 1 - I : I); ++step) {
+            const int J = BWD ? nb - 1 - step : step;
+            const int k0 = J * VT + q * 16;
+            double lv[16];
 #pragma unroll
-    for (int kk = 0; kk < 16; ++kk) s = fma(wv[kk], rhs[q * 16 + kk], s);
-    part[q][r] = s;
-    __syncthreads();
-    if (threadIdx.x < VT && r < rows) y[gi] = part[0][r] + part[1][r] + part[2][r] + part[3][r];
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) st_release(cnt + 1 + I, 1);
+            for (int kk = 0; kk < 16; ++kk)
+                lv[kk] = BWD ? ((gi < n && k0 + kk < n) ? Lm[(long long)gi * ldl + k0 + kk] : 0.0)
+                             : (gi < n ? Lm[(long long)(k0 + kk) * ldl + gi] : 0.0);
+            if (threadIdx.x == 0)
+                while (ld_acquire(fl + J) == 0) {
+                }
+            __syncthreads();
+#pragma unroll
+            for (int kk = 0; kk < 16; ++kk)
+                if (!BWD || k0 + kk < n) acc = fma(lv[kk], __ldcg(y + k0 + kk), acc);
+        }
+        part[q][r] = acc;
+        __syncthreads();
+        if (threadIdx.x < VT) rhs[r] = r < rows ? y[gi] - (part[0][r] + part[1][r] + part[2][r] + part[3][r]) : 0.0;
+        __syncthreads();
+        double s = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) s = fma(wv[kk], rhs[q * 16 + kk], s);
+        part[q][r] = s;
+        __syncthreads();
+        if (threadIdx.x < VT && r < rows) y[gi] = part[0][r] + part[1][r] + part[2][r] + part[3][r];
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) st_release(fl + I, 1);
     }
 }
 
@@ -336,21 +309,55 @@ void launch_fact_error(int n, const double* dA, long long lda, const double* dL,
     k_fact_error_final<<<1, 256, 0, s>>>(d_partials, tiles, d_nonfinite, d_partials + 2 * size_t(tiles));
 }
 
-size_t potrs_work_doubles(int n, int nrhs) { return size_t((n + VT - 1) / VT) * VT * VT; }
+size_t potrs_work_doubles(int n, int nrhs) { return potrs_batch_work_bytes(n, 1, nrhs) / sizeof(double) + 1; }
 
-void launch_potrs(int n, const double* dL, long long ldl, double* dB, long long ldb, int nrhs, int* d_counters,
+// workspace of nsys systems: W, then the flags and the two tickets
+size_t potrs_batch_work_bytes(int n, int nsys, int nrhs) {
+    const size_t nb = size_t((n + VT - 1) / VT);
+    return sizeof(double) * size_t(nsys) * nb * VT * VT + sizeof(int) * (size_t(nsys) * nrhs * nb + 2);
+}
+
+static void potrs_run(PotrsArgs a, void* work, int max_ctas, cudaStream_t s) {
+    const int nb = (a.n + VT - 1) / VT;
+    a.W = static_cast<double*>(work);
+    int* words = reinterpret_cast<int*>(a.W + size_t(a.nsys) * nb * VT * VT);
+    const size_t fbytes = sizeof(int) * (size_t(a.nsys) * a.nrhs * nb + 2);
+    a.flags = words + 2;
+    k_potrs_diaginv<<<dim3(nb, a.nsys), VT, 0, s>>>(a);
+    const long long work_items = (long long)nb * a.nsys * a.nrhs;
+    const int g = int(max_ctas > 0 && max_ctas < work_items ? max_ctas : work_items);
+    cudaMemsetAsync(words, 0, fbytes, s);
+    a.ticket = words;
+    k_potrs_sweep<false><<<g, 256, 0, s>>>(a);
+    cudaMemsetAsync(a.flags, 0, fbytes - 2 * sizeof(int), s);
+    a.ticket = words + 1;
+    k_potrs_sweep<true><<<g, 256, 0, s>>>(a);
+}
+
+void launch_potrs(int n, const double* dL, long long ldl, double* dB, long long ldb, int nrhs, int* /*d_counters*/,
                   double* d_work, cudaStream_t s, int max_ctas) {
-    const int nb = (n + VT - 1) / VT;
-    const size_t cbytes = sizeof(int) * size_t(nb + 1) * size_t(nrhs);
-    k_potrs_diaginv<<<nb, VT, 0, s>>>(n, dL, ldl, d_work);
-    cudaMemsetAsync(d_counters, 0, cbytes, s);
-    // persistent CTAs claiming block rows by ticket; a batch bounds their
-    // number (max_ctas) so concurrent solves all stay resident instead of
-    // filling the SMs with waiting CTAs
-    const int g = max_ctas > 0 && max_ctas < nb ? max_ctas : nb;
-    k_potrs_fwd<<<dim3(g, nrhs), 256, 0, s>>>(n, dL, ldl, dB, ldb, d_counters, d_work);
-    cudaMemsetAsync(d_counters, 0, cbytes, s);
-    k_potrs_bwd<<<dim3(g, nrhs), 256, 0, s>>>(n, dL, ldl, dB, ldb, d_counters, d_work);
+    PotrsArgs a{};
+    a.n = n;
+    a.nsys = 1;
+    a.nrhs = nrhs;
+    a.L0 = dL;
+    a.B0 = dB;
+    a.ldl = ldl;
+    a.ldb = ldb;
+    potrs_run(a, d_work, max_ctas, s);
+}
+
+void launch_potrs_batch(int n, int nsys, const double* const* d_Ltab, long long ldl, double* const* d_Btab,
+                        long long ldb, int nrhs, void* d_work, int max_ctas, cudaStream_t s) {
+    PotrsArgs a{};
+    a.n = n;
+    a.nsys = nsys;
+    a.nrhs = nrhs;
+    a.Ls = d_Ltab;
+    a.Bs = d_Btab;
+    a.ldl = ldl;
+    a.ldb = ldb;
+    potrs_run(a, d_work, max_ctas, s);
 }
 
 int residual_partials(int n) { return (n + VT - 1) / VT; }

@@ -95,7 +95,11 @@ void launch_fact_error(int n, const double* dA, long long lda, const double* dL,
 int fact_error_partials(int n, int* tiles_per_side);
 void launch_potrs(int n, const double* dL, long long ldl, double* dB, long long ldb, int nrhs,
                   int* d_counters, double* d_work, cudaStream_t s, int max_ctas = 0);
-size_t potrs_work_doubles(int n, int nrhs);
+size_t potrs_work_doubles(int n, int nrhs);  // incl. the flag / ticket words
+size_t potrs_batch_work_bytes(int n, int nsys, int nrhs);
+// the POTRS of nsys systems in one launch sequence (device pointer tables)
+void launch_potrs_batch(int n, int nsys, const double* const* d_Ltab, long long ldl, double* const* d_Btab,
+                        long long ldb, int nrhs, void* d_work, int max_ctas, cudaStream_t s);
 void launch_residual(int n, const double* dA, long long lda, const double* dX, const double* dB,
                      double* d_partials, cudaStream_t s);
 int residual_partials(int n);
