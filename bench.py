@@ -300,7 +300,7 @@ def run_ours(args):
         if ws > 1:
             dist.barrier()
         local, tot, fl = run_batch_on_rank(args.c4_count, args.c4_n, b, CFG, seed0=1000, concurrency=args.c4_conc,
-                                           world=ws, rank=rank)
+                                           world=ws, rank=rank, in_flight=2 * args.c4_conc)
         c4 = {"workload": f"C4: {args.c4_count} x N={args.c4_n} b={b} {CFG} POTRF+POTRS (1 RHS), sharded over "
                           f"{ws} rank(s), {args.c4_conc} plans per GPU",
               "value": tot.systems * fl / (tot.device_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
@@ -408,7 +408,7 @@ def main():
     ap.add_argument("--ref-n", dest="ref_n", type=int, default=1536)
     ap.add_argument("--c4-count", dest="c4_count", type=int, default=64)
     ap.add_argument("--c4-n", dest="c4_n", type=int, default=16384)
-    ap.add_argument("--c4-conc", dest="c4_conc", type=int, default=8)
+    ap.add_argument("--c4-conc", dest="c4_conc", type=int, default=16)
     ap.add_argument("--c5-n", dest="c5_n", type=int, default=65536,
                     help="N of the distributed single factorization run when --gpus > 1 (0: off)")
     ap.add_argument("--variants", action="store_true",
