@@ -18,81 +18,93 @@ namespace {
 
 constexpr int TS = 32;  // tile side
 
-// grid-stride over 32x32 tiles (a few thousand CTAs, not one per tile)
+// grid-stride over 64x64 tiles (a few thousand CTAs, not one per tile);
+// every thread issues all 16 of its loads before touching shared memory
+constexpr int TB = 64;  // block-table tile side (import / export / shadow)
+constexpr int TBR = (TB * TB) / 256;  // elements per thread per tile
+
 __global__ void __launch_bounds__(256) k_import(DevCtx c, const BlockDesc* blocks, int nb, int tiles) {
-    __shared__ double tile[TS][TS + 1];
+    __shared__ double tile[TB][TB + 1];
+    const int tx = threadIdx.x & (TB - 1), ty = threadIdx.x / TB;  // ty in [0, 4)
     for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-    const BlockDesc bd = blocks[find_block(blocks, nb, t)];
-    const int lt = t - bd.tile0;
-    const int i0 = (lt / bd.tiles_n) * TS, j0 = (lt % bd.tiles_n) * TS;
-    const double* a = c.ra->a_in;
-    const long long lda = c.ra->lda_in;
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+        const BlockDesc bd = blocks[find_block(blocks, nb, t)];
+        const int lt = t - bd.tile0;
+        const int i0 = (lt / bd.tiles_n) * TB, j0 = (lt % bd.tiles_n) * TB;
+        const double* a = c.ra->a_in;
+        const long long lda = c.ra->lda_in;
+        double v[TBR];
 #pragma unroll
-    for (int r = 0; r < TS; r += 8) {
-        const int i = i0 + tx, j = j0 + ty + r;
-        double v = 0.0;
-        if (i < bd.m && j < bd.n) v = a[(long long)(bd.c0 + j) * lda + bd.r0 + i];
-        tile[ty + r][tx] = v;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < TS; r += 8) {
-        const int i = i0 + ty + r, j = j0 + tx;
-        if (i < bd.m && j < bd.n) {
-            double v = tile[tx][ty + r];
-            if (bd.lower && j > i) v = 0.0;  // strict upper of a leaf square: unused
-            store_level(c, bd.level, (long long)(bd.r0 + i) * c.ldw + bd.c0 + j, v);
+        for (int r = 0; r < TBR; ++r) {  // column-major source: lanes along i
+            const int i = i0 + tx, j = j0 + ty + 4 * r;
+            v[r] = (i < bd.m && j < bd.n) ? a[(long long)(bd.c0 + j) * lda + bd.r0 + i] : 0.0;
         }
-    }
-    __syncthreads();
+#pragma unroll
+        for (int r = 0; r < TBR; ++r) tile[ty + 4 * r][tx] = v[r];
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < TBR; ++r) {  // row-major level buffer: lanes along j
+            const int i = i0 + ty + 4 * r, j = j0 + tx;
+            if (i < bd.m && j < bd.n) {
+                double x = tile[tx][ty + 4 * r];
+                if (bd.lower && j > i) x = 0.0;  // strict upper of a leaf square: unused
+                store_level(c, bd.level, (long long)(bd.r0 + i) * c.ldw + bd.c0 + j, x);
+            }
+        }
+        __syncthreads();
     }
 }
 
 __global__ void __launch_bounds__(256) k_export(DevCtx c, const BlockDesc* blocks, int nb, int tiles) {
+    // 32x32 sub-tiles of the 64x64 table tiles, each its own grid-stride
+    // work item (measured faster than the 64-wide transpose for this
+    // direction: F16 row reads, F64 column writes)
     __shared__ double tile[TS][TS + 1];
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-    const BlockDesc bd = blocks[find_block(blocks, nb, t)];
-    const int lt = t - bd.tile0;
-    const int i0 = (lt / bd.tiles_n) * TS, j0 = (lt % bd.tiles_n) * TS;
-    double* l = c.ra->l_out;
-    const long long ldl = c.ra->lda_out;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    for (int t4 = blockIdx.x; t4 < 4 * tiles; t4 += gridDim.x) {
+        const int t = t4 >> 2, q = t4 & 3;
+        const BlockDesc bd = blocks[find_block(blocks, nb, t)];
+        const int lt = t - bd.tile0;
+        double* l = c.ra->l_out;
+        const long long ldl = c.ra->lda_out;
+        const int i0 = (lt / bd.tiles_n) * TB + (q >> 1) * TS, j0 = (lt % bd.tiles_n) * TB + (q & 1) * TS;
+        if (i0 >= bd.m || j0 >= bd.n) continue;  // uniform per CTA
 #pragma unroll
-    for (int r = 0; r < TS; r += 8) {
-        const int i = i0 + ty + r, j = j0 + tx;
-        double v = 0.0;
-        if (i < bd.m && j < bd.n) v = load_level(c, bd.level, (long long)(bd.r0 + i) * c.ldw + bd.c0 + j);
-        tile[ty + r][tx] = v;
-    }
-    __syncthreads();
+        for (int r = 0; r < TS; r += 8) {
+            const int i = i0 + ty + r, j = j0 + tx;
+            double v = 0.0;
+            if (i < bd.m && j < bd.n) v = load_level(c, bd.level, (long long)(bd.r0 + i) * c.ldw + bd.c0 + j);
+            tile[ty + r][tx] = v;
+        }
+        __syncthreads();
 #pragma unroll
-    for (int r = 0; r < TS; r += 8) {
-        const int i = i0 + tx, j = j0 + ty + r;
-        if (i < bd.m && j < bd.n && !(bd.lower && j > i))
-            l[(long long)(bd.c0 + j) * ldl + bd.r0 + i] = tile[tx][ty + r];
-    }
-    __syncthreads();
+        for (int r = 0; r < TS; r += 8) {
+            const int i = i0 + tx, j = j0 + ty + r;
+            if (i < bd.m && j < bd.n && !(bd.lower && j > i))
+                l[(long long)(bd.c0 + j) * ldl + bd.r0 + i] = tile[tx][ty + r];
+        }
+        __syncthreads();
     }
 }
 
 // shadow: blocks carry their source level; target is `p`
 __global__ void __launch_bounds__(256) k_shadow(DevCtx c, const BlockDesc* blocks, int nb, int p, int tiles) {
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-    const BlockDesc bd = blocks[find_block(blocks, nb, t)];
-    const int lt = t - bd.tile0;
-    const int i0 = (lt / bd.tiles_n) * TS, j0 = (lt % bd.tiles_n) * TS;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const BlockDesc bd = blocks[find_block(blocks, nb, t)];
+        const int lt = t - bd.tile0;
+        const int i0 = (lt / bd.tiles_n) * TB, j0 = (lt % bd.tiles_n) * TB;
+        for (int r = 0; r < TB; r += 8) {
 #pragma unroll
-    for (int r = 0; r < TS; r += 8) {
-        const int i = i0 + ty + r, j = j0 + tx;
-        if (i < bd.m && j < bd.n) {
-            const long long off = (long long)(bd.r0 + i) * c.ldw + bd.c0 + j;
-            double v = load_level(c, bd.level, off);
-            if (bd.lower && j > i) v = 0.0;
-            store_level(c, p, off, v);
+            for (int h = 0; h < TB; h += 32) {
+                const int i = i0 + ty + r, j = j0 + h + tx;
+                if (i < bd.m && j < bd.n) {
+                    const long long off = (long long)(bd.r0 + i) * c.ldw + bd.c0 + j;
+                    double v = load_level(c, bd.level, off);
+                    if (bd.lower && j > i) v = 0.0;
+                    store_level(c, p, off, v);
+                }
+            }
         }
-    }
     }
 }
 
@@ -296,9 +308,9 @@ int make_block_table(const std::vector<BlockDescHost>& in, std::vector<BlockDesc
         d.level = h.level;
         d.lower = h.lower;
         d.tile0 = tiles;
-        d.tiles_n = (h.n + TS - 1) / TS;
+        d.tiles_n = (h.n + TB - 1) / TB;
         out.push_back(d);
-        tiles += tiles_of(h.m, h.n);
+        tiles += ((h.m + TB - 1) / TB) * d.tiles_n;
     }
     return tiles;
 }
@@ -308,7 +320,7 @@ void launch_import(const DevCtx& c, const BlockDesc* d_blocks, int nb, int tiles
     if (tiles > 0) k_import<<<tile_grid(tiles), 256, 0, s>>>(c, d_blocks, nb, tiles);
 }
 void launch_export(const DevCtx& c, const BlockDesc* d_blocks, int nb, int tiles, cudaStream_t s) {
-    if (tiles > 0) k_export<<<tile_grid(tiles), 256, 0, s>>>(c, d_blocks, nb, tiles);
+    if (tiles > 0) k_export<<<tile_grid(4 * tiles), 256, 0, s>>>(c, d_blocks, nb, tiles);
 }
 void launch_shadow(const DevCtx& c, const BlockDesc* d_blocks, int nb, int tiles, int p, cudaStream_t s) {
     if (tiles > 0) k_shadow<<<tile_grid(tiles), 256, 0, s>>>(c, d_blocks, nb, p, tiles);
