@@ -138,37 +138,40 @@ __global__ void __launch_bounds__(256) k_check(DevCtx c, int lv, int r0, int c0,
 // alpha slot, and a speculative alpha == 1 conversion into buffer lv
 __global__ void __launch_bounds__(256) k_quant1(DevCtx c, int lv, int r0, int c0, int m, int n, int slot,
                                                 uint32_t seq) {
-    __shared__ double tile[TS][TS + 1];
+    // 64x64 transposing tiles, all 16 loads of a thread in flight (k_import)
+    __shared__ double tile[TB][TB + 1];
     __shared__ unsigned long long smax[8], skey[8];
-    const int tiles_n = (n + TS - 1) / TS;
-    const int tiles = tiles_n * ((m + TS - 1) / TS);
+    const int tiles_n = (n + TB - 1) / TB;
+    const int tiles = tiles_n * ((m + TB - 1) / TB);
     const double* a = c.ra->a_in;
     const long long lda = c.ra->lda_in;
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int tx = threadIdx.x & (TB - 1), ty = threadIdx.x / TB;
     unsigned long long mx = 0, key = ~0ull;
-    // grid-stride over 32x32 tiles; one reduction per CTA at the end
+    // grid-stride over the tiles; one reduction per CTA at the end
     for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const int i0 = (t / tiles_n) * TS, j0 = (t % tiles_n) * TS;
+        const int i0 = (t / tiles_n) * TB, j0 = (t % tiles_n) * TB;
+        double v[TBR];
 #pragma unroll
-        for (int r = 0; r < TS; r += 8) {
-            const int i = i0 + tx, j = j0 + ty + r;
-            double v = 0.0;
-            if (i < m && j < n) {
-                v = a[(long long)(c0 + j) * lda + r0 + i];
-                if (!isfinite(v)) {
-                    const unsigned long long k = fail_key(seq, elem_local(i, j));
-                    key = k < key ? k : key;
-                }
-                const unsigned long long bits = __double_as_longlong(fabs(v));
-                mx = bits > mx ? bits : mx;
+        for (int r = 0; r < TBR; ++r) {
+            const int i = i0 + tx, j = j0 + ty + 4 * r;
+            v[r] = (i < m && j < n) ? a[(long long)(c0 + j) * lda + r0 + i] : 0.0;
+        }
+#pragma unroll
+        for (int r = 0; r < TBR; ++r) {
+            const int i = i0 + tx, j = j0 + ty + 4 * r;
+            if (i < m && j < n && !isfinite(v[r])) {
+                const unsigned long long k = fail_key(seq, elem_local(i, j));
+                key = k < key ? k : key;
             }
-            tile[ty + r][tx] = v;
+            const unsigned long long bits = __double_as_longlong(fabs(v[r]));
+            mx = (bits > mx && bits <= 0x7ff0000000000000ull) ? bits : mx;  // NaN skipped (tree.cpp:82-86)
+            tile[ty + 4 * r][tx] = v[r];
         }
         __syncthreads();
 #pragma unroll
-        for (int r = 0; r < TS; r += 8) {
-            const int i = i0 + ty + r, j = j0 + tx;
-            if (i < m && j < n) store_level(c, lv, (long long)(r0 + i) * c.ldw + c0 + j, tile[tx][ty + r]);
+        for (int r = 0; r < TBR; ++r) {
+            const int i = i0 + ty + 4 * r, j = j0 + tx;
+            if (i < m && j < n) store_level(c, lv, (long long)(r0 + i) * c.ldw + c0 + j, tile[tx][ty + 4 * r]);
         }
         __syncthreads();
     }
@@ -179,9 +182,9 @@ __global__ void __launch_bounds__(256) k_quant1(DevCtx c, int lv, int r0, int c0
         mx = x > mx ? x : mx;
         key = y < key ? y : key;
     }
-    if (tx == 0) {
-        smax[ty] = mx;
-        skey[ty] = key;
+    if ((threadIdx.x & 31) == 0) {
+        smax[threadIdx.x >> 5] = mx;
+        skey[threadIdx.x >> 5] = key;
     }
     __syncthreads();
     if (threadIdx.x == 0) {

@@ -17,8 +17,10 @@
 //             (exact in FP32), and s = sum lo_a*hi_b + hi_a*lo_b + hi_a*hi_b
 //             on kind::tf32 -- ~22 significant bits per operand, FP32 sums
 //             (the reference rounds each product to FP32, kernels.cpp:29-30).
-//             The split runs in shared memory between the TMA load and the
-//             MMA (converter warps), so the operands are read from HBM once.
+//             The tensor core reads the staged FP32 x as its TF32 hi (it drops
+//             the 13 low mantissa bits); converter warps write lo = x - hi
+//             next to it in shared memory, so the operands are read from HBM
+//             once.
 //
 // Structure (one persistent CTA per SM, warp-specialised):
 //   warp 0      TMA producer: 128x(128 B) A and BNx(128 B) B tiles, SWIZZLE_128B,
@@ -31,7 +33,7 @@
 //               32x32b -> registers -> dot_update tail -> rounding to the
 //               destination level -> global (row-major C); fused
 //               require_finite as one OR per element, located only on failure
-//   warps 10-13 (TF32X3 only) hi/lo split of each stage, then a
+//   warps 10-13 (TF32X3 only) lo half of each stage, then a
 //               fence.proxy.async so the tensor core sees the generic writes
 // A problem list (one tree_syrk = all its output blocks, or one trsm GEMM)
 // is flattened into 128xBN tiles; each problem has its own pair of TMA
@@ -246,25 +248,24 @@ __device__ __forceinline__ void load_chunk(CChunk& ch, const void* p, bool f16) 
         if (!f16 || g < 4) ch.r[g] = __ldcg(q + g);
 }
 
-// hi/lo split of one staged tile pair for the three-pass TF32 product:
-// hi = x with the 13 low mantissa bits cleared (exactly TF32), lo = x - hi
-// (exact).  Elementwise, so the TMA swizzle is preserved.  128 threads.
-__device__ __forceinline__ void split_tf32(unsigned char* hi, unsigned char* lo, int bytes, int t) {
-    float4* h = reinterpret_cast<float4*>(hi);
+// lo half of one staged tile pair for the three-pass TF32 product: the
+// tensor core reads an FP32 element as TF32 by dropping its 13 low mantissa
+// bits, so the staged x already is hi; lo = x - hi (exact) goes next to it.
+// Elementwise, so the TMA swizzle is preserved.  128 threads.  (Writing hi
+// back as well measured 23% slower on 4096^3, bit-identical results: the
+// stage is shared-memory-bandwidth bound.)
+__device__ __forceinline__ void split_tf32(const unsigned char* hi, unsigned char* lo, int bytes, int t) {
+    const float4* h = reinterpret_cast<const float4*>(hi);
     float4* l = reinterpret_cast<float4*>(lo);
     const int n4 = bytes / 16;
 #pragma unroll 4
     for (int e = t; e < n4; e += 128) {
-        float4 x = h[e], y;
-        float* xs = reinterpret_cast<float*>(&x);
-        float* ys = reinterpret_cast<float*>(&y);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const float hv = __uint_as_float(__float_as_uint(xs[q]) & 0xFFFFE000u);
-            ys[q] = xs[q] - hv;
-            xs[q] = hv;
-        }
-        h[e] = x;
+        const float4 x = h[e];
+        float4 y;
+        y.x = x.x - __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
+        y.y = x.y - __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
+        y.z = x.z - __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
+        y.w = x.w - __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
         l[e] = y;
     }
 }
@@ -389,7 +390,7 @@ __global__ void __launch_bounds__(Cfg<KIND>::NTHREADS, 1) k_gemm_tc(DevCtx c, co
             }
         }
     } else if (warp >= 10) {
-        // ---------------- hi/lo split (TF32X3) ----------------
+        // ---------------- lo halves (TF32X3) ----------------
         if constexpr (SPLIT) {
             const int t128 = threadIdx.x - 10 * 32;
             int stage = 0;
