@@ -216,6 +216,37 @@ def test_host_entry_point_pinned_graph(tc, oracle, dag):
         assert np.array_equal(l[iu], a[iu])
 
 
+@pytest.mark.parametrize("what", ["not-positive-definite", "numerical-breakdown", "alpha-above-one"])
+def test_host_entry_point_pinned_failures(tc, oracle, what):
+    """the pinned host pipeline (phased graphs, copy feeder) reports the same
+    first failure as the device path, and a later call on good data is
+    unaffected"""
+    import torch
+    n, b, cfg = 1024, 64, "[F16, F16, F32]"
+    a = oracle.spd_generate(n, 12)
+    if what == "not-positive-definite":
+        a[700, 700] = -5.0
+    elif what == "numerical-breakdown":
+        a[900, 300] = np.nan  # lower triangle, inside a late block
+    else:
+        a = _scaled(oracle, n, 12, 3.0 * 65504.0 / 0.5)
+    plan = tc.Plan(n, b, cfg)
+    host = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+    host.numpy().T[:] = a
+    st = plan.factor_host(host.numpy().T)
+    st_d, l_dev, _, _ = _run(tc, a, b, cfg)
+    assert st.status == st_d.status
+    assert st.index == st_d.index
+    assert st.detail == st_d.detail
+    if st.status == "ok":
+        assert np.array_equal(np.tril(host.numpy().T), np.tril(l_dev))
+    good = oracle.spd_generate(n, 13)
+    host.numpy().T[:] = good
+    assert plan.factor_host(host.numpy().T).status == "ok"
+    _, l_good, _, _ = _run(tc, good, b, cfg)
+    assert np.array_equal(np.tril(host.numpy().T), np.tril(l_good))
+
+
 def test_ladder_ordering_n1024(tc, oracle):
     """criteria 2-3 (acceptance.cpp:103-163) on seeds 0-2 against the
     published medians (proj/test_output.txt:19-24, 34)"""
