@@ -168,7 +168,7 @@ bool Engine::prepare(std::string* err) {
                 if (L.tiles < 0) return false;
                 L.offset = append(tp.data(), tp.size());
             } else {
-                L.tiles = simt_tiles(dp);
+                L.tiles = simt_tiles(dp, op.gclass == GC_MMA32 ? M32_TILE : 0);
                 L.offset = append(dp.data(), dp.size() * sizeof(DevProb));
             }
         }

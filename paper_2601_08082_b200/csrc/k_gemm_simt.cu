@@ -198,8 +198,10 @@ __global__ void __launch_bounds__(256) k_gemm_dmma(DevCtx c, const DevProb* prob
 // arithmetic as the tcgen05 TF32X3 kernel, without its per-launch setup
 // (TMEM allocation, descriptors, pipeline fill), which dominates the
 // 256-wide leaf-level solves and updates on the factorization's chain.
-// Same 64x64 tiles / problem tables as the SIMT kernel; 4 warps of 32x32.
+// 32x32 output tiles (simt_tiles with M32_TILE), 4 warps of 16x16.
 constexpr int MK = 32, MLD = MK + 4;  // k-slab, padded row (conflict-free fragments)
+// its own 32x32 output tiles (4x the CTAs of the 64x64 SIMT tiles: these
+// problems are latency-bound, the chain waits on each)
 
 __device__ __forceinline__ void mma_tf32x(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
     asm volatile(
@@ -218,33 +220,32 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int byt
 }
 
 __global__ void __launch_bounds__(128) k_gemm_mma32(DevCtx c, const DevProb* probs, int np) {
-    __shared__ __align__(16) float As[2][BM][MLD];
-    __shared__ __align__(16) float Bs[2][BN][MLD];
+    constexpr int TM = M32_TILE, TN = M32_TILE;  // 32 x 32 output tile: 4 warps of 16 x 16
+    __shared__ __align__(16) float As[2][TM][MLD];
+    __shared__ __align__(16) float Bs[2][TN][MLD];
     const DevProb p = probs[find_prob(probs, np, blockIdx.x)];
     const int lt = blockIdx.x - p.tile0;
     const int tm = lt / p.tiles_n, tn = lt % p.tiles_n;
-    const int i0 = tm * BM, j0 = tn * BN;
-    if (p.lower && p.c_c0 + j0 > p.c_r0 + i0 + BM - 1) return;  // tile above the diagonal
+    const int i0 = tm * TM, j0 = tn * TN;
+    if (p.lower && p.c_c0 + j0 > p.c_r0 + i0 + TM - 1) return;  // tile above the diagonal
     const float* buf = c.b32;
     // B from the FP32 leaf inverses for inverse-based solves (plan.hpp kW32Ld)
     const float* bbuf = p.b_buf == BUF_W32 ? c.w32 : c.b32;
     const long long bld = p.b_buf == BUF_W32 ? kW32Ld : c.ldw;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int wm = warp >> 1, wn = warp & 1;  // 2 x 2 warps of 32 x 32
+    const int wm = warp >> 1, wn = warp & 1;  // 2 x 2 warps of 16 x 16
     const int g = lane >> 2, tq = lane & 3;
-    float acc[2][4][4];
+    float acc[2][4];
 #pragma unroll
-    for (int x = 0; x < 2; ++x)
+    for (int y = 0; y < 2; ++y)
 #pragma unroll
-        for (int y = 0; y < 4; ++y)
-#pragma unroll
-            for (int e = 0; e < 4; ++e) acc[x][y][e] = 0.f;
-    // 64 x 32 slabs of A and B, double-buffered with cp.async (zero-filled
+        for (int e = 0; e < 4; ++e) acc[y][e] = 0.f;
+    // 32 x 32 slabs of A and B, double-buffered with cp.async (zero-filled
     // outside the problem): the next slab loads while this one multiplies
     auto load = [&](int k0, int sb) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int e = threadIdx.x + 128 * q;  // 512 x 16 B per operand
+        for (int q = 0; q < 2; ++q) {
+            const int e = threadIdx.x + 128 * q;  // 256 x 16 B per operand
             const int r = e >> 3, kq = (e & 7) * 4;
             const int kg = k0 + kq;
             const int kb = min(16, max(0, (p.k - kg) * 4));
@@ -269,60 +270,53 @@ __global__ void __launch_bounds__(128) k_gemm_mma32(DevCtx c, const DevProb* pro
         __syncthreads();
 #pragma unroll
         for (int kk = 0; kk < MK; kk += 8) {
-            uint32_t ah[2][4], al[2][4];
+            uint32_t ah[4], al[4];
+            const int rb = wm * 16;
+            split_tf32(As[sb][rb + g][kk + tq], ah[0], al[0]);
+            split_tf32(As[sb][rb + g + 8][kk + tq], ah[1], al[1]);
+            split_tf32(As[sb][rb + g][kk + tq + 4], ah[2], al[2]);
+            split_tf32(As[sb][rb + g + 8][kk + tq + 4], ah[3], al[3]);
 #pragma unroll
-            for (int x = 0; x < 2; ++x) {
-                const int rb = wm * 32 + x * 16;
-                split_tf32(As[sb][rb + g][kk + tq], ah[x][0], al[x][0]);
-                split_tf32(As[sb][rb + g + 8][kk + tq], ah[x][1], al[x][1]);
-                split_tf32(As[sb][rb + g][kk + tq + 4], ah[x][2], al[x][2]);
-                split_tf32(As[sb][rb + g + 8][kk + tq + 4], ah[x][3], al[x][3]);
-            }
-#pragma unroll
-            for (int y = 0; y < 4; ++y) {
-                const int cb = wn * 32 + y * 8;
+            for (int y = 0; y < 2; ++y) {
+                const int cb = wn * 16 + y * 8;
                 uint32_t bh[2], bl[2];
                 split_tf32(Bs[sb][cb + g][kk + tq], bh[0], bl[0]);
                 split_tf32(Bs[sb][cb + g][kk + tq + 4], bh[1], bl[1]);
-#pragma unroll
-                for (int x = 0; x < 2; ++x) {
-                    mma_tf32x(acc[x][y], al[x], bh);
-                    mma_tf32x(acc[x][y], ah[x], bl);
-                    mma_tf32x(acc[x][y], ah[x], bh);
-                }
+                mma_tf32x(acc[y], al, bh);
+                mma_tf32x(acc[y], ah, bl);
+                mma_tf32x(acc[y], ah, bh);
             }
         }
         __syncthreads();
     }
     unsigned long long bad = ~0ull;
 #pragma unroll
-    for (int x = 0; x < 2; ++x)
+    for (int y = 0; y < 2; ++y)
 #pragma unroll
-        for (int y = 0; y < 4; ++y)
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int i = i0 + wm * 32 + x * 16 + g + (e >= 2 ? 8 : 0);
-                const int j = j0 + wn * 32 + y * 8 + 2 * tq + (e & 1);
-                if (i >= p.m || j >= p.n) continue;
-                if (p.lower && p.c_c0 + j > p.c_r0 + i) continue;
-                const long long off = (long long)(p.c_r0 + i) * c.ldw + p.c_c0 + j;
-                if (epi_store_f(c, p, off, acc[x][y][e]) && p.check_seq) {
-                    const unsigned long long k =
-                        fail_key(p.check_seq, elem_local(p.c_r0 + i - p.chk_r0, p.c_c0 + j - p.chk_c0));
-                    bad = k < bad ? k : bad;
-                }
+        for (int e = 0; e < 4; ++e) {
+            const int i = i0 + wm * 16 + g + (e >= 2 ? 8 : 0);
+            const int j = j0 + wn * 16 + y * 8 + 2 * tq + (e & 1);
+            if (i >= p.m || j >= p.n) continue;
+            if (p.lower && p.c_c0 + j > p.c_r0 + i) continue;
+            const long long off = (long long)(p.c_r0 + i) * c.ldw + p.c_c0 + j;
+            if (epi_store_f(c, p, off, acc[y][e]) && p.check_seq) {
+                const unsigned long long k =
+                    fail_key(p.check_seq, elem_local(p.c_r0 + i - p.chk_r0, p.c_c0 + j - p.chk_c0));
+                bad = k < bad ? k : bad;
             }
+        }
     if (p.check_seq) warp_report_min(c, bad);
 }
 
 }  // namespace
 
-int simt_tiles(std::vector<DevProb>& probs) {
+int simt_tiles(std::vector<DevProb>& probs, int tile) {
+    const int tm = tile > 0 ? tile : BM, tn = tile > 0 ? tile : BN;
     int tiles = 0;
     for (auto& p : probs) {
         p.tile0 = tiles;
-        p.tiles_n = (p.n + BN - 1) / BN;
-        tiles += ((p.m + BM - 1) / BM) * p.tiles_n;
+        p.tiles_n = (p.n + tn - 1) / tn;
+        tiles += ((p.m + tm - 1) / tm) * p.tiles_n;
     }
     return tiles;
 }
