@@ -538,7 +538,10 @@ bool Engine::enqueue_host(double* host, long long lda, cudaStream_t stream, std:
     cudaPointerAttributes pa{};
     const bool pinned = cudaPointerGetAttributes(&pa, host) == cudaSuccess && pa.type == cudaMemoryTypeHost;
     cudaGetLastError();
-    if (use_graph && pinned && dag_graph) {
+    // the copy pipeline serves pageable buffers too: their H2D calls return
+    // once staged, their D2H calls once done -- issued only when the phase
+    // that exports the block has finished, so nothing deadlocks
+    if (use_graph && dag_graph) {
         if (hph_exec_.empty() && !build_host_phases(err)) return false;
         if (!run_host(io, stream, err)) return false;
     } else if (use_graph && pinned) {
