@@ -709,6 +709,43 @@ def factor_matrix(a: np.ndarray, config, b: int, quantize: bool = True, plan: Pl
     return rep
 
 
+def _g17(v: float) -> str:
+    """%.17g, NaN as "nan" (cli.cpp:19-24)"""
+    if v != v:
+        return "nan"
+    return "%.17g" % v
+
+
+CSV_HEADER = "n,config,leaf,quantize,seed,status,rel_error,digits,flops_f16,flops_f32,flops_f64,flops_total,wall_ms"
+
+
+def write_csv(reports, out) -> None:
+    """The reference's fixed CSV schema (cli.cpp:26-33, 123-127): header row,
+    LF endings, doubles as %.17g, the config quoted.  `out` is a text stream."""
+    out.write(CSV_HEADER + "\n")
+    for r in reports:
+        f = r.flops
+        out.write("%d,\"%s\",%d,%d,%d,%s,%s,%s,%d,%d,%d,%d,%s\n" % (
+            r.n, r.config, r.b, 1 if r.quantize else 0, r.seed, r.status, _g17(r.rel_error), _g17(r.digits),
+            f.by_level[0], f.by_level[1], f.by_level[2], f.total(), _g17(r.wall_ms)))
+
+
+def plan_report(n: int, b: int, config) -> str:
+    """The `plan` subcommand's flop report (cli.cpp:52-86)."""
+    cfg = _cfg(config)
+    fb = flop_breakdown(n, b, cfg)
+    t = float(fb.total())
+    pct = (lambda f: 100.0 * f / t if t > 0 else 0.0)
+    lines = ["n=%d leaf=%d config=%s total_flops=%d" % (n, b, cfg.to_string(), fb.total()), "", "per precision:"]
+    for i, name in enumerate(("F16", "F32", "F64")):  # precision_name (precision.cpp:9-15)
+        lines.append("  %-4s %20d  %6.2f%%" % (name, fb.by_level[i], pct(fb.by_level[i])))
+    lines.append("per kernel:")
+    for i, name in enumerate(("POTRF-leaf", "TRSM-leaf", "SYRK-leaf", "GEMM")):  # kernel_name (flops.cpp:5-12)
+        lines.append("  %-10s %14d  %6.2f%%  (%d calls)" % (name, fb.by_kernel[i], pct(fb.by_kernel[i]), fb.calls[i]))
+    lines.append("off-diagonal share (TRSM+SYRK+GEMM): %.2f%%" % pct(fb.by_kernel[1] + fb.by_kernel[2] + fb.by_kernel[3]))
+    return "\n".join(lines) + "\n"
+
+
 def accuracy_sweep(sizes, configs, b, seeds, quantize=True):
     """analysis.cpp:157-173: n-major, then config, then seed."""
     out = []

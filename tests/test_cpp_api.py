@@ -53,3 +53,38 @@ def test_reference_acceptance_gate_on_device():
     fails = [ln for ln in crit2.splitlines() if ln.strip().startswith("FAIL")]
     assert all("[F16, F32, F64] > Pure F32" in ln for ln in fails), fails
     assert "7/8 criteria passed" in out or "8/8 criteria passed" in out
+
+
+# the reference's CSV header literal (cli.cpp:124-125) and plan-report lines
+# (cli.cpp:52-86), restated here so the test needs no reference sources
+REF_CSV_HEADER = "n,config,leaf,quantize,seed,status,rel_error,digits,flops_f16,flops_f32,flops_f64,flops_total,wall_ms"
+
+
+def test_report_writers_match_python_mirror(tmp_path):
+    """treechol/cli.hpp (write_csv, print_plan) and the Python mirror
+    (write_csv, plan_report) emit the reference's schema byte for byte"""
+    import io
+    import paper_2601_08082_b200 as tc
+    exe = tmp_path / "report_main"
+    subprocess.run(["g++", "-std=c++20", "-O2", "-I" + os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "report_main.cpp"), "-L" + PKG, "-ltreechol", "-ltreechol_b200",
+                    "-Wl,-rpath," + PKG, "-o", str(exe)], check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    csv_cpp, plan_cpp = r.stdout.split("--\n")
+    fb = tc.flop_breakdown(1024, 128, "[F16, F64]")
+    a = tc.FactorReport(n=1024, config="[F16, F64]", b=128, quantize=True, seed=3, status="ok",
+                        rel_error=1.2345678901234567e-06, digits=5.9084850188786495, flops=fb, wall_ms=12.5)
+    b = tc.FactorReport(n=1024, config="[F16, F64]", b=128, quantize=False, seed=3, status="not-positive-definite",
+                        flops=fb, wall_ms=12.5)
+    out = io.StringIO()
+    tc.write_csv([a, b], out)
+    assert out.getvalue() == csv_cpp
+    lines = csv_cpp.splitlines()
+    assert lines[0] == REF_CSV_HEADER
+    assert lines[1].startswith('1024,"[F16, F64]",128,1,3,ok,1.2345678901234567e-06,5.9084850188786495,')
+    assert ",not-positive-definite,nan,nan," in lines[2] and lines[2].startswith('1024,"[F16, F64]",128,0,3,')
+    assert plan_cpp == tc.plan_report(65536, 256, "[F16, F16, F16, F32]")
+    n = 65536
+    assert plan_cpp.startswith("n=65536 leaf=256 config=[F16, F16, F16, F32] total_flops=%d\n" % (n * (n + 1) * (2 * n + 1) // 6))
+    assert "off-diagonal share (TRSM+SYRK+GEMM): " in plan_cpp
