@@ -42,7 +42,7 @@ KERNEL_NAMES = ("POTRF-leaf", "TRSM-leaf", "SYRK-leaf", "GEMM")  # flops.cpp:5-1
 TC_OK, TC_NPD, TC_BREAKDOWN, TC_SINGULAR, TC_INVALID, TC_SYNTAX, TC_VALIDATION, TC_CUDA, TC_NO_DEVICE = range(9)
 
 OP_TYPES = ("import", "export", "check", "quant", "dequant", "shadow", "potrf", "trsm", "gemm", "inverse")
-GEMM_CLASSES = ("tc16", "simt_f16", "simt_f32", "simt_f16d", "simt_f32d", "simt_f64", "tc32", "mma32")
+GEMM_CLASSES = ("tc16", "simt_f16", "simt_f32", "simt_f16d", "simt_f32d", "simt_f64", "tc32", "mma32", "mma32w")
 
 
 # ---------------------------------------------------------------- errors.hpp

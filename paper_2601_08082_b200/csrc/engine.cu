@@ -76,6 +76,7 @@ bool Engine::prepare(std::string* err) {
     TC_TRY(cudaGetDevice(&device_));
     init_leaf_attributes();
     init_tc_attributes();
+    init_mma32w_attributes();
     // level buffers: rows x ldw (n x n for a factorization plan)
     const int n = plan.rows > 0 ? plan.rows : plan.n;
     const long long ldw = (long long)align_up(size_t(plan.cols > 0 ? plan.cols : plan.n), 64);
@@ -168,7 +169,8 @@ bool Engine::prepare(std::string* err) {
                 if (L.tiles < 0) return false;
                 L.offset = append(tp.data(), tp.size());
             } else {
-                L.tiles = simt_tiles(dp, op.gclass == GC_MMA32 ? M32_TILE : 0);
+                L.tiles = op.gclass == GC_MMA32W ? simt_tiles(dp, M32_TILE, 256)
+                                                 : simt_tiles(dp, op.gclass == GC_MMA32 ? M32_TILE : 0);
                 L.offset = append(dp.data(), dp.size() * sizeof(DevProb));
             }
         }

@@ -308,10 +308,116 @@ __global__ void __launch_bounds__(128) k_gemm_mma32(DevCtx c, const DevProb* pro
     if (p.check_seq) warp_report_min(c, bad);
 }
 
+// In-place inverse leaf solves X = rn32(B W^T) (GC_MMA32W): one CTA owns
+// 32 full rows (all n <= 256 output columns), so it reads every K column of
+// its rows before it writes any of them -- no other CTA touches those rows.
+// 8 warps, each 32 rows x 32 columns (2 m16 x 4 n8 fragments).
+constexpr int WN = 256;  // widest n
+__global__ void __launch_bounds__(256) k_gemm_mma32w(DevCtx c, const DevProb* probs, int np) {
+    extern __shared__ __align__(16) float wsm[];
+    float (*As)[M32_TILE][MLD] = reinterpret_cast<float (*)[M32_TILE][MLD]>(wsm);            // [2][32][MLD]
+    float (*Bs)[WN][MLD] = reinterpret_cast<float (*)[WN][MLD]>(wsm + 2 * M32_TILE * MLD);    // [2][256][MLD]
+    const DevProb p = probs[find_prob(probs, np, blockIdx.x)];
+    const int lt = blockIdx.x - p.tile0;
+    const int i0 = lt * M32_TILE;  // tiles_n == 1
+    const float* buf = c.b32;
+    const float* bbuf = p.b_buf == BUF_W32 ? c.w32 : c.b32;
+    const long long bld = p.b_buf == BUF_W32 ? kW32Ld : c.ldw;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, tq = lane & 3;
+    float acc[2][4][4];
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[x][y][e] = 0.f;
+    auto load = [&](int k0, int sb) {
+        {  // A: 32 rows x 32 k = 256 x 16 B, one per thread
+            const int e = threadIdx.x;
+            const int r = e >> 3, kq = (e & 7) * 4;
+            const int kg = k0 + kq;
+            const int kb = min(16, max(0, (p.k - kg) * 4));
+            const int ia = i0 + r;
+            cp_async16(&As[sb][r][kq], buf + (long long)(p.a_r0 + (ia < p.m ? ia : 0)) * c.ldw + p.a_c0 + (kb ? kg : 0),
+                       ia < p.m ? kb : 0);
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {  // B: 256 rows x 32 k = 2048 x 16 B
+            const int e = threadIdx.x + 256 * q;
+            const int r = e >> 3, kq = (e & 7) * 4;
+            const int kg = k0 + kq;
+            const int kb = min(16, max(0, (p.k - kg) * 4));
+            cp_async16(&Bs[sb][r][kq], bbuf + (long long)(p.b_r0 + (r < p.n ? r : 0)) * bld + p.b_c0 + (kb ? kg : 0),
+                       r < p.n ? kb : 0);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    const int ns = (p.k + MK - 1) / MK;
+    load(0, 0);
+    for (int st = 0; st < ns; ++st) {
+        const int sb = st & 1;
+        if (st + 1 < ns) {
+            load((st + 1) * MK, sb ^ 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < MK; kk += 8) {
+            uint32_t ah[2][4], al[2][4];
+#pragma unroll
+            for (int x = 0; x < 2; ++x) {
+                const int rb = x * 16;
+                split_tf32(As[sb][rb + g][kk + tq], ah[x][0], al[x][0]);
+                split_tf32(As[sb][rb + g + 8][kk + tq], ah[x][1], al[x][1]);
+                split_tf32(As[sb][rb + g][kk + tq + 4], ah[x][2], al[x][2]);
+                split_tf32(As[sb][rb + g + 8][kk + tq + 4], ah[x][3], al[x][3]);
+            }
+#pragma unroll
+            for (int y = 0; y < 4; ++y) {
+                const int cb = warp * 32 + y * 8;
+                uint32_t bh[2], bl[2];
+                split_tf32(Bs[sb][cb + g][kk + tq], bh[0], bl[0]);
+                split_tf32(Bs[sb][cb + g][kk + tq + 4], bh[1], bl[1]);
+#pragma unroll
+                for (int x = 0; x < 2; ++x) {
+                    mma_tf32x(acc[x][y], al[x], bh);
+                    mma_tf32x(acc[x][y], ah[x], bl);
+                    mma_tf32x(acc[x][y], ah[x], bh);
+                }
+            }
+        }
+        __syncthreads();
+    }
+    // every K column of these rows has been read (the loop's last barrier):
+    // the in-place write is safe
+    unsigned long long bad = ~0ull;
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int i = i0 + x * 16 + g + (e >= 2 ? 8 : 0);
+                const int j = warp * 32 + y * 8 + 2 * tq + (e & 1);
+                if (i >= p.m || j >= p.n) continue;
+                const long long off = (long long)(p.c_r0 + i) * c.ldw + p.c_c0 + j;
+                if (epi_store_f(c, p, off, acc[x][y][e]) && p.check_seq) {
+                    const unsigned long long k =
+                        fail_key(p.check_seq, elem_local(p.c_r0 + i - p.chk_r0, p.c_c0 + j - p.chk_c0));
+                    bad = k < bad ? k : bad;
+                }
+            }
+    if (p.check_seq) warp_report_min(c, bad);
+}
+constexpr size_t kMma32wSmem = sizeof(float) * 2 * (M32_TILE + WN) * MLD;
+
 }  // namespace
 
-int simt_tiles(std::vector<DevProb>& probs, int tile) {
-    const int tm = tile > 0 ? tile : BM, tn = tile > 0 ? tile : BN;
+int simt_tiles(std::vector<DevProb>& probs, int tile, int tile_n) {
+    const int tm = tile > 0 ? tile : BM, tn = tile_n > 0 ? tile_n : tile > 0 ? tile : BN;
     int tiles = 0;
     for (auto& p : probs) {
         p.tile0 = tiles;
@@ -321,6 +427,10 @@ int simt_tiles(std::vector<DevProb>& probs, int tile) {
     return tiles;
 }
 
+void init_mma32w_attributes() {
+    cudaFuncSetAttribute(k_gemm_mma32w, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kMma32wSmem));
+}
+
 void launch_gemm_simt(const DevCtx& c, int gclass, const DevProb* d_probs, int nprob, int tiles,
                       cudaStream_t s) {
     if (tiles <= 0) return;
@@ -328,6 +438,7 @@ void launch_gemm_simt(const DevCtx& c, int gclass, const DevProb* d_probs, int n
         case GC_SIMT_F16: k_gemm_simt<0, float><<<tiles, 256, 0, s>>>(c, d_probs, nprob); break;
         case GC_SIMT_F32: k_gemm_simt<1, float><<<tiles, 256, 0, s>>>(c, d_probs, nprob); break;
         case GC_MMA32: k_gemm_mma32<<<tiles, 128, 0, s>>>(c, d_probs, nprob); break;
+        case GC_MMA32W: k_gemm_mma32w<<<tiles, 256, kMma32wSmem, s>>>(c, d_probs, nprob); break;
         // FP64 accumulation on the FP64 tensor pipe (DMMA)
         case GC_SIMT_F16D: k_gemm_dmma<0><<<tiles, 256, 0, s>>>(c, d_probs, nprob); break;
         case GC_SIMT_F32D: k_gemm_dmma<1><<<tiles, 256, 0, s>>>(c, d_probs, nprob); break;

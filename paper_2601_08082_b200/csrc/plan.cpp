@@ -167,18 +167,41 @@ void Plan::emit_trsm(Rect B, int p, int lnode) {
             g.beta = 0.0;
             g.seq = seq;
             g.ref_kernel = K_TRSM;
-            Op op;
-            op.type = OP_GEMM;
-            op.level = p;
-            op.gclass = inv16                                                        ? GC_TC16
-                        : double(g.m) * g.n * g.k <= opt.mma32_max ? GC_MMA32
-                                                                   : GC_TC32;
-            op.prob_begin = int(probs.size());
-            probs.push_back(g);
-            op.prob_end = int(probs.size());
-            op.rect = B;
-            op.flops = double(f);
-            push(std::move(op));
+            // X overwrites B in place, so no output tile may be written while
+            // another tile still reads those columns as K.  FP16: one 256-wide
+            // column tile covers n.  FP32 on mma.sync: full-width tiles
+            // (GC_MMA32W).  FP32 on tcgen05 (128-wide tiles): two ops in
+            // sequence -- columns [128, n) first (they read all of B), then
+            // [0, 128), which need only B[:, 0:128) (W is lower triangular)
+            auto emit = [&](const GemmProb& gp, int gclass, double fl) {
+                Op op;
+                op.type = OP_GEMM;
+                op.level = p;
+                op.gclass = gclass;
+                op.prob_begin = int(probs.size());
+                probs.push_back(gp);
+                op.prob_end = int(probs.size());
+                op.rect = {gp.c_r0, gp.c_c0, gp.m, gp.n};
+                op.flops = fl;
+                push(std::move(op));
+            };
+            if (inv16) {
+                emit(g, GC_TC16, double(f));
+            } else if (double(g.m) * g.n * g.k <= opt.mma32_max) {
+                emit(g, GC_MMA32W, double(f));
+            } else if (g.n <= kTc32TileN) {
+                emit(g, GC_TC32, double(f));
+            } else {
+                GemmProb r = g, l = g;
+                r.n = g.n - kTc32TileN;  // right columns [128, n): B rows of W from 128 on
+                r.b_r0 = g.b_r0 + kTc32TileN;
+                r.c_c0 = g.c_c0 + kTc32TileN;
+                l.n = kTc32TileN;        // left columns [0, 128): K = 128
+                l.k = kTc32TileN;
+                const double fr = double(f) * double(r.n) / double(g.n);
+                emit(r, GC_TC32, fr);
+                emit(l, GC_TC32, double(f) - fr);
+            }
             return;
         }
         Op op;

@@ -33,6 +33,7 @@ constexpr int kInvMinRows = 512;  // below this the substitution kernel is used 
 // FP32 leaf inverses W = inv(L) (row r0+i of a leaf, columns [0, n)), for
 // inverse-based FP32 leaf solves on the three-pass TF32 tensor-core GEMM
 constexpr int kW32Ld = 256;
+constexpr int kTc32TileN = 128;  // output tile width of the TF32X3 tcgen05 GEMM (k_gemm_tc.cu Cfg)
 enum RefKernel : int { K_POTRF = 0, K_TRSM = 1, K_SYRK = 2, K_GEMM = 3 };
 
 struct Rect {
@@ -105,6 +106,8 @@ enum GemmClass : int {
     GC_SIMT_F64 = 5,  // FP64 operands, FP64 accumulate
     GC_TC32 = 6,      // FP32 operands, three-pass TF32 split on tcgen05, FP32 accumulate (exec F32)
     GC_MMA32 = 7,     // the same arithmetic on mma.sync, for problems too small for tcgen05's setup
+    GC_MMA32W = 8,    // GC_MMA32 with full-width (32 x n) tiles: in-place inverse leaf solves X = B W^T,
+                      // where a tile must not overwrite columns another tile still reads as K
 };
 
 struct Access {

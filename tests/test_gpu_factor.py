@@ -335,3 +335,35 @@ def test_c1_ten_seed_median_within_2x(tc, oracle):
         rel_g.append(r)
         rel_o.append(r_o)
     assert np.median(rel_g) <= 2 * np.median(rel_o), (np.median(rel_g), np.median(rel_o))
+
+
+def test_c3_full_size_properties(tc):
+    """BASELINE config C3 (N=65536, b=256, [F16, F16, F16, F32]) where the CPU
+    oracle cannot go (weeks): size-independent properties.  Status ok; the
+    executed flops equal the static counter and n(n+1)(2n+1)/6
+    (criterion 6); a second factorization is bit-identical (criterion 8); and
+    on A/2 (Pure F16 overflows A's diagonal) the mixed tree's backward error
+    is at least 50x below Pure F16's (criterion 3 / the north-star target)."""
+    import torch
+    n, b, cfg = 65536, 256, "[F16, F16, F16, F32]"
+    a = tc.spd_generate_device(n, 42)
+    plan = tc.Plan(n, b, cfg)
+    l1 = a.clone()  # same strict upper in both outputs (never written)
+    assert plan.factor_device(a, l1).status == "ok"
+    fl = plan.run_flops()
+    assert fl.as_tuple() == tc.flop_breakdown(n, b, cfg).as_tuple()
+    assert fl.total() == n * (n + 1) * (2 * n + 1) // 6
+    l2 = a.clone()
+    assert plan.factor_device(a, l2).status == "ok"
+    assert torch.equal(l1, l2)
+    del l2, plan
+    torch.cuda.empty_cache()
+    a.mul_(0.5)  # exact
+    rel = {}
+    for c in (cfg, "Pure F16"):
+        p = tc.Plan(n, b, c)
+        assert p.factor_device(a, l1).status == "ok"
+        rel[c] = tc.factorization_error_device(a, l1)
+        del p
+        torch.cuda.empty_cache()
+    assert rel[cfg] * 50 <= rel["Pure F16"], rel
