@@ -129,6 +129,10 @@ int tc_plan_trace_host(tc_plan* plan, double* host, int lda, void* stream, float
  * FP16, 1..5 SIMT classes, -1 otherwise), level, algorithmic flops, rect */
 int tc_plan_op_info(const tc_plan* plan, int i, int* type, int* gclass, int* level,
                     double* flops, int* rect4);
+/* development: the GEMM problems of op i (0 for other ops), 13 ints each --
+ * m, n, k, a_r0, a_c0, a_kwrap, b_buf, b_r0, b_c0, c_r0, c_c0, exec_level,
+ * lower -- up to cap problems; returns the count */
+int tc_plan_op_probs(const tc_plan* plan, int i, int* out, int cap);
 /* dependencies of op i (indices of earlier ops); returns their count
  * (entries beyond cap are not written), -1 on a bad index */
 int tc_plan_op_deps(const tc_plan* plan, int i, int* deps, int cap);

@@ -118,6 +118,7 @@ def _load():
         "tc_potrf_host": (I, [P, P, I, C.POINTER(_Info)]),
         "tc_plan_profile": (I, [P, P, I, P, I, P, C.POINTER(C.c_float), I]),
         "tc_plan_status": (I, [P, C.POINTER(_Info)]),
+        "tc_plan_op_probs": (I, [P, I, C.POINTER(C.c_int), I]),
         "tc_plan_timeline": (I, [P, P, I, P, I, P, C.POINTER(C.c_float), C.POINTER(C.c_float), I]),
         "tc_plan_trace_host": (I, [P, P, I, P, C.POINTER(C.c_float), I, C.POINTER(C.c_float), I,
                                    C.POINTER(C.c_float), I]),
@@ -423,6 +424,18 @@ class Plan:
         _raise(_lib.tc_plan_op_info(self._h, i, C.byref(t), C.byref(g), C.byref(lv), C.byref(fl), r))
         return {"type": OP_TYPES[t.value], "gclass": GEMM_CLASSES[g.value] if g.value >= 0 else None,
                 "level": lv.value, "flops": fl.value, "rect": tuple(r)}
+
+    def op_probs(self, i: int):
+        """GEMM problems of op i: dicts of m, n, k, a_r0, a_c0, a_kwrap, b_buf,
+        b_r0, b_c0, c_r0, c_c0, exec_level, lower"""
+        keys = ("m", "n", "k", "a_r0", "a_c0", "a_kwrap", "b_buf", "b_r0", "b_c0", "c_r0", "c_c0", "exec_level",
+                "lower")
+        cnt = _lib.tc_plan_op_probs(self._h, i, None, 0)
+        if cnt < 0:
+            _raise(cnt)
+        arr = (C.c_int * (13 * max(cnt, 1)))()
+        _lib.tc_plan_op_probs(self._h, i, arr, cnt)
+        return [dict(zip(keys, arr[13 * q:13 * q + 13])) for q in range(cnt)]
 
     def op_deps(self, i: int):
         cap = 64

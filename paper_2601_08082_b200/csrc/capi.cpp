@@ -274,6 +274,22 @@ int tc_plan_op_info(const tc_plan* plan, int i, int* type, int* gclass, int* lev
     return TC_OK;
 }
 
+int tc_plan_op_probs(const tc_plan* plan, int i, int* out, int cap) {
+    if (!plan || i < 0 || i >= int(plan->eng->plan.ops.size())) return fail(TC_INVALID_ARGUMENT, "bad op index");
+    const Plan& P = plan->eng->plan;
+    const Op& op = P.ops[size_t(i)];
+    if (op.type != OP_GEMM) return 0;
+    int k = 0;
+    for (int q = op.prob_begin; q < op.prob_end; ++q, ++k) {
+        if (!out || k >= cap) continue;
+        const GemmProb& g = P.probs[size_t(q)];
+        const int v[13] = {g.m, g.n, g.k, g.a_r0, g.a_c0, g.a_kwrap, g.b_buf, g.b_r0, g.b_c0, g.c_r0, g.c_c0,
+                           g.exec_level, g.lower};
+        for (int e = 0; e < 13; ++e) out[13 * k + e] = v[e];
+    }
+    return op.prob_end - op.prob_begin;
+}
+
 int tc_plan_create_trsm(int n1, int m, int b, const int* levels, int nlevels, int leaf_size, tc_plan** out) {
     if (!out || !levels_ok(levels, nlevels)) return fail(TC_INVALID_ARGUMENT, "bad arguments");
     *out = nullptr;

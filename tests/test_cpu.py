@@ -239,3 +239,39 @@ def test_library_is_sm100a(tc):
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", tc.LIB_PATH], capture_output=True,
                          text=True).stdout
     assert "sm_100a" in out
+
+
+# output tile width per GEMM class (engine / kernels): a GEMM whose output
+# overlaps its A operand in the same buffer (the in-place inverse leaf
+# solves) is only safe when one tile spans all n output columns -- otherwise
+# a tile can overwrite columns another tile still reads as K
+_TILE_N = {"tc16": 256, "tc32": 128, "mma32": 32, "mma32w": 256, "simt_f16": 64, "simt_f32": 64,
+           "simt_f16d": 64, "simt_f32d": 64, "simt_f64": 64}
+_OPERAND_LEVEL = {"tc16": 0, "simt_f16": 0, "simt_f16d": 0, "tc32": 1, "mma32": 1, "mma32w": 1, "simt_f32": 1,
+                  "simt_f32d": 1, "simt_f64": 2}
+
+
+@pytest.mark.parametrize("n,b,cfg", [(4096, 256, "[F16, F16, F16, F32]"), (8192, 256, "[F16, F32, F64]"),
+                                     (16384, 256, "[F16, F16, F16, F32]"), (2048, 128, "Pure F32"),
+                                     (1024, 64, "[F16, F32]"), (32768, 256, "[F16, F16, F16, F32]")])
+def test_no_in_place_gemm_hazard(tc, n, b, cfg):
+    """every GEMM whose C overlaps its own A (same buffer) has one output
+    tile across all its columns (regression: N >= 32768 factorizations were
+    not bit-reproducible when 128-wide TF32 tiles solved in place)"""
+    p = tc.Plan(n, b, cfg)
+    inplace = 0
+    for i in range(p.stats()["ops"]):
+        probs = p.op_probs(i)
+        if not probs:
+            continue
+        cls = p.op_info(i)["gclass"]
+        for g in probs:
+            if g["exec_level"] != _OPERAND_LEVEL[cls]:
+                continue  # C and A live in different level buffers
+            kw = g["a_kwrap"] or g["k"]
+            rows = g["a_r0"] < g["c_r0"] + g["m"] and g["c_r0"] < g["a_r0"] + g["m"]
+            cols = g["a_c0"] < g["c_c0"] + g["n"] and g["c_c0"] < g["a_c0"] + kw
+            if rows and cols:
+                inplace += 1
+                assert g["n"] <= _TILE_N[cls], (i, cls, g)
+    assert inplace > 0 or cfg == "[F16, F32, F64]"
