@@ -64,7 +64,7 @@ extern "C" int tc_debug_gemm(int gclass, int m, int n, int k, int lower, double 
     std::string err;
     if (tc) tiles = tc_build_probs(c, gclass == GC_TC32 ? KIND_TF32X3 : KIND_F16, v, host, &err);
     else {
-        tiles = gclass == GC_MMA32W ? simt_tiles(v, M32_TILE, 256) : simt_tiles(v, gclass == GC_MMA32 ? M32_TILE : 0);
+        tiles = gclass == GC_MMA32W ? simt_tiles(v, M32W_ROWS, 256) : simt_tiles(v, gclass == GC_MMA32 ? M32_TILE : 0);
         host.assign(reinterpret_cast<unsigned char*>(v.data()), reinterpret_cast<unsigned char*>(v.data() + 1));
     }
     void* dprob = nullptr;

@@ -169,7 +169,7 @@ bool Engine::prepare(std::string* err) {
                 if (L.tiles < 0) return false;
                 L.offset = append(tp.data(), tp.size());
             } else {
-                L.tiles = op.gclass == GC_MMA32W ? simt_tiles(dp, M32_TILE, 256)
+                L.tiles = op.gclass == GC_MMA32W ? simt_tiles(dp, M32W_ROWS, 256)
                                                  : simt_tiles(dp, op.gclass == GC_MMA32 ? M32_TILE : 0);
                 L.offset = append(dp.data(), dp.size() * sizeof(DevProb));
             }

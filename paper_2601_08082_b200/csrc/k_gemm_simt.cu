@@ -309,31 +309,33 @@ __global__ void __launch_bounds__(128) k_gemm_mma32(DevCtx c, const DevProb* pro
 }
 
 // In-place inverse leaf solves X = rn32(B W^T) (GC_MMA32W): one CTA owns
-// 32 full rows (all n <= 256 output columns), so it reads every K column of
+// WM full rows (all n <= 256 output columns), so it reads every K column of
 // its rows before it writes any of them -- no other CTA touches those rows.
-// 8 warps, each 32 rows x 32 columns (2 m16 x 4 n8 fragments).
+// 8 warps, each WM rows x 32 columns (WM/16 m16 x 4 n8 fragments).
 constexpr int WN = 256;  // widest n
+constexpr int WM = M32W_ROWS;  // rows per CTA (16: twice the CTAs of 32 rows for the 256-row solves on the chain)
 __global__ void __launch_bounds__(256) k_gemm_mma32w(DevCtx c, const DevProb* probs, int np) {
     extern __shared__ __align__(16) float wsm[];
-    float (*As)[M32_TILE][MLD] = reinterpret_cast<float (*)[M32_TILE][MLD]>(wsm);            // [2][32][MLD]
-    float (*Bs)[WN][MLD] = reinterpret_cast<float (*)[WN][MLD]>(wsm + 2 * M32_TILE * MLD);    // [2][256][MLD]
+    float (*As)[WM][MLD] = reinterpret_cast<float (*)[WM][MLD]>(wsm);            // [2][WM][MLD]
+    float (*Bs)[WN][MLD] = reinterpret_cast<float (*)[WN][MLD]>(wsm + 2 * WM * MLD);  // [2][256][MLD]
     const DevProb p = probs[find_prob(probs, np, blockIdx.x)];
     const int lt = blockIdx.x - p.tile0;
-    const int i0 = lt * M32_TILE;  // tiles_n == 1
+    const int i0 = lt * WM;  // tiles_n == 1
     const float* buf = c.b32;
     const float* bbuf = p.b_buf == BUF_W32 ? c.w32 : c.b32;
     const long long bld = p.b_buf == BUF_W32 ? kW32Ld : c.ldw;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, tq = lane & 3;
-    float acc[2][4][4];
+    constexpr int XM = WM / 16;
+    float acc[XM][4][4];
 #pragma unroll
-    for (int x = 0; x < 2; ++x)
+    for (int x = 0; x < XM; ++x)
 #pragma unroll
         for (int y = 0; y < 4; ++y)
 #pragma unroll
             for (int e = 0; e < 4; ++e) acc[x][y][e] = 0.f;
     auto load = [&](int k0, int sb) {
-        {  // A: 32 rows x 32 k = 256 x 16 B, one per thread
+        if (threadIdx.x < WM * 8) {  // A: WM rows x 32 k, 16 B per thread
             const int e = threadIdx.x;
             const int r = e >> 3, kq = (e & 7) * 4;
             const int kg = k0 + kq;
@@ -366,9 +368,9 @@ __global__ void __launch_bounds__(256) k_gemm_mma32w(DevCtx c, const DevProb* pr
         __syncthreads();
 #pragma unroll
         for (int kk = 0; kk < MK; kk += 8) {
-            uint32_t ah[2][4], al[2][4];
+            uint32_t ah[XM][4], al[XM][4];
 #pragma unroll
-            for (int x = 0; x < 2; ++x) {
+            for (int x = 0; x < XM; ++x) {
                 const int rb = x * 16;
                 split_tf32(As[sb][rb + g][kk + tq], ah[x][0], al[x][0]);
                 split_tf32(As[sb][rb + g + 8][kk + tq], ah[x][1], al[x][1]);
@@ -382,7 +384,7 @@ __global__ void __launch_bounds__(256) k_gemm_mma32w(DevCtx c, const DevProb* pr
                 split_tf32(Bs[sb][cb + g][kk + tq], bh[0], bl[0]);
                 split_tf32(Bs[sb][cb + g][kk + tq + 4], bh[1], bl[1]);
 #pragma unroll
-                for (int x = 0; x < 2; ++x) {
+                for (int x = 0; x < XM; ++x) {
                     mma_tf32x(acc[x][y], al[x], bh);
                     mma_tf32x(acc[x][y], ah[x], bl);
                     mma_tf32x(acc[x][y], ah[x], bh);
@@ -395,7 +397,7 @@ __global__ void __launch_bounds__(256) k_gemm_mma32w(DevCtx c, const DevProb* pr
     // the in-place write is safe
     unsigned long long bad = ~0ull;
 #pragma unroll
-    for (int x = 0; x < 2; ++x)
+    for (int x = 0; x < XM; ++x)
 #pragma unroll
         for (int y = 0; y < 4; ++y)
 #pragma unroll
@@ -412,7 +414,7 @@ __global__ void __launch_bounds__(256) k_gemm_mma32w(DevCtx c, const DevProb* pr
             }
     if (p.check_seq) warp_report_min(c, bad);
 }
-constexpr size_t kMma32wSmem = sizeof(float) * 2 * (M32_TILE + WN) * MLD;
+constexpr size_t kMma32wSmem = sizeof(float) * 2 * (WM + WN) * MLD;
 
 }  // namespace
 

@@ -63,6 +63,7 @@ void launch_potrf_v2(const DevCtx& c, int lv, int r0, int n, uint32_t seq, uint3
 // problems must already be in device memory with tile0 / tiles_n filled by
 // the matching *_tiles() helper
 constexpr int M32_TILE = 32;  // output tile of the mma.sync FP32 kernel (GC_MMA32)
+constexpr int M32W_ROWS = 16; // rows per CTA of its full-width in-place variant (GC_MMA32W; k_gemm_simt.cu WM)
 int simt_tiles(std::vector<DevProb>& probs, int tile = 0, int tile_n = 0);  // 0: the 64x64 SIMT tile
 void init_mma32w_attributes();
 void launch_gemm_simt(const DevCtx& c, int gclass, const DevProb* d_probs, int nprob, int tiles,
