@@ -87,7 +87,12 @@ int tc_plan_flops(const tc_plan* plan, tc_flops* out);
 int tc_plan_stats(const tc_plan* plan, int* n_ops, int* n_launches, int* n_gemm_problems);
 /* execution knobs: use_graph (default 1), n_streams (default 6),
  * use_tc (default 1: tcgen05 for FP16-operand GEMMs; 0 = SIMT path),
- * use_tc32 (default 1: three-pass TF32 tcgen05 for FP32 x FP32 GEMMs) */
+ * use_tc32 (default 1: three-pass TF32 tcgen05 for FP32 x FP32 GEMMs),
+ * dag_graph (1: explicit DAG graph; 0: stream capture), inverse_trsm,
+ * fuse_checks, syrk_split_min, bulk_tiles_per_cta, bulk_max_ctas,
+ * mma32_max_log2 (FP32 GEMMs with m*n*k <= 2^v on mma.sync, default 24),
+ * mma32w_max_log2 (in-place FP32 leaf solves on full-width mma.sync tiles,
+ * default 28); the plan-shaping ones before the first run */
 int tc_plan_set_option(tc_plan* plan, const char* key, int value);
 
 /* ---- factorization (tree_potrf, tree.cpp:106-125) ---------------------- */

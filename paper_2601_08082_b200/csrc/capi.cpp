@@ -230,10 +230,10 @@ int tc_plan_set_option(tc_plan* plan, const char* key, int value) {
         plan->eng->n_streams = s;
         return TC_OK;
     }
-    if (k == "mma32_max_log2") {  // FP32 GEMMs with m*n*k <= 2^value run on mma.sync (negative: never)
+    if (k == "mma32_max_log2" || k == "mma32w_max_log2") {  // FP32 GEMMs (in-place solves) with m*n*k <= 2^value run on mma.sync (negative: never)
         if (e.ready()) return fail(TC_INVALID_ARGUMENT, k + " must be set before the first run");
         PlanOptions po = e.plan.opt;
-        po.mma32_max = value < 0 ? -1.0 : std::ldexp(1.0, value);
+        (k == "mma32_max_log2" ? po.mma32_max : po.mma32w_max) = value < 0 ? -1.0 : std::ldexp(1.0, value);
         Plan p = Plan::make(e.plan.n, e.plan.b, e.plan.levels, e.plan.quantize, e.plan.leaf_size, po);
         const bool g = e.use_graph;
         const int s = e.n_streams;

@@ -187,7 +187,7 @@ void Plan::emit_trsm(Rect B, int p, int lnode) {
             };
             if (inv16) {
                 emit(g, GC_TC16, double(f));
-            } else if (double(g.m) * g.n * g.k <= opt.mma32_max) {
+            } else if (double(g.m) * g.n * g.k <= opt.mma32w_max) {
                 emit(g, GC_MMA32W, double(f));
             } else if (g.n <= kTc32TileN) {
                 emit(g, GC_TC32, double(f));

@@ -157,6 +157,7 @@ struct FlopRec {
 struct PlanOptions {
     bool use_tc = true;      // FP16-operand GEMMs on tcgen05
     bool use_tc32 = true;    // FP32 x FP32 GEMMs on tcgen05 (three-pass TF32)
+    double mma32w_max = 268435456.0;  // in-place inverse solves at or below this m*n*k on mma.sync (2^28: panels up to 4096 rows)
     double mma32_max = 16777216.0;  // m*n*k at or below which they run on mma.sync instead (2^24: the 256^3 leaf-level ones; 2^26 is 3% faster for one N=16384 factorization but 5% slower for the C4 batch)
     bool inverse_trsm = true; // FP16 leaf solves with m >= kInvMinRows as tcgen05 GEMMs
     bool fuse_checks = true;  // require_finite inside the producing kernels
