@@ -274,4 +274,8 @@ def test_no_in_place_gemm_hazard(tc, n, b, cfg):
             if rows and cols:
                 inplace += 1
                 assert g["n"] <= _TILE_N[cls], (i, cls, g)
+            if g["b_buf"] < 0:  # B from the same level buffer: it must not overlap C at all
+                brows = g["b_r0"] < g["c_r0"] + g["m"] and g["c_r0"] < g["b_r0"] + g["n"]
+                bcols = g["b_c0"] < g["c_c0"] + g["n"] and g["c_c0"] < g["b_c0"] + g["k"]
+                assert not (brows and bcols), (i, cls, g)
     assert inplace > 0 or cfg == "[F16, F32, F64]"
