@@ -194,7 +194,7 @@ def test_host_entry_point_in_place(tc, oracle):
     assert np.array_equal(l[iu], a[iu])
 
 
-@pytest.mark.parametrize("dag", [1, 0])
+@pytest.mark.parametrize("dag", [1, 0, "eager"])
 def test_host_entry_point_pinned_graph(tc, oracle, dag):
     """pinned host buffer: the copies overlap the factorization graph (H2D /
     D2H on the copy streams, event nodes in the graph); repeated calls reuse
@@ -202,7 +202,10 @@ def test_host_entry_point_pinned_graph(tc, oracle, dag):
     import torch
     n = 1024
     plan = tc.Plan(n, 64, "[F16, F16, F32]")
-    plan.set_option("dag_graph", dag)
+    if dag == "eager":
+        plan.set_option("use_graph", 0)
+    else:
+        plan.set_option("dag_graph", dag)
     for seed in (7, 8):
         a = oracle.spd_generate(n, seed)
         host = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
