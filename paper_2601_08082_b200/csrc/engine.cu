@@ -675,7 +675,7 @@ void Engine::drop_host_phases() {
 // stall unrelated work sharing its hardware channel); at most kDepth copies
 // per direction are in flight.
 bool Engine::run_host(const HostIO& io, cudaStream_t stream, std::string* err) {
-    constexpr int kDepth = 3;
+    constexpr int kDepth = 6;
     const int n = plan.n, N = int(plan.ops.size());
     const int P = int(hph_exec_.size()), H = int(hc_rect_.size()), D = int(dc_rect_.size());
     const size_t esz = sizeof(double);
