@@ -370,3 +370,19 @@ def test_c3_full_size_properties(tc):
         del p
         torch.cuda.empty_cache()
     assert rel[cfg] * 50 <= rel["Pure F16"], rel
+
+
+@pytest.mark.parametrize("n,b,cfg", [(777, 64, "[F16, F32]"), (1000, 96, "[F16, F16, F32]"), (300, 300, "Pure F32")])
+def test_host_entry_point_pinned_ragged(tc, oracle, n, b, cfg):
+    """ragged orders and leaf sizes through the copy pipeline (chunking of
+    non-square blocks, single-leaf plans) give the device path's factor"""
+    import torch
+    a = oracle.spd_generate(n, 31)
+    host = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+    host.numpy().T[:] = a
+    plan = tc.Plan(n, b, cfg)
+    assert plan.factor_host(host.numpy().T).status == "ok"
+    _, l_dev, _, _ = _run(tc, a, b, cfg)
+    assert np.array_equal(np.tril(host.numpy().T), np.tril(l_dev))
+    iu = np.triu_indices(n, 1)
+    assert np.array_equal(host.numpy().T[iu], a[iu])
