@@ -530,10 +530,12 @@ class Batch:
         lda = _check_dev(a_list[0], self.n, "A") if k else self.n
         pa = (C.c_void_p * k)(*[_ptr(a) for a in a_list])
         pb, ldb, nrhs = None, self.n, 1
-        if b_list is not None:
-            b2 = [x if x.dim() == 2 else x.view(1, -1) for x in b_list]
-            ldb, nrhs = b2[0].shape[1], b2[0].shape[0]
-            pb = (C.c_void_p * k)(*[_ptr(x) for x in b2])
+        if b_list is not None:  # entries may be None: that system is factored only
+            b2 = [None if x is None else (x if x.dim() == 2 else x.view(1, -1)) for x in b_list]
+            first = next((x for x in b2 if x is not None), None)
+            if first is not None:
+                ldb, nrhs = first.shape[1], first.shape[0]
+            pb = (C.c_void_p * k)(*[None if x is None else _ptr(x) for x in b2])
         st = (C.c_int * max(k, 1))()
         idx = (C.c_int * max(k, 1))()
         code = _lib.tc_batch_run(self._h, k, pa, lda, pb, ldb, nrhs, st, idx)

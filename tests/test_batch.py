@@ -94,3 +94,28 @@ def test_batch_rank_driver_single_gpu(tc):
                                           in_flight=4)
     assert local.systems == 4 and tot.failed == 0
     assert tot.worst_residual < 1e-5 and flops > 0 and tot.device_ms > 0
+
+
+@pytest.mark.gpu
+def test_batch_solve_orders_agree(tc, oracle):
+    """solve_order 0 (every factorization, then all solves in one batched
+    launch sequence) and 1 (each solve behind its factorization, single-system
+    launches) give bit-identical factors and solutions, with 2 RHS, more
+    systems than plans, and one system without right-hand sides"""
+    import torch
+    n, b, cfg = 768, 64, "[F16, F16, F32]"
+    mats = [oracle.spd_generate(n, s) for s in range(5)]
+    out = []
+    for order in (0, 1):
+        a_dev = [tc.to_device(m) for m in mats]
+        rhs = [torch.from_numpy(np.stack([m.sum(axis=1), m[:, 0]])).to("cuda").contiguous() for m in mats]
+        rhs[3] = None
+        batch = tc.Batch(n, b, cfg, True, concurrency=2)
+        batch.set_option("solve_order", order)
+        st = batch.run(a_dev, rhs)
+        assert all(s == "ok" for s in st)
+        out.append(([x.cpu().numpy() for x in a_dev], [None if x is None else x.cpu().numpy() for x in rhs]))
+    for k in range(len(mats)):
+        assert np.array_equal(np.tril(out[0][0][k].T), np.tril(out[1][0][k].T))
+        if k != 3:
+            assert np.array_equal(out[0][1][k], out[1][1][k])
