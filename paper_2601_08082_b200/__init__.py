@@ -317,12 +317,16 @@ def from_device(t) -> np.ndarray:
     return np.asfortranarray(t.detach().cpu().numpy().T)
 
 
-def _check_dev(t, n, what):
+def _check_dev(t, n, what, cols=None):
+    """a contiguous CUDA float64 column-major tensor (cols', ld) with
+    ld >= n rows and cols' >= cols (default n) columns; returns ld"""
     import torch
+    cols = n if cols is None else cols
     if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float64:
         raise InvalidArgument(f"{what} must be a CUDA float64 tensor")
-    if t.dim() != 2 or t.shape[1] < n or not t.is_contiguous():
-        raise InvalidArgument(f"{what} must be a contiguous (cols, ld>=n) tensor")
+    if t.dim() != 2 or t.shape[1] < n or t.shape[0] < cols or not t.is_contiguous():
+        raise InvalidArgument(f"{what} must be a contiguous ({cols}+ columns, ld >= {n}) tensor, "
+                              f"got shape {tuple(t.shape)}")
     return t.shape[1]
 
 
@@ -351,6 +355,7 @@ class Plan:
         _raise(_lib.tc_plan_create(self.n, self.b, arr, len(self.cfg.levels), int(self.quantize), int(leaf_size),
                                    C.byref(h)))
         self._h = h
+        self._extent()
         if not use_tc:
             self.set_option("use_tc", 0)
         if not use_tc32:
@@ -372,7 +377,15 @@ class Plan:
         self.cfg = _cfg(config)
         self.n, self.b, self.quantize = int(rows), int(b), True
         self._h = h
+        self._extent()
         return self
+
+    def _extent(self):
+        """rows x cols of the column-major operand the plan reads and writes
+        (tc_plan_extent; n x n for a whole factorization)"""
+        r, c = C.c_int(), C.c_int()
+        _raise(_lib.tc_plan_extent(self._h, C.byref(r), C.byref(c)))
+        self.rows, self.cols = r.value, c.value
 
     @classmethod
     def panel_trsm(cls, n1: int, m: int, b: int, config, leaf_size: int = 0) -> "Plan":
@@ -458,10 +471,10 @@ class Plan:
     def factor_device(self, a_in, l_out=None, stream=None, sync: bool = True):
         """Device-resident tree_potrf: reads a_in, writes L's lower triangle
         into l_out (default: in place).  Returns FactorStatus when sync."""
-        n = self.n
-        lda = _check_dev(a_in, n, "a_in")
+        n, cols = self.rows, self.cols
+        lda = _check_dev(a_in, n, "a_in", cols)
         l_out = a_in if l_out is None else l_out
-        ldl = _check_dev(l_out, n, "l_out")
+        ldl = _check_dev(l_out, n, "l_out", cols)
         info = _Info()
         code = _lib.tc_potrf_device(self._h, _ptr(a_in), lda, _ptr(l_out), ldl, _stream_ptr(stream),
                                     C.byref(info) if sync else None)
@@ -479,6 +492,8 @@ class Plan:
         """tree_potrf on a host Fortran float64 array, in place (TileView contract)."""
         if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.f_contiguous):
             raise InvalidArgument("a must be a Fortran-ordered float64 array")
+        if a.ndim != 2 or a.shape[0] < self.rows or a.shape[1] < self.cols:
+            raise InvalidArgument(f"a must be at least {self.rows} x {self.cols}, got {a.shape}")
         info = _Info()
         code = _lib.tc_potrf_host(self._h, a.ctypes.data, a.shape[0], C.byref(info))
         return self._status(code, info)
@@ -487,16 +502,18 @@ class Plan:
         """eager multi-stream run; per-op (start, end) ms from the start"""
         n_ops = self.stats()["ops"]
         t0, t1 = (C.c_float * n_ops)(), (C.c_float * n_ops)()
-        _raise(_lib.tc_plan_timeline(self._h, _ptr(a_in), _check_dev(a_in, self.n, "a_in"), _ptr(l_out),
-                                     _check_dev(l_out, self.n, "l_out"), _stream_ptr(stream), t0, t1, n_ops))
+        _raise(_lib.tc_plan_timeline(self._h, _ptr(a_in), _check_dev(a_in, self.rows, "a_in", self.cols),
+                                     _ptr(l_out), _check_dev(l_out, self.rows, "l_out", self.cols),
+                                     _stream_ptr(stream), t0, t1, n_ops))
         return list(t0), list(t1)
 
     def profile(self, a_in, l_out, stream=None):
         """serialized eager run; per-op device milliseconds"""
         n_ops = self.stats()["ops"]
         out = (C.c_float * n_ops)()
-        _raise(_lib.tc_plan_profile(self._h, _ptr(a_in), _check_dev(a_in, self.n, "a_in"), _ptr(l_out),
-                                    _check_dev(l_out, self.n, "l_out"), _stream_ptr(stream), out, n_ops))
+        _raise(_lib.tc_plan_profile(self._h, _ptr(a_in), _check_dev(a_in, self.rows, "a_in", self.cols),
+                                    _ptr(l_out), _check_dev(l_out, self.rows, "l_out", self.cols),
+                                    _stream_ptr(stream), out, n_ops))
         return list(out)
 
 
@@ -526,15 +543,33 @@ class Batch:
         """factor every a_list[k] in place (device column-major tensors, see
         to_device) and solve with b_list[k] (device tensors (nrhs, n)) if
         given; returns the per-system status names"""
+        import torch
         k = len(a_list)
-        lda = _check_dev(a_list[0], self.n, "A") if k else self.n
+        lda = _check_dev(a_list[0], self.n, "A[0]") if k else self.n
+        for i, a in enumerate(a_list):  # one leading dimension for the whole batch
+            if _check_dev(a, self.n, f"A[{i}]") != lda or a.shape != a_list[0].shape:
+                raise InvalidArgument(f"A[{i}] must have the shape of A[0] {tuple(a_list[0].shape)}")
         pa = (C.c_void_p * k)(*[_ptr(a) for a in a_list])
         pb, ldb, nrhs = None, self.n, 1
         if b_list is not None:  # entries may be None: that system is factored only
-            b2 = [None if x is None else (x if x.dim() == 2 else x.view(1, -1)) for x in b_list]
+            if len(b_list) != k:
+                raise InvalidArgument("b_list must have one entry (or None) per system")
+            b2 = []
+            for i, x in enumerate(b_list):
+                if x is not None:
+                    if not (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.float64
+                            and x.is_contiguous() and x.dim() in (1, 2)):
+                        raise InvalidArgument(f"B[{i}] must be a contiguous CUDA float64 tensor (nrhs, ldb)")
+                    x = x if x.dim() == 2 else x.view(1, -1)
+                b2.append(x)
             first = next((x for x in b2 if x is not None), None)
             if first is not None:
                 ldb, nrhs = first.shape[1], first.shape[0]
+                if ldb < self.n:
+                    raise InvalidArgument(f"B rows ({ldb}) < n ({self.n})")
+                for i, x in enumerate(b2):
+                    if x is not None and x.shape != first.shape:
+                        raise InvalidArgument(f"B[{i}] must have the shape of the first B {tuple(first.shape)}")
             pb = (C.c_void_p * k)(*[None if x is None else _ptr(x) for x in b2])
         st = (C.c_int * max(k, 1))()
         idx = (C.c_int * max(k, 1))()

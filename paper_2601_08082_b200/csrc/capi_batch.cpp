@@ -142,6 +142,12 @@ int tc_batch_run(tc_batch* bt, int count, double* const* dA, int lda, double* co
             return bfail(TC_CUDA_ERROR, "POTRS pointer tables");
         bt->tab_cap = count;
     }
+    // on a failure partway through, drain what is already queued before
+    // returning: earlier systems' graphs and solves still write dA/dB
+    auto drain_fail = [&](const std::string& why) {
+        for (auto s : bt->streams) cudaStreamSynchronize(s);
+        return bfail(TC_CUDA_ERROR, why);
+    };
     auto factor = [&](int k) {
         const int e = k % C;
         Engine& eng = *bt->eng[size_t(e)];
@@ -161,7 +167,7 @@ int tc_batch_run(tc_batch* bt, int count, double* const* dA, int lda, double* co
         // (persistent CTAs over all (block, system) pairs; the waiting CTAs
         // never sit beside a factorization)
         for (int k = 0; k < count; ++k)
-            if (!factor(k)) return bfail(TC_CUDA_ERROR, err);
+            if (!factor(k)) return drain_fail(err);
         int ns = 0;
         for (int k = 0; dB && k < count; ++k)
             if (dB[k]) {
@@ -186,7 +192,7 @@ int tc_batch_run(tc_batch* bt, int count, double* const* dA, int lda, double* co
         // each system's solve right behind its factorization: the solves of
         // one stream overlap the other streams' factorizations
         for (int k = 0; k < count; ++k) {
-            if (!factor(k)) return bfail(TC_CUDA_ERROR, err);
+            if (!factor(k)) return drain_fail(err);
             solve(k);
         }
     }

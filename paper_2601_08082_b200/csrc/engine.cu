@@ -675,6 +675,17 @@ void Engine::drop_host_phases() {
 // stall unrelated work sharing its hardware channel); at most kDepth copies
 // per direction are in flight.
 bool Engine::run_host(const HostIO& io, cudaStream_t stream, std::string* err) {
+    if (run_host_pipeline(io, stream, err)) return true;
+    // error path: up to kDepth copies per direction may still read from or
+    // write into the caller's host buffer; drain them (errors ignored) so the
+    // caller may free or reuse it once this returns
+    cudaStreamSynchronize(cs_h2d_);
+    cudaStreamSynchronize(cs_d2h_);
+    cudaStreamSynchronize(stream);
+    return false;
+}
+
+bool Engine::run_host_pipeline(const HostIO& io, cudaStream_t stream, std::string* err) {
     constexpr int kDepth = 6;
     const int n = plan.n, N = int(plan.ops.size());
     const int P = int(hph_exec_.size()), H = int(hc_rect_.size()), D = int(dc_rect_.size());

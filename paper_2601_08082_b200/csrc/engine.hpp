@@ -108,6 +108,7 @@ class Engine {
     std::vector<cudaEvent_t>* tl_d2h_ = nullptr;
     bool ensure_stage(std::string* err);
     bool run_host(const HostIO& io, cudaStream_t stream, std::string* err);
+    bool run_host_pipeline(const HostIO& io, cudaStream_t stream, std::string* err);
     std::vector<Rect> hc_rect_, dc_rect_;      // H2D chunks (block order), D2H chunks (by phase)
     std::vector<int> dc_phase_, ph_need_;      // phase of each D2H chunk; last H2D chunk a phase reads
     std::vector<cudaEvent_t> ev_hc_, ev_dc_;   // per chunk: copy done
