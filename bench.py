@@ -263,18 +263,26 @@ def run_ours(args):
     # contract): pinned host doubles -> H2D -> factor -> D2H lower triangle
     e2e = None
     if args.e2e_steps > 0:
+        # every step factors A itself: the pinned buffer is refilled from the
+        # device copy of A between steps (outside the timed calls)
         host = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
-        host.copy_(a)
         hnp = host.numpy().T  # Fortran view of the column-major bytes
         l = None
         torch.cuda.empty_cache()
-        plan.factor_host(hnp)  # warm (allocates the staging buffer)
-        barrier()
-        t0 = time.perf_counter()
+        host.copy_(a)
+        st_h = plan.factor_host(hnp)  # warm (allocates the staging buffer)
+        if st_h.status != "ok":
+            raise SystemExit(f"e2e factorization failed: {st_h.status} {st_h.detail}")
+        e2e_s = 0.0
         for _ in range(args.e2e_steps):
-            plan.factor_host(hnp)
+            host.copy_(a)
+            barrier()
+            t0 = time.perf_counter()
+            st_h = plan.factor_host(hnp)
+            e2e_s += time.perf_counter() - t0
+            if st_h.status != "ok":
+                raise SystemExit(f"e2e factorization failed: {st_h.status} {st_h.detail}")
         barrier()
-        e2e_s = time.perf_counter() - t0
         if ws > 1:
             t = torch.tensor([e2e_s], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -285,7 +293,9 @@ def run_ours(args):
         d2h = h2d
         e2e = {"value": ws * args.e2e_steps * flops / e2e_s / 1e12, "unit": "TFLOP/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
-               "note": "each step re-factors the previous step's in-place output (SPD lower triangle)"}
+               "status": st_h.status,
+               "note": "each step: tc_potrf_host on pinned host doubles holding A (refilled between steps, "
+                       "untimed), H2D + factor + D2H of the lower triangle inside the timed call"}
 
     # C4: a batch of independent N=16384 systems (POTRF + POTRS), sharded
     # across the ranks with no data-path collective
@@ -306,7 +316,13 @@ def run_ours(args):
               "value": tot.systems * fl / (tot.device_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
               "solves_per_s": tot.systems / (tot.device_ms * 1e-3), "systems": tot.systems, "failed": tot.failed,
               "ms_max_over_ranks": tot.device_ms, "worst_solve_residual": tot.worst_residual,
-              "data": "device-generated SPD of spd_generate's distribution (not the mt19937_64 stream)"}
+              "potrs_ms": tot.solve_ms,
+              # POTRS reads L twice (forward + backward sweep): n(n+1) * 8 bytes per system and RHS
+              "potrs_gbs": (tot.systems * args.c4_n * (args.c4_n + 1) * 8 / (tot.solve_ms * 1e-3) / 1e9
+                            if tot.solve_ms > 0 else None),
+              "potrs_gbs_note": "algorithmic bytes n(n+1)*8 per system / batched solve phase device time "
+                                "(max over ranks)",
+              "data": "spd_generate(16384, 1000 + k), bit-identical (mt19937_64 stream), b = A * ones"}
 
     # C5: one factorization split over the ranks (NCCL broadcast of L11,
     # all-reduce of the panel alpha, all-gather of the solved panel), at the
@@ -411,9 +427,21 @@ def main():
     ap.add_argument("--c4-conc", dest="c4_conc", type=int, default=16)
     ap.add_argument("--c5-n", dest="c5_n", type=int, default=65536,
                     help="N of the distributed single factorization run when --gpus > 1 (0: off)")
-    ap.add_argument("--variants", action="store_true",
-                    help="also time Pure F16 / Pure F64 trees (bounds) at N; slow (F64 runs on SIMT)")
+    ap.add_argument("--no-variants", dest="variants", action="store_false",
+                    help="skip the Pure F16 / Pure F64 bound runs (on by default)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-run this command under torchrun
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        raise SystemExit(subprocess.call(cmd))
+    ws, _, _ = dist_env()
+    if args.impl == "ours" and ws != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ws}")
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -157,6 +157,12 @@ int tc_info_message(const tc_plan* plan, const tc_info* info, char* buf, int buf
 int tc_potrs_device(int n, const double* dL, int ldl, double* dB, int ldb, int nrhs,
                     void* stream);
 
+/* The solves of nsys independent systems in one launch sequence: system k
+ * has its factor at dL[k] and right-hand sides at dB[k] (arrays of device
+ * pointers on the host; common n, ldl, ldb, nrhs).  Synchronous. */
+int tc_potrs_batch_device(int n, int nsys, const double* const* dL, int ldl, double* const* dB, int ldb,
+                          int nrhs, void* stream);
+
 /* ---- distributed single factorization (BASELINE config C5) ------------- */
 
 /* The two pieces a rank runs for the top split of an order-N factorization
@@ -205,6 +211,10 @@ int tc_batch_set_option(tc_batch* batch, const char* key, int value);
  * argument / device error. */
 int tc_batch_run(tc_batch* batch, int count, double* const* dA, int lda, double* const* dB, int ldb,
                  int nrhs, int* status, int* index);
+
+/* device milliseconds of the last tc_batch_run's batched solve phase (every
+ * POTRS of the call in one launch sequence; solve_order 0), 0 if none ran */
+int tc_batch_solve_ms(const tc_batch* batch, float* ms);
 
 /* ---- analysis (analysis.cpp) ------------------------------------------- */
 
@@ -261,6 +271,22 @@ int tc_gemm_mixed_device(int m, int n, int k, double* dC, int ldc, const double*
  * *avg_us = mean device time of `iters` back-to-back launches */
 int tc_debug_gemm(int gclass, int m, int n, int k, int lower, double beta, int exec_level, int iters,
                   float* avg_us);
+
+/* one problem of grouped-GEMM class gclass on caller device level buffers
+ * (row-major, ld = ldw; the engine's layout): C(c_r0.., c_c0..) =
+ * epi(C, alpha * A(a_r0.., a_c0..) B(b_r0.., b_c0..)^T) with the dot_update
+ * tail of kernels.cpp:23-38 at exec_level, optional lower mask (syrk_leaf).
+ * prob = {m, n, k, a_r0, a_c0, b_r0, b_c0, c_r0, c_c0, exec_level, lower}.
+ * Operands come from the operand level's buffer (b16 for FP16 classes, b32
+ * for FP32 classes, b64 for SIMT F64), C from the exec level's buffer.
+ * Synchronous.  Kernel-level parity tests (tests/test_gpu_kernels.py). */
+/* process-wide kernel settings for measurements: "tc_kchunk" = K chunk
+ * (elements) of FP32-exec tensor-core accumulations, 0 = one accumulation.
+ * Applies to plans built (graphs captured) afterwards. */
+int tc_set_global_option(const char* key, int value);
+
+int tc_gemm_problem_device(int gclass, void* b16, void* b32, void* b64, long long ldw, const int* prob,
+                           double alpha, double beta, void* stream);
 
 /* ---- misc --------------------------------------------------------------- */
 

@@ -126,11 +126,14 @@ def _load():
                                       C.POINTER(C.c_float), I, C.POINTER(C.c_float), I]),
         "tc_info_message": (I, [P, C.POINTER(_Info), C.c_char_p, I]),
         "tc_potrs_device": (I, [I, P, I, P, I, I, P]),
+        "tc_potrs_batch_device": (I, [I, I, C.POINTER(P), I, C.POINTER(P), I, I, P]),
         "tc_spd_generate_host": (I, [I, U64, P, I]),
         "tc_spd_generate_device": (I, [I, U64, P, I, P]),
         "tc_factorization_error_device": (I, [I, P, I, P, I, C.POINTER(D), P]),
         "tc_solve_residual_device": (I, [I, P, I, P, P, C.POINTER(D), P]),
         "tc_debug_gemm": (I, [I, I, I, I, I, D, I, I, C.POINTER(C.c_float)]),
+        "tc_gemm_problem_device": (I, [I, P, P, P, C.c_longlong, PI, D, D, P]),
+        "tc_set_global_option": (I, [C.c_char_p, I]),
         "tc_plan_create_trsm": (I, [I, I, I, PI, I, I, C.POINTER(P)]),
         "tc_plan_create_syrk_rows": (I, [I, I, I, PI, I, I, I, C.POINTER(P)]),
         "tc_plan_set_external_absmax": (I, [P, D]),
@@ -140,6 +143,7 @@ def _load():
         "tc_batch_destroy": (None, [P]),
         "tc_batch_set_option": (I, [P, C.c_char_p, I]),
         "tc_batch_run": (I, [P, I, C.POINTER(P), I, C.POINTER(P), I, I, PI, PI]),
+        "tc_batch_solve_ms": (I, [P, C.POINTER(C.c_float)]),
         "tc_round_host": (I, [I, I, P, I, I, I]),
         "tc_quantize_host": (I, [I, I, P, I, I, C.POINTER(D)]),
         "tc_dequantize_host": (I, [I, I, P, I, I, D]),
@@ -578,6 +582,12 @@ class Batch:
             _raise(code)
         return [_STATUS_NAMES[st[i]] for i in range(k)]
 
+    def last_solve_ms(self) -> float:
+        """device ms of the last run's batched solve phase (0 if none)"""
+        ms = C.c_float()
+        _raise(_lib.tc_batch_solve_ms(self._h, C.byref(ms)))
+        return ms.value
+
 
 # ---------------------------------------------------------------- kernels.hpp / tree.hpp block ops
 # The reference's kernel-level API on host Fortran float64 arrays, executed
@@ -699,6 +709,33 @@ def potrs_device(l_dev, b_dev, n: int | None = None, stream=None):
     return b_dev
 
 
+def potrs_batch_device(l_list, b_list, n: int | None = None, stream=None):
+    """the solves of independent systems in one launch sequence
+    (tc_potrs_batch_device): l_list[k] factors (column-major device tensors
+    of one shape), b_list[k] right-hand sides (nrhs, ldb) overwritten by X"""
+    import torch
+    k = len(l_list)
+    if k != len(b_list):
+        raise InvalidArgument("one right-hand side tensor per factor")
+    if k == 0:
+        return b_list
+    n = n or l_list[0].shape[0]
+    ldl = _check_dev(l_list[0], n, "L[0]")
+    b2 = []
+    for i, (l, b) in enumerate(zip(l_list, b_list)):
+        if _check_dev(l, n, f"L[{i}]") != ldl or l.shape != l_list[0].shape:
+            raise InvalidArgument(f"L[{i}] must have the shape of L[0]")
+        if not (isinstance(b, torch.Tensor) and b.is_cuda and b.dtype == torch.float64 and b.is_contiguous()):
+            raise InvalidArgument(f"B[{i}] must be a contiguous CUDA float64 tensor")
+        b2.append(b if b.dim() == 2 else b.view(1, -1))
+        if b2[-1].shape != b2[0].shape or b2[0].shape[1] < n:
+            raise InvalidArgument(f"B[{i}] must be (nrhs, ldb >= n) like B[0]")
+    pl = (C.c_void_p * k)(*[_ptr(x) for x in l_list])
+    pb = (C.c_void_p * k)(*[_ptr(x) for x in b2])
+    _raise(_lib.tc_potrs_batch_device(n, k, pl, ldl, pb, b2[0].shape[1], b2[0].shape[0], _stream_ptr(stream)))
+    return b_list
+
+
 def debug_gemm(gclass: str, m: int, n: int, k: int, lower: bool = False, beta: float = 1.0, exec_level: int = 0,
                iters: int = 20) -> float:
     """development: mean device microseconds of one grouped-GEMM launch"""
@@ -706,6 +743,23 @@ def debug_gemm(gclass: str, m: int, n: int, k: int, lower: bool = False, beta: f
     _raise(_lib.tc_debug_gemm(GEMM_CLASSES.index(gclass), m, n, k, int(lower), float(beta), exec_level, iters,
                               C.byref(out)))
     return out.value
+
+
+def set_global_option(key: str, value: int):
+    """process-wide kernel settings (tc_set_global_option), for measurements"""
+    _raise(_lib.tc_set_global_option(key.encode(), int(value)))
+
+
+def gemm_problem_device(gclass: str, b16, b32, b64, ldw: int, m: int, n: int, k: int, a_r0: int, a_c0: int,
+                        b_r0: int, b_c0: int, c_r0: int, c_c0: int, exec_level: int, lower: bool = False,
+                        alpha: float = -1.0, beta: float = 1.0, stream=None):
+    """one problem of a factorization GEMM class on caller level buffers
+    (torch tensors or None, row-major with ld = ldw): the launch path the
+    factorization graph uses (tc_gemm_problem_device)"""
+    pr = (C.c_int * 11)(m, n, k, a_r0, a_c0, b_r0, b_c0, c_r0, c_c0, exec_level, int(bool(lower)))
+    _raise(_lib.tc_gemm_problem_device(GEMM_CLASSES.index(gclass), None if b16 is None else _ptr(b16),
+                                       None if b32 is None else _ptr(b32), None if b64 is None else _ptr(b64),
+                                       int(ldw), pr, float(alpha), float(beta), _stream_ptr(stream)))
 
 
 def solve_residual_device(a_dev, x_dev, b_dev, n: int | None = None, stream=None) -> float:

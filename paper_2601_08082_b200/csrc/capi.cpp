@@ -597,6 +597,38 @@ int tc_potrs_device(int n, const double* dL, int ldl, double* dB, int ldb, int n
     return TC_OK;
 }
 
+int tc_potrs_batch_device(int n, int nsys, const double* const* dL, int ldl, double* const* dB, int ldb, int nrhs,
+                          void* stream) {
+    if (!dL || !dB || n < 1 || nsys < 0 || nrhs < 1 || ldl < n || ldb < n)
+        return fail(TC_INVALID_ARGUMENT, "bad arguments");
+    for (int k = 0; k < nsys; ++k)
+        if (!dL[k] || !dB[k]) return fail(TC_INVALID_ARGUMENT, "null system pointer");
+    if (nsys == 0) return TC_OK;
+    if (!tc_device_available()) return fail(TC_NO_DEVICE, "no CUDA device");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    // pointer tables (L then B) right behind the workspace
+    const size_t wbytes = (potrs_batch_work_bytes(n, nsys, nrhs) + 15) / 16 * 16;
+    void* d_work = nullptr;
+    cudaError_t e = cudaMallocAsync(&d_work, wbytes + 2 * sizeof(void*) * size_t(nsys), s);
+    if (e != cudaSuccess) return cuda_fail(e, "alloc");
+    std::vector<const void*> tab(2 * size_t(nsys));
+    for (int k = 0; k < nsys; ++k) {
+        tab[size_t(k)] = dL[k];
+        tab[size_t(nsys + k)] = dB[k];
+    }
+    void** d_tab = reinterpret_cast<void**>(static_cast<char*>(d_work) + wbytes);
+    e = cudaMemcpyAsync(d_tab, tab.data(), tab.size() * sizeof(void*), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) {
+        launch_potrs_batch(n, nsys, reinterpret_cast<const double* const*>(d_tab), ldl,
+                           reinterpret_cast<double* const*>(d_tab + nsys), ldb, nrhs, d_work, 148 * 6, s);
+        e = cudaStreamSynchronize(s);  // the host table must outlive the copy
+    }
+    cudaFreeAsync(d_work, s);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "potrs batch");
+    return TC_OK;
+}
+
 int tc_solve_residual_device(int n, const double* dA, int lda, const double* dX, const double* dB, double* out,
                              void* stream) {
     if (!dA || !dX || !dB || !out || n < 1) return fail(TC_INVALID_ARGUMENT, "bad arguments");

@@ -40,7 +40,12 @@ struct tc_batch {
     void** d_tab = nullptr;
     int tab_cap = 0;
     cudaEvent_t join = nullptr;
+    // device time of the last run's batched solve phase (solve_order 0)
+    cudaEvent_t solve_ev[2] = {nullptr, nullptr};
+    int solve_timed = 0;
     ~tc_batch() {
+        for (auto e : solve_ev)
+            if (e) cudaEventDestroy(e);
         for (auto s : streams) cudaStreamDestroy(s);
         for (auto w : work) cudaFree(w);
         if (h_status) cudaFreeHost(h_status);
@@ -162,6 +167,7 @@ int tc_batch_run(tc_batch* bt, int count, double* const* dA, int lda, double* co
         double* d_work = static_cast<double*>(bt->work[size_t(e)]);
         launch_potrs(n, dA[k], lda, dB[k], ldb, nrhs, nullptr, d_work, bt->streams[size_t(e)], 64);
     };
+    bt->solve_timed = 0;
     if (bt->solve_order == 0) {
         // all factorizations first, then every solve in one launch sequence
         // (persistent CTAs over all (block, system) pairs; the waiting CTAs
@@ -182,11 +188,18 @@ int tc_batch_run(tc_batch* bt, int count, double* const* dA, int lda, double* co
                 cudaEventRecord(bt->join, bt->streams[size_t(e)]);
                 cudaStreamWaitEvent(s0, bt->join, 0);
             }
+            if (!bt->solve_ev[0]) {
+                cudaEventCreate(&bt->solve_ev[0]);
+                cudaEventCreate(&bt->solve_ev[1]);
+            }
+            cudaEventRecord(bt->solve_ev[0], s0);
             // compact the B half right behind the L half
             for (int i = 0; i < ns; ++i) bt->h_tab[ns + i] = bt->h_tab[count + i];
             cudaMemcpyAsync(bt->d_tab, bt->h_tab, 2 * sizeof(void*) * size_t(ns), cudaMemcpyHostToDevice, s0);
             launch_potrs_batch(n, ns, reinterpret_cast<const double* const*>(bt->d_tab), lda,
                                reinterpret_cast<double* const*>(bt->d_tab + ns), ldb, nrhs, bt->work[0], 148 * 6, s0);
+            cudaEventRecord(bt->solve_ev[1], s0);
+            bt->solve_timed = 1;
         }
     } else {
         // each system's solve right behind its factorization: the solves of
@@ -209,6 +222,14 @@ int tc_batch_run(tc_batch* bt, int count, double* const* dA, int lda, double* co
         if (f.status && worst == TC_OK) worst = f.status;
     }
     return worst;
+}
+
+int tc_batch_solve_ms(const tc_batch* bt, float* ms) {
+    if (!bt || !ms) return bfail(TC_INVALID_ARGUMENT, "null argument");
+    *ms = 0.f;
+    if (!bt->solve_timed) return TC_OK;
+    const cudaError_t e = cudaEventElapsedTime(ms, bt->solve_ev[0], bt->solve_ev[1]);
+    return e == cudaSuccess ? TC_OK : bfail(TC_CUDA_ERROR, cudaGetErrorString(e));
 }
 
 }  // extern "C"

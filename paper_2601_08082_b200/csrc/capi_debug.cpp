@@ -115,3 +115,81 @@ extern "C" int tc_debug_gemm(int gclass, int m, int n, int k, int lower, double 
     }
     return TC_OK;
 }
+
+// one problem of grouped-GEMM class gclass on CALLER level buffers (the
+// engine's row-major layout, ld = ldw): the exact launch path the
+// factorization graph uses, for kernel-level parity tests against
+// gemm_mixed / syrk_leaf (kernels.cpp:94-132).  prob = {m, n, k, a_r0,
+// a_c0, b_r0, b_c0, c_r0, c_c0, exec_level, lower}; A and B are read from
+// the operand level's buffer (F16 for the FP16 classes, F32 for the FP32
+// ones, F64 for GC_SIMT_F64), C from / to the exec level's buffer.
+extern "C" int tc_gemm_problem_device(int gclass, void* b16, void* b32, void* b64, long long ldw, const int* prob,
+                                      double alpha, double beta, void* stream) {
+    if (!prob || ldw < 1 || gclass < 0 || gclass > GC_MMA32W) return TC_INVALID_ARGUMENT;
+    DevProb d{};
+    d.m = prob[0];
+    d.n = prob[1];
+    d.k = prob[2];
+    d.a_r0 = prob[3];
+    d.a_c0 = prob[4];
+    d.b_r0 = prob[5];
+    d.b_c0 = prob[6];
+    d.c_r0 = prob[7];
+    d.c_c0 = prob[8];
+    d.exec_level = prob[9];
+    d.lower = prob[10];
+    d.alpha = alpha;
+    d.beta = beta;
+    d.b_buf = -1;
+    if (d.m < 1 || d.n < 1 || d.k < 1) return TC_INVALID_ARGUMENT;
+    if (!tc_device_available()) return TC_NO_DEVICE;
+    DevCtx c{};
+    c.ldw = ldw;
+    c.b16 = static_cast<__half*>(b16);
+    c.b32 = static_cast<float*>(b32);
+    c.b64 = static_cast<double*>(b64);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    unsigned long long* words = nullptr;
+    if (cudaMallocAsync(&words, 64, s) != cudaSuccess) return TC_CUDA_ERROR;
+    cudaMemsetAsync(words, 0xFF, 64, s);
+    c.status = words;
+    init_tc_attributes();
+    init_mma32w_attributes();
+    std::vector<DevProb> v{d};
+    std::vector<unsigned char> host;
+    int tiles = 0;
+    const bool tc = gclass == GC_TC16 || gclass == GC_TC32;
+    std::string err;
+    if (tc) {
+        tiles = tc_build_probs(c, gclass == GC_TC32 ? KIND_TF32X3 : KIND_F16, v, host, &err);
+        if (tiles <= 0) {
+            cudaFreeAsync(words, s);
+            set_last_error("tc_build_probs: " + err);
+            return TC_INVALID_ARGUMENT;
+        }
+    } else {
+        tiles = gclass == GC_MMA32W ? simt_tiles(v, M32W_ROWS, 256) : simt_tiles(v, gclass == GC_MMA32 ? M32_TILE : 0);
+        host.assign(reinterpret_cast<unsigned char*>(v.data()), reinterpret_cast<unsigned char*>(v.data() + 1));
+    }
+    void* dprob = nullptr;
+    if (cudaMallocAsync(&dprob, host.size(), s) != cudaSuccess) return TC_CUDA_ERROR;
+    cudaMemcpyAsync(dprob, host.data(), host.size(), cudaMemcpyHostToDevice, s);
+    if (tc) launch_gemm_tc(c, gclass == GC_TC32 ? KIND_TF32X3 : KIND_F16, dprob, 1, tiles, s);
+    else launch_gemm_simt(c, gclass, static_cast<DevProb*>(dprob), 1, tiles, s);
+    cudaFreeAsync(dprob, s);
+    cudaFreeAsync(words, s);
+    const cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+        set_last_error(cudaGetErrorString(e));
+        return TC_CUDA_ERROR;
+    }
+    return TC_OK;
+}
+
+// process-wide kernel settings (development / A-B measurements)
+extern "C" int tc_set_global_option(const char* key, int value) {
+    if (!key) return TC_INVALID_ARGUMENT;
+    if (tc_set_option(key, value)) return TC_OK;
+    set_last_error(std::string("unknown global option '") + key + "'");
+    return TC_INVALID_ARGUMENT;
+}

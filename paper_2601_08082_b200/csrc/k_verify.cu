@@ -175,64 +175,155 @@ __global__ void __launch_bounds__(VT) k_potrs_diaginv(PotrsArgs a) {
 // forward y = L^-1 b / backward x = L^-T y, in place.  Persistent CTAs claim
 // tickets t -> (block index t / P, problem t % P): every problem's blocks are
 // claimed in chain order, so a CTA only ever waits on blocks already claimed
-// by running CTAs.  Block I accumulates L(I,J) y_J (forward) or L(J,I) x_J
-// (backward) over the finished J as their flags appear -- the L reads are
-// issued before each wait, off the chain -- then y_I = W_I (b_I - sum) /
-// x_I = W_I^T (y_I - sum): a 64x64 product, no dependent chain.
+// by running CTAs.  Block I accumulates L(I,J) y_J (forward) or L(J,I)^T x_J
+// (backward) over the finished J as their flags appear -- the L tile of the
+// next J is in flight while the CTA waits for the current one -- then
+// y_I = W_I (b_I - sum) / x_I = W_I^T (y_I - sum): a 64x64 product from
+// shared memory (W_I staged off the chain), no dependent chain.
+//
+// HBM access (L read once per sweep, n(n+1)/2 * 8 bytes): every
+// warp load instruction reads 512 contiguous bytes of one column of L as 16-
+// byte vectors.  Forward: the block's rows are contiguous within a column, so
+// lanes run along the rows (thread = 2 rows x 8 columns of the 64-wide tile).
+// Backward: the tile L(J, I) is read along its columns too -- lanes run along
+// J's rows (k), each warp owns 8 of I's columns and reduces them with
+// shuffles at the end -- instead of striding by ldl across lanes.
 template <bool BWD>
-__global__ void __launch_bounds__(256) k_potrs_sweep(PotrsArgs a) {
+__global__ void __launch_bounds__(256, 2) k_potrs_sweep(PotrsArgs a) {
     const int n = a.n, nb = (n + VT - 1) / VT, P = a.nsys * a.nrhs;
     __shared__ int sT;
-    __shared__ double part[4][VT];
+    __shared__ __align__(16) double Ws[VT][VT + 2];
+    __shared__ double part[8][VT];
     __shared__ double rhs[VT];
-    const int r = threadIdx.x & 63, q = threadIdx.x >> 6;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // forward: rows 2*rp, 2*rp+1 of the block, columns kq*8 .. +8 of a tile
+    // backward: rows 2*lane, 2*lane+1 of tile J, columns warp*8 .. +8 of block I
+    const int rp = tid & 31, kq = tid >> 5;
     const long long ldl = a.ldl;
     for (;;) {
-        if (threadIdx.x == 0) sT = atomicAdd(a.ticket, 1);
+        if (tid == 0) sT = atomicAdd(a.ticket, 1);
         __syncthreads();
         const int t = sT;
         if (t >= nb * P) break;
         const int p = t % P, sys = p / a.nrhs, rr = p % a.nrhs;
         const int I = BWD ? nb - 1 - t / P : t / P;
-        const double* Lm = potrs_L(a, sys);
+        const double* __restrict__ Lm = potrs_L(a, sys);
         double* y = potrs_B(a, sys) + rr * a.ldb;
         int* fl = a.flags + size_t(p) * nb;
-        const int i0 = I * VT, rows = min(VT, n - i0), gi = i0 + r;
-        // this block's W segment does not depend on the chain: load it first
-        const double* Wi = a.W + (size_t(sys) * nb + I) * VT * VT;
-        double wv[16];
+        const int i0 = I * VT, rows = min(VT, n - i0);
+        const bool vec = ((ldl & 1) == 0) && ((reinterpret_cast<uintptr_t>(Lm) & 15) == 0);
+        // W_I into shared memory (off the chain; read after the last wait)
+        {
+            const double* Wi = a.W + (size_t(sys) * nb + I) * VT * VT;
+            for (int e = tid; e < VT * VT / 2; e += 256) {
+                const double2 w = reinterpret_cast<const double2*>(Wi)[e];
+                const int r = (2 * e) / VT, c = (2 * e) % VT;
+                Ws[r][c] = w.x;
+                Ws[r][c + 1] = w.y;
+            }
+        }
+        const int nsteps = BWD ? nb - 1 - I : I;
+        // one 64x64 tile of L as 8 double2 per thread
+        auto load_tile = [&](int J, double2* lv) {
+            const int k0 = J * VT;
 #pragma unroll
-        for (int kk = 0; kk < 16; ++kk) wv[kk] = BWD ? Wi[(q * 16 + kk) * VT + r] : Wi[r * VT + q * 16 + kk];
-        double acc = 0.0;
-        for (int step = 0; step < (BWD ? nb - 1 - I : I); ++step) {
+            for (int kk = 0; kk < 8; ++kk) {
+                // forward: L(i0 + 2rp + {0,1}, k0 + kq*8 + kk); backward: L(k0 + 2lane + {0,1}, i0 + warp*8 + kk)
+                const int row = BWD ? k0 + 2 * lane : i0 + 2 * rp;
+                const int col = BWD ? i0 + warp * 8 + kk : k0 + kq * 8 + kk;
+                const double* src = Lm + (long long)col * ldl + row;
+                if (col < n && row + 1 < n && vec) {
+                    lv[kk] = __ldcs(reinterpret_cast<const double2*>(src));
+                } else {
+                    lv[kk].x = (col < n && row < n) ? __ldcs(src) : 0.0;
+                    lv[kk].y = (col < n && row + 1 < n) ? __ldcs(src + 1) : 0.0;
+                }
+            }
+        };
+        double acc0 = 0.0, acc1 = 0.0;  // forward: rows 2rp, 2rp+1
+        double accb[8];                 // backward: columns warp*8 + kk
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) accb[kk] = 0.0;
+        double2 cur[8], nxt[8];
+        if (nsteps > 0) load_tile(BWD ? nb - 1 : 0, cur);
+        for (int step = 0; step < nsteps; ++step) {
             const int J = BWD ? nb - 1 - step : step;
-            const int k0 = J * VT + q * 16;
-            double lv[16];
-#pragma unroll
-            for (int kk = 0; kk < 16; ++kk)
-                lv[kk] = BWD ? ((gi < n && k0 + kk < n) ? Lm[(long long)gi * ldl + k0 + kk] : 0.0)
-                             : (gi < n ? Lm[(long long)(k0 + kk) * ldl + gi] : 0.0);
-            if (threadIdx.x == 0)
+            if (step + 1 < nsteps) load_tile(BWD ? J - 1 : J + 1, nxt);
+            if (tid == 0)
                 while (ld_acquire(fl + J) == 0) {
                 }
             __syncthreads();
+            const int k0 = J * VT;
+            if (!BWD) {
 #pragma unroll
-            for (int kk = 0; kk < 16; ++kk)
-                if (!BWD || k0 + kk < n) acc = fma(lv[kk], __ldcg(y + k0 + kk), acc);
+                for (int kk = 0; kk < 8; ++kk) {
+                    const int k = k0 + kq * 8 + kk;
+                    const double yk = k < n ? __ldcg(y + k) : 0.0;
+                    acc0 = fma(cur[kk].x, yk, acc0);
+                    acc1 = fma(cur[kk].y, yk, acc1);
+                }
+            } else {
+                const int k = k0 + 2 * lane;
+                const double x0 = k < n ? __ldcg(y + k) : 0.0;
+                const double x1 = k + 1 < n ? __ldcg(y + k + 1) : 0.0;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) accb[kk] = fma(cur[kk].y, x1, fma(cur[kk].x, x0, accb[kk]));
+            }
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) cur[kk] = nxt[kk];
         }
-        part[q][r] = acc;
-        __syncthreads();
-        if (threadIdx.x < VT) rhs[r] = r < rows ? y[gi] - (part[0][r] + part[1][r] + part[2][r] + part[3][r]) : 0.0;
-        __syncthreads();
-        double s = 0.0;
+        if (!BWD) {
+            part[kq][2 * rp] = acc0;
+            part[kq][2 * rp + 1] = acc1;
+        } else {
 #pragma unroll
-        for (int kk = 0; kk < 16; ++kk) s = fma(wv[kk], rhs[q * 16 + kk], s);
-        part[q][r] = s;
+            for (int kk = 0; kk < 8; ++kk) {
+                double v = accb[kk];
+#pragma unroll
+                for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (lane == 0) part[0][warp * 8 + kk] = v;
+            }
+        }
         __syncthreads();
-        if (threadIdx.x < VT && r < rows) y[gi] = part[0][r] + part[1][r] + part[2][r] + part[3][r];
+        if (tid < VT) {
+            double sum = 0.0;
+            if (!BWD) {
+#pragma unroll
+                for (int g = 0; g < 8; ++g) sum += part[g][tid];
+            } else {
+                sum = part[0][tid];
+            }
+            rhs[tid] = tid < rows ? __ldcg(y + i0 + tid) - sum : 0.0;
+        }
+        __syncthreads();
+        // y_I = W_I rhs (forward) / x_I = W_I^T rhs (backward); thread: rows
+        // 2rp, 2rp+1, terms kq*8 .. +8
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+            const int c = kq * 8 + kk;
+            const double r = rhs[c];
+            if (!BWD) {
+                s0 = fma(Ws[2 * rp][c], r, s0);
+                s1 = fma(Ws[2 * rp + 1][c], r, s1);
+            } else {
+                s0 = fma(Ws[c][2 * rp], r, s0);
+                s1 = fma(Ws[c][2 * rp + 1], r, s1);
+            }
+        }
+        __syncthreads();
+        part[kq][2 * rp] = s0;
+        part[kq][2 * rp + 1] = s1;
+        __syncthreads();
+        if (tid < rows) {
+            double v = 0.0;
+#pragma unroll
+            for (int g = 0; g < 8; ++g) v += part[g][tid];
+            y[i0 + tid] = v;
+        }
         __threadfence();
         __syncthreads();
-        if (threadIdx.x == 0) st_release(fl + I, 1);
+        if (tid == 0) st_release(fl + I, 1);
     }
 }
 

@@ -79,6 +79,8 @@ int tc_build_probs(const DevCtx& c, int kind, const std::vector<DevProb>& probs,
 void launch_gemm_tc(const DevCtx& c, int kind, const void* d_probs, int nprob, int tiles, cudaStream_t s,
                     int max_ctas = 0, int tiles_per_cta = 0);
 bool tc_supported();
+// process-wide tensor-core GEMM settings ("tc_kchunk"); false: unknown key
+bool tc_set_option(const std::string& key, int value);
 
 // standalone block operations on column-major doubles (k_blockops.cu)
 void bo_round(double* a, long long lda, int m, int n, int lv, int lower, cudaStream_t s);

@@ -119,3 +119,34 @@ def test_batch_solve_orders_agree(tc, oracle):
         assert np.array_equal(np.tril(out[0][0][k].T), np.tril(out[1][0][k].T))
         if k != 3:
             assert np.array_equal(out[0][1][k], out[1][1][k])
+
+
+@pytest.mark.gpu
+def test_c4_unit_matches_golden(tc):
+    """BASELINE config C4's unit system at full size (N=16384, b=256,
+    [F16, F16, F16, F32], spd_generate seeds 0 and 1 -- bit-identical device
+    generation) through tc_batch_run: status and flops exactly, backward
+    error and the solve residual for b = A * ones within 2x of the oracle's
+    (tests/golden/c4.json, made by tests/golden/make_golden_c4.py)"""
+    import json
+    import torch
+    with open(os.path.join(os.path.dirname(__file__), "golden", "c4.json")) as f:
+        gold = json.load(f)
+    n, b, cfg = gold["n"], gold["b"], gold["config"]
+    assert tuple(tc.flop_breakdown(n, b, cfg).as_tuple()) == tuple(gold["cases"][0]["flops"])
+    batch = tc.Batch(n, b, cfg, True, concurrency=2)
+    a_list, keep, rhs, rhs0 = [], [], [], []
+    for case in gold["cases"]:
+        a = tc.spd_generate_device(n, case["seed"])
+        bv = a.cpu().numpy().T.sum(axis=1)  # b = A * ones exactly as the golden script sums it
+        a_list.append(a)
+        keep.append(a.clone())
+        rhs.append(torch.from_numpy(bv).reshape(1, n).to("cuda"))
+        rhs0.append(rhs[-1].clone())
+    st = batch.run(a_list, rhs)
+    for k, case in enumerate(gold["cases"]):
+        assert st[k] == case["status"] == "ok"
+        rel = tc.factorization_error_device(keep[k], a_list[k])
+        res = tc.solve_residual_device(keep[k], rhs[k][0].contiguous(), rhs0[k][0].contiguous())
+        assert rel <= 2 * case["rel_error"], (case["seed"], rel, case["rel_error"])
+        assert res <= 2 * case["potrs_residual"], (case["seed"], res, case["potrs_residual"])

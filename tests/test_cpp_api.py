@@ -88,3 +88,61 @@ def test_report_writers_match_python_mirror(tmp_path):
     n = 65536
     assert plan_cpp.startswith("n=65536 leaf=256 config=[F16, F16, F16, F32] total_flops=%d\n" % (n * (n + 1) * (2 * n + 1) // 6))
     assert "off-diagonal share (TRSM+SYRK+GEMM): " in plan_cpp
+
+
+MTX = os.path.join(ROOT, "tests", "golden", "plate2d_24.mtx")
+MTX_CONFIGS = ("[F16, F32]", "[F16, F16, F32]", "Pure F64")
+
+
+def _build_mtx_factor(tmp_path):
+    exe = tmp_path / "mtx_factor"
+    subprocess.run(["g++", "-std=c++20", "-O2", "-I" + os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "mtx_factor.cpp"), "-L" + PKG, "-ltreechol", "-ltreechol_b200",
+                    "-Wl,-rpath," + PKG, "-o", str(exe)], check=True)
+    return str(exe)
+
+
+def _mtx_dense():
+    """the fixture densified by scipy (independent of the library's reader)"""
+    import numpy as np
+    import scipy.io
+    return np.asfortranarray(scipy.io.mmread(MTX).toarray(), dtype=np.float64)
+
+
+def test_matrix_market_reader_matches_scipy(tmp_path):
+    """load_matrix_market (reference mtx.cpp:60-159 semantics: coordinate
+    real symmetric, 1-based, mirrored) densifies the fixture exactly as
+    scipy.io.mmread does"""
+    import numpy as np
+    r = subprocess.run([_build_mtx_factor(tmp_path), MTX, "--checksum"], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 0, r.stderr
+    n, s, s2, w = r.stdout.strip().split("|")
+    a = _mtx_dense()
+    i = np.arange(a.shape[0])[:, None] + 1.0
+    j = np.arange(a.shape[1])[None, :] + 2.0
+    assert int(n[2:]) == a.shape[0] == 576
+    tol = 1e-14 * float(np.abs(a).sum())  # the two summation orders differ
+    assert float(s) == pytest.approx(a.sum(), abs=tol)
+    assert float(s2) == pytest.approx((a * a).sum(), rel=1e-14)
+    assert float(w) == pytest.approx((i * j * a).sum(), abs=tol * a.shape[0] ** 2 * 4)
+
+
+@pytest.mark.gpu
+def test_matrix_market_to_device_matches_oracle(tmp_path, oracle):
+    """Matrix Market -> device: the fixture read by
+    load_matrix_market and factored by factor_matrix (tc_potrf_host: H2D, the
+    CUDA graph, D2H) gives the oracle's status and flops, and a backward error
+    within 2x of the oracle's on the same matrix (scipy-densified)"""
+    from pyoracle import parse_levels
+    b = 128
+    r = subprocess.run([_build_mtx_factor(tmp_path), MTX, str(b)] + list(MTX_CONFIGS), capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    rows = [ln.split("|") for ln in r.stdout.strip().splitlines()[1:]]
+    assert len(rows) == len(MTX_CONFIGS)
+    a = _mtx_dense()
+    for cfg, (cfg_out, status, rel, total) in zip(MTX_CONFIGS, rows):
+        st_o, det_o, _, rel_o, fl_o = oracle.factor(a, b, parse_levels(cfg))
+        assert status == st_o == "ok", (cfg, status, st_o, det_o)
+        assert int(total) == fl_o.total()
+        assert float(rel) <= 2 * rel_o, (cfg, float(rel), rel_o)
