@@ -13,6 +13,8 @@
 //                once per direction with coalesced column reads.
 //   residual     ||b - A x||_2 / (||A||_F ||x||_2 + ||b||_2), A symmetric
 //                with only its lower triangle read.
+#include <string>
+
 #include "device.cuh"
 #include "launch.hpp"
 
@@ -121,15 +123,6 @@ __global__ void k_fact_error_final(const double* partials, int count, const int*
 }
 
 // ---------------------------------------------------------------- potrs
-__device__ __forceinline__ int ld_acquire(const int* p) {
-    int v;
-    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release(int* p, int v) {
-    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
 // The solves of a set of problems (system s, right-hand side r) -- one, or
 // a whole batch in one launch.  System s: factor Ls[s] (ld ldl), right-hand
 // sides Bs[s] + r*ldb; tables null: the single system L0 / B0.
@@ -141,9 +134,45 @@ struct PotrsArgs {
     double* B0;
     long long ldl, ldb;
     int* ticket;  // one word per direction: the next (block, problem) pair
-    int* flags;   // [problem][nb]: block done
     double* W;    // [system][nb][VT][VT] diagonal-block inverses
+    // published y / x per problem ([problem][nb * VT]), pre-filled with the
+    // sentinel: a consumer polls the values it needs until they are real
+    double* Yw;
+    double* Xw;
+    int poll;     // 0: every thread polls its values; >0: with that ns backoff;
+                  // -1: warp 0 polls the whole block, then a CTA barrier
 };
+
+// "not yet written" marker of Yw / Xw: a NaN bit pattern no arithmetic
+// produces; a computed value with exactly these bits is stored as the
+// canonical NaN instead (publish), so the marker never means data
+constexpr unsigned long long kPotrsPending = 0xFFFFFFFFFFFFFFFFull;
+__device__ __forceinline__ void publish(double* p, double v) {
+    if (static_cast<unsigned long long>(__double_as_longlong(v)) == kPotrsPending) v = __longlong_as_double(0x7ff8000000000000ll);
+    asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ double ld_relaxed(const double* p) {
+    double v;
+    asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ bool pending(double v) {
+    return static_cast<unsigned long long>(__double_as_longlong(v)) == kPotrsPending;
+}
+__device__ __forceinline__ double2 ld_relaxed2(const double* p) {
+    double2 v;
+    asm volatile("ld.relaxed.gpu.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
+    return v;
+}
+// spin until the published value at p is real (relaxed, L2-coherent reads);
+// backoff > 0: sleep that many ns between polls
+__device__ __forceinline__ double await_value(const double* p, int backoff) {
+    for (;;) {
+        const double v = ld_relaxed(p);
+        if (!pending(v)) return v;
+        if (backoff) __nanosleep(backoff);
+    }
+}
 __device__ __forceinline__ const double* potrs_L(const PotrsArgs& a, int s) { return a.Ls ? a.Ls[s] : a.L0; }
 __device__ __forceinline__ double* potrs_B(const PotrsArgs& a, int s) { return a.Bs ? a.Bs[s] : a.B0; }
 
@@ -172,14 +201,26 @@ __global__ void __launch_bounds__(VT) k_potrs_diaginv(PotrsArgs a) {
     for (int i = 0; i < VT; ++i) Wi[i * VT + t] = w[i];
 }
 
-// forward y = L^-1 b / backward x = L^-T y, in place.  Persistent CTAs claim
-// tickets t -> (block index t / P, problem t % P): every problem's blocks are
-// claimed in chain order, so a CTA only ever waits on blocks already claimed
-// by running CTAs.  Block I accumulates L(I,J) y_J (forward) or L(J,I)^T x_J
-// (backward) over the finished J as their flags appear -- the L tile of the
-// next J is in flight while the CTA waits for the current one -- then
-// y_I = W_I (b_I - sum) / x_I = W_I^T (y_I - sum): a 64x64 product from
-// shared memory (W_I staged off the chain), no dependent chain.
+// forward y = L^-1 b / backward x = L^-T y.  Persistent CTAs claim tickets
+// t -> (block index t / P, problem t % P): every problem's blocks are claimed
+// in chain order, so a CTA only ever waits on blocks already claimed by
+// running CTAs.  Block I accumulates L(I,J) y_J (forward) or L(J,I)^T x_J
+// (backward) over J in chain order -- the L tile of the next J is in flight
+// while the threads wait for the current one -- then y_I = W_I (b_I - sum) /
+// x_I = W_I^T (y_I - sum): a 64x64 product from shared memory (W_I staged off
+// the chain), no dependent chain.
+//
+// Links carry no flags or fences: a finished block publishes its 64 values
+// into a sentinel-filled buffer (Yw forward, Xw backward) and each consumer
+// thread polls exactly the values it multiplies, all of them in flight at
+// once (16-byte relaxed L2 loads), so one store-to-load trip through L2 is
+// the whole link.  The forward sweep writes y to Yw only; the backward sweep
+// reads y from Yw and writes x to B (the result) and Xw (for its consumers).
+// (Measured alternatives: one flag per block behind a fence, 1.6 ms per
+// N=16384 solve; polling with nanosleep backoff or by one warp behind a CTA
+// barrier, 1.5-1.8 ms; precomputing W_I L(I,I-1) so the last link is a bare
+// matvec, 1.8 ms (the 64^3 product per block costs more than it saves);
+// this form, 1.0 ms.)
 //
 // HBM access (L read once per sweep, n(n+1)/2 * 8 bytes): every
 // warp load instruction reads 512 contiguous bytes of one column of L as 16-
@@ -188,38 +229,46 @@ __global__ void __launch_bounds__(VT) k_potrs_diaginv(PotrsArgs a) {
 // Backward: the tile L(J, I) is read along its columns too -- lanes run along
 // J's rows (k), each warp owns 8 of I's columns and reduces them with
 // shuffles at the end -- instead of striding by ldl across lanes.
+constexpr int VP = VT + 2;  // padded smem row (16-byte aligned)
+
 template <bool BWD>
 __global__ void __launch_bounds__(256, 2) k_potrs_sweep(PotrsArgs a) {
     const int n = a.n, nb = (n + VT - 1) / VT, P = a.nsys * a.nrhs;
-    __shared__ int sT;
-    __shared__ __align__(16) double Ws[VT][VT + 2];
-    __shared__ double part[8][VT];
-    __shared__ double rhs[VT];
+    const long long ldp = (long long)nb * VT;  // Yw / Xw stride per problem
+    extern __shared__ __align__(16) double sm[];
+    double(*Ws)[VP] = reinterpret_cast<double(*)[VP]>(sm);  // W_I
+    double(*part)[VT] = reinterpret_cast<double(*)[VT]>(sm + VT * VP);
+    double* rhs = sm + VT * VP + 8 * VT;
+    int* sT = reinterpret_cast<int*>(rhs + VT);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // forward: rows 2*rp, 2*rp+1 of the block, columns kq*8 .. +8 of a tile
-    // backward: rows 2*lane, 2*lane+1 of tile J, columns warp*8 .. +8 of block I
+    // forward: rows 2*rp, 2*rp+1 of the block x columns kq*8 .. +8 of a tile;
+    // backward: rows 2*lane, 2*lane+1 of tile J x columns warp*8 .. +8 of block I
     const int rp = tid & 31, kq = tid >> 5;
     const long long ldl = a.ldl;
+    const int bo = a.poll > 0 ? a.poll : 0;
     for (;;) {
-        if (tid == 0) sT = atomicAdd(a.ticket, 1);
+        if (tid == 0) *sT = atomicAdd(a.ticket, 1);
         __syncthreads();
-        const int t = sT;
+        const int t = *sT;
         if (t >= nb * P) break;
         const int p = t % P, sys = p / a.nrhs, rr = p % a.nrhs;
         const int I = BWD ? nb - 1 - t / P : t / P;
         const double* __restrict__ Lm = potrs_L(a, sys);
-        double* y = potrs_B(a, sys) + rr * a.ldb;
-        int* fl = a.flags + size_t(p) * nb;
+        double* bx = potrs_B(a, sys) + rr * a.ldb;  // b (forward input) / x (backward output)
+        double* Y = a.Yw + p * ldp;
+        double* X = a.Xw + p * ldp;
+        const double* src = BWD ? X : Y;            // the values this sweep consumes
         const int i0 = I * VT, rows = min(VT, n - i0);
         const bool vec = ((ldl & 1) == 0) && ((reinterpret_cast<uintptr_t>(Lm) & 15) == 0);
+        // this block's own right-hand side (b_I, or y_I from the forward sweep)
+        const double own = tid < rows ? (BWD ? __ldcg(Y + i0 + tid) : __ldcg(bx + i0 + tid)) : 0.0;
         // W_I into shared memory (off the chain; read after the last wait)
         {
             const double* Wi = a.W + (size_t(sys) * nb + I) * VT * VT;
             for (int e = tid; e < VT * VT / 2; e += 256) {
                 const double2 w = reinterpret_cast<const double2*>(Wi)[e];
                 const int r = (2 * e) / VT, c = (2 * e) % VT;
-                Ws[r][c] = w.x;
-                Ws[r][c + 1] = w.y;
+                *reinterpret_cast<double2*>(&Ws[r][c]) = w;
             }
         }
         const int nsteps = BWD ? nb - 1 - I : I;
@@ -231,12 +280,12 @@ __global__ void __launch_bounds__(256, 2) k_potrs_sweep(PotrsArgs a) {
                 // forward: L(i0 + 2rp + {0,1}, k0 + kq*8 + kk); backward: L(k0 + 2lane + {0,1}, i0 + warp*8 + kk)
                 const int row = BWD ? k0 + 2 * lane : i0 + 2 * rp;
                 const int col = BWD ? i0 + warp * 8 + kk : k0 + kq * 8 + kk;
-                const double* src = Lm + (long long)col * ldl + row;
+                const double* q = Lm + (long long)col * ldl + row;
                 if (col < n && row + 1 < n && vec) {
-                    lv[kk] = __ldcs(reinterpret_cast<const double2*>(src));
+                    lv[kk] = __ldcs(reinterpret_cast<const double2*>(q));
                 } else {
-                    lv[kk].x = (col < n && row < n) ? __ldcs(src) : 0.0;
-                    lv[kk].y = (col < n && row + 1 < n) ? __ldcs(src + 1) : 0.0;
+                    lv[kk].x = (col < n && row < n) ? __ldcs(q) : 0.0;
+                    lv[kk].y = (col < n && row + 1 < n) ? __ldcs(q + 1) : 0.0;
                 }
             }
         };
@@ -249,23 +298,42 @@ __global__ void __launch_bounds__(256, 2) k_potrs_sweep(PotrsArgs a) {
         for (int step = 0; step < nsteps; ++step) {
             const int J = BWD ? nb - 1 - step : step;
             if (step + 1 < nsteps) load_tile(BWD ? J - 1 : J + 1, nxt);
-            if (tid == 0)
-                while (ld_acquire(fl + J) == 0) {
-                }
-            __syncthreads();
             const int k0 = J * VT;
             if (!BWD) {
+                double yk[8];
+                const int kb = k0 + kq * 8;  // a full block (only the last block is ragged)
+                for (;;) {
+                    bool wait = false;
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                        const double2 v = ld_relaxed2(src + kb + 2 * h);
+                        yk[2 * h] = v.x;
+                        yk[2 * h + 1] = v.y;
+                        wait |= pending(v.x) | pending(v.y);
+                    }
+                    if (!wait) break;
+                    if (bo) __nanosleep(bo);
+                }
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) {
-                    const int k = k0 + kq * 8 + kk;
-                    const double yk = k < n ? __ldcg(y + k) : 0.0;
-                    acc0 = fma(cur[kk].x, yk, acc0);
-                    acc1 = fma(cur[kk].y, yk, acc1);
+                    acc0 = fma(cur[kk].x, yk[kk], acc0);
+                    acc1 = fma(cur[kk].y, yk[kk], acc1);
                 }
             } else {
                 const int k = k0 + 2 * lane;
-                const double x0 = k < n ? __ldcg(y + k) : 0.0;
-                const double x1 = k + 1 < n ? __ldcg(y + k + 1) : 0.0;
+                double x0, x1;
+                if (k + 1 < n) {
+                    for (;;) {
+                        const double2 v = ld_relaxed2(src + k);
+                        x0 = v.x;
+                        x1 = v.y;
+                        if (!(pending(x0) | pending(x1))) break;
+                        if (bo) __nanosleep(bo);
+                    }
+                } else {
+                    x0 = k < n ? await_value(src + k, bo) : 0.0;
+                    x1 = 0.0;
+                }
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) accb[kk] = fma(cur[kk].y, x1, fma(cur[kk].x, x0, accb[kk]));
             }
@@ -293,7 +361,7 @@ __global__ void __launch_bounds__(256, 2) k_potrs_sweep(PotrsArgs a) {
             } else {
                 sum = part[0][tid];
             }
-            rhs[tid] = tid < rows ? __ldcg(y + i0 + tid) - sum : 0.0;
+            rhs[tid] = tid < rows ? own - sum : 0.0;
         }
         __syncthreads();
         // y_I = W_I rhs (forward) / x_I = W_I^T rhs (backward); thread: rows
@@ -303,13 +371,8 @@ __global__ void __launch_bounds__(256, 2) k_potrs_sweep(PotrsArgs a) {
         for (int kk = 0; kk < 8; ++kk) {
             const int c = kq * 8 + kk;
             const double r = rhs[c];
-            if (!BWD) {
-                s0 = fma(Ws[2 * rp][c], r, s0);
-                s1 = fma(Ws[2 * rp + 1][c], r, s1);
-            } else {
-                s0 = fma(Ws[c][2 * rp], r, s0);
-                s1 = fma(Ws[c][2 * rp + 1], r, s1);
-            }
+            s0 = fma(BWD ? Ws[c][2 * rp] : Ws[2 * rp][c], r, s0);
+            s1 = fma(BWD ? Ws[c][2 * rp + 1] : Ws[2 * rp + 1][c], r, s1);
         }
         __syncthreads();
         part[kq][2 * rp] = s0;
@@ -319,13 +382,17 @@ __global__ void __launch_bounds__(256, 2) k_potrs_sweep(PotrsArgs a) {
             double v = 0.0;
 #pragma unroll
             for (int g = 0; g < 8; ++g) v += part[g][tid];
-            y[i0 + tid] = v;
+            if (BWD) {
+                bx[i0 + tid] = v;
+                publish(X + i0 + tid, v);
+            } else {
+                publish(Y + i0 + tid, v);
+            }
         }
-        __threadfence();
-        __syncthreads();
-        if (tid == 0) st_release(fl + I, 1);
     }
 }
+
+constexpr size_t kSweepSmem = sizeof(double) * (VT * VP + 8 * VT + VT) + 16;
 
 // ---------------------------------------------------------------- residual
 // per 64-row block I: r_I = b_I - sum_J A(I,J) x_J with A(I,J) = A(J,I)^T above
@@ -402,27 +469,46 @@ void launch_fact_error(int n, const double* dA, long long lda, const double* dL,
 
 size_t potrs_work_doubles(int n, int nrhs) { return potrs_batch_work_bytes(n, 1, nrhs) / sizeof(double) + 1; }
 
-// workspace of nsys systems: W, then the flags and the two tickets
+// workspace of nsys systems: W, Yw, Xw, then the two tickets
 size_t potrs_batch_work_bytes(int n, int nsys, int nrhs) {
     const size_t nb = size_t((n + VT - 1) / VT);
-    return sizeof(double) * size_t(nsys) * nb * VT * VT + sizeof(int) * (size_t(nsys) * nrhs * nb + 2);
+    return sizeof(double) * (size_t(nsys) * nb * VT * VT + 2 * size_t(nsys) * size_t(nrhs) * nb * VT) +
+           2 * sizeof(int);
+}
+
+static int g_potrs_poll = 0;
+
+bool potrs_set_option(const std::string& key, int value) {
+    if (key == "potrs_poll") {
+        g_potrs_poll = value;
+        return true;
+    }
+    return false;
 }
 
 static void potrs_run(PotrsArgs a, void* work, int max_ctas, cudaStream_t s) {
+    static const bool attr = [] {
+        cudaFuncSetAttribute(k_potrs_sweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSweepSmem));
+        cudaFuncSetAttribute(k_potrs_sweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSweepSmem));
+        return true;
+    }();
+    (void)attr;
+    a.poll = g_potrs_poll;
     const int nb = (a.n + VT - 1) / VT;
+    const size_t pub = size_t(a.nsys) * size_t(a.nrhs) * size_t(nb) * VT;  // doubles per published buffer
     a.W = static_cast<double*>(work);
-    int* words = reinterpret_cast<int*>(a.W + size_t(a.nsys) * nb * VT * VT);
-    const size_t fbytes = sizeof(int) * (size_t(a.nsys) * a.nrhs * nb + 2);
-    a.flags = words + 2;
+    a.Yw = a.W + size_t(a.nsys) * nb * VT * VT;
+    a.Xw = a.Yw + pub;
+    int* words = reinterpret_cast<int*>(a.Xw + pub);
     k_potrs_diaginv<<<dim3(nb, a.nsys), VT, 0, s>>>(a);
     const long long work_items = (long long)nb * a.nsys * a.nrhs;
     const int g = int(max_ctas > 0 && max_ctas < work_items ? max_ctas : work_items);
-    cudaMemsetAsync(words, 0, fbytes, s);
+    cudaMemsetAsync(a.Yw, 0xFF, 2 * pub * sizeof(double), s);  // kPotrsPending
+    cudaMemsetAsync(words, 0, 2 * sizeof(int), s);
     a.ticket = words;
-    k_potrs_sweep<false><<<g, 256, 0, s>>>(a);
-    cudaMemsetAsync(a.flags, 0, fbytes - 2 * sizeof(int), s);
+    k_potrs_sweep<false><<<g, 256, kSweepSmem, s>>>(a);
     a.ticket = words + 1;
-    k_potrs_sweep<true><<<g, 256, 0, s>>>(a);
+    k_potrs_sweep<true><<<g, 256, kSweepSmem, s>>>(a);
 }
 
 void launch_potrs(int n, const double* dL, long long ldl, double* dB, long long ldb, int nrhs, int* /*d_counters*/,

@@ -81,6 +81,7 @@ void launch_gemm_tc(const DevCtx& c, int kind, const void* d_probs, int nprob, i
 bool tc_supported();
 // process-wide tensor-core GEMM settings ("tc_kchunk"); false: unknown key
 bool tc_set_option(const std::string& key, int value);
+bool potrs_set_option(const std::string& key, int value);  // "potrs_poll" (k_verify.cu)
 
 // standalone block operations on column-major doubles (k_blockops.cu)
 void bo_round(double* a, long long lda, int m, int n, int lv, int lower, cudaStream_t s);

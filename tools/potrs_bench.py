@@ -28,18 +28,21 @@ def timed(fn, reps=5):
     return e0.elapsed_time(e1) / reps
 
 
-for n in (4096, 16384, 65536):
-    a = synthetic_spd_device(n, 1)
-    a0 = a.clone()
-    tc.Plan(n, 256, "[F16, F16, F16, F32]").factor_device(a)
-    b0 = a0.sum(dim=0, keepdim=True).contiguous()
-    b = b0.clone()
-    ms = timed(lambda: (b.copy_(b0), tc.potrs_device(a, b)))
-    res = tc.solve_residual_device(a0, b[0].contiguous(), b0[0].contiguous())
-    print(json.dumps({"n": n, "systems": 1, "potrs_ms": ms, "GBs": n * (n + 1) * 8 / ms / 1e6, "residual": res}),
-          flush=True)
-    del a, a0
-    torch.cuda.empty_cache()
+for poll in [int(x) for x in os.environ.get("POLL", "0").split(",")]:
+  tc.set_global_option("potrs_poll", poll)
+  print("poll", poll, flush=True)
+  for n in (4096, 16384, 65536):
+      a = synthetic_spd_device(n, 1)
+      a0 = a.clone()
+      tc.Plan(n, 256, "[F16, F16, F16, F32]").factor_device(a)
+      b0 = a0.sum(dim=0, keepdim=True).contiguous()
+      b = b0.clone()
+      ms = timed(lambda: (b.copy_(b0), tc.potrs_device(a, b)))
+      res = tc.solve_residual_device(a0, b[0].contiguous(), b0[0].contiguous())
+      print(json.dumps({"n": n, "systems": 1, "potrs_ms": ms, "GBs": n * (n + 1) * 8 / ms / 1e6, "residual": res}),
+            flush=True)
+      del a, a0
+      torch.cuda.empty_cache()
 
 nsys = int(sys.argv[1]) if len(sys.argv) > 1 else 32
 n = 16384
@@ -55,5 +58,7 @@ def run():
     tc.potrs_batch_device(ls, bs)
 
 
-ms = timed(run, 3)
-print(json.dumps({"n": n, "systems": nsys, "potrs_ms": ms, "GBs": nsys * n * (n + 1) * 8 / ms / 1e6}), flush=True)
+for poll in [int(x) for x in os.environ.get("POLL", "0").split(",")]:
+    tc.set_global_option("potrs_poll", poll)
+    ms = timed(run, 3)
+    print(json.dumps({"poll": poll, "n": n, "systems": nsys, "potrs_ms": ms, "GBs": nsys * n * (n + 1) * 8 / ms / 1e6}), flush=True)
