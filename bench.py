@@ -176,6 +176,15 @@ def cpu_baseline_sample(args):
 
 
 # --------------------------------------------------------------------- ours
+def allreduce_max(x: float, host: bool) -> float:
+    """max over ranks of a host float (device tensor on NCCL, CPU on gloo)"""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cpu" if host else "cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -183,9 +192,17 @@ def run_ours(args):
     import paper_2601_08082_b200 as tc
 
     ws, rank, local = dist_env()
-    torch.cuda.set_device(local)
+    ndev = torch.cuda.device_count()
+    # one process per GPU; with fewer GPUs than ranks (a dry run of --gpus N
+    # on a smaller box) ranks share devices and the host-side reductions go
+    # over gloo (NCCL refuses two ranks on one device)
+    shared = ws > ndev
+    torch.cuda.set_device(local % ndev)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     n, b = args.n, args.b
     peaks, peak_kind = measured_peaks()
 
@@ -218,9 +235,7 @@ def run_ours(args):
     ms = ev0.elapsed_time(ev1)
     st = plan.status()
     if ws > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = allreduce_max(ms, shared)
     flops = potrf_flops(n)
     value = ws * args.steps * flops / (ms * 1e-3) / 1e12
     ms_per_step = ms / args.steps
@@ -284,9 +299,7 @@ def run_ours(args):
                 raise SystemExit(f"e2e factorization failed: {st_h.status} {st_h.detail}")
         barrier()
         if ws > 1:
-            t = torch.tensor([e2e_s], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_s = float(t.item())
+            e2e_s = allreduce_max(e2e_s, shared)
         # lower triangle in leaf-column strips (the diagonal leaf squares whole),
         # both directions (Engine::enqueue_host)
         h2d = sum((n - j0) * min(b, n - j0) for j0 in range(0, n, b)) * 8
@@ -328,7 +341,7 @@ def run_ours(args):
     # all-reduce of the panel alpha, all-gather of the solved panel), at the
     # C3 size so it compares with the single-GPU value above
     c5 = None
-    if ws > 1 and args.c5_n > 0:
+    if ws > 1 and args.c5_n > 0 and not shared:
         from paper_2601_08082_b200.distributed import potrf_top_split, synthetic_pieces
         a11, a21, a22 = synthetic_pieces(args.c5_n, b, SEED, ws, rank)
         cache = {}
@@ -336,9 +349,7 @@ def run_ours(args):
         for it in range(3):  # the first call builds the plans
             res = potrf_top_split(args.c5_n, b, CFG, a11=a11.clone() if a11 is not None else None, a21_rows=a21,
                                   a22_rows=a22, cache=cache)
-            t = torch.tensor([res.device_ms], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            times.append(float(t.item()))
+            times.append(allreduce_max(res.device_ms, shared))
         ms5 = min(times[1:])
         c5 = {"workload": f"C5-style: one N={args.c5_n} factorization, top TRSM/SYRK row-split over {ws} GPUs, "
                           f"L11 broadcast + alpha all-reduce + panel all-gather over NCCL",
@@ -362,6 +373,7 @@ def run_ours(args):
                 "vs_baseline": None, "dtype": "f16 tensor-core (FP32 acc) / f32 / f64 per precision tree",
                 "data": "synthetic: spd_generate(65536, 42 + rank), bit-identical to analysis.cpp:12-28",
                 "config": {"workload": f"C3: N={n} b={b} {CFG}, quantize on, one factorization per step",
+                           "ranks_per_gpu": (ws + ndev - 1) // ndev,
                            "n": n, "b": b, "precision_tree": CFG,
                            "parallelism": f"independent systems x{ws}" if ws > 1 else "single",
                            "l2": "inputs (34 GB) larger than L2; no flush needed"},
@@ -417,7 +429,9 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=N_DEFAULT)
+    # (not --n: torchrun's own parser would take it for a prefix of --nnodes
+    # when this script re-launches itself under torchrun)
+    ap.add_argument("--size", dest="n", type=int, default=N_DEFAULT)
     ap.add_argument("--b", type=int, default=B_DEFAULT)
     ap.add_argument("--e2e-steps", dest="e2e_steps", type=int, default=2)
     ap.add_argument("--cpu-n", dest="cpu_n", type=int, default=1536)

@@ -280,6 +280,13 @@ int tc_debug_gemm(int gclass, int m, int n, int k, int lower, double beta, int e
  * Operands come from the operand level's buffer (b16 for FP16 classes, b32
  * for FP32 classes, b64 for SIMT F64), C from the exec level's buffer.
  * Synchronous.  Kernel-level parity tests (tests/test_gpu_kernels.py). */
+/* development: 15 %globaltimer stamps (ns) of CTA 0 of the last
+ * tc_debug_gemm launch (tcgen05 classes; 0 = not reached): entry, after
+ * setup, first TMA issued, first stage landed, accumulator ready, epilogue
+ * done, exit, then epilogue detail (C staged, computed, synced, stores
+ * issued) */
+int tc_debug_gemm_stamps(unsigned long long* out15);
+
 /* process-wide kernel settings for measurements: "tc_kchunk" = K chunk
  * (elements) of FP32-exec tensor-core accumulations, 0 = one accumulation.
  * Applies to plans built (graphs captured) afterwards. */

@@ -134,6 +134,7 @@ def _load():
         "tc_debug_gemm": (I, [I, I, I, I, I, D, I, I, C.POINTER(C.c_float)]),
         "tc_gemm_problem_device": (I, [I, P, P, P, C.c_longlong, PI, D, D, P]),
         "tc_set_global_option": (I, [C.c_char_p, I]),
+        "tc_debug_gemm_stamps": (I, [C.POINTER(C.c_uint64)]),
         "tc_plan_create_trsm": (I, [I, I, I, PI, I, I, C.POINTER(P)]),
         "tc_plan_create_syrk_rows": (I, [I, I, I, PI, I, I, I, C.POINTER(P)]),
         "tc_plan_set_external_absmax": (I, [P, D]),
@@ -760,6 +761,14 @@ def gemm_problem_device(gclass: str, b16, b32, b64, ldw: int, m: int, n: int, k:
     _raise(_lib.tc_gemm_problem_device(GEMM_CLASSES.index(gclass), None if b16 is None else _ptr(b16),
                                        None if b32 is None else _ptr(b32), None if b64 is None else _ptr(b64),
                                        int(ldw), pr, float(alpha), float(beta), _stream_ptr(stream)))
+
+
+def debug_gemm_stamps():
+    """ns offsets from kernel entry of CTA 0's phases in the last debug_gemm
+    launch: setup, first TMA, first stage, accumulator, epilogue, exit"""
+    arr = (C.c_uint64 * 15)()
+    _raise(_lib.tc_debug_gemm_stamps(arr))
+    return [int(arr[i]) - int(arr[0]) if arr[i] else None for i in range(1, 15)]
 
 
 def solve_residual_device(a_dev, x_dev, b_dev, n: int | None = None, stream=None) -> float:

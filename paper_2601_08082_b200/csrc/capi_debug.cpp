@@ -17,6 +17,17 @@ namespace tcb {
 void set_last_error(const std::string& msg);  // capi.cpp
 }
 
+static unsigned long long g_last_stamps[15];
+
+// %globaltimer stamps (ns) of CTA 0 of the last tc_debug_gemm launch:
+// entry, after setup, first TMA issued, first stage landed, accumulator
+// ready, epilogue done, exit (tcgen05 classes)
+extern "C" int tc_debug_gemm_stamps(unsigned long long* out7) {
+    if (!out7) return TC_INVALID_ARGUMENT;
+    for (int i = 0; i < 15; ++i) out7[i] = g_last_stamps[i];
+    return TC_OK;
+}
+
 extern "C" int tc_debug_gemm(int gclass, int m, int n, int k, int lower, double beta, int exec_level, int iters,
                              float* avg_us) {
     if (m < 1 || n < 1 || k < 1 || iters < 1 || !avg_us) return TC_INVALID_ARGUMENT;
@@ -28,13 +39,15 @@ extern "C" int tc_debug_gemm(int gclass, int m, int n, int k, int lower, double 
     unsigned long long* words = nullptr;
     const size_t elems = size_t(rows) * size_t(ldw);
     if (cudaMalloc(&buf, elems * (2 + 4 + 8)) != cudaSuccess) return TC_CUDA_ERROR;
-    cudaMalloc(&words, 64);
+    cudaMalloc(&words, 256);
     cudaMemset(buf, 0, elems * 14);
     cudaMemset(words, 0xFF, 8);
+    cudaMemset(words + 1, 0, 128);
     c.b16 = static_cast<__half*>(buf);
     c.b32 = reinterpret_cast<float*>(c.b16 + elems);
     c.b64 = reinterpret_cast<double*>(c.b32 + elems);
     c.status = words;
+    c.stamps = words + 1;  // 15 stamps of the last launch's CTA 0 (words: 256 bytes)
     init_tc_attributes();
     init_mma32w_attributes();
     DevProb d{};
@@ -103,6 +116,7 @@ extern "C" int tc_debug_gemm(int gclass, int m, int n, int k, int lower, double 
     float ms = 0;
     cudaEventElapsedTime(&ms, e0, e1);
     *avg_us = ms * 1000.f / float(iters);
+    cudaMemcpy(g_last_stamps, words + 1, sizeof(g_last_stamps), cudaMemcpyDeviceToHost);
     const cudaError_t e = cudaGetLastError();
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);

@@ -37,6 +37,7 @@ struct DevCtx {
     __half* w16;      // leaf inverses, hi | lo (ld kW16Ld), for inverse FP16 solves
     float* wscale;    // per leaf (indexed by its first row): 2^-e the W16 entries carry
     float* w32;       // FP32 leaf inverses (ld kW32Ld), for inverse FP32 solves
+    unsigned long long* stamps;  // development: %globaltimer stamps of CTA 0 (null = off)
 };
 
 // failure key: seq in the high 24 bits, a position inside the op below.

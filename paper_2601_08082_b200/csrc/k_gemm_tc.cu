@@ -53,6 +53,7 @@ namespace tcb {
 struct alignas(128) TcProb {
     CUtensorMap ta;  // A rows [a_r0, a_r0+m) x cols [a_c0, a_c0+k) (extents end there)
     CUtensorMap tb;  // B rows [b_r0, b_r0+n) x cols [b_c0, b_c0+k)
+    CUtensorMap tcm; // C rows [c_r0, c_r0+m) x cols [c_c0, c_c0+n) at the exec level (128 x 128-byte boxes)
     int m, n, k;
     int a_r0, a_c0, b_r0, b_c0, c_r0, c_c0;
     int exec_level, lower, tile0, tiles_n;
@@ -61,6 +62,7 @@ struct alignas(128) TcProb {
     uint32_t check_seq;  // fused require_finite (0 = none), element relative to chk origin
     int chk_r0, chk_c0;
     int nkc, kb_per_chunk;  // FP32-exec K chunks (1, 0: one accumulation)
+    int c_tma;              // C's columns start 16-byte aligned: epilogue through TMA boxes
 };
 
 size_t tc_prob_size() { return sizeof(TcProb); }
@@ -88,12 +90,19 @@ int g_tc_kchunk = 0;
 //   idesc: D=F32 (bits 4-5 = 1), A/B format at bits 7-9 / 10-12 (F16 = 0,
 //   TF32 = 2), both K-major, N>>3 at bits 17-22, M>>4 at bits 24-28
 template <int KIND> struct Cfg;
+#ifndef TC_F16_STAGES
+#define TC_F16_STAGES 4  // smem ring depth of the FP16 kind (3: 16384^3 1371 vs 1592 TF/s)
+#endif
+#ifndef TC_F16_STG
+#define TC_F16_STG 2     // C staging boxes (16 KB each) of the FP16 kind
+#endif
 template <> struct Cfg<KIND_F16> {
-    static constexpr int BN = 256, ESZ = 2, BK = 64, STAGES = 4, NTHREADS = 320, PASSES = 1;
+    static constexpr int BN = 256, ESZ = 2, BK = 64, STAGES = TC_F16_STAGES, NTHREADS = 320, PASSES = 1,
+                         STG_BOXES = TC_F16_STG;
     static constexpr uint32_t FMT = 0;
 };
 template <> struct Cfg<KIND_TF32X3> {
-    static constexpr int BN = 128, ESZ = 4, BK = 32, STAGES = 3, NTHREADS = 448, PASSES = 3;
+    static constexpr int BN = 128, ESZ = 4, BK = 32, STAGES = 3, NTHREADS = 448, PASSES = 3, STG_BOXES = 2;
     static constexpr uint32_t FMT = 2;
 };
 template <int KIND> struct Geo {
@@ -104,11 +113,14 @@ template <int KIND> struct Geo {
     static constexpr int TILE_BYTES = A_BYTES + B_BYTES;  // TMA bytes per stage
     // TF32X3 keeps a lo copy of both tiles next to the (hi) TMA tiles
     static constexpr int STAGE_BYTES = TILE_BYTES * (C::PASSES > 1 ? 2 : 1);
-    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+    // C staging for the epilogue: STG_BOXES boxes of 128 rows x 128 bytes
+    // (SWIZZLE_128B, the TMA load / store layout of C)
+    static constexpr int STG_BYTES = C::STG_BOXES * BM * 128;
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + STG_BYTES + 1024 /*align*/ + 256 /*barriers*/;
     static constexpr uint32_t TMEM_COLS = 2 * BN;  // two accumulators
     static constexpr uint32_t IDESC = (1u << 4) | (C::FMT << 7) | (C::FMT << 10) | (uint32_t(BN >> 3) << 17) |
                                       (uint32_t(BM >> 4) << 24);
-    static_assert(STAGES * STAGE_BYTES + 2048 <= 227 * 1024, "shared memory");
+    static_assert(STAGES * STAGE_BYTES + STG_BYTES + 1024 + 256 <= 227 * 1024, "shared memory");
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -145,6 +157,18 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
         "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y)
         : "memory");
 }
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int x, int y) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(smem_u32(src)), "r"(x), "r"(y)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// the 8 epilogue warps only (named barrier 1)
+__device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
 __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
@@ -197,6 +221,14 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void stamp(const DevCtx& c, int slot) {
+    if (c.stamps && blockIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        c.stamps[slot] = t;
+    }
 }
 
 __device__ __forceinline__ int find_tc_prob(const TcProb* p, int np, int tile) {
@@ -300,14 +332,17 @@ __global__ void __launch_bounds__(Cfg<KIND>::NTHREADS, 1) k_gemm_tc(DevCtx c, co
     auto sB = [&](int s) { return smem + s * G::STAGE_BYTES + G::A_BYTES; };
     auto sAl = [&](int s) { return smem + s * G::STAGE_BYTES + G::TILE_BYTES; };
     auto sBl = [&](int s) { return smem + s * G::STAGE_BYTES + G::TILE_BYTES + G::A_BYTES; };
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * G::STAGE_BYTES);
+    unsigned char* stg = smem + STAGES * G::STAGE_BYTES;  // C staging (1024-aligned)
+    uint64_t* full = reinterpret_cast<uint64_t*>(stg + G::STG_BYTES);
     uint64_t* empty = full + STAGES;
     uint64_t* split = empty + STAGES;  // TF32X3: hi/lo ready
     uint64_t* tfull = split + STAGES;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* cfull = tempty + 2;      // C staged
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cfull + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) stamp(c, 0);
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -319,6 +354,7 @@ __global__ void __launch_bounds__(Cfg<KIND>::NTHREADS, 1) k_gemm_tc(DevCtx c, co
             mbar_init(&tfull[s], 1);
             mbar_init(&tempty[s], 8);
         }
+        mbar_init(cfull, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -330,6 +366,7 @@ __global__ void __launch_bounds__(Cfg<KIND>::NTHREADS, 1) k_gemm_tc(DevCtx c, co
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    if (threadIdx.x == 0) stamp(c, 1);
 
     if (warp == 0) {
         if (lane == 0) {
@@ -349,6 +386,7 @@ __global__ void __launch_bounds__(Cfg<KIND>::NTHREADS, 1) k_gemm_tc(DevCtx c, co
                     const int ka = p->a_kwrap ? (kb * G::BK) % p->a_kwrap : kb * G::BK;
                     tma_load_2d(sA(stage), &p->ta, &full[stage], p->a_c0 + ka, p->a_r0 + tm * BM);
                     tma_load_2d(sB(stage), &p->tb, &full[stage], p->b_c0 + kb * G::BK, p->b_r0 + tn * BN);
+                    if (kb == 0) stamp(c, 2);
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
@@ -377,6 +415,7 @@ __global__ void __launch_bounds__(Cfg<KIND>::NTHREADS, 1) k_gemm_tc(DevCtx c, co
             for (int kb = kb0; kb < kb1; ++kb) {
                 mbar_wait(SPLIT ? &split[stage] : &full[stage], phase);
                 tc_fence_after();
+                if (lane == 0 && kb == kb0) stamp(c, 3);
                 if (lane == 0) {
                     const uint64_t da = sdesc(sA(stage));
                     const uint64_t db = sdesc(sB(stage));
@@ -437,22 +476,166 @@ __global__ void __launch_bounds__(Cfg<KIND>::NTHREADS, 1) k_gemm_tc(DevCtx c, co
         }
     } else {
         // ---------------- epilogue (warps 2..9) ----------------
+        // C goes through shared memory in TMA boxes (128 rows x 128 bytes,
+        // SWIZZLE_128B): loaded by one bulk-tensor copy, updated in place by
+        // the thread that owns each row (TMEM lane = row), stored back by one
+        // bulk-tensor copy.  Direct per-thread global access would touch 32
+        // rows -- 32 separate sectors -- per warp instruction.  A round covers
+        // the columns the staging holds (256 F16 / 128 F32 for the FP16 kind,
+        // 64 for TF32X3); warp (q, h) takes rows q*32.., half h of the round.
         const int q = warp & 3;             // TMEM lane quarter this warp may access
-        const int half = (warp - 2) >> 2;   // column half of the tile
-        constexpr int HW = BN / 2;          // columns per epilogue warp
+        const int half = (warp - 2) >> 2;   // column half of the round
+        const bool leader = warp == 2 && lane == 0;
+        const int row_l = q * 32 + lane;    // row inside the tile
         int as = 0;
-        uint32_t aphase = 0;
+        uint32_t aphase = 0, cphase = 0;
         for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
             int pi, tm, tn;
             if (!tile_coords<BN>(probs, np, t, pi, tm, tn)) continue;
             const TcProb& p = probs[pi];
+            if (!p.c_tma) {
+                // C columns not 16-byte aligned in global memory (ragged
+                // leaf sizes): direct per-thread access, C prefetched one
+                // 32-column chunk ahead
+                constexpr int HW = BN / 2;          // columns per epilogue warp
+                const int nkc = p.nkc;
+                for (int kc = 0; kc < nkc; ++kc) {
+                const bool last_chunk = kc == nkc - 1;
+                const int i = tm * BM + q * 32 + lane;  // row of C inside the problem
+                const bool row_ok = i < p.m;
+                const bool f16 = p.exec_level == LV_F16;
+                const long long rowoff = (long long)(p.c_r0 + (row_ok ? i : 0)) * c.ldw + p.c_c0;
+                Epi epi;
+                // inverse solves carry W scaled by 2^e; undo it exactly here
+                epi.alpha = p.a_kwrap ? double(c.wscale[p.b_r0]) : p.alpha;
+                // later K chunks add into the C the previous chunk wrote (FP32)
+                epi.beta = kc == 0 ? p.beta : 1.0;
+                epi.fast = pow2_or_one(epi.alpha) && (epi.beta == 0.0 || epi.beta == 1.0);
+                epi.af = float(epi.alpha);
+                const bool has_c = epi.beta != 0.0;
+                // columns [jlo, jhi) of this row are written (bounds, lower mask)
+                const int jbase = tn * BN + half * HW;
+                int jhi = min(p.n, jbase + HW);
+                if (p.lower) jhi = min(jhi, (p.c_r0 + i) - p.c_c0 + 1);
+                const int nch = row_ok && jhi > jbase ? (jhi - jbase + 31) >> 5 : 0;  // live chunks
+                auto cptr = [&](int j0) -> const void* {
+                    return f16 ? static_cast<const void*>(c.b16 + rowoff + j0) : static_cast<const void*>(c.b32 + rowoff + j0);
+                };
+                auto full_chunk = [&](int j0) {
+                    return j0 + 32 <= jhi && ((reinterpret_cast<uintptr_t>(cptr(j0)) & 15) == 0);
+                };
+                // C of the first chunk does not depend on the accumulator: load it
+                // before waiting for the MMA
+                CChunk cur, nxt;
+                if (has_c && nch > 0 && full_chunk(jbase)) load_chunk(cur, cptr(jbase), f16);
+                mbar_wait(&tfull[as], aphase);
+                tc_fence_after();
+                uint32_t anybad = 0;
+                int badj = -1;
+                for (int cc = 0; cc < HW; cc += 32) {
+                    float v[32];
+                    __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge first
+                    tmem_ld32(tmem + (uint32_t(q * 32) << 16) + uint32_t(as * BN + half * HW + cc), v);
+                    if (cc == HW - 32) {
+                        // accumulator drained: hand it back to the MMA warp
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&tempty[as]);
+                    }
+                    const int ch = cc >> 5;
+                    if (ch >= nch) continue;
+                    const int j0 = jbase + cc;
+                    if (has_c && ch + 1 < nch && full_chunk(j0 + 32)) load_chunk(nxt, cptr(j0 + 32), f16);
+                    uint32_t bad = 0;
+                    if (full_chunk(j0)) {
+                        if (f16) {
+                            uint4* C = reinterpret_cast<uint4*>(c.b16 + rowoff + j0);
+    #pragma unroll
+                            for (int g = 0; g < 4; ++g) {
+                                uint4 raw = has_c ? cur.r[g] : make_uint4(0, 0, 0, 0);
+                                uint32_t* w = reinterpret_cast<uint32_t*>(&raw);
+    #pragma unroll
+                                for (int e = 0; e < 4; ++e) {
+                                    const float2 cf = __half22float2(*reinterpret_cast<__half2*>(&w[e]));
+                                    const __half2 o = __floats2half2_rn(epi(v[8 * g + 2 * e], cf.x),
+                                                                        epi(v[8 * g + 2 * e + 1], cf.y));
+                                    w[e] = *reinterpret_cast<const uint32_t*>(&o);
+                                    bad |= ((w[e] & 0x7c00u) == 0x7c00u) | ((w[e] & 0x7c000000u) == 0x7c000000u);
+                                }
+                                C[g] = raw;
+                            }
+                        } else {
+                            float4* C = reinterpret_cast<float4*>(c.b32 + rowoff + j0);
+    #pragma unroll
+                            for (int g = 0; g < 8; ++g) {
+                                float4 cv = has_c ? *reinterpret_cast<const float4*>(&cur.r[g]) : make_float4(0, 0, 0, 0);
+                                cv.x = epi(v[4 * g + 0], cv.x);
+                                cv.y = epi(v[4 * g + 1], cv.y);
+                                cv.z = epi(v[4 * g + 2], cv.z);
+                                cv.w = epi(v[4 * g + 3], cv.w);
+                                bad |= ((__float_as_uint(cv.x) & 0x7f800000u) == 0x7f800000u) |
+                                       ((__float_as_uint(cv.y) & 0x7f800000u) == 0x7f800000u) |
+                                       ((__float_as_uint(cv.z) & 0x7f800000u) == 0x7f800000u) |
+                                       ((__float_as_uint(cv.w) & 0x7f800000u) == 0x7f800000u);
+                                C[g] = cv;
+                            }
+                        }
+                    } else {
+                        // ragged / unaligned chunk: element by element
+                        const int jm = min(32, jhi - j0);
+    #pragma unroll
+                        for (int e = 0; e < 32; ++e)
+                            if (e < jm) {
+                                if (f16) {
+                                    __half* C = c.b16 + rowoff + j0 + e;
+                                    const __half o = f2h(epi(v[e], has_c ? __half2float(*C) : 0.f));
+                                    bad |= h_bad(o);
+                                    *C = o;
+                                } else {
+                                    float* C = c.b32 + rowoff + j0 + e;
+                                    const float o = epi(v[e], has_c ? *C : 0.f);
+                                    bad |= !isfinite(o);
+                                    *C = o;
+                                }
+                            }
+                    }
+                    if (bad && badj < 0) {
+                        // locate the first non-finite value of this chunk (rare path)
+                        const int jm = min(32, jhi - j0);
+                        for (int e = 0; e < jm && badj < 0; ++e) {
+                            const bool b = f16 ? h_bad(c.b16[rowoff + j0 + e]) : !isfinite(c.b32[rowoff + j0 + e]);
+                            if (b) badj = j0 + e;
+                        }
+                    }
+                    anybad |= bad;
+                    cur = nxt;
+                }
+                if (p.check_seq != 0 && last_chunk) {
+                    // fused require_finite: first bad element in column-major order
+                    unsigned long long key = ~0ull;
+                    if (badj >= 0)
+                        key = fail_key(p.check_seq, elem_local(p.c_r0 + i - p.chk_r0, p.c_c0 + badj - p.chk_c0));
+                    __syncwarp();
+                    warp_report_min(c, key);
+                }
+                (void)anybad;
+                if (++as == 2) {
+                    as = 0;
+                    aphase ^= 1;
+                }
+                }  // chunks
+                continue;
+            }
             const int nkc = p.nkc;
+            const bool f16 = p.exec_level == LV_F16;
+            const int box_cols = f16 ? 64 : 32;                 // columns per 128-byte box
+            const int rc = min(BN, Cfg<KIND>::STG_BOXES * box_cols);  // columns per round
+            const int rounds = BN / rc;
+            const int hw = rc / 2;                              // columns per warp per round
+            const int i = tm * BM + row_l;                      // row of C inside the problem
+            const bool row_ok = i < p.m;
             for (int kc = 0; kc < nkc; ++kc) {
             const bool last_chunk = kc == nkc - 1;
-            const int i = tm * BM + q * 32 + lane;  // row of C inside the problem
-            const bool row_ok = i < p.m;
-            const bool f16 = p.exec_level == LV_F16;
-            const long long rowoff = (long long)(p.c_r0 + (row_ok ? i : 0)) * c.ldw + p.c_c0;
             Epi epi;
             // inverse solves carry W scaled by 2^e; undo it exactly here
             epi.alpha = p.a_kwrap ? double(c.wscale[p.b_r0]) : p.alpha;
@@ -461,102 +644,164 @@ __global__ void __launch_bounds__(Cfg<KIND>::NTHREADS, 1) k_gemm_tc(DevCtx c, co
             epi.fast = pow2_or_one(epi.alpha) && (epi.beta == 0.0 || epi.beta == 1.0);
             epi.af = float(epi.alpha);
             const bool has_c = epi.beta != 0.0;
-            // columns [jlo, jhi) of this row are written (bounds, lower mask)
-            const int jbase = tn * BN + half * HW;
-            int jhi = min(p.n, jbase + HW);
+            // lower tiles write back the staged C above the diagonal untouched
+            const bool load_c = has_c || p.lower;
+            // columns [.., jhi) of this row are computed (bounds, lower mask)
+            int jhi = p.n;
             if (p.lower) jhi = min(jhi, (p.c_r0 + i) - p.c_c0 + 1);
-            const int nch = row_ok && jhi > jbase ? (jhi - jbase + 31) >> 5 : 0;  // live chunks
-            auto cptr = [&](int j0) -> const void* {
-                return f16 ? static_cast<const void*>(c.b16 + rowoff + j0) : static_cast<const void*>(c.b32 + rowoff + j0);
-            };
-            auto full_chunk = [&](int j0) {
-                return j0 + 32 <= jhi && ((reinterpret_cast<uintptr_t>(cptr(j0)) & 15) == 0);
-            };
-            // C of the first chunk does not depend on the accumulator: load it
-            // before waiting for the MMA
-            CChunk cur, nxt;
-            if (has_c && nch > 0 && full_chunk(jbase)) load_chunk(cur, cptr(jbase), f16);
-            mbar_wait(&tfull[as], aphase);
-            tc_fence_after();
-            uint32_t anybad = 0;
+            if (!row_ok) jhi = 0;
             int badj = -1;
-            for (int cc = 0; cc < HW; cc += 32) {
-                float v[32];
-                __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge first
-                tmem_ld32(tmem + (uint32_t(q * 32) << 16) + uint32_t(as * BN + half * HW + cc), v);
-                if (cc == HW - 32) {
-                    // accumulator drained: hand it back to the MMA warp
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&tempty[as]);
+            for (int rd = 0; rd < rounds; ++rd) {
+                const int col0 = tn * BN + rd * rc;  // first column of the round (in the problem)
+                // boxes with columns inside the problem (0: a round past its
+                // edge -- its TMEM columns are still read, for the hand-back)
+                const int nbox = col0 < p.n ? min(Cfg<KIND>::STG_BOXES, (p.n - col0 + box_cols - 1) / box_cols) : 0;
+                const bool do_load = load_c && nbox > 0;
+                // the staging is free once the previous round's store has read it
+                if (leader) {
+                    bulk_wait_read0();
+                    if (do_load) {
+                        mbar_expect_tx(cfull, uint32_t(nbox) * BM * 128);
+                        for (int bx = 0; bx < nbox; ++bx)
+                            tma_load_2d(stg + bx * BM * 128, &p.tcm, cfull, p.c_c0 + col0 + bx * box_cols,
+                                        p.c_r0 + tm * BM);
+                    }
                 }
-                const int ch = cc >> 5;
-                if (ch >= nch) continue;
-                const int j0 = jbase + cc;
-                if (has_c && ch + 1 < nch && full_chunk(j0 + 32)) load_chunk(nxt, cptr(j0 + 32), f16);
-                uint32_t bad = 0;
-                if (full_chunk(j0)) {
-                    if (f16) {
-                        uint4* C = reinterpret_cast<uint4*>(c.b16 + rowoff + j0);
+                if (rd == 0) {
+                    mbar_wait(&tfull[as], aphase);
+                    tc_fence_after();
+                    if (warp == 2 && lane == 0) stamp(c, 4);
+                }
+                if (do_load) {
+                    mbar_wait(cfull, cphase);
+                    cphase ^= 1;
+                    if (leader) stamp(c, 7);
+                } else {
+                    epi_sync();  // nobody writes the staging before the leader's wait above
+                }
+                for (int cc = 0; cc < hw; cc += 32) {
+                    float v[32];
+                    const int jt = rd * rc + half * hw + cc;   // column inside the tile
+                    __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge first
+                    if (leader && cc == 0) stamp(c, 11);
+                    tmem_ld32(tmem + (uint32_t(q * 32) << 16) + uint32_t(as * BN + jt), v);
+                    if (leader && cc == 0) stamp(c, 12);
+                    if (leader && cc == 32) stamp(c, 14);
+                    if (rd == rounds - 1 && cc == hw - 32) {
+                        // accumulator drained: hand it back to the MMA warp
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&tempty[as]);
+                    }
+                    const int j0 = tn * BN + jt;               // column inside the problem
+                    if (j0 >= jhi) continue;
+                    const int jm = min(32, jhi - j0);          // live columns of this chunk
+                    // swizzled 16-byte chunks of this row inside its box
+                    const int bx = (jt - rd * rc) / box_cols;
+                    unsigned char* rowp = stg + bx * BM * 128 + row_l * 128;
+                    const int c16 = ((jt - rd * rc) % box_cols) * (f16 ? 2 : 4) / 16;  // first 16-byte chunk
+                    uint32_t bad = 0;
+                    if (epi.fast && jm == 32) {
+                        // common case (alpha = +-2^e, beta in {0, 1}, a full
+                        // chunk): straight-line FP32, no per-element branches
+                        const float af = epi.af;
+                        if (f16) {
+#pragma unroll
+                            for (int g = 0; g < 4; ++g) {
+                                uint4* cp = reinterpret_cast<uint4*>(rowp + (((c16 + g) ^ (row_l & 7)) << 4));
+                                uint4 raw = has_c ? *cp : make_uint4(0, 0, 0, 0);
+                                uint32_t* w = reinterpret_cast<uint32_t*>(&raw);
+#pragma unroll
+                                for (int e = 0; e < 4; ++e) {
+                                    const float2 cf = __half22float2(*reinterpret_cast<__half2*>(&w[e]));
+                                    const __half2 o = __floats2half2_rn(fmaf(af, v[8 * g + 2 * e], cf.x),
+                                                                        fmaf(af, v[8 * g + 2 * e + 1], cf.y));
+                                    w[e] = *reinterpret_cast<const uint32_t*>(&o);
+                                    bad |= ((w[e] & 0x7c00u) == 0x7c00u) | ((w[e] & 0x7c000000u) == 0x7c000000u);
+                                }
+                                *cp = raw;
+                            }
+                        } else {
+#pragma unroll
+                            for (int g = 0; g < 8; ++g) {
+                                float4* cp = reinterpret_cast<float4*>(rowp + (((c16 + g) ^ (row_l & 7)) << 4));
+                                float4 o = has_c ? *cp : make_float4(0.f, 0.f, 0.f, 0.f);
+                                o.x = fmaf(af, v[4 * g + 0], o.x);
+                                o.y = fmaf(af, v[4 * g + 1], o.y);
+                                o.z = fmaf(af, v[4 * g + 2], o.z);
+                                o.w = fmaf(af, v[4 * g + 3], o.w);
+                                bad |= ((__float_as_uint(o.x) & 0x7f800000u) == 0x7f800000u) |
+                                       ((__float_as_uint(o.y) & 0x7f800000u) == 0x7f800000u) |
+                                       ((__float_as_uint(o.z) & 0x7f800000u) == 0x7f800000u) |
+                                       ((__float_as_uint(o.w) & 0x7f800000u) == 0x7f800000u);
+                                *cp = o;
+                            }
+                        }
+                    } else if (f16) {
 #pragma unroll
                         for (int g = 0; g < 4; ++g) {
-                            uint4 raw = has_c ? cur.r[g] : make_uint4(0, 0, 0, 0);
+                            uint4* cp = reinterpret_cast<uint4*>(rowp + (((c16 + g) ^ (row_l & 7)) << 4));
+                            uint4 orig = load_c ? *cp : make_uint4(0, 0, 0, 0);  // staged (masked columns)
+                            uint4 raw = has_c ? orig : make_uint4(0, 0, 0, 0);
                             uint32_t* w = reinterpret_cast<uint32_t*>(&raw);
+                            uint32_t* wo = reinterpret_cast<uint32_t*>(&orig);
 #pragma unroll
                             for (int e = 0; e < 4; ++e) {
+                                const int jj = 8 * g + 2 * e;
                                 const float2 cf = __half22float2(*reinterpret_cast<__half2*>(&w[e]));
-                                const __half2 o = __floats2half2_rn(epi(v[8 * g + 2 * e], cf.x),
-                                                                    epi(v[8 * g + 2 * e + 1], cf.y));
-                                w[e] = *reinterpret_cast<const uint32_t*>(&o);
-                                bad |= ((w[e] & 0x7c00u) == 0x7c00u) | ((w[e] & 0x7c000000u) == 0x7c000000u);
+                                const __half2 o = __floats2half2_rn(epi(v[jj], cf.x), epi(v[jj + 1], cf.y));
+                                uint32_t ou = *reinterpret_cast<const uint32_t*>(&o);
+                                // masked columns keep the staged C
+                                if (jj >= jm) ou = (ou & 0xFFFF0000u) | (wo[e] & 0xFFFFu);
+                                if (jj + 1 >= jm) ou = (ou & 0xFFFFu) | (wo[e] & 0xFFFF0000u);
+                                w[e] = ou;
+                                bad |= (jj < jm && (ou & 0x7c00u) == 0x7c00u) |
+                                       (jj + 1 < jm && (ou & 0x7c000000u) == 0x7c000000u);
                             }
-                            C[g] = raw;
+                            *cp = raw;
                         }
                     } else {
-                        float4* C = reinterpret_cast<float4*>(c.b32 + rowoff + j0);
 #pragma unroll
                         for (int g = 0; g < 8; ++g) {
-                            float4 cv = has_c ? *reinterpret_cast<const float4*>(&cur.r[g]) : make_float4(0, 0, 0, 0);
-                            cv.x = epi(v[4 * g + 0], cv.x);
-                            cv.y = epi(v[4 * g + 1], cv.y);
-                            cv.z = epi(v[4 * g + 2], cv.z);
-                            cv.w = epi(v[4 * g + 3], cv.w);
-                            bad |= ((__float_as_uint(cv.x) & 0x7f800000u) == 0x7f800000u) |
-                                   ((__float_as_uint(cv.y) & 0x7f800000u) == 0x7f800000u) |
-                                   ((__float_as_uint(cv.z) & 0x7f800000u) == 0x7f800000u) |
-                                   ((__float_as_uint(cv.w) & 0x7f800000u) == 0x7f800000u);
-                            C[g] = cv;
+                            float4* cp = reinterpret_cast<float4*>(rowp + (((c16 + g) ^ (row_l & 7)) << 4));
+                            const float4 co = has_c ? *cp : make_float4(0, 0, 0, 0);
+                            const float4 cm = p.lower ? *cp : co;  // staged values (masked columns)
+                            float4 o;
+                            const int jj = 4 * g;
+                            o.x = jj + 0 < jm ? epi(v[jj + 0], co.x) : cm.x;
+                            o.y = jj + 1 < jm ? epi(v[jj + 1], co.y) : cm.y;
+                            o.z = jj + 2 < jm ? epi(v[jj + 2], co.z) : cm.z;
+                            o.w = jj + 3 < jm ? epi(v[jj + 3], co.w) : cm.w;
+                            bad |= (jj + 0 < jm && (__float_as_uint(o.x) & 0x7f800000u) == 0x7f800000u) |
+                                   (jj + 1 < jm && (__float_as_uint(o.y) & 0x7f800000u) == 0x7f800000u) |
+                                   (jj + 2 < jm && (__float_as_uint(o.z) & 0x7f800000u) == 0x7f800000u) |
+                                   (jj + 3 < jm && (__float_as_uint(o.w) & 0x7f800000u) == 0x7f800000u);
+                            *cp = o;
                         }
                     }
-                } else {
-                    // ragged / unaligned chunk: element by element
-                    const int jm = min(32, jhi - j0);
-#pragma unroll
-                    for (int e = 0; e < 32; ++e)
-                        if (e < jm) {
-                            if (f16) {
-                                __half* C = c.b16 + rowoff + j0 + e;
-                                const __half o = f2h(epi(v[e], has_c ? __half2float(*C) : 0.f));
-                                bad |= h_bad(o);
-                                *C = o;
-                            } else {
-                                float* C = c.b32 + rowoff + j0 + e;
-                                const float o = epi(v[e], has_c ? *C : 0.f);
-                                bad |= !isfinite(o);
-                                *C = o;
-                            }
+                    if (leader && cc == 0) stamp(c, 13);
+                    if (bad && badj < 0) {
+                        // locate the first non-finite value of this chunk (rare path)
+                        for (int e = 0; e < jm && badj < 0; ++e) {
+                            const int cb = (c16 * 16 + e * (f16 ? 2 : 4)) / 16, off = (e * (f16 ? 2 : 4)) % 16;
+                            const unsigned char* ep = rowp + ((cb ^ (row_l & 7)) << 4) + off;
+                            const bool b = f16 ? h_bad(*reinterpret_cast<const __half*>(ep))
+                                               : !isfinite(*reinterpret_cast<const float*>(ep));
+                            if (b) badj = j0 + e;
                         }
-                }
-                if (bad && badj < 0) {
-                    // locate the first non-finite value of this chunk (rare path)
-                    const int jm = min(32, jhi - j0);
-                    for (int e = 0; e < jm && badj < 0; ++e) {
-                        const bool b = f16 ? h_bad(c.b16[rowoff + j0 + e]) : !isfinite(c.b32[rowoff + j0 + e]);
-                        if (b) badj = j0 + e;
                     }
                 }
-                anybad |= bad;
-                cur = nxt;
+                // generic-proxy smem writes -> visible to the bulk copy; then
+                // one thread stores the round's boxes
+                if (leader) stamp(c, 8);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                epi_sync();
+                if (leader) stamp(c, 9);
+                if (leader && nbox > 0) {
+                    for (int bx = 0; bx < nbox; ++bx)
+                        tma_store_2d(&p.tcm, stg + bx * BM * 128, p.c_c0 + col0 + bx * box_cols, p.c_r0 + tm * BM);
+                    bulk_commit();
+                }
             }
             if (p.check_seq != 0 && last_chunk) {
                 // fused require_finite: first bad element in column-major order
@@ -566,19 +811,23 @@ __global__ void __launch_bounds__(Cfg<KIND>::NTHREADS, 1) k_gemm_tc(DevCtx c, co
                 __syncwarp();
                 warp_report_min(c, key);
             }
-            (void)anybad;
             if (++as == 2) {
                 as = 0;
                 aphase ^= 1;
             }
             }  // chunks
+            // the next tile's staging loads wait for these stores (leader)
         }
+        if (leader) stamp(c, 10);
+        if (leader) bulk_wait0();  // every store complete before the CTA exits
     }
 
+    if (warp == 2 && lane == 0) stamp(c, 5);
     tc_fence_before();
     __syncthreads();
     if (warp == 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(G::TMEM_COLS));
+    if (threadIdx.x == 32) stamp(c, 6);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
@@ -647,6 +896,17 @@ int tc_build_probs(const DevCtx& c, int kind, const std::vector<DevProb>& probs,
         const long long bld = d.b_buf == BUF_W16 ? kW16Ld : d.b_buf == BUF_W32 ? kW32Ld : c.ldw;
         const bool bf32 = d.b_buf == BUF_W32 || (f32 && d.b_buf != BUF_W16);
         if (!make_map(&p.tb, bbuf, bf32, bld, d.b_r0 + d.n, d.b_c0 + d.k, BN, err)) return -1;
+        {
+            const bool cf32 = d.exec_level == LV_F32;
+            const void* cbuf = cf32 ? static_cast<const void*>(c.b32) : static_cast<const void*>(c.b16);
+            if (d.exec_level != LV_F16 && !cf32) {
+                if (err) *err = "tensor-core GEMM: exec level must be F16 or F32";
+                return -1;
+            }
+            if (!make_map(&p.tcm, cbuf, cf32, c.ldw, d.c_r0 + d.m, d.c_c0 + d.n, BM, err)) return -1;
+            // bulk-tensor boxes must start 16-byte aligned in global memory
+            p.c_tma = (d.c_c0 * (cf32 ? 4 : 2)) % 16 == 0 && (c.ldw * (cf32 ? 4 : 2)) % 16 == 0;
+        }
         p.a_kwrap = d.a_kwrap;
         p.check_seq = d.check_seq;
         p.chk_r0 = d.chk_r0;

@@ -2,7 +2,7 @@
 import json
 import sys
 
-sys.path.insert(0, ".")
+sys.path.insert(0, __import__("os").environ.get("TC_ROOT", "."))
 import paper_2601_08082_b200 as tc  # noqa: E402
 
 SHAPES = [  # (m, n, k, lower, beta, exec)

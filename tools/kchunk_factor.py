@@ -4,7 +4,7 @@ import os
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-sys.path.insert(0, ROOT)
+sys.path.insert(0, os.environ.get("TC_ROOT", ROOT))
 import torch  # noqa: E402
 
 import paper_2601_08082_b200 as tc  # noqa: E402
