@@ -343,12 +343,12 @@ def run_ours(args):
     c5 = None
     if ws > 1 and args.c5_n > 0 and not shared:
         from paper_2601_08082_b200.distributed import potrf_top_split, synthetic_pieces
-        a11, a21, a22 = synthetic_pieces(args.c5_n, b, SEED, ws, rank)
+        a11, a21, a22, l22 = synthetic_pieces(args.c5_n, b, SEED, ws, rank)
         cache = {}
         times = []
         for it in range(3):  # the first call builds the plans
-            res = potrf_top_split(args.c5_n, b, CFG, a11=a11.clone() if a11 is not None else None, a21_rows=a21,
-                                  a22_rows=a22, cache=cache)
+            res = potrf_top_split(args.c5_n, b, CFG, a11=a11.clone() if a11 is not None else None,
+                                  a21_rows=a21.clone(), a22_rows=a22.clone(), l22=l22, cache=cache)
             times.append(allreduce_max(res.device_ms, shared))
         ms5 = min(times[1:])
         c5 = {"workload": f"C5-style: one N={args.c5_n} factorization, top TRSM/SYRK row-split over {ws} GPUs, "
@@ -356,7 +356,7 @@ def run_ours(args):
               "value": potrf_flops(args.c5_n) / (ms5 * 1e-3) / 1e12, "unit": "TFLOP/s", "ms": ms5,
               "status": res.status, "scaling": "strong",
               "data": "device-generated SPD of spd_generate's distribution"}
-        del a11, a21, a22, cache, res
+        del a11, a21, a22, l22, cache, res
         torch.cuda.empty_cache()
 
     variants = None

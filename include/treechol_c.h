@@ -165,6 +165,32 @@ int tc_potrs_batch_device(int n, int nsys, const double* const* dL, int ldl, dou
 
 /* ---- distributed single factorization (BASELINE config C5) ------------- */
 
+/* Compact forms of the two distributed pieces (BASELINE config C5 at
+ * N = 131072; paper_2601_08082_b200/distributed.py):
+ *  _trsm_ext: L11 is not imported from doubles -- the caller writes rn_p(L11)
+ *    (p = the panel level) into the plan's level buffer rows [0, n1)
+ *    (tc_plan_level_buffer, tc_level_image_device); the caller's doubles hold
+ *    only the m panel rows.
+ *  _syrk_rows_ext: the solved panel is written by the caller into the level
+ *    buffer rows [row_hi, row_hi + n2); the caller's doubles hold only A22's
+ *    rows [row_lo, row_hi).
+ * tc_plan_input_rows gives the caller operand's first row (its pointer refers
+ * to that row) and row count (the leading dimension must be at least that). */
+int tc_plan_create_trsm_ext(int n1, int m, int b, const int* levels, int nlevels, int leaf_size, tc_plan** out);
+int tc_plan_create_syrk_rows_ext(int n2, int k, int b, const int* levels, int nlevels, int row_lo, int row_hi,
+                                 tc_plan** out);
+int tc_plan_input_rows(const tc_plan* plan, int* row0, int* rows);
+/* device bytes the plan's workspace takes (level-buffer windows, leaf
+ * inverses); no device needed */
+int tc_plan_device_bytes(const tc_plan* plan, unsigned long long* bytes);
+/* the allocated window of a level buffer (row-major, ld elements): *ptr is
+ * row *row_lo; rows [*row_lo, *row_hi) exist.  Allocates on first use. */
+int tc_plan_level_buffer(tc_plan* plan, int level, void** ptr, long long* ld, int* row_lo, int* row_hi);
+/* dst (row-major, ldd) = rn_level(src) of an m x n column-major double
+ * block, strict upper triangle zero when lower != 0 (asynchronous) */
+int tc_level_image_device(int m, int n, const double* src, int lds, int level, int lower, void* dst, long long ldd,
+                          void* stream);
+
 /* The two pieces a rank runs for the top split of an order-N factorization
  * (n1 = N/2, n2 = N - n1) besides whole factorizations; levels are the big
  * tree's (the split's subtrees sit at depth 1, its panel at depth 0).

@@ -138,6 +138,12 @@ def _load():
         "tc_plan_create_trsm": (I, [I, I, I, PI, I, I, C.POINTER(P)]),
         "tc_plan_create_syrk_rows": (I, [I, I, I, PI, I, I, I, C.POINTER(P)]),
         "tc_plan_set_external_absmax": (I, [P, D]),
+        "tc_plan_create_trsm_ext": (I, [I, I, I, PI, I, I, C.POINTER(P)]),
+        "tc_plan_create_syrk_rows_ext": (I, [I, I, I, PI, I, I, I, C.POINTER(P)]),
+        "tc_plan_input_rows": (I, [P, PI, PI]),
+        "tc_plan_device_bytes": (I, [P, C.POINTER(C.c_ulonglong)]),
+        "tc_plan_level_buffer": (I, [P, I, C.POINTER(P), C.POINTER(C.c_longlong), PI, PI]),
+        "tc_level_image_device": (I, [I, I, P, I, I, I, P, C.c_longlong, P]),
         "tc_plan_extent": (I, [P, PI, PI]),
         "tc_absmax_device": (I, [I, I, P, I, C.POINTER(D), P]),
         "tc_batch_create": (I, [I, I, PI, I, I, I, C.POINTER(P)]),
@@ -322,6 +328,23 @@ def from_device(t) -> np.ndarray:
     return np.asfortranarray(t.detach().cpu().numpy().T)
 
 
+class _DevView:
+    """__cuda_array_interface__ over raw device memory owned elsewhere"""
+
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+def level_image_device(src, m: int, n: int, level: int, dst, ldd: int, lower: bool = True, stream=None):
+    """dst (row-major, ld ldd) = rn_level of the m x n column-major double
+    block src (torch tensor (n, lds)), strict upper triangle zeroed when
+    lower (tc_level_image_device)"""
+    lds = src.shape[1] if src.dim() == 2 else m
+    _raise(_lib.tc_level_image_device(m, n, _ptr(src), lds, int(level), int(bool(lower)), _ptr(dst), int(ldd),
+                                      _stream_ptr(stream)))
+
+
 def _check_dev(t, n, what, cols=None):
     """a contiguous CUDA float64 column-major tensor (cols', ld) with
     ld >= n rows and cols' >= cols (default n) columns; returns ld"""
@@ -387,10 +410,32 @@ class Plan:
 
     def _extent(self):
         """rows x cols of the column-major operand the plan reads and writes
-        (tc_plan_extent; n x n for a whole factorization)"""
+        (tc_plan_extent / tc_plan_input_rows; n x n for a whole
+        factorization; the compact distributed pieces take only their rows)"""
         r, c = C.c_int(), C.c_int()
         _raise(_lib.tc_plan_extent(self._h, C.byref(r), C.byref(c)))
-        self.rows, self.cols = r.value, c.value
+        r0, nr = C.c_int(), C.c_int()
+        _raise(_lib.tc_plan_input_rows(self._h, C.byref(r0), C.byref(nr)))
+        self.row0, self.rows, self.cols = r0.value, nr.value, c.value
+
+    def device_bytes(self) -> int:
+        """device workspace of the plan (level-buffer windows, leaf inverses)"""
+        out = C.c_ulonglong()
+        _raise(_lib.tc_plan_device_bytes(self._h, C.byref(out)))
+        return out.value
+
+    def level_buffer(self, level: int):
+        """(tensor, row_lo): the allocated window of a level buffer as a torch
+        tensor view (rows x ld, row-major) whose row 0 is buffer row row_lo;
+        valid while the plan lives"""
+        import torch
+        ptr, ld, lo, hi = C.c_void_p(), C.c_longlong(), C.c_int(), C.c_int()
+        _raise(_lib.tc_plan_level_buffer(self._h, int(level), C.byref(ptr), C.byref(ld), C.byref(lo), C.byref(hi)))
+        typestr = ("<f2", "<f4", "<f8")[level]
+        view = _DevView(ptr.value, (hi.value - lo.value, ld.value), typestr)
+        t = torch.as_tensor(view, device="cuda")
+        t._tc_owner = self  # keep the plan (and its workspace) alive
+        return t, lo.value
 
     @classmethod
     def panel_trsm(cls, n1: int, m: int, b: int, config, leaf_size: int = 0) -> "Plan":
@@ -402,6 +447,29 @@ class Plan:
         h = C.c_void_p()
         _raise(_lib.tc_plan_create_trsm(n1, m, b, arr, len(cfg.levels), leaf_size, C.byref(h)))
         return cls._wrap(h, n1, b, cfg, n1 + m)
+
+    @classmethod
+    def panel_trsm_ext(cls, n1: int, m: int, b: int, config, leaf_size: int = 0) -> "Plan":
+        """compact distributed TRSM piece (tc_plan_create_trsm_ext): the
+        caller writes rn_p(L11) into level buffer p rows [0, n1); the
+        operand is only the m panel rows (tensor (n1, m))"""
+        cfg = _cfg(config)
+        arr = (C.c_int * len(cfg.levels))(*cfg.levels)
+        h = C.c_void_p()
+        _raise(_lib.tc_plan_create_trsm_ext(n1, m, b, arr, len(cfg.levels), leaf_size, C.byref(h)))
+        return cls._wrap(h, n1, b, cfg, n1 + m)
+
+    @classmethod
+    def panel_syrk_rows_ext(cls, n2: int, k: int, b: int, config, row_lo: int, row_hi: int) -> "Plan":
+        """compact distributed SYRK piece (tc_plan_create_syrk_rows_ext): the
+        caller writes the solved panel's level image into level buffer p rows
+        [row_hi, row_hi + n2); the operand is A22's rows [row_lo, row_hi)
+        only (tensor (n2, row_hi - row_lo))"""
+        cfg = _cfg(config)
+        arr = (C.c_int * len(cfg.levels))(*cfg.levels)
+        h = C.c_void_p()
+        _raise(_lib.tc_plan_create_syrk_rows_ext(n2, k, b, arr, len(cfg.levels), row_lo, row_hi, C.byref(h)))
+        return cls._wrap(h, n2, b, cfg, row_hi + n2)
 
     @classmethod
     def panel_syrk_rows(cls, n2: int, k: int, b: int, config, row_lo: int, row_hi: int) -> "Plan":

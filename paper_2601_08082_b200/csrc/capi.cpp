@@ -320,6 +320,70 @@ int tc_plan_create_syrk_rows(int n2, int k, int b, const int* levels, int nlevel
     }
 }
 
+int tc_plan_create_trsm_ext(int n1, int m, int b, const int* levels, int nlevels, int leaf_size, tc_plan** out) {
+    if (!out || !levels_ok(levels, nlevels)) return fail(TC_INVALID_ARGUMENT, "bad arguments");
+    *out = nullptr;
+    try {
+        Plan p = Plan::make_trsm(n1, m, b, std::vector<int>(levels, levels + nlevels), leaf_size, PlanOptions{},
+                                 true);
+        auto* h = new tc_plan;
+        h->eng = std::make_unique<Engine>(std::move(p));
+        *out = h;
+        return TC_OK;
+    } catch (const std::exception& e) {
+        return fail(TC_INVALID_ARGUMENT, e.what());
+    }
+}
+
+int tc_plan_create_syrk_rows_ext(int n2, int k, int b, const int* levels, int nlevels, int row_lo, int row_hi,
+                                 tc_plan** out) {
+    if (!out || !levels_ok(levels, nlevels)) return fail(TC_INVALID_ARGUMENT, "bad arguments");
+    *out = nullptr;
+    try {
+        Plan p = Plan::make_syrk_rows(n2, k, b, std::vector<int>(levels, levels + nlevels), row_lo, row_hi,
+                                      PlanOptions{}, true);
+        auto* h = new tc_plan;
+        h->eng = std::make_unique<Engine>(std::move(p));
+        *out = h;
+        return TC_OK;
+    } catch (const std::exception& e) {
+        return fail(TC_INVALID_ARGUMENT, e.what());
+    }
+}
+
+int tc_plan_input_rows(const tc_plan* plan, int* row0, int* rows) {
+    if (!plan) return fail(TC_INVALID_ARGUMENT, "null plan");
+    const Plan& P = plan->eng->plan;
+    if (row0) *row0 = P.user_row0;
+    if (rows) *rows = P.caller_rows();
+    return TC_OK;
+}
+
+int tc_plan_device_bytes(const tc_plan* plan, unsigned long long* bytes) {
+    if (!plan || !bytes) return fail(TC_INVALID_ARGUMENT, "null argument");
+    *bytes = plan->eng->plan.device_bytes();
+    return TC_OK;
+}
+
+int tc_plan_level_buffer(tc_plan* plan, int level, void** ptr, long long* ld, int* row_lo, int* row_hi) {
+    if (!plan || !ptr || !ld || !row_lo || !row_hi) return fail(TC_INVALID_ARGUMENT, "null argument");
+    if (!tc_device_available()) return fail(TC_NO_DEVICE, "no CUDA device (there is no CPU fallback)");
+    std::string err;
+    if (!plan->eng->level_buffer(level, ptr, ld, row_lo, row_hi, &err)) return fail(TC_INVALID_ARGUMENT, err);
+    return TC_OK;
+}
+
+int tc_level_image_device(int m, int n, const double* src, int lds, int level, int lower, void* dst, long long ldd,
+                          void* stream) {
+    if (!src || !dst || m < 0 || n < 0 || lds < m || ldd < n || level < 0 || level > 2)
+        return fail(TC_INVALID_ARGUMENT, "bad arguments");
+    if (!tc_device_available()) return fail(TC_NO_DEVICE, "no CUDA device (there is no CPU fallback)");
+    if (m == 0 || n == 0) return TC_OK;
+    launch_level_image(m, n, src, lds, level, lower, dst, ldd, static_cast<cudaStream_t>(stream));
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? TC_OK : cuda_fail(e, "level image");
+}
+
 int tc_plan_set_external_absmax(tc_plan* plan, double absmax) {
     if (!plan) return fail(TC_INVALID_ARGUMENT, "null plan");
     std::string err;
@@ -364,7 +428,8 @@ int tc_plan_op_deps(const tc_plan* plan, int i, int* deps, int cap) {
 int tc_potrf_device(tc_plan* plan, const double* dA_in, int lda_in, double* dL_out, int lda_out, void* stream,
                     tc_info* info) {
     if (!plan || !dA_in || !dL_out) return fail(TC_INVALID_ARGUMENT, "null argument");
-    const int n = plan->eng->plan.rows > 0 ? plan->eng->plan.rows : plan->eng->plan.n;
+    const Plan& P = plan->eng->plan;
+    const int n = P.caller_rows();  // rows of the caller's operand
     if (lda_in < n || lda_out < n) return fail(TC_INVALID_ARGUMENT, "leading dimension < rows");
     if (!tc_device_available()) return fail(TC_NO_DEVICE, "no CUDA device (there is no CPU fallback)");
     std::string err;
@@ -400,6 +465,8 @@ int tc_info_message(const tc_plan*, const tc_info* info, char* buf, int buflen) 
 int tc_potrf_host(tc_plan* plan, double* A, int lda, tc_info* info) {
     if (!plan || !A) return fail(TC_INVALID_ARGUMENT, "null argument");
     const int n = plan->eng->plan.n;
+    if ((plan->eng->plan.rows > 0 && plan->eng->plan.rows != n) || plan->eng->plan.user_row0 != 0)
+        return fail(TC_INVALID_ARGUMENT, "the host entry point takes whole-factorization plans only");
     if (lda < n) return fail(TC_INVALID_ARGUMENT, "leading dimension < n");
     if (!tc_device_available()) return fail(TC_NO_DEVICE, "no CUDA device (there is no CPU fallback)");
     std::string err;

@@ -38,6 +38,9 @@ struct DevCtx {
     float* wscale;    // per leaf (indexed by its first row): 2^-e the W16 entries carry
     float* w32;       // FP32 leaf inverses (ld kW32Ld), for inverse FP32 solves
     unsigned long long* stamps;  // development: %globaltimer stamps of CTA 0 (null = off)
+    // first allocated row of each level buffer (b16/b32/b64 are virtual bases:
+    // rows below are never accessed, but TMA descriptors need real addresses)
+    int win_lo[3];
 };
 
 // failure key: seq in the high 24 bits, a position inside the op below.

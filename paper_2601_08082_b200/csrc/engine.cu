@@ -77,24 +77,33 @@ bool Engine::prepare(std::string* err) {
     init_leaf_attributes();
     init_tc_attributes();
     init_mma32w_attributes();
-    // level buffers: rows x ldw (n x n for a factorization plan)
+    // level buffers: rows [win_lo, win_hi) x ldw of each level the plan
+    // touches (all n rows for a factorization plan), one allocation with
+    // 256-byte aligned sub-buffers.  The context holds VIRTUAL bases (the
+    // allocation minus win_lo rows), so every kernel keeps addressing
+    // base + row * ldw + col with absolute rows; no op touches a row
+    // outside its level's window (Plan::compute_windows).
     const int n = plan.rows > 0 ? plan.rows : plan.n;
-    const long long ldw = (long long)align_up(size_t(plan.cols > 0 ? plan.cols : plan.n), 64);
+    const long long ldw = plan.ldw();
     ctx_.ldw = ldw;
-    // level buffers: one allocation, 256-byte aligned sub-buffers
-    size_t sz[3] = {0, 0, 0}, off[3] = {0, 0, 0}, total = 0;
+    size_t sz[3] = {0, 0, 0}, total = 0;
     const size_t esz[3] = {2, 4, 8};
     for (int l = 0; l < 3; ++l)
         if (plan.needs_buf[l]) {
-            sz[l] = size_t(n) * size_t(ldw) * esz[l];
-            off[l] = total;
+            sz[l] = size_t(plan.win_hi[l] - plan.win_lo[l]) * size_t(ldw) * esz[l];
+            buf_off_[l] = total;
             total = align_up(total + sz[l], 256);
         }
     if (total) TC_TRY(cudaMalloc(&d_bufs_, total));
     unsigned char* base = static_cast<unsigned char*>(d_bufs_);
-    ctx_.b16 = plan.needs_buf[0] ? reinterpret_cast<__half*>(base + off[0]) : nullptr;
-    ctx_.b32 = plan.needs_buf[1] ? reinterpret_cast<float*>(base + off[1]) : nullptr;
-    ctx_.b64 = plan.needs_buf[2] ? reinterpret_cast<double*>(base + off[2]) : nullptr;
+    auto vbase = [&](int l) -> unsigned char* {
+        return plan.needs_buf[l] ? base + buf_off_[l] - ptrdiff_t(plan.win_lo[l]) * ptrdiff_t(ldw) * ptrdiff_t(esz[l])
+                                 : nullptr;
+    };
+    for (int l = 0; l < 3; ++l) ctx_.win_lo[l] = plan.needs_buf[l] ? plan.win_lo[l] : 0;
+    ctx_.b16 = reinterpret_cast<__half*>(vbase(0));
+    ctx_.b32 = reinterpret_cast<float*>(vbase(1));
+    ctx_.b64 = reinterpret_cast<double*>(vbase(2));
     if (plan.needs_w16) {
         // leaf inverses (hi | lo, zero outside the written triangles) + scales
         TC_TRY(cudaMalloc(&d_w16_, sizeof(__half) * size_t(n) * kW16Ld + sizeof(float) * size_t(n)));
@@ -231,6 +240,19 @@ void Engine::reset_words(cudaStream_t s) {
     if (plan.ext_alpha_slot >= 0 && h_ext_)
         cudaMemcpyAsync(d_words_ + 1 + plan.ext_alpha_slot, h_ext_, sizeof(unsigned long long),
                         cudaMemcpyHostToDevice, s);
+}
+
+bool Engine::level_buffer(int level, void** ptr, long long* ld, int* row_lo, int* row_hi, std::string* err) {
+    if (!prepare(err)) return false;
+    if (level < 0 || level > 2 || !plan.needs_buf[level]) {
+        if (err) *err = "the plan has no buffer at that level";
+        return false;
+    }
+    *ptr = static_cast<unsigned char*>(d_bufs_) + buf_off_[level];
+    *ld = ctx_.ldw;
+    *row_lo = plan.win_lo[level];
+    *row_hi = plan.win_hi[level];
+    return true;
 }
 
 bool Engine::set_external_absmax(double amax, std::string* err) {
@@ -397,8 +419,9 @@ bool Engine::enqueue(const double* a_in, long long lda_in, double* l_out, long l
     if (!prepare(err)) return false;
     RunArgs* slot = next_args(err);
     if (!slot) return false;
-    slot->a_in = a_in;
-    slot->l_out = l_out;
+    // the caller's pointers refer to row plan.user_row0 (compact pieces)
+    slot->a_in = a_in - plan.user_row0;
+    slot->l_out = l_out - plan.user_row0;
     slot->lda_in = lda_in;
     slot->lda_out = lda_out;
     TC_TRY(cudaMemcpyAsync(d_ra_, slot, sizeof(RunArgs), cudaMemcpyHostToDevice, stream));
@@ -822,8 +845,9 @@ bool Engine::timeline(const double* a_in, long long lda_in, double* l_out, long 
     if (!prepare(err)) return false;
     RunArgs* slot = next_args(err);
     if (!slot) return false;
-    slot->a_in = a_in;
-    slot->l_out = l_out;
+    // the caller's pointers refer to row plan.user_row0 (compact pieces)
+    slot->a_in = a_in - plan.user_row0;
+    slot->l_out = l_out - plan.user_row0;
     slot->lda_in = lda_in;
     slot->lda_out = lda_out;
     TC_TRY(cudaMemcpyAsync(d_ra_, slot, sizeof(RunArgs), cudaMemcpyHostToDevice, stream));
@@ -968,8 +992,9 @@ bool Engine::profile(const double* a_in, long long lda_in, double* l_out, long l
     if (!prepare(err)) return false;
     RunArgs* slot = next_args(err);
     if (!slot) return false;
-    slot->a_in = a_in;
-    slot->l_out = l_out;
+    // the caller's pointers refer to row plan.user_row0 (compact pieces)
+    slot->a_in = a_in - plan.user_row0;
+    slot->l_out = l_out - plan.user_row0;
     slot->lda_in = lda_in;
     slot->lda_out = lda_out;
     TC_TRY(cudaMemcpyAsync(d_ra_, slot, sizeof(RunArgs), cudaMemcpyHostToDevice, stream));

@@ -71,6 +71,9 @@ class Engine {
     bool ready() const { return ready_; }
     // distributed panel plans: the all-reduced max|B| of the panel rows
     bool set_external_absmax(double amax, std::string* err);
+    // the real start (row row_lo) of a level buffer's allocated window, its
+    // row stride in elements and the window rows (allocates if needed)
+    bool level_buffer(int level, void** ptr, long long* ld, int* row_lo, int* row_hi, std::string* err);
     bool prepare(std::string* err);
 
    private:
@@ -82,6 +85,7 @@ class Engine {
     unsigned long long* h_status_ = nullptr;
     unsigned long long* h_ext_ = nullptr;     // pinned: external max|B| bits
     void* d_bufs_ = nullptr;
+    size_t buf_off_[3] = {0, 0, 0};          // level windows inside d_bufs_
     unsigned long long* d_words_ = nullptr;  // status + alpha slots
     void* d_w16_ = nullptr;                  // leaf inverses + scales
     void* d_w32_ = nullptr;                  // FP32 leaf inverses

@@ -293,6 +293,38 @@ __global__ void __launch_bounds__(256) k_symmetrize(double* a, long long lda, in
 
 }  // namespace
 
+// row-major level image of a column-major double block: dst[i * ldd + j] =
+// rn_L(src[j * lds + i]) (direct RNE, d2h for binary16), strict upper
+// triangle zero when `lower` -- how a distributed piece receives a factor
+// block it reads through rn_p (kernels.cpp:29, 78)
+template <typename T>
+__global__ void __launch_bounds__(256) k_level_image(int m, int n, const double* __restrict__ src, long long lds,
+                                                     int lower, T* __restrict__ dst, long long ldd) {
+    __shared__ double t[32][33];
+    const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+    for (int r = ty; r < 32; r += 8) {
+        const int i = i0 + tx, j = j0 + r;  // coalesced down a column
+        t[r][tx] = (i < m && j < n) ? src[(long long)j * lds + i] : 0.0;
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {
+        const int i = i0 + r, j = j0 + tx;  // coalesced along a row
+        if (i < m && j < n) dst[(long long)i * ldd + j] = (lower && j > i) ? from_double<T>(0.0) : from_double<T>(t[tx][r]);
+    }
+}
+
+void launch_level_image(int m, int n, const double* src, long long lds, int level, int lower, void* dst,
+                        long long ldd, cudaStream_t s) {
+    const dim3 grid((n + 31) / 32, (m + 31) / 32);
+    if (level == 0)
+        k_level_image<__half><<<grid, 256, 0, s>>>(m, n, src, lds, lower, static_cast<__half*>(dst), ldd);
+    else if (level == 1)
+        k_level_image<float><<<grid, 256, 0, s>>>(m, n, src, lds, lower, static_cast<float*>(dst), ldd);
+    else
+        k_level_image<double><<<grid, 256, 0, s>>>(m, n, src, lds, lower, static_cast<double*>(dst), ldd);
+}
+
 void launch_symmetrize(double* a, long long lda, int n, cudaStream_t s) {
     const int T = (n + TS - 1) / TS;
     k_symmetrize<<<T * (T + 1) / 2, 256, 0, s>>>(a, lda, n);

@@ -63,6 +63,7 @@ struct alignas(128) TcProb {
     int chk_r0, chk_c0;
     int nkc, kb_per_chunk;  // FP32-exec K chunks (1, 0: one accumulation)
     int c_tma;              // C's columns start 16-byte aligned: epilogue through TMA boxes
+    int ya, yb, yc;         // first row of each map (the level buffer window): TMA y = row - y*
 };
 
 size_t tc_prob_size() { return sizeof(TcProb); }
@@ -384,8 +385,8 @@ __global__ void __launch_bounds__(Cfg<KIND>::NTHREADS, 1) k_gemm_tc(DevCtx c, co
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_expect_tx(&full[stage], G::TILE_BYTES);
                     const int ka = p->a_kwrap ? (kb * G::BK) % p->a_kwrap : kb * G::BK;
-                    tma_load_2d(sA(stage), &p->ta, &full[stage], p->a_c0 + ka, p->a_r0 + tm * BM);
-                    tma_load_2d(sB(stage), &p->tb, &full[stage], p->b_c0 + kb * G::BK, p->b_r0 + tn * BN);
+                    tma_load_2d(sA(stage), &p->ta, &full[stage], p->a_c0 + ka, p->a_r0 - p->ya + tm * BM);
+                    tma_load_2d(sB(stage), &p->tb, &full[stage], p->b_c0 + kb * G::BK, p->b_r0 - p->yb + tn * BN);
                     if (kb == 0) stamp(c, 2);
                     if (++stage == STAGES) {
                         stage = 0;
@@ -664,7 +665,7 @@ __global__ void __launch_bounds__(Cfg<KIND>::NTHREADS, 1) k_gemm_tc(DevCtx c, co
                         mbar_expect_tx(cfull, uint32_t(nbox) * BM * 128);
                         for (int bx = 0; bx < nbox; ++bx)
                             tma_load_2d(stg + bx * BM * 128, &p.tcm, cfull, p.c_c0 + col0 + bx * box_cols,
-                                        p.c_r0 + tm * BM);
+                                        p.c_r0 - p.yc + tm * BM);
                     }
                 }
                 if (rd == 0) {
@@ -799,7 +800,8 @@ __global__ void __launch_bounds__(Cfg<KIND>::NTHREADS, 1) k_gemm_tc(DevCtx c, co
                 if (leader) stamp(c, 9);
                 if (leader && nbox > 0) {
                     for (int bx = 0; bx < nbox; ++bx)
-                        tma_store_2d(&p.tcm, stg + bx * BM * 128, p.c_c0 + col0 + bx * box_cols, p.c_r0 + tm * BM);
+                        tma_store_2d(&p.tcm, stg + bx * BM * 128, p.c_c0 + col0 + bx * box_cols,
+                                     p.c_r0 - p.yc + tm * BM);
                     bulk_commit();
                 }
             }
@@ -889,13 +891,23 @@ int tc_build_probs(const DevCtx& c, int kind, const std::vector<DevProb>& probs,
         TcProb& p = tp[i];
         // A extent ends at the problem's K edge (an inverse solve's A is the
         // n-wide leaf column block read twice: its extent is n, period a_kwrap)
-        if (!make_map(&p.ta, obuf, f32, c.ldw, d.a_r0 + d.m, d.a_c0 + (d.a_kwrap ? d.n : d.k), BM, err)) return -1;
+        // maps start at the level buffer's first allocated row (the context's
+        // bases are virtual: rows below the window are not memory)
+        const int olv = f32 ? LV_F32 : LV_F16;
+        const int ylo = c.win_lo[olv];
+        const size_t oesz = f32 ? 4 : 2;
+        const void* obase = static_cast<const unsigned char*>(obuf) + size_t(ylo) * size_t(c.ldw) * oesz;
+        p.ya = ylo;
+        if (!make_map(&p.ta, obase, f32, c.ldw, d.a_r0 + d.m - ylo, d.a_c0 + (d.a_kwrap ? d.n : d.k), BM, err))
+            return -1;
+        const bool bw = d.b_buf == BUF_W16 || d.b_buf == BUF_W32;
         const void* bbuf = d.b_buf == BUF_W16 ? static_cast<const void*>(c.w16)
                            : d.b_buf == BUF_W32 ? static_cast<const void*>(c.w32)
-                                                : obuf;
+                                                : obase;
         const long long bld = d.b_buf == BUF_W16 ? kW16Ld : d.b_buf == BUF_W32 ? kW32Ld : c.ldw;
         const bool bf32 = d.b_buf == BUF_W32 || (f32 && d.b_buf != BUF_W16);
-        if (!make_map(&p.tb, bbuf, bf32, bld, d.b_r0 + d.n, d.b_c0 + d.k, BN, err)) return -1;
+        p.yb = bw ? 0 : ylo;
+        if (!make_map(&p.tb, bbuf, bf32, bld, d.b_r0 + d.n - p.yb, d.b_c0 + d.k, BN, err)) return -1;
         {
             const bool cf32 = d.exec_level == LV_F32;
             const void* cbuf = cf32 ? static_cast<const void*>(c.b32) : static_cast<const void*>(c.b16);
@@ -903,7 +915,9 @@ int tc_build_probs(const DevCtx& c, int kind, const std::vector<DevProb>& probs,
                 if (err) *err = "tensor-core GEMM: exec level must be F16 or F32";
                 return -1;
             }
-            if (!make_map(&p.tcm, cbuf, cf32, c.ldw, d.c_r0 + d.m, d.c_c0 + d.n, BM, err)) return -1;
+            p.yc = c.win_lo[cf32 ? LV_F32 : LV_F16];
+            const void* cbase = static_cast<const unsigned char*>(cbuf) + size_t(p.yc) * size_t(c.ldw) * (cf32 ? 4 : 2);
+            if (!make_map(&p.tcm, cbase, cf32, c.ldw, d.c_r0 + d.m - p.yc, d.c_c0 + d.n, BM, err)) return -1;
             // bulk-tensor boxes must start 16-byte aligned in global memory
             p.c_tma = (d.c_c0 * (cf32 ? 4 : 2)) % 16 == 0 && (c.ldw * (cf32 ? 4 : 2)) % 16 == 0;
         }

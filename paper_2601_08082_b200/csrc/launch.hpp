@@ -32,6 +32,9 @@ void launch_dequant(const DevCtx& c, int lv, int r0, int c0, int m, int n, int s
 void launch_gate(volatile int* host_flag, cudaStream_t s);
 void launch_stamp(unsigned long long* out, cudaStream_t s);
 
+// row-major level image of a column-major double block (k_elementwise.cu)
+void launch_level_image(int m, int n, const double* src, long long lds, int level, int lower, void* dst,
+                        long long ldd, cudaStream_t s);
 // spd_generate symmetrization of raw draws (k_elementwise.cu)
 void launch_symmetrize(double* a, long long lda, int n, cudaStream_t s);
 

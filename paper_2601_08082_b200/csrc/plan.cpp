@@ -602,6 +602,40 @@ void Plan::build_deps() {
     }
 }
 
+void Plan::compute_windows() {
+    for (int l = 0; l < 3; ++l) {
+        win_lo[l] = 1 << 30;
+        win_hi[l] = 0;
+    }
+    auto touch = [&](int buf, const Rect& r) {
+        if (buf < 0 || buf > 2 || r.m <= 0) return;
+        win_lo[buf] = std::min(win_lo[buf], r.r0);
+        win_hi[buf] = std::max(win_hi[buf], r.r0 + r.m);
+    };
+    for (const Op& op : ops)
+        for (const Access& a : op.acc) touch(a.buf, a.rect);
+    for (const Block& blk : blocks)
+        if (blk.external) touch(blk.level, blk.rect);
+    for (int l = 0; l < 3; ++l) {
+        if (win_hi[l] <= win_lo[l]) {
+            win_lo[l] = win_hi[l] = 0;
+        } else {
+            needs_buf[l] = true;
+        }
+    }
+}
+
+size_t Plan::device_bytes() const {
+    const size_t esz[3] = {2, 4, 8};
+    const int nr = rows > 0 ? rows : n;
+    size_t total = 0;
+    for (int l = 0; l < 3; ++l)
+        if (needs_buf[l]) total += ((size_t(win_hi[l] - win_lo[l]) * size_t(ldw()) * esz[l] + 255) / 256) * 256;
+    if (needs_w16) total += sizeof(uint16_t) * size_t(nr) * kW16Ld + sizeof(float) * size_t(nr);
+    if (needs_w32) total += sizeof(float) * size_t(nr) * kW32Ld;
+    return total;
+}
+
 Plan Plan::make(int n, int b, const std::vector<int>& levels, bool quantize, int leaf_size,
                 const PlanOptions& opt) {
     if (b < 1) throw std::invalid_argument("leaf size must be >= 1");
@@ -677,6 +711,7 @@ Plan Plan::make(int n, int b, const std::vector<int>& levels, bool quantize, int
     }
     P.finalize_accesses();
     P.build_deps();
+    P.compute_windows();
     return P;
 }
 
@@ -773,7 +808,8 @@ static void check_args(int b, const std::vector<int>& levels) {
         if (l < LV_F16 || l > LV_F64) throw std::invalid_argument("precision level out of range");
 }
 
-Plan Plan::make_trsm(int n1, int m, int b, const std::vector<int>& levels, int leaf_size, const PlanOptions& opt) {
+Plan Plan::make_trsm(int n1, int m, int b, const std::vector<int>& levels, int leaf_size, const PlanOptions& opt,
+                     bool ext) {
     check_args(b, levels);
     if (n1 < 1 || m < 1) throw std::invalid_argument("panel TRSM needs n1, m >= 1");
     Plan P;
@@ -786,6 +822,16 @@ Plan Plan::make_trsm(int n1, int m, int b, const std::vector<int>& levels, int l
     P.quantize = true;
     P.opt = opt;
     P.build_node(0, n1, 1);  // L11 = the big tree's diag1
+    if (ext) {
+        // tree_trsm reads L only through rn_p (kernels.cpp:29, 78): L11 is
+        // supplied as that image, every block at the panel level p, so no
+        // import and no shadow copies; the caller's doubles start at row n1
+        for (Block& blk : P.blocks) {
+            blk.level = P.at_depth(0);
+            blk.external = true;
+        }
+        P.user_row0 = n1;
+    }
     Block pb;
     pb.rect = {n1, 0, m, n1};
     pb.level = P.at_depth(0);
@@ -798,7 +844,7 @@ Plan Plan::make_trsm(int n1, int m, int b, const std::vector<int>& levels, int l
     P.block_order = dfs_blocks(P, 0);
     P.block_order.push_back(pbi);
     for (int i : P.block_order)
-        if (!P.blocks[i].spine_quant) {
+        if (!P.blocks[i].spine_quant && !P.blocks[i].external) {
             Op imp;
             imp.type = OP_IMPORT;
             imp.blocks.push_back(i);
@@ -818,11 +864,12 @@ Plan Plan::make_trsm(int n1, int m, int b, const std::vector<int>& levels, int l
     P.push(std::move(exp));
     P.finalize_accesses();
     P.build_deps();
+    P.compute_windows();
     return P;
 }
 
 Plan Plan::make_syrk_rows(int n2, int k, int b, const std::vector<int>& levels, int row_lo, int row_hi,
-                          const PlanOptions& opt) {
+                          const PlanOptions& opt, bool ext) {
     check_args(b, levels);
     if (n2 < 1 || k < 1 || k > n2 || row_lo < 0 || row_hi > n2 || row_lo >= row_hi)
         throw std::invalid_argument("panel SYRK: bad sizes or row range");
@@ -852,17 +899,27 @@ Plan Plan::make_syrk_rows(int n2, int k, int b, const std::vector<int>& levels, 
         mine.push_back(int(P.blocks.size()));
         P.blocks.push_back(pb);
     }
+    // the solved panel: rows [n2, 2 n2) (ext: rows [row_hi, row_hi + n2),
+    // supplied by the caller as its level image; the problems clipped to
+    // output rows < row_hi read only its rows < row_hi)
+    const int pr0 = ext ? row_hi : n2;
     Block ab;
-    ab.rect = {n2, 0, n2, k};
+    ab.rect = {pr0, 0, n2, k};
     ab.level = p;
+    ab.external = ext;
     const int abi = int(P.blocks.size());
     P.blocks.push_back(ab);
+    if (ext) {
+        P.rows = row_hi + n2;
+        P.user_row0 = row_lo;
+        P.user_rows = row_hi - row_lo;
+    }
     P.has_shadow.assign(P.blocks.size(), std::vector<uint8_t>(3, 0));
     P.has_inverse.assign(P.blocks.size(), 0);
     P.needs_buf[p] = true;
     for (int i : mine) P.needs_buf[P.blocks[i].level] = true;
     P.block_order = mine;
-    P.block_order.push_back(abi);
+    if (!ext) P.block_order.push_back(abi);
     for (int i : P.block_order) {
         Op imp;
         imp.type = OP_IMPORT;
@@ -900,6 +957,7 @@ Plan Plan::make_syrk_rows(int n2, int k, int b, const std::vector<int>& levels, 
     }
     P.finalize_accesses();
     P.build_deps();
+    P.compute_windows();
     return P;
 }
 

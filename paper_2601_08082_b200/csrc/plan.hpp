@@ -61,6 +61,7 @@ struct Block {
     int level = LV_F64;
     bool leaf = false;         // diagonal leaf (lower triangle only)
     bool spine_quant = false;  // quantized from the caller's doubles (see planner)
+    bool external = false;     // values placed in the level buffer by the caller (no import / export)
     int node = -1;
 };
 
@@ -170,6 +171,15 @@ struct Plan {
     // factorization, larger for the distributed panel plans below
     int rows = 0, cols = 0;
     int ext_alpha_slot = -1;  // alpha slot filled from outside before every run (distributed TRSM)
+    // the caller's operand pointer refers to this row: rows below it are
+    // never touched (the compact distributed pieces pass only their rows)
+    int user_row0 = 0;
+    int user_rows = 0;  // rows of the caller's operand (0: rows - user_row0)
+    int caller_rows() const { return user_rows > 0 ? user_rows : (rows > 0 ? rows : n) - user_row0; }
+    // rows [win_lo, win_hi) of each level buffer that any op or external
+    // block touches: only that window is allocated (a virtual base keeps
+    // absolute row coordinates in every kernel)
+    int win_lo[3] = {0, 0, 0}, win_hi[3] = {0, 0, 0};
     std::vector<int> levels;
     bool quantize = true;
     PlanOptions opt;
@@ -204,10 +214,24 @@ struct Plan {
     //    tree_syrk(A22, A21) restricted to output rows [row_lo, row_hi)
     //    (GEMM rows are independent: the restriction changes no element's
     //    arithmetic); only those rows of A22 are imported and exported.
+    //  compact (ext) forms, for N = 131072 on 8 GPUs:
+    //  make_trsm ext: L11 is supplied by the caller directly as its
+    //    panel-level image (rn_p(L11), what tree_trsm reads: kernels.cpp:29,
+    //    78) in the F16/F32 level buffer rows [0, n1); the caller's doubles
+    //    hold only the m panel rows (user_row0 = n1).
+    //  make_syrk_rows ext: the solved panel is supplied by the caller as its
+    //    level image at rows [row_hi, row_hi + n2) (only rows < 2 row_hi are
+    //    read); the caller's doubles hold only A22's rows [row_lo, row_hi)
+    //    (user_row0 = row_lo).
     static Plan make_trsm(int n1, int m, int b, const std::vector<int>& levels, int leaf_size,
-                          const PlanOptions& opt);
+                          const PlanOptions& opt, bool ext = false);
     static Plan make_syrk_rows(int n2, int k, int b, const std::vector<int>& levels, int row_lo, int row_hi,
-                               const PlanOptions& opt);
+                               const PlanOptions& opt, bool ext = false);
+
+    // device bytes the engine allocates for this plan (level windows, leaf
+    // inverses, status words; excludes the launch tables, a few MB)
+    size_t device_bytes() const;
+    long long ldw() const { return (long long)((((cols > 0 ? cols : n) + 63) / 64) * 64); }
 
     int at_depth(int d) const { return levels[d < int(levels.size()) ? d : int(levels.size()) - 1]; }
     int leaf_level() const { return levels.back(); }
@@ -239,6 +263,7 @@ struct Plan {
     int gemm_class(int op_level, int exec_level, const GemmProb* g) const;
     void finalize_accesses();
     void build_deps();
+    void compute_windows();
 };
 
 // static flop count (analysis.cpp:64-120 StaticCounter restated)
