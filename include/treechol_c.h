@@ -313,6 +313,14 @@ int tc_debug_gemm(int gclass, int m, int n, int k, int lower, double beta, int e
  * issued) */
 int tc_debug_gemm_stamps(unsigned long long* out15);
 
+/* development: FP64 FLOP/s of the whole GPU, `ctas` CTAs of 256 threads
+ * issuing `iters` x 4 independent instructions per warp: kind 0 DMMA
+ * (mma.sync m8n8k4 f64, the FP64 tensor pipe), 1 DFMA (SIMT).  The
+ * denominator of the FP64 rooflines (profiles/r02_fp64_peak.json). */
+double tc_debug_fp64_probe(int kind, int iters, int ctas);
+/* development: FMA/s of one SM on mma.sync (0 tf32 m16n8k8, 1 f16 m16n8k16) */
+double tc_debug_mma_probe(int kind, int iters);
+
 /* process-wide kernel settings for measurements: "tc_kchunk" = K chunk
  * (elements) of FP32-exec tensor-core accumulations, 0 = one accumulation.
  * Applies to plans built (graphs captured) afterwards. */

@@ -135,6 +135,8 @@ def _load():
         "tc_gemm_problem_device": (I, [I, P, P, P, C.c_longlong, PI, D, D, P]),
         "tc_set_global_option": (I, [C.c_char_p, I]),
         "tc_debug_gemm_stamps": (I, [C.POINTER(C.c_uint64)]),
+        "tc_debug_fp64_probe": (D, [I, I, I]),
+        "tc_debug_mma_probe": (D, [I, I]),
         "tc_plan_create_trsm": (I, [I, I, I, PI, I, I, C.POINTER(P)]),
         "tc_plan_create_syrk_rows": (I, [I, I, I, PI, I, I, I, C.POINTER(P)]),
         "tc_plan_set_external_absmax": (I, [P, D]),

@@ -80,7 +80,8 @@ def synthetic_spd_device(n: int, seed: int, device="cuda"):
 
 
 def run_batch_on_rank(count: int, n: int, b: int, config, seed0: int = 0, nrhs: int = 1, concurrency: int = 8,
-                      world: int = 1, rank: int = 0, group=None, check: int = 1, in_flight: int = 16):
+                      world: int = 1, rank: int = 0, group=None, check: int = 1, in_flight: int = 16,
+                      options: dict | None = None):
     """factor + solve this rank's share of a batch of `count` systems
     A_k = spd_generate(n, seed0 + k) (bit-identical), b_k = A_k * ones.
     Returns (local ShardResult, reduced ShardResult, flops per system)."""
@@ -88,6 +89,8 @@ def run_batch_on_rank(count: int, n: int, b: int, config, seed0: int = 0, nrhs: 
     import paper_2601_08082_b200 as tc
     mine = shard(count, world, rank)
     batch = tc.Batch(n, b, config, True, concurrency)
+    for k, v in (options or {}).items():
+        batch.set_option(k, v)
     # warm-up (untimed): builds every plan's workspace and CUDA graph
     warm = [synthetic_spd_device(n, seed0 + 10 ** 6 + k) for k in range(concurrency)]
     wb = [a.sum(dim=0, keepdim=True).repeat(nrhs, 1).contiguous() for a in warm]

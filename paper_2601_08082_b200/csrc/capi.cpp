@@ -190,6 +190,49 @@ int tc_plan_stats(const tc_plan* plan, int* n_ops, int* n_launches, int* n_gemm_
     return TC_OK;
 }
 
+}  // extern "C"
+
+namespace tcb {
+// plan-level options (they change the op list): rebuild the engine's plan
+// with the option applied, keeping its run settings.  1 = applied, 0 = not a
+// plan-level key, -1 = error (*err)
+int apply_plan_option(std::unique_ptr<Engine>& eng, const std::string& k, int value, std::string* err) {
+    static const char* keys[] = {"use_tc", "use_tc32", "inverse_trsm", "fuse_checks", "mma32_max_log2",
+                                 "mma32w_max_log2", "syrk_split_min", "shadow_per_block", "sub32_max_rows"};
+    bool known = false;
+    for (const char* x : keys) known = known || k == x;
+    if (!known) return 0;
+    Engine& e = *eng;
+    if (e.ready()) {
+        *err = k + " must be set before the first run";
+        return -1;
+    }
+    PlanOptions po = e.plan.opt;
+    if (k == "use_tc") po.use_tc = value != 0;
+    else if (k == "use_tc32") po.use_tc32 = value != 0;
+    else if (k == "inverse_trsm") po.inverse_trsm = value != 0;
+    else if (k == "fuse_checks") po.fuse_checks = value != 0;
+    // FP32 GEMMs (in-place solves) with m*n*k <= 2^value run on mma.sync (negative: never)
+    else if (k == "mma32_max_log2") po.mma32_max = value < 0 ? -1.0 : std::ldexp(1.0, value);
+    else if (k == "mma32w_max_log2") po.mma32w_max = value < 0 ? -1.0 : std::ldexp(1.0, value);
+    else if (k == "syrk_split_min") po.syrk_split_min = value < 1 ? (1 << 30) : value;
+    else if (k == "sub32_max_rows") po.sub32_max_rows = value < 0 ? 0 : value;
+    else po.shadow_per_block = value != 0;
+    Plan p = Plan::make(e.plan.n, e.plan.b, e.plan.levels, e.plan.quantize, e.plan.leaf_size, po);
+    const bool g = e.use_graph, dg = e.dag_graph;
+    const int s = e.n_streams, bt = e.bulk_tiles_per_cta, bm = e.bulk_max_ctas;
+    eng = std::make_unique<Engine>(std::move(p));
+    eng->use_graph = g;
+    eng->dag_graph = dg;
+    eng->n_streams = s;
+    eng->bulk_tiles_per_cta = bt;
+    eng->bulk_max_ctas = bm;
+    return 1;
+}
+}  // namespace tcb
+
+extern "C" {
+
 int tc_plan_set_option(tc_plan* plan, const char* key, int value) {
     if (!plan || !key) return fail(TC_INVALID_ARGUMENT, "null argument");
     Engine& e = *plan->eng;
@@ -208,52 +251,20 @@ int tc_plan_set_option(tc_plan* plan, const char* key, int value) {
         (k == "bulk_tiles_per_cta" ? e.bulk_tiles_per_cta : e.bulk_max_ctas) = value < 0 ? 0 : value;
         return TC_OK;
     }
+    if (k == "dev_skip") {  // development: see Engine::dev_skip
+        if (e.ready() && e.use_graph) return fail(TC_INVALID_ARGUMENT, k + " must be set before the first run");
+        e.dev_skip = value;
+        return TC_OK;
+    }
     if (k == "n_streams") {
         if (e.ready()) return fail(TC_INVALID_ARGUMENT, "n_streams must be set before the first run");
         e.n_streams = value < 1 ? 1 : value;
         return TC_OK;
     }
-    if (k == "use_tc" || k == "use_tc32" || k == "inverse_trsm" || k == "fuse_checks") {
-        if (e.ready()) return fail(TC_INVALID_ARGUMENT, k + " must be set before the first run");
-        PlanOptions po = e.plan.opt;
-        bool& field = k == "use_tc"       ? po.use_tc
-                      : k == "use_tc32"   ? po.use_tc32
-                      : k == "inverse_trsm" ? po.inverse_trsm
-                                          : po.fuse_checks;
-        if (bool(value) == field) return TC_OK;
-        field = value != 0;
-        Plan p = Plan::make(e.plan.n, e.plan.b, e.plan.levels, e.plan.quantize, e.plan.leaf_size, po);
-        const bool g = e.use_graph;
-        const int s = e.n_streams;
-        plan->eng = std::make_unique<Engine>(std::move(p));
-        plan->eng->use_graph = g;
-        plan->eng->n_streams = s;
-        return TC_OK;
-    }
-    if (k == "mma32_max_log2" || k == "mma32w_max_log2") {  // FP32 GEMMs (in-place solves) with m*n*k <= 2^value run on mma.sync (negative: never)
-        if (e.ready()) return fail(TC_INVALID_ARGUMENT, k + " must be set before the first run");
-        PlanOptions po = e.plan.opt;
-        (k == "mma32_max_log2" ? po.mma32_max : po.mma32w_max) = value < 0 ? -1.0 : std::ldexp(1.0, value);
-        Plan p = Plan::make(e.plan.n, e.plan.b, e.plan.levels, e.plan.quantize, e.plan.leaf_size, po);
-        const bool g = e.use_graph;
-        const int s = e.n_streams;
-        plan->eng = std::make_unique<Engine>(std::move(p));
-        plan->eng->use_graph = g;
-        plan->eng->n_streams = s;
-        return TC_OK;
-    }
-    if (k == "syrk_split_min") {
-        if (e.ready()) return fail(TC_INVALID_ARGUMENT, k + " must be set before the first run");
-        PlanOptions po = e.plan.opt;
-        po.syrk_split_min = value < 1 ? (1 << 30) : value;
-        Plan p = Plan::make(e.plan.n, e.plan.b, e.plan.levels, e.plan.quantize, e.plan.leaf_size, po);
-        const bool g = e.use_graph;
-        const int s = e.n_streams;
-        plan->eng = std::make_unique<Engine>(std::move(p));
-        plan->eng->use_graph = g;
-        plan->eng->n_streams = s;
-        return TC_OK;
-    }
+    std::string err;
+    const int r = apply_plan_option(plan->eng, k, value, &err);
+    if (r == 1) return TC_OK;
+    if (r < 0) return fail(TC_INVALID_ARGUMENT, err);
     return fail(TC_INVALID_ARGUMENT, "unknown option '" + k + "'");
 }
 

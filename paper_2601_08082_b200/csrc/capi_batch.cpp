@@ -24,6 +24,7 @@ using namespace tcb;
 
 namespace tcb {
 void set_last_error(const std::string& msg);  // capi.cpp
+int apply_plan_option(std::unique_ptr<Engine>& eng, const std::string& k, int value, std::string* err);  // capi.cpp
 }
 
 struct tc_batch {
@@ -93,6 +94,10 @@ int tc_batch_set_option(tc_batch* bt, const char* key, int value) {
     }
     for (auto& e : bt->eng) {
         if (e->ready()) return bfail(TC_INVALID_ARGUMENT, k + " must be set before the first run");
+        std::string err;
+        const int r = apply_plan_option(e, k, value, &err);
+        if (r < 0) return bfail(TC_INVALID_ARGUMENT, err);
+        if (r == 1) continue;
         if (k == "bulk_tiles_per_cta") e->bulk_tiles_per_cta = value < 0 ? 0 : value;
         else if (k == "dag_graph") e->dag_graph = value != 0;
         else if (k == "use_graph") e->use_graph = value != 0;

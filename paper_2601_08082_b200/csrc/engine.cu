@@ -205,6 +205,10 @@ void Engine::launch_op(int i, cudaStream_t s) {
     const OpLaunch& L = launch_[i];
     const Rect& r = op.rect;
     unsigned char* tab = d_arena_ + L.offset;
+    if (dev_skip && ((dev_skip >> op.type) & 1 || (op.type == OP_GEMM && (dev_skip >> (16 + op.gclass)) & 1))) {
+        launch_noop(s);
+        return;
+    }
     switch (op.type) {
         case OP_IMPORT: launch_import(ctx_, reinterpret_cast<BlockDesc*>(tab), L.count, L.tiles, s); break;
         case OP_EXPORT: launch_export(ctx_, reinterpret_cast<BlockDesc*>(tab), L.count, L.tiles, s); break;

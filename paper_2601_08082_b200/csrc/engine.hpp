@@ -43,6 +43,10 @@ class Engine {
     Plan plan;
     bool use_graph = true;
     int n_streams = 6;
+    // development (measurements only; results are garbage): ops whose type
+    // bit (1 << OpType) or GEMM class bit (1 << (16 + GemmClass)) is set
+    // launch an empty kernel instead
+    int dev_skip = 0;
     int bulk_tiles_per_cta = 1;  // trailing-update GEMMs: 0 persistent, else tiles per CTA (1: SMs free up after every tile, so concurrent work -- other systems of a batch, the factorization chain -- gets them)
     int bulk_max_ctas = 0;       // persistent trailing-update GEMMs: CTA cap (0 = one per SM)
     bool dag_graph = true;       // explicit DAG graph (else: captured multi-stream enqueue)

@@ -237,21 +237,24 @@ __global__ void __launch_bounds__(256) k_quant2(DevCtx c, int lv, int r0, int c0
 __global__ void __launch_bounds__(256) k_dequant(DevCtx c, int lv, int r0, int c0, int m, int n, int slot,
                                                  uint32_t chk_seq) {
     const double alpha = slot_alpha(c, lv, slot);
-    if (alpha == 1.0) return;  // tree.cpp:98
-    const int j = blockIdx.x * 256 + threadIdx.x;
+    if (alpha == 1.0) return;  // tree.cpp:98 (the common case: a bounded grid, so the no-op launch is short)
     unsigned long long bad = ~0ull;
-    if (j < n)
-        for (int ii = 0; ii < 16; ++ii) {
-            const int i = blockIdx.y * 16 + ii;
-            if (i >= m) break;
-            const long long off = (long long)(r0 + i) * c.ldw + c0 + j;
-            const double v = load_level(c, lv, off) * alpha;
-            store_level(c, lv, off, v);
-            if (!isfinite(round_level(lv, v))) {
-                const unsigned long long k = fail_key(chk_seq, elem_local(i, j));
-                bad = k < bad ? k : bad;
+    const int cols = (n + 255) / 256, items = cols * ((m + 15) / 16);
+    for (int it = blockIdx.x; it < items; it += gridDim.x) {
+        const int j = (it % cols) * 256 + threadIdx.x, i0 = (it / cols) * 16;
+        if (j < n)
+            for (int ii = 0; ii < 16; ++ii) {
+                const int i = i0 + ii;
+                if (i >= m) break;
+                const long long off = (long long)(r0 + i) * c.ldw + c0 + j;
+                const double v = load_level(c, lv, off) * alpha;
+                store_level(c, lv, off, v);
+                if (!isfinite(round_level(lv, v))) {
+                    const unsigned long long k = fail_key(chk_seq, elem_local(i, j));
+                    bad = k < bad ? k : bad;
+                }
             }
-        }
+    }
     if (chk_seq) warp_report_min(c, bad);
 }
 
@@ -374,7 +377,8 @@ void launch_quant(const DevCtx& c, int lv, int r0, int c0, int m, int n, int slo
 }
 void launch_dequant(const DevCtx& c, int lv, int r0, int c0, int m, int n, int slot, uint32_t chk_seq,
                     cudaStream_t s) {
-    dim3 g((n + 255) / 256, (m + 15) / 16);
+    const long long items = (long long)((n + 255) / 256) * ((m + 15) / 16);
+    const int g = int(items < 148 * 8 ? items : 148 * 8);
     k_dequant<<<g, 256, 0, s>>>(c, lv, r0, c0, m, n, slot, chk_seq);
 }
 
@@ -392,6 +396,7 @@ __global__ void k_gate(volatile int* flag) {
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     } while (*flag == 0 && t - t0 < 5000000000ull);
 }
+__global__ void k_noop() {}
 // development trace: the global timer (ns) when this node runs
 __global__ void k_stamp(unsigned long long* out) {
     unsigned long long t;
@@ -400,5 +405,6 @@ __global__ void k_stamp(unsigned long long* out) {
 }
 }  // namespace
 void launch_gate(volatile int* host_flag, cudaStream_t s) { k_gate<<<1, 1, 0, s>>>(host_flag); }
+void launch_noop(cudaStream_t s) { k_noop<<<1, 32, 0, s>>>(); }
 void launch_stamp(unsigned long long* out, cudaStream_t s) { k_stamp<<<1, 1, 0, s>>>(out); }
 }  // namespace tcb

@@ -29,6 +29,7 @@ void launch_dequant(const DevCtx& c, int lv, int r0, int c0, int m, int n, int s
                     cudaStream_t s);
 
 // spin until *host_flag (mapped pinned memory) becomes non-zero (profiling)
+void launch_noop(cudaStream_t s);
 void launch_gate(volatile int* host_flag, cudaStream_t s);
 void launch_stamp(unsigned long long* out, cudaStream_t s);
 

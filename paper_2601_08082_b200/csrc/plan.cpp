@@ -109,12 +109,27 @@ void Plan::ensure_shadows(int node, int p) {
     }
     if (todo.empty()) return;
     std::sort(todo.begin(), todo.end());
+    needs_buf[p] = true;
+    if (opt.shadow_per_block) {
+        // one op per block: the TRSM that reads the shadow (its leaf solves
+        // and GEMMs walk lnode's tree block by block) starts on a block as
+        // soon as that block of L is final, i.e. it pipelines with the
+        // factorization of lnode instead of waiting for all of it
+        for (int blk : todo) {
+            Op op;
+            op.type = OP_SHADOW;
+            op.level = p;
+            op.blocks = {blk};
+            op.rect = blocks[blk].rect;
+            push(std::move(op));
+        }
+        return;
+    }
     Op op;
     op.type = OP_SHADOW;
     op.level = p;
     op.blocks = todo;
     for (int blk : todo) op.rect = op.rect.unite(blocks[blk].rect);
-    needs_buf[p] = true;
     push(std::move(op));
 }
 
@@ -136,7 +151,8 @@ void Plan::emit_trsm(Rect B, int p, int lnode) {
         const bool inv16 = opt.use_tc && opt.inverse_trsm && p == LV_F16 && L.leaf && L.n <= kW16Lo &&
                            B.m >= kInvMinRows && B.c0 % 8 == 0 && L.r0 % 8 == 0;
         const bool inv32 = opt.use_tc && opt.use_tc32 && opt.inverse_trsm && p == LV_F32 && L.leaf &&
-                           L.n <= kW32Ld && L.n % 32 == 0 && B.c0 % 4 == 0 && L.r0 % 4 == 0;
+                           L.n <= kW32Ld && L.n % 32 == 0 && B.c0 % 4 == 0 && L.r0 % 4 == 0 &&
+                           B.m > opt.sub32_max_rows;
         if (inv16 || inv32) {
             const int lb = nodes[lnode].block;
             const uint8_t bit = inv16 ? 1 : 2;

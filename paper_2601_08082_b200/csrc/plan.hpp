@@ -162,6 +162,8 @@ struct PlanOptions {
     double mma32_max = 16777216.0;  // m*n*k at or below which they run on mma.sync instead (2^24: the 256^3 leaf-level ones; 2^26 is 3% faster for one N=16384 factorization but 5% slower for the C4 batch)
     bool inverse_trsm = true; // FP16 leaf solves with m >= kInvMinRows as tcgen05 GEMMs
     bool fuse_checks = true;  // require_finite inside the producing kernels
+    int sub32_max_rows = 0;  // F32 leaf solves of at most this many rows by substitution (k_trsm_cm) instead of inverse + GEMM
+    bool shadow_per_block = true;  // one OP_SHADOW per block of L (pipelines the lower-level TRSM with the factorization it reads)
     int syrk_split_min = 1 << 30; // tree_syrk nodes at least this large launch per region (lookahead; off by default: it shortens the critical path but adds launches, a net loss for batches)
 };
 
