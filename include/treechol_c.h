@@ -318,6 +318,12 @@ int tc_debug_gemm_stamps(unsigned long long* out15);
  * (mma.sync m8n8k4 f64, the FP64 tensor pipe), 1 DFMA (SIMT).  The
  * denominator of the FP64 rooflines (profiles/r02_fp64_peak.json). */
 double tc_debug_fp64_probe(int kind, int iters, int ctas);
+/* development: accumulated phase cycles of the leaf kernels since the last
+ * reset (CTA 0 of each launch).  potrf: load, a, b1, b2, store, launches;
+ * inverse: load, reciprocals, diagonal inverses, products, triangular
+ * multiplies, store, launches */
+int tc_debug_potrf_clocks(long long* out8, int reset);
+int tc_debug_inv_clocks(long long* out8, int reset);
 /* development: FMA/s of one SM on mma.sync (0 tf32 m16n8k8, 1 f16 m16n8k16) */
 double tc_debug_mma_probe(int kind, int iters);
 

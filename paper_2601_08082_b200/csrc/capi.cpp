@@ -219,11 +219,12 @@ int apply_plan_option(std::unique_ptr<Engine>& eng, const std::string& k, int va
     else if (k == "sub32_max_rows") po.sub32_max_rows = value < 0 ? 0 : value;
     else po.shadow_per_block = value != 0;
     Plan p = Plan::make(e.plan.n, e.plan.b, e.plan.levels, e.plan.quantize, e.plan.leaf_size, po);
-    const bool g = e.use_graph, dg = e.dag_graph;
+    const bool g = e.use_graph, dg = e.dag_graph, pdl = e.use_pdl;
     const int s = e.n_streams, bt = e.bulk_tiles_per_cta, bm = e.bulk_max_ctas;
     eng = std::make_unique<Engine>(std::move(p));
     eng->use_graph = g;
     eng->dag_graph = dg;
+    eng->use_pdl = pdl;
     eng->n_streams = s;
     eng->bulk_tiles_per_cta = bt;
     eng->bulk_max_ctas = bm;
@@ -249,6 +250,11 @@ int tc_plan_set_option(tc_plan* plan, const char* key, int value) {
     if (k == "bulk_tiles_per_cta" || k == "bulk_max_ctas") {
         if (e.ready() && e.use_graph) return fail(TC_INVALID_ARGUMENT, k + " must be set before the first run");
         (k == "bulk_tiles_per_cta" ? e.bulk_tiles_per_cta : e.bulk_max_ctas) = value < 0 ? 0 : value;
+        return TC_OK;
+    }
+    if (k == "use_pdl") {
+        if (e.ready() && e.use_graph) return fail(TC_INVALID_ARGUMENT, k + " must be set before the first run");
+        e.use_pdl = value != 0;
         return TC_OK;
     }
     if (k == "dev_skip") {  // development: see Engine::dev_skip
@@ -737,5 +743,12 @@ extern "C" int tc_debug_potrf_clocks(long long* out8, int reset) {
 }
 extern "C" int tc_debug_leaf_clocks(long long* out4, int reset) {
     tcb::leaf_debug_clocks(out4, reset != 0);
+    return TC_OK;
+}
+namespace tcb {
+void inv_debug_clocks(long long* out, bool reset);
+}
+extern "C" int tc_debug_inv_clocks(long long* out8, int reset) {
+    tcb::inv_debug_clocks(out8, reset != 0);
     return TC_OK;
 }

@@ -100,6 +100,7 @@ int tc_batch_set_option(tc_batch* bt, const char* key, int value) {
         if (r == 1) continue;
         if (k == "bulk_tiles_per_cta") e->bulk_tiles_per_cta = value < 0 ? 0 : value;
         else if (k == "dag_graph") e->dag_graph = value != 0;
+        else if (k == "use_pdl") e->use_pdl = value != 0;
         else if (k == "use_graph") e->use_graph = value != 0;
         else return bfail(TC_INVALID_ARGUMENT, "unknown option '" + k + "'");
     }

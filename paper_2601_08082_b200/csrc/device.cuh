@@ -122,6 +122,13 @@ __device__ __forceinline__ double round_level(int lv, double x) {
     return x;
 }
 
+// programmatic dependent launch: every factorization kernel waits here
+// before it reads anything a preceding kernel wrote (a no-op unless it was
+// launched through a programmatic graph edge); chain kernels signal their
+// dependents near their end so those are scheduled while they finish
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ double range_max(int lv) {
     return lv == 0 ? 65504.0 : lv == 1 ? 3.4028234663852886e38 : 1.7976931348623157e308;
 }

@@ -461,6 +461,10 @@ bool Engine::enqueue(const double* a_in, long long lda_in, double* l_out, long l
     return true;
 }
 
+// any kernel may be the source of a programmatic edge (it triggers its
+// dependents explicitly near its end, or implicitly when it exits)
+bool Engine::pdl_src_ok(int) const { return true; }
+
 bool Engine::build_dag_graph(cudaGraph_t* out, int phase, std::string* err) {
     *out = nullptr;
     // phase >= 0: only the ops of that host-path phase (edges to earlier
@@ -476,30 +480,56 @@ bool Engine::build_dag_graph(cudaGraph_t* out, int phase, std::string* err) {
     TC_TRY(cudaStreamCreateWithPriority(&cap_lo, cudaStreamNonBlocking, lo));
     bool ok = true;
     std::string e2;
-    // capture fn on stream s into a child graph and add it with deps
-    auto add = [&](cudaStream_t s, const std::vector<cudaGraphNode_t>& deps, auto&& fn,
-                   cudaGraphNode_t* node) -> bool {
+    // op index -> 1 if its node is a plain kernel node (programmatic edges
+    // need a kernel node on both ends)
+    std::vector<char> is_kernel(size_t(N), 0);
+    // capture fn on stream s and add it with deps: a single kernel launch
+    // becomes a kernel node of g (its parameters copied from the capture),
+    // anything else a child-graph node.  pdl[j] != 0: the edge from deps[j]
+    // is programmatic (the kernel may launch while deps[j] finishes and
+    // waits for it in griddepcontrol.wait)
+    auto add = [&](cudaStream_t s, const std::vector<cudaGraphNode_t>& deps, auto&& fn, cudaGraphNode_t* node,
+                   const std::vector<char>* pdl = nullptr, bool* kernel_node = nullptr) -> bool {
         cudaGraph_t child = nullptr;
         if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return false;
         fn(s);
         if (cudaStreamEndCapture(s, &child) != cudaSuccess || !child) return false;
         // the scheduling priority of the capture stream, made explicit on
         // every kernel node: the chain's CTAs go first when SMs free up
+        cudaKernelNodeAttrValue pv{};
+        pv.priority = s == cap_hi ? hi : lo;
         size_t nn = 0;
         cudaGraphGetNodes(child, nullptr, &nn);
         std::vector<cudaGraphNode_t> kids(nn);
         if (nn) cudaGraphGetNodes(child, kids.data(), &nn);
+        int nk = 0;
         for (cudaGraphNode_t k : kids) {
             cudaGraphNodeType ty;
             if (cudaGraphNodeGetType(k, &ty) == cudaSuccess && ty == cudaGraphNodeTypeKernel) {
-                cudaKernelNodeAttrValue v{};
-                v.priority = s == cap_hi ? hi : lo;
-                cudaGraphKernelNodeSetAttribute(k, cudaKernelNodeAttributePriority, &v);
+                ++nk;
+                cudaGraphKernelNodeSetAttribute(k, cudaKernelNodeAttributePriority, &pv);
             }
         }
         cudaGetLastError();
-        const cudaError_t e =
-            cudaGraphAddChildGraphNode(node, g, deps.empty() ? nullptr : deps.data(), deps.size(), child);
+        cudaError_t e = cudaErrorUnknown;
+        if (use_pdl && nn == 1 && nk == 1) {
+            cudaKernelNodeParams kp{};
+            e = cudaGraphKernelNodeGetParams(kids[0], &kp);
+            if (e == cudaSuccess) e = cudaGraphAddKernelNode(node, g, nullptr, 0, &kp);
+            if (e == cudaSuccess) e = cudaGraphKernelNodeSetAttribute(*node, cudaKernelNodeAttributePriority, &pv);
+            for (size_t j = 0; e == cudaSuccess && j < deps.size(); ++j) {
+                cudaGraphEdgeData ed{};
+                if (pdl && (*pdl)[j]) {
+                    ed.from_port = cudaGraphKernelNodePortProgrammatic;
+                    ed.type = cudaGraphDependencyTypeProgrammatic;
+                }
+                e = cudaGraphAddDependencies_v2(g, &deps[j], node, &ed, 1);
+            }
+            if (kernel_node) *kernel_node = e == cudaSuccess;
+        } else {
+            e = cudaGraphAddChildGraphNode(node, g, deps.empty() ? nullptr : deps.data(), deps.size(), child);
+            if (kernel_node) *kernel_node = false;
+        }
         cudaGraphDestroy(child);
         return e == cudaSuccess;
     };
@@ -518,10 +548,24 @@ bool Engine::build_dag_graph(cudaGraph_t* out, int phase, std::string* err) {
         if (!in(i)) continue;
         const Op& op = plan.ops[i];
         std::vector<cudaGraphNode_t> deps;
+        std::vector<char> pdl;
+        // programmatic edges into the chain's ops (not the bulk trailing
+        // updates, whose waiting CTAs would hold SMs the chain needs), from
+        // kernel nodes only
+        const bool pdl_dst = use_pdl && !op.bulk && !d_trace_;
         for (int d : op.deps)
-            if (in(d)) deps.push_back(node[size_t(d)]);
-        if (deps.empty() && root) deps.push_back(root);
-        ok = add(op.bulk ? cap_lo : cap_hi, deps, [&](cudaStream_t s) { launch_op(i, s); }, &node[size_t(i)]);
+            if (in(d)) {
+                deps.push_back(node[size_t(d)]);
+                pdl.push_back(pdl_dst && is_kernel[size_t(d)] && pdl_src_ok(d));
+            }
+        if (deps.empty() && root) {
+            deps.push_back(root);
+            pdl.push_back(0);
+        }
+        bool kn = false;
+        ok = add(op.bulk ? cap_lo : cap_hi, deps, [&](cudaStream_t s) { launch_op(i, s); }, &node[size_t(i)], &pdl,
+                 &kn);
+        is_kernel[size_t(i)] = kn;
     }
     if (d_trace_)
         for (int i = 0; i < N; ++i) stamp(node[size_t(i)], 1 + i);

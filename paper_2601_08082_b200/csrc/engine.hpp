@@ -47,6 +47,12 @@ class Engine {
     // bit (1 << OpType) or GEMM class bit (1 << (16 + GemmClass)) is set
     // launch an empty kernel instead
     int dev_skip = 0;
+    // DAG graph: single-kernel ops as kernel nodes, with programmatic
+    // dependent launch (PDL) on the edges into the chain's ops: the kernel
+    // is launched while its producer finishes and waits in
+    // griddepcontrol.wait (every factorization kernel starts with it)
+    bool use_pdl = false;  // measured no faster (N=16384 12.62 -> 12.80 ms, C4 425 -> 420 TF/s): off
+    bool pdl_src_ok(int i) const;
     int bulk_tiles_per_cta = 1;  // trailing-update GEMMs: 0 persistent, else tiles per CTA (1: SMs free up after every tile, so concurrent work -- other systems of a batch, the factorization chain -- gets them)
     int bulk_max_ctas = 0;       // persistent trailing-update GEMMs: CTA cap (0 = one per SM)
     bool dag_graph = true;       // explicit DAG graph (else: captured multi-stream enqueue)

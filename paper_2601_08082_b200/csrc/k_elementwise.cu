@@ -24,6 +24,7 @@ constexpr int TB = 64;  // block-table tile side (import / export / shadow)
 constexpr int TBR = (TB * TB) / 256;  // elements per thread per tile
 
 __global__ void __launch_bounds__(256) k_import(DevCtx c, const BlockDesc* blocks, int nb, int tiles) {
+    pdl_wait();
     __shared__ double tile[TB][TB + 1];
     const int tx = threadIdx.x & (TB - 1), ty = threadIdx.x / TB;  // ty in [0, 4)
     for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
@@ -54,33 +55,110 @@ __global__ void __launch_bounds__(256) k_import(DevCtx c, const BlockDesc* block
     }
 }
 
+// export: 64x64 tiles, 16-byte accesses on both sides.  Thread (r, q) =
+// (tid / 4, tid % 4) reads 16 consecutive row-major elements of row r
+// (2 / 4 / 8 vector loads for F16 / F32 / F64, all issued before the first
+// shared-memory store), converts them to double and stores them transposed
+// (tile[col][row], an even row pitch so double2 reads stay aligned; rows
+// offset by 8 per 16-column quarter so the 32 lanes of a store hit every
+// bank pair twice, the minimum for doubles); then each warp
+// writes 8 columns as 512-byte runs of double2 (lanes along the rows).
+// Edge and diagonal tiles (and unaligned operands) take per-element paths.
+constexpr int EX_LD = TB + 2;
+__device__ __forceinline__ int ex_phys(int c, int r) { return c * EX_LD + ((r + 8 * (c >> 4)) & (TB - 1)); }
+
 __global__ void __launch_bounds__(256) k_export(DevCtx c, const BlockDesc* blocks, int nb, int tiles) {
-    // 32x32 sub-tiles of the 64x64 table tiles, each its own grid-stride
-    // work item (measured faster than the 64-wide transpose for this
-    // direction: F16 row reads, F64 column writes)
-    __shared__ double tile[TS][TS + 1];
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-    for (int t4 = blockIdx.x; t4 < 4 * tiles; t4 += gridDim.x) {
-        const int t = t4 >> 2, q = t4 & 3;
+    pdl_wait();
+    __shared__ __align__(16) double tile[TB * EX_LD];
+    const int tid = threadIdx.x, r = tid >> 2, q = tid & 3, lane = tid & 31, warp = tid >> 5;
+    double* l = c.ra->l_out;
+    const long long ldl = c.ra->lda_out;
+    const bool out_vec = (ldl % 2 == 0) && ((reinterpret_cast<uintptr_t>(l) & 15) == 0);
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
         const BlockDesc bd = blocks[find_block(blocks, nb, t)];
         const int lt = t - bd.tile0;
-        double* l = c.ra->l_out;
-        const long long ldl = c.ra->lda_out;
-        const int i0 = (lt / bd.tiles_n) * TB + (q >> 1) * TS, j0 = (lt % bd.tiles_n) * TB + (q & 1) * TS;
-        if (i0 >= bd.m || j0 >= bd.n) continue;  // uniform per CTA
+        const int i0 = (lt / bd.tiles_n) * TB, j0 = (lt % bd.tiles_n) * TB;
+        const int mi = min(TB, bd.m - i0), nj = min(TB, bd.n - j0);
+        // ---- row-major level buffer -> registers (16 elements per thread)
+        double v[16];
+        const int i = i0 + r, jq = j0 + 16 * q;
+        const long long off = (long long)(bd.r0 + i) * c.ldw + bd.c0 + jq;
+        const bool row_in = r < mi;
+        const int cnt = row_in ? max(0, min(16, nj - 16 * q)) : 0;
+        if (bd.level == 0) {
+            const __half* p = c.b16 + off;
+            if (cnt == 16 && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+                uint4 w[2];
+                w[0] = __ldcs(reinterpret_cast<const uint4*>(p));
+                w[1] = __ldcs(reinterpret_cast<const uint4*>(p) + 1);
+                const __half2* h = reinterpret_cast<const __half2*>(w);
 #pragma unroll
-        for (int r = 0; r < TS; r += 8) {
-            const int i = i0 + ty + r, j = j0 + tx;
-            double v = 0.0;
-            if (i < bd.m && j < bd.n) v = load_level(c, bd.level, (long long)(bd.r0 + i) * c.ldw + bd.c0 + j);
-            tile[ty + r][tx] = v;
+                for (int e = 0; e < 8; ++e) {
+                    const float2 f = __half22float2(h[e]);
+                    v[2 * e] = f.x;
+                    v[2 * e + 1] = f.y;
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < 16; ++e) v[e] = e < cnt ? to_d(p[e]) : 0.0;
+            }
+        } else if (bd.level == 1) {
+            const float* p = c.b32 + off;
+            if (cnt == 16 && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+                float4 w[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) w[k] = __ldcs(reinterpret_cast<const float4*>(p) + k);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    v[4 * k] = w[k].x;
+                    v[4 * k + 1] = w[k].y;
+                    v[4 * k + 2] = w[k].z;
+                    v[4 * k + 3] = w[k].w;
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < 16; ++e) v[e] = e < cnt ? double(p[e]) : 0.0;
+            }
+        } else {
+            const double* p = c.b64 + off;
+            if (cnt == 16 && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+                double2 w[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) w[k] = __ldcs(reinterpret_cast<const double2*>(p) + k);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    v[2 * k] = w[k].x;
+                    v[2 * k + 1] = w[k].y;
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < 16; ++e) v[e] = e < cnt ? p[e] : 0.0;
+            }
         }
-        __syncthreads();
 #pragma unroll
-        for (int r = 0; r < TS; r += 8) {
-            const int i = i0 + tx, j = j0 + ty + r;
-            if (i < bd.m && j < bd.n && !(bd.lower && j > i))
-                l[(long long)(bd.c0 + j) * ldl + bd.r0 + i] = tile[tx][ty + r];
+        for (int e = 0; e < 16; ++e) tile[ex_phys(16 * q + e, r)] = v[e];
+        __syncthreads();
+        // ---- column-major doubles: warp w writes columns 8w .. 8w+7
+        const bool full = mi == TB && nj == TB && !(bd.lower && j0 + TB - 1 > i0);
+        const long long base = (long long)(bd.c0 + j0) * ldl + bd.r0 + i0;
+        if (full && out_vec && ((bd.r0 + i0) & 1) == 0) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int cc = 8 * warp + k;
+                const double2 x = *reinterpret_cast<const double2*>(&tile[ex_phys(cc, 2 * lane)]);
+                __stcs(reinterpret_cast<double2*>(l + base + (long long)cc * ldl) + lane, x);
+            }
+        } else {
+            for (int k = 0; k < 8; ++k) {
+                const int cc = 8 * warp + k;
+                if (cc >= nj) break;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int rr = lane + 32 * h;
+                    if (rr < mi && !(bd.lower && j0 + cc > i0 + rr))
+                        l[base + (long long)cc * ldl + rr] = tile[ex_phys(cc, rr)];
+                }
+            }
         }
         __syncthreads();
     }
@@ -88,22 +166,26 @@ __global__ void __launch_bounds__(256) k_export(DevCtx c, const BlockDesc* block
 
 // shadow: blocks carry their source level; target is `p`
 __global__ void __launch_bounds__(256) k_shadow(DevCtx c, const BlockDesc* blocks, int nb, int p, int tiles) {
+    pdl_wait();
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
         const BlockDesc bd = blocks[find_block(blocks, nb, t)];
         const int lt = t - bd.tile0;
         const int i0 = (lt / bd.tiles_n) * TB, j0 = (lt % bd.tiles_n) * TB;
-        for (int r = 0; r < TB; r += 8) {
+        // all 16 loads of a thread first (the level buffers may alias as far
+        // as the compiler knows, so an interleaved load / store loop would
+        // pay one L2 round trip per element)
+        double v[16];
 #pragma unroll
-            for (int h = 0; h < TB; h += 32) {
-                const int i = i0 + ty + r, j = j0 + h + tx;
-                if (i < bd.m && j < bd.n) {
-                    const long long off = (long long)(bd.r0 + i) * c.ldw + bd.c0 + j;
-                    double v = load_level(c, bd.level, off);
-                    if (bd.lower && j > i) v = 0.0;
-                    store_level(c, p, off, v);
-                }
-            }
+        for (int k = 0; k < 16; ++k) {
+            const int i = i0 + ty + 8 * (k >> 1), j = j0 + 32 * (k & 1) + tx;
+            v[k] = (i < bd.m && j < bd.n) ? load_level(c, bd.level, (long long)(bd.r0 + i) * c.ldw + bd.c0 + j) : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            const int i = i0 + ty + 8 * (k >> 1), j = j0 + 32 * (k & 1) + tx;
+            if (i < bd.m && j < bd.n)
+                store_level(c, p, (long long)(bd.r0 + i) * c.ldw + bd.c0 + j, (bd.lower && j > i) ? 0.0 : v[k]);
         }
     }
 }
@@ -111,6 +193,7 @@ __global__ void __launch_bounds__(256) k_shadow(DevCtx c, const BlockDesc* block
 // require_finite over rect (lower: leaf lower triangle) of buffer `lv`
 __global__ void __launch_bounds__(256) k_check(DevCtx c, int lv, int r0, int c0, int m, int n, int lower,
                                                uint32_t seq) {
+    pdl_wait();
     const int j = blockIdx.x * 256 + threadIdx.x;
     const int ib = blockIdx.y * 16;
     unsigned long long best = ~0ull;
@@ -138,6 +221,7 @@ __global__ void __launch_bounds__(256) k_check(DevCtx c, int lv, int r0, int c0,
 // alpha slot, and a speculative alpha == 1 conversion into buffer lv
 __global__ void __launch_bounds__(256) k_quant1(DevCtx c, int lv, int r0, int c0, int m, int n, int slot,
                                                 uint32_t seq) {
+    pdl_wait();
     // 64x64 transposing tiles, all 16 loads of a thread in flight (k_import)
     __shared__ double tile[TB][TB + 1];
     __shared__ unsigned long long smax[8], skey[8];
@@ -207,6 +291,7 @@ __device__ __forceinline__ double slot_alpha(const DevCtx& c, int lv, int slot) 
 
 // quantize pass 2: only when alpha != 1, B <- rn(B / alpha) from the doubles
 __global__ void __launch_bounds__(256) k_quant2(DevCtx c, int lv, int r0, int c0, int m, int n, int slot) {
+    pdl_wait();
     const double alpha = slot_alpha(c, lv, slot);
     if (alpha == 1.0) return;
     __shared__ double tile[TS][TS + 1];
@@ -236,6 +321,7 @@ __global__ void __launch_bounds__(256) k_quant2(DevCtx c, int lv, int r0, int c0
 // post-dequantize require_finite (tree.cpp:121) is fused here too
 __global__ void __launch_bounds__(256) k_dequant(DevCtx c, int lv, int r0, int c0, int m, int n, int slot,
                                                  uint32_t chk_seq) {
+    pdl_wait();
     const double alpha = slot_alpha(c, lv, slot);
     if (alpha == 1.0) return;  // tree.cpp:98 (the common case: a bounded grid, so the no-op launch is short)
     unsigned long long bad = ~0ull;
@@ -358,7 +444,7 @@ void launch_import(const DevCtx& c, const BlockDesc* d_blocks, int nb, int tiles
     if (tiles > 0) k_import<<<tile_grid(tiles), 256, 0, s>>>(c, d_blocks, nb, tiles);
 }
 void launch_export(const DevCtx& c, const BlockDesc* d_blocks, int nb, int tiles, cudaStream_t s) {
-    if (tiles > 0) k_export<<<tile_grid(4 * tiles), 256, 0, s>>>(c, d_blocks, nb, tiles);
+    if (tiles > 0) k_export<<<tile_grid(tiles), 256, 0, s>>>(c, d_blocks, nb, tiles);
 }
 void launch_shadow(const DevCtx& c, const BlockDesc* d_blocks, int nb, int tiles, int p, cudaStream_t s) {
     if (tiles > 0) k_shadow<<<tile_grid(tiles), 256, 0, s>>>(c, d_blocks, nb, p, tiles);

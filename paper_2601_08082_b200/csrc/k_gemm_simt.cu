@@ -48,6 +48,7 @@ __device__ __forceinline__ bool epi_store_d(const DevCtx& c, const DevProb& p, l
 
 template <int OPL, typename Acc>
 __global__ void __launch_bounds__(256) k_gemm_simt(DevCtx c, const DevProb* probs, int np) {
+    pdl_wait();
     using T = typename LvT<OPL>::T;
     __shared__ Acc As[BK][BM + 4];
     __shared__ Acc Bs[BK][BN + 4];
@@ -129,6 +130,7 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
 
 template <int OPL>
 __global__ void __launch_bounds__(256) k_gemm_dmma(DevCtx c, const DevProb* probs, int np) {
+    pdl_wait();
     using T = typename LvT<OPL>::T;
     __shared__ double As[BM][DLD];
     __shared__ double Bs[BN][DLD];
@@ -220,6 +222,8 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int byt
 }
 
 __global__ void __launch_bounds__(128) k_gemm_mma32(DevCtx c, const DevProb* probs, int np) {
+    pdl_wait();
+    pdl_trigger();  // short kernel: let the dependents launch right away
     constexpr int TM = M32_TILE, TN = M32_TILE;  // 32 x 32 output tile: 4 warps of 16 x 16
     __shared__ __align__(16) float As[2][TM][MLD];
     __shared__ __align__(16) float Bs[2][TN][MLD];
@@ -315,6 +319,8 @@ __global__ void __launch_bounds__(128) k_gemm_mma32(DevCtx c, const DevProb* pro
 constexpr int WN = 256;  // widest n
 constexpr int WM = M32W_ROWS;  // rows per CTA (16: twice the CTAs of 32 rows for the 256-row solves on the chain)
 __global__ void __launch_bounds__(256) k_gemm_mma32w(DevCtx c, const DevProb* probs, int np) {
+    pdl_wait();
+    pdl_trigger();  // short kernel: let the dependents launch right away
     extern __shared__ __align__(16) float wsm[];
     float (*As)[WM][MLD] = reinterpret_cast<float (*)[WM][MLD]>(wsm);            // [2][WM][MLD]
     float (*Bs)[WN][MLD] = reinterpret_cast<float (*)[WN][MLD]>(wsm + 2 * WM * MLD);  // [2][256][MLD]

@@ -368,6 +368,8 @@ __global__ void __launch_bounds__(Cfg<KIND>::NTHREADS, 1) k_gemm_tc(DevCtx c, co
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     if (threadIdx.x == 0) stamp(c, 1);
+    // setup done: from here on operands written by the preceding kernels are read
+    pdl_wait();
 
     if (warp == 0) {
         if (lane == 0) {
@@ -450,6 +452,9 @@ __global__ void __launch_bounds__(Cfg<KIND>::NTHREADS, 1) k_gemm_tc(DevCtx c, co
             }
             }  // chunks
         }
+        // every MMA issued: the dependents may be scheduled (they wait for
+        // this grid's completion in pdl_wait)
+        pdl_trigger();
     } else if (warp >= 10) {
         // ---------------- lo halves (TF32X3) ----------------
         if constexpr (SPLIT) {

@@ -24,6 +24,10 @@ namespace tcb {
 namespace {
 
 constexpr int IT = 512;
+
+// development counters (CTA 0 of every launch): cycles in load, reciprocals,
+// diagonal inverses, products, triangular multiplies, store; launches
+__device__ unsigned long long g_inv_clk[8];
 constexpr int WLD = 36, WBS = 32 * WLD;  // W / inverse / partial blocks: row-major, padded rows
 
 __device__ __forceinline__ void mma_tf32_i(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
@@ -42,6 +46,7 @@ __device__ __forceinline__ int isw(int r, int c) { return (c << 5) + (r ^ ((c & 
 
 template <int MODE>
 __global__ void __launch_bounds__(IT, 1) k_leaf_inv2(DevCtx c, int r0, int n, uint32_t seq) {
+    pdl_wait();
     using T = typename LvT<MODE == 0 ? 0 : 1>::T;
     extern __shared__ __align__(16) float ism[];
     const int NT = n >> 5, cb = blockIdx.x;
@@ -56,6 +61,7 @@ __global__ void __launch_bounds__(IT, 1) k_leaf_inv2(DevCtx c, int r0, int n, ui
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     auto tl = [&](int I, int K) { return Ls + ((((I - cb) * (I - cb + 1)) >> 1) + (K - cb)) * 1024; };
 
+    long long ck0 = clock64(), ck_prod = 0, ck_tri = 0, ck1, ck2, ck3;
     // load the needed lower part (coalesced rows)
     const int ntile = (NB * (NB + 1)) >> 1;
     for (int k = warp; k < ntile; k += IT / 32) {
@@ -70,6 +76,7 @@ __global__ void __launch_bounds__(IT, 1) k_leaf_inv2(DevCtx c, int r0, int n, ui
         for (int rr = 0; rr < 32; ++rr) t[isw(rr, lane)] = v[rr];
     }
     __syncthreads();
+    ck1 = clock64();
     for (int j = tid; j < NB * 32; j += IT) {
         const int I = cb + (j >> 5), r = j & 31;
         Rd[j] = 1.0f / tl(I, I)[isw(r, r)];
@@ -80,6 +87,7 @@ __global__ void __launch_bounds__(IT, 1) k_leaf_inv2(DevCtx c, int r0, int n, ui
         if (tid == 0 && bad) report(c, seq, uint64_t(cb * 32 + __ffs(bad) - 1));
     }
     __syncthreads();
+    ck2 = clock64();
 
     // inv(L(I,I)) of every diagonal block, one warp each, in place (the
     // diagonal tiles are read only as these inverses afterwards): lane =
@@ -103,9 +111,11 @@ __global__ void __launch_bounds__(IT, 1) k_leaf_inv2(DevCtx c, int r0, int n, ui
         for (int r = 0; r < 32; ++r) Lt[isw(r, lane)] = x[r];
     }
     __syncthreads();
+    ck3 = clock64();
 
     const int gq = lane >> 2, tq = lane & 3;
     for (int I = cb; I < NT; ++I) {
+        const long long ca = clock64();
         float* Wi = Wb + (I - cb) * WBS;
         const float* Dc = tl(I, I);  // inv(L(I,I)), tile layout
         // (1) P = sum_{cb <= K < I} L(I,K) W(K,cb) on the tensor cores: 8
@@ -113,8 +123,11 @@ __global__ void __launch_bounds__(IT, 1) k_leaf_inv2(DevCtx c, int r0, int n, ui
         if (I > cb) {
             const int tile = warp & 7, kg = warp >> 3;
             const int mt = tile >> 2, nb = tile & 3;
-            float acc[4] = {0.f, 0.f, 0.f, 0.f};
+            // one accumulator per hi/lo term: three independent MMA chains
+            // (a single accumulator serializes all three per k-step)
+            float acc[4] = {0.f, 0.f, 0.f, 0.f}, acc1[4] = {0.f, 0.f, 0.f, 0.f}, acc2[4] = {0.f, 0.f, 0.f, 0.f};
             const int nk = 4 * (I - cb);  // k-steps of 8
+#pragma unroll 2
             for (int ks = kg * nk / 2; ks < (kg + 1) * nk / 2; ++ks) {
                 const int K = cb + (ks >> 2), kk = (ks & 3) * 8;
                 const float* Lt = tl(I, K);
@@ -127,10 +140,12 @@ __global__ void __launch_bounds__(IT, 1) k_leaf_inv2(DevCtx c, int r0, int n, ui
                 tf32_split(Lt[isw(r + 8, kk + tq + 4)], ah[3], al[3]);
                 tf32_split(Wk[(kk + tq) * WLD + nb * 8 + gq], bh[0], bl[0]);
                 tf32_split(Wk[(kk + tq + 4) * WLD + nb * 8 + gq], bh[1], bl[1]);
-                mma_tf32_i(acc, al, bh);
-                mma_tf32_i(acc, ah, bl);
+                mma_tf32_i(acc1, al, bh);
+                mma_tf32_i(acc2, ah, bl);
                 mma_tf32_i(acc, ah, bh);
             }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[e] += acc1[e] + acc2[e];  // small terms first
             float* P = Pq + kg * WBS;
             const int r = mt * 16 + gq, col = nb * 8 + 2 * tq;
             P[r * WLD + col] = acc[0];
@@ -139,6 +154,8 @@ __global__ void __launch_bounds__(IT, 1) k_leaf_inv2(DevCtx c, int r0, int n, ui
             P[(r + 8) * WLD + col + 1] = acc[3];
         }
         __syncthreads();
+        const long long cb2 = clock64();
+        ck_prod += cb2 - ca;
         // (2) W(I,cb) = inv(L(I,I)) (delta - P) on warps 0-7
         if (warp < 8) {
             const int mt = warp >> 2, nb = warp & 3;
@@ -146,7 +163,7 @@ __global__ void __launch_bounds__(IT, 1) k_leaf_inv2(DevCtx c, int r0, int n, ui
                 const float dl = (I == cb && rr == cc) ? 1.f : 0.f;
                 return I > cb ? dl - Pq[rr * WLD + cc] - Pq[WBS + rr * WLD + cc] : dl;
             };
-            float acc[4] = {0.f, 0.f, 0.f, 0.f};
+            float acc[4] = {0.f, 0.f, 0.f, 0.f}, acc1[4] = {0.f, 0.f, 0.f, 0.f}, acc2[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
             for (int kk = 0; kk < 32; kk += 8) {
                 const int r = mt * 16 + gq;
@@ -157,10 +174,12 @@ __global__ void __launch_bounds__(IT, 1) k_leaf_inv2(DevCtx c, int r0, int n, ui
                 tf32_split(Dc[isw(r + 8, kk + tq + 4)], ah[3], al[3]);
                 tf32_split(rhs(kk + tq, nb * 8 + gq), bh[0], bl[0]);
                 tf32_split(rhs(kk + tq + 4, nb * 8 + gq), bh[1], bl[1]);
-                mma_tf32_i(acc, al, bh);
-                mma_tf32_i(acc, ah, bl);
+                mma_tf32_i(acc1, al, bh);
+                mma_tf32_i(acc2, ah, bl);
                 mma_tf32_i(acc, ah, bh);
             }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[e] += acc1[e] + acc2[e];
             const int r = mt * 16 + gq, col = nb * 8 + 2 * tq;
             Wi[r * WLD + col] = acc[0];
             Wi[r * WLD + col + 1] = acc[1];
@@ -168,7 +187,10 @@ __global__ void __launch_bounds__(IT, 1) k_leaf_inv2(DevCtx c, int r0, int n, ui
             Wi[(r + 8) * WLD + col + 1] = acc[3];
         }
         __syncthreads();
+        ck_tri += clock64() - cb2;
     }
+    const long long ck4 = clock64();
+    pdl_trigger();  // only the stores remain
 
     // write column block cb of W (rows < 32 cb are zero)
     if constexpr (MODE == 0) {
@@ -198,6 +220,15 @@ __global__ void __launch_bounds__(IT, 1) k_leaf_inv2(DevCtx c, int r0, int n, ui
             W[(long long)i * kW32Ld + t] = i >= t ? w : 0.f;
         }
     }
+    if (cb == 0 && tid == 0) {
+        atomicAdd(&g_inv_clk[0], (unsigned long long)(ck1 - ck0));
+        atomicAdd(&g_inv_clk[1], (unsigned long long)(ck2 - ck1));
+        atomicAdd(&g_inv_clk[2], (unsigned long long)(ck3 - ck2));
+        atomicAdd(&g_inv_clk[3], (unsigned long long)ck_prod);
+        atomicAdd(&g_inv_clk[4], (unsigned long long)ck_tri);
+        atomicAdd(&g_inv_clk[5], (unsigned long long)(clock64() - ck4));
+        atomicAdd(&g_inv_clk[6], 1ull);
+    }
 }
 
 size_t inv2_smem(int n) {
@@ -206,6 +237,14 @@ size_t inv2_smem(int n) {
 }
 
 }  // namespace
+
+void inv_debug_clocks(long long* out, bool reset) {
+    cudaMemcpyFromSymbol(out, g_inv_clk, sizeof(long long) * 8);
+    if (reset) {
+        long long z[8] = {0};
+        cudaMemcpyToSymbol(g_inv_clk, z, sizeof(z));
+    }
+}
 
 bool inv2_ok(int n) { return n % 32 == 0 && n >= 32 && n <= 256; }
 

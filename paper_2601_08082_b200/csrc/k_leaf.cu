@@ -121,6 +121,7 @@ __device__ __forceinline__ void below_rows(const AccT& A, const Acc* P, const Ac
 template <int L, bool SMEM>
 __global__ void __launch_bounds__(POTRF_THREADS, 1) k_potrf_leaf(DevCtx c, int r0, int n, uint32_t seq,
                                                               uint32_t chk_seq) {
+    pdl_wait();
     using T = typename LvT<L>::T;
     using Acc = typename LvT<L>::Acc;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -243,6 +244,7 @@ __global__ void __launch_bounds__(POTRF_THREADS, 1) k_potrf_leaf(DevCtx c, int r
 template <int L, bool BS>
 __global__ void __launch_bounds__(128) k_trsm_leaf(DevCtx c, int br0, int bc0, int m, int n, int lr0,
                                                   uint32_t seq, uint32_t chk_seq, int chk_r0, int chk_c0) {
+    pdl_wait();
     using T = typename LvT<L>::T;
     using Acc = typename LvT<L>::Acc;
     constexpr int TSL = 128;  // staged slice of finished columns
@@ -366,6 +368,7 @@ __global__ void __launch_bounds__(128) k_trsm_leaf(DevCtx c, int br0, int bc0, i
 constexpr int INV_COLS = 32;
 
 __global__ void __launch_bounds__(128) k_leaf_inverse(DevCtx c, int r0, int n, uint32_t seq) {
+    pdl_wait();
     extern __shared__ __align__(16) float inv_smem[];
     float* Ls = inv_smem;                          // packed lower triangle, n(n+1)/2
     float* Wc = Ls + (n * (n + 1)) / 2;            // [INV_COLS][n] this CTA's columns

@@ -102,6 +102,7 @@ __device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast
 template <int L>
 __global__ void __launch_bounds__(POT_THREADS, 1) k_potrf_cm(DevCtx c, int r0, int n, uint32_t seq,
                                                             uint32_t chk_seq) {
+    pdl_wait();
     using T = typename LvT<L>::T;
     extern __shared__ __align__(16) float sm[];
     float* S = sm;                              // cm_size(n)
@@ -237,6 +238,7 @@ __global__ void __launch_bounds__(POT_THREADS, 1) k_potrf_cm(DevCtx c, int r0, i
 template <int L>
 __global__ void __launch_bounds__(TR_THREADS, 1) k_trsm_cm(DevCtx c, int br0, int bc0, int m, int n, int lr0,
                                                           uint32_t seq, uint32_t chk_seq, int chk_r0, int chk_c0) {
+    pdl_wait();
     using T = typename LvT<L>::T;
     extern __shared__ __align__(16) float sm[];
     float* S = sm;                         // leaf, CM layout

@@ -2,6 +2,7 @@
 // tensor-core path (mma.sync) on one SM, to size leaf-kernel choices.
 #include <cuda_runtime.h>
 
+#include "device.cuh"
 #include "launch.hpp"
 
 namespace tcb {
@@ -129,3 +130,4 @@ double probe_mma(int kind, int iters) {
 
 extern "C" double tc_debug_mma_probe(int kind, int iters) { return tcb::probe_mma(kind, iters); }
 extern "C" double tc_debug_fp64_probe(int kind, int iters, int ctas) { return tcb::probe_fp64(kind, iters, ctas); }
+
