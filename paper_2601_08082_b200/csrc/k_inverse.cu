@@ -54,8 +54,8 @@ __global__ void __launch_bounds__(IT, 1) k_leaf_inv2(DevCtx c, int r0, int n, ui
     // tiles (I, K), cb <= K <= I, local index (I-cb)(I-cb+1)/2 + (K-cb)
     float* Ls = ism;
     float* Wb = Ls + ((NB * (NB + 1)) >> 1) * 1024;  // [NB][32][WLD] row-major W(I, cb)
-    float* Pq = Wb + NB * WBS;                        // [2][32][WLD] K-split partials of the product
-    float* Rd = Pq + 2 * WBS;                         // [NB*32] reciprocal diagonal
+    float* Pq = Wb + NB * WBS;                        // [4][32][WLD] K-split partials of the product
+    float* Rd = Pq + 4 * WBS;                         // [NB*32] reciprocal diagonal
     const T* g = lvbuf<MODE == 0 ? 0 : 1>(c) + (long long)r0 * c.ldw + r0;
     const long long ld = c.ldw;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -118,40 +118,47 @@ __global__ void __launch_bounds__(IT, 1) k_leaf_inv2(DevCtx c, int r0, int n, ui
         const long long ca = clock64();
         float* Wi = Wb + (I - cb) * WBS;
         const float* Dc = tl(I, I);  // inv(L(I,I)), tile layout
-        // (1) P = sum_{cb <= K < I} L(I,K) W(K,cb) on the tensor cores: 8
-        //     16x8 output tiles, the K range split over two warp groups
+        // (1) P = sum_{cb <= K < I} L(I,K) W(K,cb) on the tensor cores: the
+        //     K range split over 4 warp groups, each warp a 16x16 output
+        //     block (two n8 tiles sharing the A fragment), one accumulator
+        //     per hi/lo term (independent MMA chains)
         if (I > cb) {
-            const int tile = warp & 7, kg = warp >> 3;
-            const int mt = tile >> 2, nb = tile & 3;
-            // one accumulator per hi/lo term: three independent MMA chains
-            // (a single accumulator serializes all three per k-step)
-            float acc[4] = {0.f, 0.f, 0.f, 0.f}, acc1[4] = {0.f, 0.f, 0.f, 0.f}, acc2[4] = {0.f, 0.f, 0.f, 0.f};
+            const int kg = warp >> 2, wt = warp & 3;
+            const int mt = wt >> 1, np = wt & 1;
+            float acc[2][4] = {}, acc1[2][4] = {}, acc2[2][4] = {};
             const int nk = 4 * (I - cb);  // k-steps of 8
+            const int k0 = kg * nk / 4, k1 = (kg + 1) * nk / 4;
+            const int r = mt * 16 + gq;
 #pragma unroll 2
-            for (int ks = kg * nk / 2; ks < (kg + 1) * nk / 2; ++ks) {
+            for (int ks = k0; ks < k1; ++ks) {
                 const int K = cb + (ks >> 2), kk = (ks & 3) * 8;
                 const float* Lt = tl(I, K);
                 const float* Wk = Wb + (K - cb) * WBS;
-                const int r = mt * 16 + gq;
-                uint32_t ah[4], al[4], bh[2], bl[2];
+                uint32_t ah[4], al[4];
                 tf32_split(Lt[isw(r, kk + tq)], ah[0], al[0]);
                 tf32_split(Lt[isw(r + 8, kk + tq)], ah[1], al[1]);
                 tf32_split(Lt[isw(r, kk + tq + 4)], ah[2], al[2]);
                 tf32_split(Lt[isw(r + 8, kk + tq + 4)], ah[3], al[3]);
-                tf32_split(Wk[(kk + tq) * WLD + nb * 8 + gq], bh[0], bl[0]);
-                tf32_split(Wk[(kk + tq + 4) * WLD + nb * 8 + gq], bh[1], bl[1]);
-                mma_tf32_i(acc1, al, bh);
-                mma_tf32_i(acc2, ah, bl);
-                mma_tf32_i(acc, ah, bh);
-            }
 #pragma unroll
-            for (int e = 0; e < 4; ++e) acc[e] += acc1[e] + acc2[e];  // small terms first
+                for (int h = 0; h < 2; ++h) {
+                    const int col = np * 16 + h * 8 + gq;
+                    uint32_t bh[2], bl[2];
+                    tf32_split(Wk[(kk + tq) * WLD + col], bh[0], bl[0]);
+                    tf32_split(Wk[(kk + tq + 4) * WLD + col], bh[1], bl[1]);
+                    mma_tf32_i(acc1[h], al, bh);
+                    mma_tf32_i(acc2[h], ah, bl);
+                    mma_tf32_i(acc[h], ah, bh);
+                }
+            }
             float* P = Pq + kg * WBS;
-            const int r = mt * 16 + gq, col = nb * 8 + 2 * tq;
-            P[r * WLD + col] = acc[0];
-            P[r * WLD + col + 1] = acc[1];
-            P[(r + 8) * WLD + col] = acc[2];
-            P[(r + 8) * WLD + col + 1] = acc[3];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int col = np * 16 + h * 8 + 2 * tq;
+                P[r * WLD + col] = acc[h][0] + (acc1[h][0] + acc2[h][0]);  // small terms first
+                P[r * WLD + col + 1] = acc[h][1] + (acc1[h][1] + acc2[h][1]);
+                P[(r + 8) * WLD + col] = acc[h][2] + (acc1[h][2] + acc2[h][2]);
+                P[(r + 8) * WLD + col + 1] = acc[h][3] + (acc1[h][3] + acc2[h][3]);
+            }
         }
         __syncthreads();
         const long long cb2 = clock64();
@@ -161,7 +168,9 @@ __global__ void __launch_bounds__(IT, 1) k_leaf_inv2(DevCtx c, int r0, int n, ui
             const int mt = warp >> 2, nb = warp & 3;
             auto rhs = [&](int rr, int cc) {
                 const float dl = (I == cb && rr == cc) ? 1.f : 0.f;
-                return I > cb ? dl - Pq[rr * WLD + cc] - Pq[WBS + rr * WLD + cc] : dl;
+                return I > cb ? dl - ((Pq[rr * WLD + cc] + Pq[WBS + rr * WLD + cc]) +
+                                      (Pq[2 * WBS + rr * WLD + cc] + Pq[3 * WBS + rr * WLD + cc]))
+                              : dl;
             };
             float acc[4] = {0.f, 0.f, 0.f, 0.f}, acc1[4] = {0.f, 0.f, 0.f, 0.f}, acc2[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -233,7 +242,7 @@ __global__ void __launch_bounds__(IT, 1) k_leaf_inv2(DevCtx c, int r0, int n, ui
 
 size_t inv2_smem(int n) {
     const int NB = n / 32;
-    return (size_t(NB * (NB + 1) / 2) * 1024 + size_t(NB + 2) * WBS + size_t(NB) * 32) * sizeof(float);
+    return (size_t(NB * (NB + 1) / 2) * 1024 + size_t(NB + 4) * WBS + size_t(NB) * 32) * sizeof(float);
 }
 
 }  // namespace
