@@ -122,6 +122,42 @@ __device__ __forceinline__ double round_level(int lv, double x) {
     return x;
 }
 
+// ---------------------------------------------------------------------------
+// leaf kernels' shared-memory tiles: a lower triangle of nt x nt blocks of
+// 32 x 32, tile k = a(a+1)/2 + b holding block (off + a, off + b), each tile
+// column-major with the row index XOR-swizzled by 4 (c & 7): one column
+// across a warp's 32 rows and 4 consecutive rows of one column are both
+// bank-conflict free.  (k_potrf.cu, k_inverse.cu)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int tri_sw(int r, int c) { return (c << 5) + (r ^ ((c & 7) << 2)); }
+__device__ __forceinline__ void tri_tile_ab(int k, int& a, int& b) {
+    a = 0;
+    while (((a + 1) * (a + 2)) / 2 <= k) ++a;
+    b = k - ((a * (a + 1)) >> 1);
+}
+// tiles -> global, whole tiles as 16-byte row chunks (a diagonal tile's
+// strict upper part goes back as loaded)
+template <typename T, int NTHREADS>
+__device__ __forceinline__ void tri_store_vec(const float* S, T* g, long long ld, int nt, int off, int tid) {
+    constexpr int VEC = 16 / int(sizeof(T)), CPR = 32 / VEC, CPT = 32 * CPR, KSTEP = NTHREADS / CPT;
+    const int ntile = (nt * (nt + 1)) >> 1;
+    const int row = (tid % CPT) / CPR, col = (tid % CPR) * VEC;
+#pragma unroll 1
+    for (int k = tid / CPT; k < ntile; k += KSTEP) {
+        int a, b;
+        tri_tile_ab(k, a, b);
+        const float* t = S + k * 1024;
+        uint4 w;
+        T* e = reinterpret_cast<T*>(&w);
+#pragma unroll
+        for (int u = 0; u < VEC; ++u) e[u] = from_float<T>(t[tri_sw(row, col + u)]);
+        *reinterpret_cast<uint4*>(g + (long long)((off + a) * 32 + row) * ld + (off + b) * 32 + col) = w;
+    }
+}
+__device__ __forceinline__ bool vec16_ok(const void* g, long long ld_bytes) {
+    return (reinterpret_cast<uintptr_t>(g) & 15) == 0 && (ld_bytes & 15) == 0;
+}
+
 // programmatic dependent launch: every factorization kernel waits here
 // before it reads anything a preceding kernel wrote (a no-op unless it was
 // launched through a programmatic graph edge); chain kernels signal their

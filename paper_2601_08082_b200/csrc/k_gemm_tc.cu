@@ -382,6 +382,7 @@ __global__ void __launch_bounds__(Cfg<KIND>::NTHREADS, 1) k_gemm_tc(DevCtx c, co
                 const TcProb* p = probs + pi;
                 prefetch_map(&p->ta);
                 prefetch_map(&p->tb);
+                prefetch_map(&p->tcm);  // the epilogue's C loads / stores
                 const int nk = (p->k + G::BK - 1) / G::BK;
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);

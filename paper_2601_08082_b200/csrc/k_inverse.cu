@@ -222,11 +222,22 @@ __global__ void __launch_bounds__(IT, 1) k_leaf_inv2(DevCtx c, int r0, int n, ui
             W[(long long)i * kW16Ld + kW16Lo + t] = lo;
         }
     } else {
-        float* W = c.w32 + (long long)r0 * kW32Ld;
-        for (int e2 = tid; e2 < n * 32; e2 += IT) {
-            const int i = e2 >> 5, j = e2 & 31, t = cb * 32 + j;
-            const float w = (i >= cb * 32) ? Wb[((i >> 5) - cb) * WBS + (i & 31) * WLD + j] : 0.f;
-            W[(long long)i * kW32Ld + t] = i >= t ? w : 0.f;
+        // rows of column block cb: 16-byte chunks (4 columns), zero above
+        // the diagonal
+        float* W = c.w32 + (long long)r0 * kW32Ld + cb * 32;
+        for (int e2 = tid; e2 < n * 8; e2 += IT) {
+            const int i = e2 >> 3, j = (e2 & 7) * 4, t = cb * 32 + j;
+            float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (i >= cb * 32) {
+                w = *reinterpret_cast<const float4*>(&Wb[((i >> 5) - cb) * WBS + (i & 31) * WLD + j]);
+                if (i < t + 3) {  // the diagonal tile: strict upper part zero
+                    w.x = i >= t ? w.x : 0.f;
+                    w.y = i >= t + 1 ? w.y : 0.f;
+                    w.z = i >= t + 2 ? w.z : 0.f;
+                    w.w = 0.f;
+                }
+            }
+            *reinterpret_cast<float4*>(W + (long long)i * kW32Ld + j) = w;
         }
     }
     if (cb == 0 && tid == 0) {
