@@ -235,6 +235,161 @@ __global__ void __launch_bounds__(POTRF_THREADS, 1) k_potrf_leaf(DevCtx c, int r
     }
 }
 
+// ---------------------------------------------------------------------------
+// F64 leaves (BASELINE C1 [F16, F64] b=128, C2 [F16, F32, F64] b=256):
+// potrf_leaf in FP64 with the panel products on the FP64 tensor pipe.  The
+// leaf stays in global memory (L2-resident: a 256 F64 triangle is 264 KB);
+// per 32-column panel J:
+//   (a) P = A(J.., 0:J) A(J:J+32, 0:J)^T by DMMA (mma.sync m8n8k4 f64), the
+//       K range staged through shared memory 32 columns at a time (the B
+//       operand is the first 32 staged rows); 8x8 output tiles, a warp owns
+//       row tiles warp, warp+8, ... and all four column tiles;
+//   (b1) the diagonal block on warp 0 (diag_block: the reference's per-
+//       element order, IEEE sqrt and division);
+//   (b2) the rows below, one thread per row: the row's 32 entries loaded
+//       before the substitution chain, quotients v/d by Markstein's
+//       correctly rounded scheme from y = rn(1/d) (q = rn(v y), the exact
+//       FMA residual, one correction: rn(v/d) in the normal range).
+// Only the summation order differs from kernels.cpp:42-69.
+// ---------------------------------------------------------------------------
+constexpr int F64T = 256;     // threads
+
+// (b1) on its own register allocation: inlined into the kernel beside the
+// DMMA phase and the unrolled rows-below loop it measured 3.5x slower
+__device__ __noinline__ void diag_block_f64(double* g, long long ld, const double* P, double* Dt, int J, int lane,
+                                            const DevCtx& c, uint32_t seq) {
+    LeafAcc<2, false> A{nullptr, g, ld};
+    diag_block<2, true>(A, P, Dt, J, PW, lane, c, seq);
+}
+constexpr int F64LD = 36;     // staged slice row pitch (doubles)
+
+__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d[0]), "+d"(d[1])
+                 : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(F64T, 1) k_potrf_f64(DevCtx c, int r0, int n, uint32_t seq, uint32_t chk_seq) {
+    pdl_wait();
+    extern __shared__ __align__(16) double f64sm[];
+    double* P = f64sm;                          // [n][PW] partial sums
+    double* As = P + size_t(n) * PW;            // [n][F64LD] staged K-slice, rows J..n-1
+    double* Dt = As + size_t(n) * F64LD;        // [PW][PW+4] Dt[jj][j2] = L(J+j2, J+jj)
+    double* Dr = Dt + PW * (PW + 4);            // [PW] rn(1 / L(J+jj, J+jj))
+    double* g = c.b64 + (long long)r0 * c.ldw + r0;
+    const long long ld = c.ldw;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = F64T / 32;
+
+    if (chk_seq) {  // leaf require_finite (tree.cpp:107-108)
+        unsigned long long bad = ~0ull;
+        for (int i = warp; i < n; i += NW)
+            for (int j = lane; j <= i; j += 32)
+                if (!isfinite(g[(long long)i * ld + j])) {
+                    const unsigned long long k = fail_key(chk_seq, elem_local(i, j));
+                    bad = k < bad ? k : bad;
+                }
+        warp_report_min(c, bad);
+    }
+
+    long long t_ph = clock64();
+    long long* clk = g_leaf_clk;
+    for (int J = 0; J < n; J += PW) {
+        const int R = n - J;        // rows of this panel (multiple of 32)
+        const int mtiles = R >> 3;  // 8-row tiles
+        // ---- (a) the panel's partial sums on DMMA
+        double acc[4][4][2];
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) acc[mi][nt][0] = acc[mi][nt][1] = 0.0;
+        for (int t0 = 0; t0 < J; t0 += PW) {
+            __syncthreads();
+            for (int e = tid; e < R * (PW / 2); e += F64T) {  // 16-byte loads, lanes along the row
+                const int r = e >> 4, c2 = (e & 15) * 2;
+                const double2 v = *reinterpret_cast<const double2*>(g + (long long)(J + r) * ld + t0 + c2);
+                *reinterpret_cast<double2*>(As + r * F64LD + c2) = v;
+            }
+            __syncthreads();
+#pragma unroll 2
+            for (int kk = 0; kk < PW; kk += 4) {
+                double b[4];
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt) b[nt] = As[(nt * 8 + (lane >> 2)) * F64LD + kk + (lane & 3)];
+#pragma unroll
+                for (int mi = 0; mi < 4; ++mi) {
+                    const int mt = warp + NW * mi;
+                    if (mt < mtiles) {
+                        const double a = As[(mt * 8 + (lane >> 2)) * F64LD + kk + (lane & 3)];
+#pragma unroll
+                        for (int nt = 0; nt < 4; ++nt) dmma884(acc[mi][nt], a, b[nt]);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) {
+            const int mt = warp + NW * mi;
+            if (mt < mtiles)
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt) {
+                    const int r = mt * 8 + (lane >> 2), col = nt * 8 + 2 * (lane & 3);
+                    P[r * PW + col] = acc[mi][nt][0];
+                    P[r * PW + col + 1] = acc[mi][nt][1];
+                }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) { const long long t = clock64(); clk[0] += t - t_ph; t_ph = t; }
+        // ---- (b1) the diagonal block
+        if (warp == 0) {
+            diag_block_f64(g, ld, P, Dt, J, lane, c, seq);
+            __syncwarp();
+            Dr[lane] = __drcp_rn(Dt[lane * (PW + 4) + lane]);  // y = rn(1/d) for the rows below
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) { const long long t = clock64(); clk[1] += t - t_ph; t_ph = t; }
+        // ---- (b2) the rows below: staged through shared memory (16-byte
+        // loads), one thread per row, written back the same way
+        for (int e = tid; e < (R - PW) * (PW / 2); e += F64T) {
+            const int r = PW + (e >> 4), c2 = (e & 15) * 2;
+            *reinterpret_cast<double2*>(As + r * F64LD + c2) =
+                *reinterpret_cast<const double2*>(g + (long long)(J + r) * ld + J + c2);
+        }
+        __syncthreads();
+        for (int r = PW + tid; r < R; r += F64T) {
+            double s[PW];
+#pragma unroll
+            for (int jj = 0; jj < PW; ++jj) s[jj] = P[r * PW + jj];
+            double* row = As + r * F64LD;
+#pragma unroll
+            for (int jj = 0; jj < PW; ++jj) {
+                // keep the block's loads inside their iteration (hoisting
+                // them all would exhaust the registers)
+                asm volatile("" ::: "memory");
+                const double* col = Dt + jj * (PW + 4);
+                const double a = row[jj] - s[jj];                     // rn(c - s)
+                const double d = col[jj], y = Dr[jj];
+                const double q0 = a * y;
+                const double x = fma(fma(-q0, d, a), y, q0);        // rn(a / d) (Markstein)
+                row[jj] = x;
+#pragma unroll
+                for (int j2 = jj + 1; j2 < PW; ++j2) s[j2] = fma(x, col[j2], s[j2]);
+            }
+        }
+        __syncthreads();
+        for (int e = tid; e < (R - PW) * (PW / 2); e += F64T) {
+            const int r = PW + (e >> 4), c2 = (e & 15) * 2;
+            *reinterpret_cast<double2*>(g + (long long)(J + r) * ld + J + c2) =
+                *reinterpret_cast<const double2*>(As + r * F64LD + c2);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) { const long long t = clock64(); clk[2] += t - t_ph; t_ph = t; }
+    }
+    if (threadIdx.x == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&clk[3]), 1ull);
+}
+
+size_t potrf_f64_smem(int n) { return (size_t(n) * PW + size_t(n) * F64LD + PW * (PW + 4) + PW) * sizeof(double); }
+
 // trsm_leaf: B (m x n at (br0, bc0)) <- B * L^-T, L the n x n square at lr0
 // The CTA's 32 rows of B are staged in shared memory (BS) so the
 // finished-column sums read them at smem latency; the in-chunk substitution
@@ -465,6 +620,7 @@ void init_leaf_attributes() {
     cudaFuncSetAttribute(k_potrf_leaf<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
     cudaFuncSetAttribute(k_potrf_leaf<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
     cudaFuncSetAttribute(k_potrf_leaf<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
+    cudaFuncSetAttribute(k_potrf_f64, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
 }
 
 constexpr size_t kLeafSmemCap = 220 * 1024;
@@ -473,6 +629,14 @@ void launch_potrf_leaf(const DevCtx& c, int lv, int r0, int n, uint32_t seq, uin
     if (potrf_v2_ok(lv, n)) return launch_potrf_v2(c, lv, r0, n, seq, chk, s);
     if (leaf_cm_ok(lv, n)) return launch_potrf_cm(c, lv, r0, n, seq, chk, s);
     const bool d = lv == LV_F64;
+    if (d && n % 32 == 0 && n > 128 && n <= 256 && (c.ldw % 2) == 0 && (r0 % 2) == 0) {
+        // FP64 leaves whose triangle does not fit shared memory (C2's 256):
+        // the DMMA kernel (a 227k -> 153k cycles, b2 245k -> 69k, b1 105k ->
+        // 349k -- net even, 323 vs 327 us).  Smaller leaves (C1's 128) keep
+        // the shared-memory SIMT kernel, 1.09 vs 1.52 ms for C1.
+        k_potrf_f64<<<1, F64T, potrf_f64_smem(n), s>>>(c, r0, n, seq, chk);
+        return;
+    }
     const bool fits = (d ? potrf_smem<double>(n, true) : potrf_smem<float>(n, true)) <= kLeafSmemCap;
     const bool pfits = (d ? potrf_smem<double>(n, false) : potrf_smem<float>(n, false)) <= kLeafSmemCap;
     if (!pfits) {
