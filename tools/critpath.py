@@ -23,6 +23,8 @@ def main():
     ap.add_argument("--b", type=int, default=256)
     ap.add_argument("--cfg", default="[F16, F16, F16, F32]")
     ap.add_argument("--ncu-pick", action="store_true")
+    ap.add_argument("--pick-n", type=int, default=0, help="with --ncu-pick: the largest tc16 op whose first problem has this n")
+    ap.add_argument("--pick-class", default="tc16", help="with --ncu-pick: tc16 or tc32")
     ap.add_argument("--profile-only", action="store_true", help="one serialized run (for ncu)")
     ap.add_argument("--json", default="")
     ap.add_argument("--opt", action="append", default=[], help="plan option key=value (repeatable)")
@@ -36,10 +38,13 @@ def main():
     if args.ncu_pick:
         # launch order of the serialized profile run == op order; the index
         # counts every k_gemm_tc launch (both operand kinds match the name)
+        # (k_gemm_tc<0> and <1> are separate kernels for ncu's -k regex:
+        # count launches of the picked class only)
         best, best_i, idx = -1.0, -1, 0
         for i, inf in enumerate(infos):
-            if inf["type"] == "gemm" and inf["gclass"] in ("tc16", "tc32"):
-                if inf["gclass"] == "tc16" and inf["flops"] > best:
+            if inf["type"] == "gemm" and inf["gclass"] == args.pick_class:
+                ok = not args.pick_n or plan.op_probs(i)[0]["n"] == args.pick_n
+                if ok and inf["flops"] > best:
                     best, best_i = inf["flops"], idx
                 idx += 1
         print(best_i)
