@@ -247,6 +247,11 @@ def run_ours(args):
     # from a serialized profiling replay (kernel timed alone -> burst peak)
     op_ms = plan.profile(a, l, stream=stream)
     tc_ms, tc_fl, tot_ms = 0.0, 0.0, sum(op_ms)
+    # per-launch roofline of the same kernel: each launch is bound by the
+    # slower of its flops at the tensor peak and its algorithmic bytes (A, B
+    # read once, C written -- and read when beta != 0) at the HBM peak; the
+    # small-K trailing updates are HBM-bound on their C traffic
+    t_bound, n_hbm = 0.0, 0
     by_type = {}
     for i, t in enumerate(op_ms):
         info = plan.op_info(i)
@@ -258,6 +263,16 @@ def run_ours(args):
         if info["gclass"] == "tc16":
             tc_ms += t
             tc_fl += info["flops"]
+            nbytes = 0.0
+            for pr in plan.op_probs(i):
+                beta = 0 if pr["a_kwrap"] else 1  # in-place inverse solves write C only
+                celems = pr["m"] * pr["n"] / (2.0 if pr["lower"] else 1.0)
+                nbytes += 2.0 * pr["m"] * (pr["a_kwrap"] or pr["k"]) + 2.0 * pr["n"] * pr["k"]
+                nbytes += celems * (2.0 if pr["exec_level"] == 0 else 4.0) * (1 + beta)
+            tb_t = info["flops"] / (peaks["bf16_tflops"] * 1e12) * 1e3
+            tb_h = nbytes / (peaks["hbm_gbs"] * 1e9) * 1e3
+            t_bound += max(tb_t, tb_h)
+            n_hbm += tb_h > tb_t
     achieved = tc_fl / (tc_ms * 1e-3) / 1e12 if tc_ms else 0.0
     # DRAM traffic per launch of the same kernel, from the committed ncu
     # launch list of this command (profiles/ncu_traffic.json)
@@ -271,7 +286,10 @@ def run_ours(args):
                 "frac": achieved / peaks["bf16_tflops"], "traffic": traffic, "traffic_unit": "bytes/launch (ncu)",
                 "peak_kind": f"{peak_kind} bf16 burst (MEASURED_PEAKS.json)",
                 "share_of_step": tc_ms / tot_ms if tot_ms else None,
-                "launches": by_type.get("gemm/tc16", [0, 0, 0])[2]}
+                "launches": by_type.get("gemm/tc16", [0, 0, 0])[2],
+                "per_launch_bound": {"frac": t_bound / tc_ms if tc_ms else None, "hbm_bound_launches": n_hbm,
+                                     "note": "sum over launches of max(flops / tensor peak, algorithmic bytes / "
+                                             "HBM peak) / sum of measured launch times"}}
     del op_ms
 
     # e2e: the public host entry point (tc_potrf_host, reference TileView

@@ -215,7 +215,10 @@ void Engine::launch_op(int i, cudaStream_t s) {
         case OP_SHADOW: launch_shadow(ctx_, reinterpret_cast<BlockDesc*>(tab), L.count, L.tiles, op.level, s); break;
         case OP_CHECK: launch_check(ctx_, op.src, r.r0, r.c0, r.m, r.n, op.lower, op.seq, s); break;
         case OP_QUANT: launch_quant(ctx_, op.level, r.r0, r.c0, r.m, r.n, op.slot, op.seq, s); break;
-        case OP_DEQUANT: launch_dequant(ctx_, op.level, r.r0, r.c0, r.m, r.n, op.slot, op.check_seq, s); break;
+        case OP_DEQUANT:
+            launch_dequant(ctx_, op.level, r.r0, r.c0, r.m, r.n, op.slot, op.check_seq,
+                           op.check_seq ? r.r0 - op.chk.r0 : 0, op.check_seq ? r.c0 - op.chk.c0 : 0, s);
+            break;
         case OP_POTRF: launch_potrf_leaf(ctx_, op.level, r.r0, r.m, op.seq, op.check_seq, s); break;
         case OP_TRSM:
             launch_trsm_leaf(ctx_, op.level, r.r0, r.c0, r.m, r.n, op.lrect.r0, op.seq, op.check_seq, op.chk.r0,

@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(256) k_quant2(DevCtx c, int lv, int r0, int c0
 // dequantize_block; when alpha != 1 it is the panel's last writer, so the
 // post-dequantize require_finite (tree.cpp:121) is fused here too
 __global__ void __launch_bounds__(256) k_dequant(DevCtx c, int lv, int r0, int c0, int m, int n, int slot,
-                                                 uint32_t chk_seq) {
+                                                 uint32_t chk_seq, int chk_dr, int chk_dc) {
     pdl_wait();
     const double alpha = slot_alpha(c, lv, slot);
     if (alpha == 1.0) return;  // tree.cpp:98 (the common case: a bounded grid, so the no-op launch is short)
@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(256) k_dequant(DevCtx c, int lv, int r0, int c
                 const double v = load_level(c, lv, off) * alpha;
                 store_level(c, lv, off, v);
                 if (!isfinite(round_level(lv, v))) {
-                    const unsigned long long k = fail_key(chk_seq, elem_local(i, j));
+                    const unsigned long long k = fail_key(chk_seq, elem_local(i + chk_dr, j + chk_dc));
                     bad = k < bad ? k : bad;
                 }
             }
@@ -462,10 +462,10 @@ void launch_quant(const DevCtx& c, int lv, int r0, int c0, int m, int n, int slo
     k_quant2<<<g, 256, 0, s>>>(c, lv, r0, c0, m, n, slot);
 }
 void launch_dequant(const DevCtx& c, int lv, int r0, int c0, int m, int n, int slot, uint32_t chk_seq,
-                    cudaStream_t s) {
+                    int chk_dr, int chk_dc, cudaStream_t s) {
     const long long items = (long long)((n + 255) / 256) * ((m + 15) / 16);
     const int g = int(items < 148 * 8 ? items : 148 * 8);
-    k_dequant<<<g, 256, 0, s>>>(c, lv, r0, c0, m, n, slot, chk_seq);
+    k_dequant<<<g, 256, 0, s>>>(c, lv, r0, c0, m, n, slot, chk_seq, chk_dr, chk_dc);
 }
 
 }  // namespace tcb

@@ -25,8 +25,10 @@ void launch_check(const DevCtx& c, int lv, int r0, int c0, int m, int n, int low
                   cudaStream_t s);
 void launch_quant(const DevCtx& c, int lv, int r0, int c0, int m, int n, int slot, uint32_t seq,
                   cudaStream_t s);
-void launch_dequant(const DevCtx& c, int lv, int r0, int c0, int m, int n, int slot, uint32_t chk_seq,
-                    cudaStream_t s);
+// chk_dr, chk_dc: offset of (r0, c0) from the checked block's origin (the
+// failure element is reported relative to that block)
+void launch_dequant(const DevCtx& c, int lv, int r0, int c0, int m, int n, int slot, uint32_t chk_seq, int chk_dr,
+                    int chk_dc, cudaStream_t s);
 
 // spin until *host_flag (mapped pinned memory) becomes non-zero (profiling)
 void launch_noop(cudaStream_t s);

@@ -137,8 +137,10 @@ void Plan::ensure_shadows(int node, int p) {
 // tree_trsm (tree.cpp:127-138)
 // ---------------------------------------------------------------------------
 
-void Plan::emit_trsm(Rect B, int p, int lnode) {
+void Plan::emit_trsm(Rect B, int p, int lnode, const RowSplit* rows) {
     const Node& L = nodes[lnode];
+    // the row parts of B this call's device ops cover
+    RowSplit parts = rows ? *rows : RowSplit{{B.r0, B.m}};
     if (L.leaf || std::min(B.m, B.n) <= leaf_size) {
         const uint32_t seq = next_seq();
         const uint64_t f = uint64_t(B.m) * uint64_t(B.n) * uint64_t(B.n);
@@ -166,17 +168,18 @@ void Plan::emit_trsm(Rect B, int p, int lnode) {
                 iv.seq = seq;  // singular diagonal is reported for its first solve
                 push(std::move(iv));
             }
+            for (const auto& part : parts) {
             GemmProb g;
-            g.m = B.m;
+            g.m = part.second;
             g.n = L.n;
             g.k = inv16 ? 2 * kW16Lo : L.n;
-            g.a_r0 = B.r0;
+            g.a_r0 = part.first;
             g.a_c0 = B.c0;
             g.a_kwrap = inv16 ? kW16Lo : 0;
             g.b_r0 = L.r0;
             g.b_c0 = 0;
             g.b_buf = inv16 ? BUF_W16 : BUF_W32;
-            g.c_r0 = B.r0;
+            g.c_r0 = part.first;
             g.c_c0 = B.c0;
             g.exec_level = p;
             g.alpha = 1.0;
@@ -201,12 +204,13 @@ void Plan::emit_trsm(Rect B, int p, int lnode) {
                 op.flops = fl;
                 push(std::move(op));
             };
+            const double fp = double(f) * double(g.m) / double(B.m);  // this part's share
             if (inv16) {
-                emit(g, GC_TC16, double(f));
+                emit(g, GC_TC16, fp);
             } else if (double(g.m) * g.n * g.k <= opt.mma32w_max) {
-                emit(g, GC_MMA32W, double(f));
+                emit(g, GC_MMA32W, fp);
             } else if (g.n <= kTc32TileN) {
-                emit(g, GC_TC32, double(f));
+                emit(g, GC_TC32, fp);
             } else {
                 GemmProb r = g, l = g;
                 r.n = g.n - kTc32TileN;  // right columns [128, n): B rows of W from 128 on
@@ -214,20 +218,23 @@ void Plan::emit_trsm(Rect B, int p, int lnode) {
                 r.c_c0 = g.c_c0 + kTc32TileN;
                 l.n = kTc32TileN;        // left columns [0, 128): K = 128
                 l.k = kTc32TileN;
-                const double fr = double(f) * double(r.n) / double(g.n);
+                const double fr = fp * double(r.n) / double(g.n);
                 emit(r, GC_TC32, fr);
-                emit(l, GC_TC32, double(f) - fr);
+                emit(l, GC_TC32, fp - fr);
             }
+            }  // row parts
             return;
         }
-        Op op;
-        op.type = OP_TRSM;
-        op.level = p;
-        op.rect = B;
-        op.lrect = {L.r0, L.r0, L.n, L.n};
-        op.seq = seq;
-        op.flops = double(f);
-        push(std::move(op));
+        for (const auto& part : parts) {
+            Op op;
+            op.type = OP_TRSM;
+            op.level = p;
+            op.rect = {part.first, B.c0, part.second, B.n};
+            op.lrect = {L.r0, L.r0, L.n, L.n};
+            op.seq = seq;
+            op.flops = double(f) * double(part.second) / double(B.m);
+            push(std::move(op));
+        }
         return;
     }
     const int n1 = L.n1;
@@ -235,33 +242,36 @@ void Plan::emit_trsm(Rect B, int p, int lnode) {
     const Rect off = blocks[L.block].rect;
     Rect B1{B.r0, B.c0, B.m, n1};
     Rect B2{B.r0, B.c0 + n1, B.m, B.n - n1};
-    emit_trsm(B1, p, d1);
-    GemmProb g;
-    g.m = B.m;
-    g.n = B.n - n1;
-    g.k = n1;
-    g.a_r0 = B1.r0;
-    g.a_c0 = B1.c0;
-    g.b_r0 = off.r0;
-    g.b_c0 = off.c0;
-    g.c_r0 = B2.r0;
-    g.c_c0 = B2.c0;
-    g.exec_level = p;
-    g.seq = next_seq();
-    g.ref_kernel = K_GEMM;
-    const uint64_t f = 2ull * uint64_t(g.m) * uint64_t(g.n) * uint64_t(g.k);
-    add_flops(g.seq, p, K_GEMM, f);
-    Op op;
-    op.type = OP_GEMM;
-    op.level = p;
-    op.gclass = gemm_class(p, p, &g);
-    op.prob_begin = int(probs.size());
-    probs.push_back(g);
-    op.prob_end = int(probs.size());
-    op.rect = B2;
-    op.flops = double(f);
-    push(std::move(op));
-    emit_trsm(B2, p, d2);
+    emit_trsm(B1, p, d1, rows);
+    const uint32_t gseq = next_seq();
+    const uint64_t f = 2ull * uint64_t(B.m) * uint64_t(B.n - n1) * uint64_t(n1);
+    add_flops(gseq, p, K_GEMM, f);
+    for (const auto& part : parts) {
+        GemmProb g;
+        g.m = part.second;
+        g.n = B.n - n1;
+        g.k = n1;
+        g.a_r0 = part.first;
+        g.a_c0 = B1.c0;
+        g.b_r0 = off.r0;
+        g.b_c0 = off.c0;
+        g.c_r0 = part.first;
+        g.c_c0 = B2.c0;
+        g.exec_level = p;
+        g.seq = gseq;
+        g.ref_kernel = K_GEMM;
+        Op op;
+        op.type = OP_GEMM;
+        op.level = p;
+        op.gclass = gemm_class(p, p, &g);
+        op.prob_begin = int(probs.size());
+        probs.push_back(g);
+        op.prob_end = int(probs.size());
+        op.rect = {part.first, B2.c0, part.second, B2.n};
+        op.flops = double(f) * double(part.second) / double(B.m);
+        push(std::move(op));
+    }
+    emit_trsm(B2, p, d2, rows);
 }
 
 // ---------------------------------------------------------------------------
@@ -377,7 +387,7 @@ void Plan::emit_syrk(int cnode, Rect A, int p) {
 // quantize (spine panels; ext_slot >= 0: an alpha slot already allocated,
 // e.g. filled from outside by a distributed driver), tree_trsm against the
 // factored diag1 tree rooted at lnode, dequantize, require_finite
-void Plan::emit_panel(int bi, int lnode, int ext_slot) {
+void Plan::emit_panel(int bi, int lnode, int ext_slot, int d2node) {
     const Block blk = blocks[bi];
     const int p = blk.level;
     int slot = -1;
@@ -423,17 +433,29 @@ void Plan::emit_panel(int bi, int lnode, int ext_slot) {
         }
     }
     ensure_shadows(lnode, p);
+    // lookahead: a tall panel's TRSM as two row parts split where diag2
+    // splits, so diag2.diag1's SYRK part and factorization wait only for the
+    // first (the SYRK below is then emitted per region, syrk_split_min)
+    RowSplit split;
+    if (opt.trsm_row_split_min > 0 && d2node >= 0 && blk.rect.m >= opt.trsm_row_split_min &&
+        !nodes[d2node].leaf) {
+        const int h = nodes[d2node].n1;
+        split = {{blk.rect.r0, h}, {blk.rect.r0 + h, blk.rect.m - h}};
+    }
     const int op0 = int(ops.size()), pr0 = int(probs.size());
-    emit_trsm(blk.rect, p, lnode);
+    emit_trsm(blk.rect, p, lnode, split.empty() ? nullptr : &split);
     const int op1 = int(ops.size()), pr1 = int(probs.size());
-    int dq_op = -1;
+    std::vector<int> dq_ops;
     if (blk.spine_quant) {
-        Op dq;
-        dq.type = OP_DEQUANT;
-        dq.level = p;
-        dq.rect = blk.rect;
-        dq.slot = slot;
-        dq_op = push(std::move(dq));
+        const RowSplit dparts = split.empty() ? RowSplit{{blk.rect.r0, blk.rect.m}} : split;
+        for (const auto& part : dparts) {
+            Op dq;
+            dq.type = OP_DEQUANT;
+            dq.level = p;
+            dq.rect = {part.first, blk.rect.c0, part.second, blk.rect.n};
+            dq.slot = slot;
+            dq_ops.push_back(push(std::move(dq)));
+        }
     }
     // require_finite after dequantize (tree.cpp:121): every panel element's
     // last writer is the leaf solve of its column block (or the dequantize
@@ -452,7 +474,7 @@ void Plan::emit_panel(int bi, int lnode, int ext_slot) {
                 probs[i].chk_r0 = blk.rect.r0;
                 probs[i].chk_c0 = blk.rect.c0;
             }
-        if (dq_op >= 0) {
+        for (int dq_op : dq_ops) {
             ops[dq_op].check_seq = post;
             ops[dq_op].chk = blk.rect;
         }
@@ -501,7 +523,7 @@ void Plan::emit_potrf(int node) {
     emit_potrf(nd.d1);
     const Block blk = blocks[nd.block];
     const int p = blk.level;
-    emit_panel(nd.block, nd.d1, -1);
+    emit_panel(nd.block, nd.d1, -1, nd.d2);
     emit_syrk(nd.d2, blk.rect, p);
     emit_potrf(nd.d2);
 }

@@ -163,6 +163,7 @@ struct PlanOptions {
     bool inverse_trsm = true; // FP16 leaf solves with m >= kInvMinRows as tcgen05 GEMMs
     bool fuse_checks = true;  // require_finite inside the producing kernels
     int sub32_max_rows = 0;  // F32 leaf solves of at most this many rows by substitution (k_trsm_cm) instead of inverse + GEMM
+    int trsm_row_split_min = 0;   // off-diagonal panels with at least this many rows: TRSM ops split at diag2's first split (lookahead: diag2.diag1's SYRK and factorization start after the first row part)
     bool shadow_per_block = true;  // one OP_SHADOW per block of L (pipelines the lower-level TRSM with the factorization it reads)
     int syrk_split_min = 1 << 30; // tree_syrk nodes at least this large launch per region (lookahead; off by default: it shortens the critical path but adds launches, a net loss for batches)
 };
@@ -250,8 +251,12 @@ struct Plan {
     std::vector<uint8_t> has_inverse;              // [block] bit 0: W16 ready, bit 1: W32 ready
     int build_node(int r0, int n, int depth);
     void emit_potrf(int node);
-    void emit_panel(int block, int lnode, int ext_slot);
-    void emit_trsm(Rect brect, int p, int lnode);
+    // row ranges [r0, r0 + m) of a TRSM's B emitted as separate device ops
+    // (rows are independent, tree.cpp:133-134); the reference's calls, their
+    // flops and sequence numbers stay one per call
+    using RowSplit = std::vector<std::pair<int, int>>;
+    void emit_panel(int block, int lnode, int ext_slot, int d2node = -1);
+    void emit_trsm(Rect brect, int p, int lnode, const RowSplit* rows = nullptr);
     void emit_syrk(int cnode, Rect arect, int p);
     void collect_syrk(int cnode, Rect arect, int p, std::vector<GemmProb>& out);
     GemmProb syrk_offdiag(int cnode, Rect arect);

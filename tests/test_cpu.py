@@ -279,3 +279,20 @@ def test_no_in_place_gemm_hazard(tc, n, b, cfg):
                 bcols = g["b_c0"] < g["c_c0"] + g["n"] and g["c_c0"] < g["b_c0"] + g["k"]
                 assert not (brows and bcols), (i, cls, g)
     assert inplace > 0 or cfg == "[F16, F32, F64]"
+
+
+def test_lookahead_splits_keep_the_accounting():
+    """row-split panel TRSMs / region-split SYRKs: same flop records (one per
+    reference call, static == instrumented), and every GEMM problem inside
+    its operand blocks (host-only planner check, no device)"""
+    import paper_2601_08082_b200 as tc
+    for n, b, cfg in [(4096, 256, "[F16, F16, F16, F32]"), (2000, 64, "[F16, F32, F64]")]:
+        base = tc.Plan(n, b, cfg)
+        split = tc.Plan(n, b, cfg)
+        split.set_option("trsm_row_split_min", 256)
+        split.set_option("syrk_split_min", 256)
+        assert split.stats()["ops"] > base.stats()["ops"]
+        assert split.run_flops().as_tuple() == base.run_flops().as_tuple() == tc.flop_breakdown(n, b, cfg).as_tuple()
+        for i in range(split.stats()["ops"]):
+            for pr in (split.op_probs(i) if split.op_info(i)["type"] == "gemm" else []):
+                assert 0 <= pr["c_r0"] and pr["c_r0"] + pr["m"] <= n and pr["a_r0"] + pr["m"] <= n

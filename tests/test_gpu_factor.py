@@ -386,3 +386,52 @@ def test_host_entry_point_pinned_ragged(tc, oracle, n, b, cfg):
     assert np.array_equal(np.tril(host.numpy().T), np.tril(l_dev))
     iu = np.triu_indices(n, 1)
     assert np.array_equal(host.numpy().T[iu], a[iu])
+
+
+LOOKAHEAD = {"trsm_row_split_min": 256, "syrk_split_min": 256}
+
+
+def _run_opts(tc, a, b, cfg, opts):
+    import torch
+    plan = tc.Plan(a.shape[0], b, cfg)
+    for k, v in opts.items():
+        plan.set_option(k, v)
+    a_dev = tc.to_device(a)
+    l_dev = a_dev.clone()
+    st = plan.factor_device(a_dev, l_dev)
+    torch.cuda.synchronize()
+    return st, tc.from_device(l_dev), plan.run_flops()
+
+
+@pytest.mark.parametrize("n,b,cfg,seed", [(2048, 128, "[F16, F16, F16, F32]", 3), (1000, 64, "[F16, F32]", 8),
+                                          (777, 100, "[F16, F16, F32, F64]", 12)])
+def test_lookahead_splits_are_bit_identical(tc, oracle, n, b, cfg, seed):
+    """row-split panel TRSMs and region-split SYRKs (lookahead) only cut the
+    reference's calls into row / region parts: every element sees the same
+    operations in the same order, so L is bit-identical to the default plan,
+    with the same status and flop accounting"""
+    a = oracle.spd_generate(n, seed)
+    st0, l0, fl0 = _run_opts(tc, a, b, cfg, {})
+    st1, l1, fl1 = _run_opts(tc, a, b, cfg, LOOKAHEAD)
+    assert st0.status == st1.status == "ok"
+    assert fl0.as_tuple() == fl1.as_tuple()
+    assert np.array_equal(np.tril(l0).view(np.uint64), np.tril(l1).view(np.uint64))
+
+
+def test_lookahead_splits_keep_first_failure(tc, oracle):
+    """a panel that overflows F16 and an indefinite trailing block: the split
+    plan reports the same first failure (status, index, text) as the default"""
+    a = oracle.spd_generate(1024, 2)
+    a[700:, 700:] -= 2.0 * 1024 * np.eye(324)  # not positive definite from row 700 on
+    st0, _, _ = _run_opts(tc, a, 64, "[F16, F16, F32]", {})
+    st1, _, _ = _run_opts(tc, a, 64, "[F16, F16, F32]", LOOKAHEAD)
+    assert st0.status == st1.status == "not-positive-definite"
+    assert st0.index == st1.index
+    b = oracle.spd_generate(1024, 2)
+    b[600:700, 0:100] = 1e6  # off-diagonal block values beyond F16 range before quantize -> alpha > 1 path
+    st0, l0, _ = _run_opts(tc, b, 64, "[F16, F16, F32]", {})
+    st1, l1, _ = _run_opts(tc, b, 64, "[F16, F16, F32]", LOOKAHEAD)
+    assert st0.status == st1.status
+    assert (st0.detail, st0.index) == (st1.detail, st1.index)
+    if st0.status == "ok":
+        assert np.array_equal(np.tril(l0).view(np.uint64), np.tril(l1).view(np.uint64))
