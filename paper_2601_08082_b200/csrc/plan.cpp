@@ -192,11 +192,13 @@ void Plan::emit_trsm(Rect B, int p, int lnode, const RowSplit* rows) {
             // (GC_MMA32W).  FP32 on tcgen05 (128-wide tiles): two ops in
             // sequence -- columns [128, n) first (they read all of B), then
             // [0, 128), which need only B[:, 0:128) (W is lower triangular)
+            const bool later_part = opt.lookahead_prio && &part != &parts.front();  // lookahead: low priority
             auto emit = [&](const GemmProb& gp, int gclass, double fl) {
                 Op op;
                 op.type = OP_GEMM;
                 op.level = p;
                 op.gclass = gclass;
+                op.bulk = later_part ? 1 : 0;
                 op.prob_begin = int(probs.size());
                 probs.push_back(gp);
                 op.prob_end = int(probs.size());
@@ -229,6 +231,7 @@ void Plan::emit_trsm(Rect B, int p, int lnode, const RowSplit* rows) {
             Op op;
             op.type = OP_TRSM;
             op.level = p;
+            op.bulk = (opt.lookahead_prio && &part != &parts.front()) ? 1 : 0;
             op.rect = {part.first, B.c0, part.second, B.n};
             op.lrect = {L.r0, L.r0, L.n, L.n};
             op.seq = seq;
@@ -264,6 +267,7 @@ void Plan::emit_trsm(Rect B, int p, int lnode, const RowSplit* rows) {
         op.type = OP_GEMM;
         op.level = p;
         op.gclass = gemm_class(p, p, &g);
+        op.bulk = (opt.lookahead_prio && &part != &parts.front()) ? 1 : 0;
         op.prob_begin = int(probs.size());
         probs.push_back(g);
         op.prob_end = int(probs.size());
@@ -335,7 +339,7 @@ void Plan::collect_syrk(int cnode, Rect A, int p, std::vector<GemmProb>& out) {
 }
 
 // one launch per operand class, classes in order of first appearance
-void Plan::push_gemm_group(const std::vector<GemmProb>& all, int p) {
+void Plan::push_gemm_group(const std::vector<GemmProb>& all, int p, int bulk) {
     std::vector<int> classes;
     for (const auto& g : all) {
         const int c = gemm_class(p, g.exec_level, &g);
@@ -354,7 +358,7 @@ void Plan::push_gemm_group(const std::vector<GemmProb>& all, int p) {
                 op.flops += double(g.lower ? 2.0 * g.m * g.n * g.k / 2.0 : 2.0 * g.m * g.n * g.k);
             }
         op.prob_end = int(probs.size());
-        op.bulk = 1;
+        op.bulk = bulk;
         push(std::move(op));
     }
 }
@@ -365,18 +369,21 @@ void Plan::push_gemm_group(const std::vector<GemmProb>& all, int p) {
 // tree_potrf(diag2.diag1) -> ...) then starts as soon as the region it reads
 // is updated, while the rest of the update runs beside it (lookahead).  The
 // sequence numbers keep the reference's order either way.
-void Plan::emit_syrk(int cnode, Rect A, int p) {
+void Plan::emit_syrk(int cnode, Rect A, int p, bool critical, bool via_split) {
     const Node& C = nodes[cnode];
     if (!C.leaf && C.n >= opt.syrk_split_min) {
+        // lookahead_prio: the diag1 chain of the split regions is what the
+        // factorization that follows waits for first -- high priority; the
+        // off-diagonal and diag2 regions low
         const int n1 = C.n1, d1 = C.d1, d2 = C.d2;
-        emit_syrk(d1, Rect{A.r0, A.c0, n1, A.n}, p);
+        emit_syrk(d1, Rect{A.r0, A.c0, n1, A.n}, p, critical, true);
         push_gemm_group({syrk_offdiag(cnode, A)}, p);
-        emit_syrk(d2, Rect{A.r0 + n1, A.c0, A.m - n1, A.n}, p);
+        emit_syrk(d2, Rect{A.r0 + n1, A.c0, A.m - n1, A.n}, p, false, true);
         return;
     }
     std::vector<GemmProb> all;
     collect_syrk(cnode, A, p, all);
-    push_gemm_group(all, p);
+    push_gemm_group(all, p, (opt.lookahead_prio && critical && via_split) ? 0 : 1);
 }
 
 // ---------------------------------------------------------------------------

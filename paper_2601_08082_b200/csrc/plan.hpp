@@ -163,6 +163,7 @@ struct PlanOptions {
     bool inverse_trsm = true; // FP16 leaf solves with m >= kInvMinRows as tcgen05 GEMMs
     bool fuse_checks = true;  // require_finite inside the producing kernels
     int sub32_max_rows = 0;  // F32 leaf solves of at most this many rows by substitution (k_trsm_cm) instead of inverse + GEMM
+    bool lookahead_prio = true;   // with the splits below: the first row part / the diag1 chain of a split SYRK at high priority, the rest low
     int trsm_row_split_min = 0;   // off-diagonal panels with at least this many rows: TRSM ops split at diag2's first split (lookahead: diag2.diag1's SYRK and factorization start after the first row part)
     bool shadow_per_block = true;  // one OP_SHADOW per block of L (pipelines the lower-level TRSM with the factorization it reads)
     int syrk_split_min = 1 << 30; // tree_syrk nodes at least this large launch per region (lookahead; off by default: it shortens the critical path but adds launches, a net loss for batches)
@@ -257,10 +258,10 @@ struct Plan {
     using RowSplit = std::vector<std::pair<int, int>>;
     void emit_panel(int block, int lnode, int ext_slot, int d2node = -1);
     void emit_trsm(Rect brect, int p, int lnode, const RowSplit* rows = nullptr);
-    void emit_syrk(int cnode, Rect arect, int p);
+    void emit_syrk(int cnode, Rect arect, int p, bool critical = true, bool via_split = false);
     void collect_syrk(int cnode, Rect arect, int p, std::vector<GemmProb>& out);
     GemmProb syrk_offdiag(int cnode, Rect arect);
-    void push_gemm_group(const std::vector<GemmProb>& all, int p);
+    void push_gemm_group(const std::vector<GemmProb>& all, int p, int bulk = 1);
     void ensure_shadows(int node, int p);
     int push(Op op);
     uint32_t next_seq() { return ++n_seq; }
