@@ -39,9 +39,10 @@ for k, a in sorted(agg.items(), key=lambda x: -x[1][1])[:18]:
 a = agg["k_gemm_tc<0>"]
 json.dump({"kernel": "k_gemm_tc<KIND_F16>", "launches": a[0], "dram_bytes_total": a[2],
            "dram_bytes_per_launch": a[2] / a[0],
-           "source": "profiles/r01c_launches_bench.csv.gz: ncu --replay-mode application --metrics "
+           "source": (sys.argv[2] if len(sys.argv) > 2 else src) + ": ncu --metrics "
                      "gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none of "
-                     "`bench.py --steps 1 --warmup 0 --e2e-steps 0 --cpu-n 0 --c4-count 0` (tools/launch_list.sh)"},
+                     "`bench.py --steps 1 --warmup 0 --e2e-steps 0 --cpu-n 0 --c4-count 0 --no-variants` "
+                     "(tools/r02_prof.sh)"},
           open("profiles/ncu_traffic.json", "w"), indent=1)
 if len(sys.argv) > 2:
     with open(src, "rb") as f, gzip.open(sys.argv[2], "wb") as g:
