@@ -539,6 +539,25 @@ void Plan::emit_potrf(int node) {
 // dependencies
 // ---------------------------------------------------------------------------
 
+bool potrf_v2_ok(int lv, int n);  // k_potrf.cu: the shared-memory leaf kernel handles (lv, n)
+
+// an F32 leaf's inverse (W32, for the FP32 panel solves) is computed by its
+// POTRF kernel from the factor still in shared memory
+void Plan::fuse_leaf_inverses() {
+    if (!opt.fuse_inverse) return;
+    for (Op& iv : ops) {
+        if (iv.type != OP_INVERSE || iv.level != LV_F32) continue;
+        for (Op& pf : ops)
+            if (pf.type == OP_POTRF && pf.level == LV_F32 && pf.rect.r0 == iv.rect.r0 && pf.rect.m == iv.rect.m &&
+                potrf_v2_ok(pf.level, pf.rect.m)) {
+                pf.fuse_inv = 1;
+                pf.inv_seq = iv.seq;
+                iv.fused = 1;
+                break;
+            }
+    }
+}
+
 void Plan::finalize_accesses() {
     for (Op& op : ops) {
         op.acc.clear();
@@ -575,8 +594,10 @@ void Plan::finalize_accesses() {
                 break;
             case OP_POTRF:
                 op.acc.push_back({op.level, op.rect, true});
+                if (op.fuse_inv) op.acc.push_back({BUF_W32, {op.rect.r0, 0, op.rect.m, kW32Ld}, true});
                 break;
             case OP_INVERSE:
+                if (op.fused) break;  // no accesses: nothing waits on it
                 op.acc.push_back({op.level, op.rect, false});
                 if (op.level == LV_F16) op.acc.push_back({BUF_W16, {op.rect.r0, 0, op.rect.m, kW16Ld}, true});
                 else op.acc.push_back({BUF_W32, {op.rect.r0, 0, op.rect.m, kW32Ld}, true});
@@ -747,6 +768,7 @@ Plan Plan::make(int n, int b, const std::vector<int>& levels, bool quantize, int
             P.push(std::move(imp));
         }
     P.emit_potrf(0);
+    P.fuse_leaf_inverses();
     for (int i : order) {
         Op exp;
         exp.type = OP_EXPORT;

@@ -435,3 +435,19 @@ def test_lookahead_splits_keep_first_failure(tc, oracle):
     assert (st0.detail, st0.index) == (st1.detail, st1.index)
     if st0.status == "ok":
         assert np.array_equal(np.tril(l0).view(np.uint64), np.tril(l1).view(np.uint64))
+
+
+def test_fused_leaf_inverse_matches_oracle(tc, oracle):
+    """option fuse_inverse: the F32 leaves' W = inv(L) computed inside the
+    leaf POTRF kernel instead of a separate launch (a measured alternative,
+    off by default): same status and flops, rel within 2x of the reference's"""
+    a = oracle.spd_generate(2048, 11)
+    cfg, b = "[F16, F16, F16, F32]", 128
+    st_o, _, _, rel_o, fl_o = oracle.factor(a, b, parse_levels(cfg))
+    st, l, fl = _run_opts(tc, a, b, cfg, {"fuse_inverse": 1})
+    assert st.status == st_o == "ok"
+    assert fl.as_tuple() == fl_o.as_tuple()
+    import torch
+    rel = tc.factorization_error_device(tc.to_device(a), tc.to_device(l))
+    torch.cuda.synchronize()
+    assert rel <= 2 * rel_o + FLOOR, (rel, rel_o)

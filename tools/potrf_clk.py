@@ -22,8 +22,8 @@ for n, cfg in [(16384, "[F16, F16, F16, F32]"), (4096, "Pure F16")]:
     k = max(out[5], 1)
     pot = [ms[i] for i in range(len(ms)) if p.op_info(i)["type"] == "potrf"]
     inv = [ms[i] for i in range(len(ms)) if p.op_info(i)["type"] == "inverse"]
-    print(cfg, n, "leaves", out[5], "potrf cycles/leaf: load %.0f a %.0f b1 %.0f b2 %.0f store %.0f | event %.1f us" % (
-        out[0] / k, out[1] / k, out[2] / k, out[3] / k, out[4] / k, 1e3 * sum(pot) / max(len(pot), 1)))
+    print(cfg, n, "leaves", out[5], "potrf cycles/leaf: load %.0f a %.0f b1 %.0f b2 %.0f store %.0f fused-inverse %.0f (rows %.0f) | event %.1f us" % (
+        out[0] / k, out[1] / k, out[2] / k, out[3] / k, out[4] / k, out[6] / k, out[7] / k, 1e3 * sum(pot) / max(len(pot), 1)))
     fi(out, 1)
     k = max(out[6], 1)
     print(cfg, n, "inverses", out[6], "CTA0 cycles: load %.0f rcp %.0f diag %.0f prod %.0f tri %.0f store %.0f | event %.1f us"
