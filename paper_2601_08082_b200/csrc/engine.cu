@@ -176,6 +176,16 @@ bool Engine::prepare(std::string* err) {
                 std::vector<unsigned char> tp;
                 L.tiles = tc_build_probs(ctx_, op.gclass == GC_TC32 ? KIND_TF32X3 : KIND_F16, dp, tp, err);
                 if (L.tiles < 0) return false;
+                if (op.gclass == GC_TC16 && tc_pair_min_tiles() > 0 && L.tiles >= tc_pair_min_tiles()) {
+                    // a large FP16-kind list: 256x256 tiles on CTA pairs
+                    std::vector<unsigned char> tp2;
+                    const int t2 = tc_build_probs(ctx_, KIND_F16, dp, tp2, nullptr, 1);
+                    if (t2 > 0) {
+                        tp.swap(tp2);
+                        L.tiles = t2;
+                        L.pair = 1;
+                    }
+                }
                 L.offset = append(tp.data(), tp.size());
             } else {
                 L.tiles = op.gclass == GC_MMA32W ? simt_tiles(dp, M32W_ROWS, 256)
@@ -230,7 +240,9 @@ void Engine::launch_op(int i, cudaStream_t s) {
             else launch_leaf_inverse(ctx_, r.r0, r.m, op.seq, s);
             break;
         case OP_GEMM:
-            if (op.gclass == GC_TC16 || op.gclass == GC_TC32)
+            if (L.pair)
+                launch_gemm_tc_pair(ctx_, tab, L.count, L.tiles, s);
+            else if (op.gclass == GC_TC16 || op.gclass == GC_TC32)
                 launch_gemm_tc(ctx_, op.gclass == GC_TC32 ? KIND_TF32X3 : KIND_F16, tab, L.count, L.tiles, s,
                                op.bulk ? bulk_max_ctas : 0, op.bulk ? bulk_tiles_per_cta : 0);
             else launch_gemm_simt(ctx_, op.gclass, reinterpret_cast<DevProb*>(tab), L.count, L.tiles, s);

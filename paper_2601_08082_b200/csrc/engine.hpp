@@ -21,6 +21,7 @@ namespace tcb {
 struct OpLaunch {
     int tiles = 0;
     int count = 0;
+    int pair = 0;       // tcgen05 FP16 kind on CTA pairs (k_gemm_tc2)
     size_t offset = 0;  // into the table arena
 };
 

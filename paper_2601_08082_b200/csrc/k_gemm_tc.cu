@@ -54,6 +54,7 @@ struct alignas(128) TcProb {
     CUtensorMap ta;  // A rows [a_r0, a_r0+m) x cols [a_c0, a_c0+k) (extents end there)
     CUtensorMap tb;  // B rows [b_r0, b_r0+n) x cols [b_c0, b_c0+k)
     CUtensorMap tcm; // C rows [c_r0, c_r0+m) x cols [c_c0, c_c0+n) at the exec level (128 x 128-byte boxes)
+    CUtensorMap tbh; // B as tb, 128-row boxes: one CTA's half of a CTA pair's 256-row B tile (FP16 kind)
     int m, n, k;
     int a_r0, a_c0, b_r0, b_c0, c_r0, c_c0;
     int exec_level, lower, tile0, tiles_n;
@@ -244,7 +245,7 @@ __device__ __forceinline__ int find_tc_prob(const TcProb* p, int np, int tile) {
 
 // tile -> (problem, tm, tn); false for a lower problem's tile strictly above
 // the diagonal (nothing to write).  Every role evaluates the same predicate.
-template <int BN>
+template <int BN, int BMT = BM>
 __device__ __forceinline__ bool tile_coords(const TcProb* probs, int np, int t, int& pi, int& tm, int& tn) {
     pi = find_tc_prob(probs, np, t);
     const TcProb& p = probs[pi];
@@ -252,14 +253,14 @@ __device__ __forceinline__ bool tile_coords(const TcProb* probs, int np, int t, 
     // grouped raster: bands of GROUP tile rows, column-major inside a band,
     // so the CTAs resident at once share a few A and B panels per k-block
     // (L2 reuse; a plain row-major order streams ~tiles_n B panels from DRAM)
-    constexpr int GROUP = 16;
-    const int tiles_m = (p.m + BM - 1) / BM;
+    constexpr int GROUP = 16 * BM / BMT;
+    const int tiles_m = (p.m + BMT - 1) / BMT;
     const int band = GROUP * p.tiles_n;
     const int g = lt / band, r = lt - g * band;
     const int rows = min(GROUP, tiles_m - g * GROUP);
     tm = g * GROUP + r % rows;
     tn = r / rows;
-    return !(p.lower && p.c_c0 + tn * BN > p.c_r0 + tm * BM + BM - 1);
+    return !(p.lower && p.c_c0 + tn * BN > p.c_r0 + tm * BMT + BMT - 1);
 }
 
 // dot_update's tail (kernels.cpp:33-37) for an FP32 accumulator s:
@@ -838,6 +839,343 @@ __global__ void __launch_bounds__(Cfg<KIND>::NTHREADS, 1) k_gemm_tc(DevCtx c, co
     if (threadIdx.x == 32) stamp(c, 6);
 }
 
+// ---------------------------------------------------------------------------
+// CTA-pair variant of the FP16 kind (tcgen05.mma.cta_group::2): a cluster of
+// two CTAs computes 256 x 256 tiles.  Each CTA stages its own 128 rows of A
+// and one 128-row half of B per k-block (32 KB instead of 48 KB), the
+// leader (rank 0) issues M=256, N=256 MMAs that read A from both CTAs' own
+// halves and B from both halves, and each CTA's TMEM holds its 128 rows of
+// the accumulator.  Per SM the operand bytes per flop fall by a third, and
+// the ring holds 6 stages (1.1 us of MMA at full rate) instead of 4: the big
+// trailing updates are short of operand latency hiding with 128x256 tiles.
+// Barriers: full[s] in the leader (its expect_tx covers both CTAs' loads,
+// which complete on it through .cta_group::2), empty[s] / tfull in both
+// (the leader's commits multicast), tempty in the leader (both CTAs'
+// epilogue warps arrive).  Epilogue as in k_gemm_tc (TMA-staged C only).
+// ---------------------------------------------------------------------------
+constexpr int P_STAGES = 6;
+constexpr int P_BN = 256;                       // pair tile columns (N of the MMA)
+constexpr int P_A_BYTES = BM * 128;             // this CTA's A rows, one k-block
+constexpr int P_B_BYTES = BM * 128;             // this CTA's half of B
+constexpr int P_STAGE_BYTES = P_A_BYTES + P_B_BYTES;
+constexpr int P_STG_BYTES = 2 * BM * 128;
+constexpr int P_SMEM_BYTES = P_STAGES * P_STAGE_BYTES + P_STG_BYTES + 1024 + 256;
+constexpr uint32_t P_TMEM_COLS = 2 * P_BN;
+constexpr uint32_t P_IDESC = (1u << 4) | (uint32_t(P_BN >> 3) << 17) | (uint32_t((2 * BM) >> 4) << 24);
+static_assert(P_SMEM_BYTES <= 227 * 1024, "pair shared memory");
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t saddr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// TMA load whose completion goes to the leader's barrier (cluster address)
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t mbar_cluster, int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+        "[%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(mbar_cluster), "r"(x), "r"(y)
+        : "memory");
+}
+__device__ __forceinline__ void mma_pair(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accum) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(P_IDESC), "r"(accum));
+}
+// arrive on the barrier at this offset in both CTAs of the pair once the
+// leader's MMAs so far have completed
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+    asm volatile(
+        "{\n"
+        ".reg .b16 m;\n"
+        "mov.b16 m, 3;\n"
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n"
+        "}\n" ::"r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
+__global__ void __launch_bounds__(320, 1) k_gemm_tc2(DevCtx c, const TcProb* __restrict__ probs, int np, int tiles) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                                           ~uintptr_t(1023));
+    auto sA = [&](int st) { return smem + st * P_STAGE_BYTES; };
+    auto sB = [&](int st) { return smem + st * P_STAGE_BYTES + P_A_BYTES; };
+    unsigned char* stg = smem + P_STAGES * P_STAGE_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(stg + P_STG_BYTES);
+    uint64_t* empty = full + P_STAGES;
+    uint64_t* tfull = empty + P_STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint64_t* cfull = tempty + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cfull + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    const bool leader = rank == 0;
+    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+
+    if (warp == 0 && lane == 0) {
+        for (int st = 0; st < P_STAGES; ++st) {
+            mbar_init(&full[st], 1);
+            mbar_init(&empty[st], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 16);  // 8 epilogue warps x 2 CTAs (leader's copy)
+        }
+        mbar_init(cfull, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(P_TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    tc_fence_before();
+    cluster_sync_all();  // both CTAs' barriers initialised, TMEM allocated
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---------------- TMA producer (both CTAs) ----------------
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = pair; t < tiles; t += npairs) {
+                int pi, tm, tn;
+                if (!tile_coords<P_BN, 2 * BM>(probs, np, t, pi, tm, tn)) continue;
+                const TcProb* p = probs + pi;
+                prefetch_map(&p->ta);
+                prefetch_map(&p->tbh);
+                prefetch_map(&p->tcm);
+                const int nk = (p->k + 63) / 64;
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    if (leader) mbar_expect_tx(&full[stage], 2 * P_STAGE_BYTES);
+                    const uint32_t fb = mapa_rank(smem_u32(&full[stage]), 0);
+                    const int ka = p->a_kwrap ? (kb * 64) % p->a_kwrap : kb * 64;
+                    tma_load_2d_pair(sA(stage), &p->ta, fb, p->a_c0 + ka, p->a_r0 - p->ya + tm * 2 * BM + int(rank) * BM);
+                    tma_load_2d_pair(sB(stage), &p->tbh, fb, p->b_c0 + kb * 64,
+                                     p->b_r0 - p->yb + tn * P_BN + int(rank) * BM);
+                    if (++stage == P_STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer (leader only) ----------------
+        if (leader) {
+            int stage = 0;
+            uint32_t phase = 0;
+            int as = 0;
+            uint32_t aphase = 0;
+            for (int t = pair; t < tiles; t += npairs) {
+                int pi, tm, tn;
+                if (!tile_coords<P_BN, 2 * BM>(probs, np, t, pi, tm, tn)) continue;
+                const int nk = (probs[pi].k + 63) / 64;
+                mbar_wait(&tempty[as], aphase ^ 1);
+                tc_fence_after();
+                const uint32_t dcol = tmem + uint32_t(as * P_BN);
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    if (lane == 0) {
+                        const uint64_t da = sdesc(sA(stage));
+                        const uint64_t db = sdesc(sB(stage));
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const uint64_t o = uint64_t(2 * k);
+                            mma_pair(dcol, da + o, db + o, (kb | k) != 0);
+                        }
+                        mma_commit_pair(&empty[stage]);
+                        if (kb == nk - 1) mma_commit_pair(&tfull[as]);
+                    }
+                    __syncwarp();
+                    if (++stage == P_STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                if (++as == 2) {
+                    as = 0;
+                    aphase ^= 1;
+                }
+            }
+        }
+    } else {
+        // ---------------- epilogue (warps 2..9, both CTAs) ----------------
+        const int q = warp & 3;
+        const int half = (warp - 2) >> 2;
+        const bool ldr = warp == 2 && lane == 0;
+        const int row_l = q * 32 + lane;
+        const uint32_t tempty_leader0 = mapa_rank(smem_u32(&tempty[0]), 0);
+        const uint32_t tempty_leader1 = mapa_rank(smem_u32(&tempty[1]), 0);
+        int as = 0;
+        uint32_t aphase = 0, cphase = 0;
+        for (int t = pair; t < tiles; t += npairs) {
+            int pi, tm, tn;
+            if (!tile_coords<P_BN, 2 * BM>(probs, np, t, pi, tm, tn)) continue;
+            const TcProb& p = probs[pi];
+            const bool f16 = p.exec_level == LV_F16;
+            const int box_cols = f16 ? 64 : 32;
+            const int rc = min(P_BN, 2 * box_cols);  // columns per round
+            const int rounds = P_BN / rc;
+            const int hw = rc / 2;
+            const int i = tm * 2 * BM + int(rank) * BM + row_l;  // row of C inside the problem
+            const int crow = tm * 2 * BM + int(rank) * BM;        // first row of this CTA's half tile
+            const bool row_ok = i < p.m;
+            Epi epi;
+            epi.alpha = p.a_kwrap ? double(c.wscale[p.b_r0]) : p.alpha;
+            epi.beta = p.beta;
+            epi.fast = pow2_or_one(epi.alpha) && (epi.beta == 0.0 || epi.beta == 1.0);
+            epi.af = float(epi.alpha);
+            const bool has_c = epi.beta != 0.0;
+            const bool load_c = has_c || p.lower;
+            int jhi = p.n;
+            if (p.lower) jhi = min(jhi, (p.c_r0 + i) - p.c_c0 + 1);
+            if (!row_ok) jhi = 0;
+            const bool half_live = crow < p.m;  // this CTA's rows exist in the problem
+            int badj = -1;
+            for (int rd = 0; rd < rounds; ++rd) {
+                const int col0 = tn * P_BN + rd * rc;
+                const int nbox = (col0 < p.n && half_live) ? min(2, (p.n - col0 + box_cols - 1) / box_cols) : 0;
+                const bool do_load = load_c && nbox > 0;
+                if (ldr) {
+                    bulk_wait_read0();
+                    if (do_load) {
+                        mbar_expect_tx(cfull, uint32_t(nbox) * BM * 128);
+                        for (int bx = 0; bx < nbox; ++bx)
+                            tma_load_2d(stg + bx * BM * 128, &p.tcm, cfull, p.c_c0 + col0 + bx * box_cols,
+                                        p.c_r0 - p.yc + crow);
+                    }
+                }
+                if (rd == 0) {
+                    mbar_wait(&tfull[as], aphase);
+                    tc_fence_after();
+                }
+                if (do_load) {
+                    mbar_wait(cfull, cphase);
+                    cphase ^= 1;
+                } else {
+                    epi_sync();
+                }
+                for (int cc = 0; cc < hw; cc += 32) {
+                    float v[32];
+                    const int jt = rd * rc + half * hw + cc;
+                    __syncwarp();
+                    tmem_ld32(tmem + (uint32_t(q * 32) << 16) + uint32_t(as * P_BN + jt), v);
+                    if (rd == rounds - 1 && cc == hw - 32) {
+                        // accumulator drained: tell the leader's MMA warp
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_cluster(as == 0 ? tempty_leader0 : tempty_leader1);
+                    }
+                    const int j0 = tn * P_BN + jt;
+                    if (j0 >= jhi) continue;
+                    const int jm = min(32, jhi - j0);
+                    const int bx = (jt - rd * rc) / box_cols;
+                    unsigned char* rowp = stg + bx * BM * 128 + row_l * 128;
+                    const int c16 = ((jt - rd * rc) % box_cols) * (f16 ? 2 : 4) / 16;
+                    uint32_t bad = 0;
+                    if (f16) {
+#pragma unroll
+                        for (int g = 0; g < 4; ++g) {
+                            uint4* cp = reinterpret_cast<uint4*>(rowp + (((c16 + g) ^ (row_l & 7)) << 4));
+                            uint4 orig = load_c ? *cp : make_uint4(0, 0, 0, 0);
+                            uint4 raw = has_c ? orig : make_uint4(0, 0, 0, 0);
+                            uint32_t* w = reinterpret_cast<uint32_t*>(&raw);
+                            uint32_t* wo = reinterpret_cast<uint32_t*>(&orig);
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                const int jj = 8 * g + 2 * e;
+                                const float2 cf = __half22float2(*reinterpret_cast<__half2*>(&w[e]));
+                                const __half2 o = epi.fast
+                                                      ? __floats2half2_rn(fmaf(epi.af, v[jj], cf.x), fmaf(epi.af, v[jj + 1], cf.y))
+                                                      : __floats2half2_rn(epi(v[jj], cf.x), epi(v[jj + 1], cf.y));
+                                uint32_t ou = *reinterpret_cast<const uint32_t*>(&o);
+                                if (jj >= jm) ou = (ou & 0xFFFF0000u) | (wo[e] & 0xFFFFu);
+                                if (jj + 1 >= jm) ou = (ou & 0xFFFFu) | (wo[e] & 0xFFFF0000u);
+                                w[e] = ou;
+                                bad |= (jj < jm && (ou & 0x7c00u) == 0x7c00u) |
+                                       (jj + 1 < jm && (ou & 0x7c000000u) == 0x7c000000u);
+                            }
+                            *cp = raw;
+                        }
+                    } else {
+#pragma unroll
+                        for (int g = 0; g < 8; ++g) {
+                            float4* cp = reinterpret_cast<float4*>(rowp + (((c16 + g) ^ (row_l & 7)) << 4));
+                            const float4 co = has_c ? *cp : make_float4(0, 0, 0, 0);
+                            const float4 cm = p.lower ? *cp : co;
+                            float4 o;
+                            const int jj = 4 * g;
+                            o.x = jj + 0 < jm ? epi(v[jj + 0], co.x) : cm.x;
+                            o.y = jj + 1 < jm ? epi(v[jj + 1], co.y) : cm.y;
+                            o.z = jj + 2 < jm ? epi(v[jj + 2], co.z) : cm.z;
+                            o.w = jj + 3 < jm ? epi(v[jj + 3], co.w) : cm.w;
+                            bad |= (jj + 0 < jm && (__float_as_uint(o.x) & 0x7f800000u) == 0x7f800000u) |
+                                   (jj + 1 < jm && (__float_as_uint(o.y) & 0x7f800000u) == 0x7f800000u) |
+                                   (jj + 2 < jm && (__float_as_uint(o.z) & 0x7f800000u) == 0x7f800000u) |
+                                   (jj + 3 < jm && (__float_as_uint(o.w) & 0x7f800000u) == 0x7f800000u);
+                            *cp = o;
+                        }
+                    }
+                    if (bad && badj < 0) {
+                        for (int e = 0; e < jm && badj < 0; ++e) {
+                            const int cb = (c16 * 16 + e * (f16 ? 2 : 4)) / 16, off = (e * (f16 ? 2 : 4)) % 16;
+                            const unsigned char* ep = rowp + ((cb ^ (row_l & 7)) << 4) + off;
+                            const bool b = f16 ? h_bad(*reinterpret_cast<const __half*>(ep))
+                                               : !isfinite(*reinterpret_cast<const float*>(ep));
+                            if (b) badj = j0 + e;
+                        }
+                    }
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                epi_sync();
+                if (ldr && nbox > 0) {
+                    for (int bx = 0; bx < nbox; ++bx)
+                        tma_store_2d(&p.tcm, stg + bx * BM * 128, p.c_c0 + col0 + bx * box_cols, p.c_r0 - p.yc + crow);
+                    bulk_commit();
+                }
+            }
+            if (p.check_seq != 0) {
+                unsigned long long key = ~0ull;
+                if (badj >= 0)
+                    key = fail_key(p.check_seq, elem_local(p.c_r0 + i - p.chk_r0, p.c_c0 + badj - p.chk_c0));
+                __syncwarp();
+                warp_report_min(c, key);
+            }
+            if (++as == 2) {
+                as = 0;
+                aphase ^= 1;
+            }
+        }
+        if (ldr) bulk_wait0();
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();  // the peer's last arrivals and TMEM reads are done
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(P_TMEM_COLS));
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     static std::once_flag once;
@@ -885,7 +1223,7 @@ bool tc_supported() {
 }
 
 int tc_build_probs(const DevCtx& c, int kind, const std::vector<DevProb>& probs, std::vector<unsigned char>& out,
-                   std::string* err) {
+                   std::string* err, int pair) {
     out.assign(probs.size() * sizeof(TcProb), 0);
     TcProb* tp = reinterpret_cast<TcProb*>(out.data());
     const bool f32 = kind == KIND_TF32X3;
@@ -914,6 +1252,7 @@ int tc_build_probs(const DevCtx& c, int kind, const std::vector<DevProb>& probs,
         const bool bf32 = d.b_buf == BUF_W32 || (f32 && d.b_buf != BUF_W16);
         p.yb = bw ? 0 : ylo;
         if (!make_map(&p.tb, bbuf, bf32, bld, d.b_r0 + d.n - p.yb, d.b_c0 + d.k, BN, err)) return -1;
+        if (!f32 && !make_map(&p.tbh, bbuf, bf32, bld, d.b_r0 + d.n - p.yb, d.b_c0 + d.k, BM, err)) return -1;
         {
             const bool cf32 = d.exec_level == LV_F32;
             const void* cbuf = cf32 ? static_cast<const void*>(c.b32) : static_cast<const void*>(c.b16);
@@ -952,16 +1291,27 @@ int tc_build_probs(const DevCtx& c, int kind, const std::vector<DevProb>& probs,
             p.nkc = d.exec_level == LV_F32 && kc > 0 && d.k > kc ? (d.k + kc - 1) / kc : 1;
             p.kb_per_chunk = kc / bk;
         }
-        tiles += ((d.m + BM - 1) / BM) * p.tiles_n;
+        const int bmt = pair ? 2 * BM : BM;  // CTA pairs: 256-row tiles
+        tiles += ((d.m + bmt - 1) / bmt) * p.tiles_n;
+        if (pair && (f32 || !p.c_tma || p.nkc != 1)) return -2;  // the pair kernel: FP16 kind, TMA-staged C, one K chunk
     }
     return tiles;
 }
+
+// CTA pairs for FP16-kind problem lists of at least this many 128x256 tiles
+// (0 = never); process-wide, read when a plan's tables are built
+static int g_tc_pair_min_tiles = 0;
+int tc_pair_min_tiles() { return g_tc_pair_min_tiles; }
 
 static int g_sms = 148;
 
 bool tc_set_option(const std::string& key, int value) {
     if (key == "tc_kchunk") {
         g_tc_kchunk = value < 0 ? 0 : value;
+        return true;
+    }
+    if (key == "tc_pair_min_tiles") {
+        g_tc_pair_min_tiles = value < 0 ? 0 : value;
         return true;
     }
     return false;
@@ -971,6 +1321,7 @@ void init_tc_attributes() {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(k_gemm_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM_BYTES);
     cudaFuncSetAttribute(k_gemm_tc<KIND_F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo<KIND_F16>::SMEM_BYTES);
     cudaFuncSetAttribute(k_gemm_tc<KIND_TF32X3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          Geo<KIND_TF32X3>::SMEM_BYTES);
@@ -992,6 +1343,27 @@ void launch_gemm_tc(const DevCtx& c, int kind, const void* d_probs, int nprob, i
                                                                                                     tiles);
     else
         k_gemm_tc<KIND_F16><<<grid, Cfg<KIND_F16>::NTHREADS, Geo<KIND_F16>::SMEM_BYTES, s>>>(c, p, nprob, tiles);
+}
+
+// CTA-pair launch (k_gemm_tc2): problem table built with pair = 1; persistent
+// pairs (one per two SMs, or fewer when there are fewer tiles)
+void launch_gemm_tc_pair(const DevCtx& c, const void* d_probs, int nprob, int tiles, cudaStream_t s) {
+    if (tiles <= 0) return;
+    int pairs = g_sms / 2;
+    if (pairs > tiles) pairs = tiles;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * pairs, 1, 1);
+    cfg.blockDim = dim3(320, 1, 1);
+    cfg.dynamicSmemBytes = P_SMEM_BYTES;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_gemm_tc2, c, static_cast<const TcProb*>(d_probs), nprob, tiles);
 }
 
 }  // namespace tcb

@@ -85,7 +85,12 @@ size_t tc_prob_size();
 // operand kinds of the tensor-core GEMM (k_gemm_tc.cu)
 enum { KIND_F16 = 0, KIND_TF32X3 = 1 };
 int tc_build_probs(const DevCtx& c, int kind, const std::vector<DevProb>& probs, std::vector<unsigned char>& out,
-                   std::string* err);
+                   std::string* err,
+                   int pair = 0);
+// FP16 kind on CTA pairs (tcgen05 cta_group::2, 256x256 tiles); the table
+// built with tc_build_probs(..., pair = 1)
+int tc_pair_min_tiles();
+void launch_gemm_tc_pair(const DevCtx& c, const void* d_probs, int nprob, int tiles, cudaStream_t s);
 void launch_gemm_tc(const DevCtx& c, int kind, const void* d_probs, int nprob, int tiles, cudaStream_t s,
                     int max_ctas = 0, int tiles_per_cta = 0);
 bool tc_supported();

@@ -7,7 +7,7 @@ import json
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.environ.get("TC_ROOT", os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch  # noqa: E402
 
 import paper_2601_08082_b200 as tc  # noqa: E402
@@ -22,8 +22,15 @@ args = ap.parse_args()
 a = tc.spd_generate_device(args.n, 42)
 l = torch.empty_like(a)
 for var in args.set or [""]:
+    # "g:key=value": a process-wide kernel option (tc_set_global_option), set before the plan's tables are built
+    for kv in filter(None, var.split(",")):
+        if kv.startswith("g:"):
+            k, v = kv[2:].split("=")
+            tc.set_global_option(k, int(v))
     plan = tc.Plan(args.n, args.b, args.cfg)
     for kv in filter(None, var.split(",")):
+        if kv.startswith("g:"):
+            continue
         k, v = kv.split("=")
         plan.set_option(k, int(v))
     st = plan.factor_device(a, l)
@@ -41,3 +48,4 @@ for var in args.set or [""]:
                       "med_ms": times[len(times) // 2], "tflops": tc.potrf_flops(args.n) / times[0] / 1e9,
                       "ops": plan.stats()["ops"], "rel_error": rel}), flush=True)
     del plan
+    tc.set_global_option("tc_pair_min_tiles", 0)
