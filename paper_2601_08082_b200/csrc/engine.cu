@@ -241,7 +241,7 @@ void Engine::launch_op(int i, cudaStream_t s) {
             break;
         case OP_GEMM:
             if (L.pair)
-                launch_gemm_tc_pair(ctx_, tab, L.count, L.tiles, s);
+                launch_gemm_tc_pair(ctx_, tab, L.count, L.tiles, s, op.bulk ? bulk_tiles_per_cta : 0);
             else if (op.gclass == GC_TC16 || op.gclass == GC_TC32)
                 launch_gemm_tc(ctx_, op.gclass == GC_TC32 ? KIND_TF32X3 : KIND_F16, tab, L.count, L.tiles, s,
                                op.bulk ? bulk_max_ctas : 0, op.bulk ? bulk_tiles_per_cta : 0);

@@ -1299,8 +1299,9 @@ int tc_build_probs(const DevCtx& c, int kind, const std::vector<DevProb>& probs,
 }
 
 // CTA pairs for FP16-kind problem lists of at least this many 128x256 tiles
-// (0 = never); process-wide, read when a plan's tables are built
-static int g_tc_pair_min_tiles = 0;
+// (0 = never); process-wide, read when a plan's tables are built.  Below ~2
+// waves the pair's 256x256 tiles leave SMs idle (8192x1024x1024: 22 -> 26 us)
+static int g_tc_pair_min_tiles = 512;
 int tc_pair_min_tiles() { return g_tc_pair_min_tiles; }
 
 static int g_sms = 148;
@@ -1347,9 +1348,12 @@ void launch_gemm_tc(const DevCtx& c, int kind, const void* d_probs, int nprob, i
 
 // CTA-pair launch (k_gemm_tc2): problem table built with pair = 1; persistent
 // pairs (one per two SMs, or fewer when there are fewer tiles)
-void launch_gemm_tc_pair(const DevCtx& c, const void* d_probs, int nprob, int tiles, cudaStream_t s) {
+void launch_gemm_tc_pair(const DevCtx& c, const void* d_probs, int nprob, int tiles, cudaStream_t s,
+                         int tiles_per_pair) {
     if (tiles <= 0) return;
-    int pairs = g_sms / 2;
+    // persistent (tiles_per_pair = 0) or a bounded number of tiles per pair,
+    // so SMs free up between tiles for concurrent work (the chain)
+    int pairs = tiles_per_pair > 0 ? (tiles + tiles_per_pair - 1) / tiles_per_pair : g_sms / 2;
     if (pairs > tiles) pairs = tiles;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(2 * pairs, 1, 1);

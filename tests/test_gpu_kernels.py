@@ -153,3 +153,33 @@ def test_gemm_class_matches_gemm_mixed(tc, oracle, gclass, lvl, lower, m, n, k):
     bound = (gamma + extra) * mag + ulp
     assert np.all(e_gpu <= bound), float((e_gpu / bound).max())
     assert np.all(e_or <= (gamma * mag + ulp)), "oracle outside its own bound"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,n,k,ex,lower", [(512, 512, 512, 0, 0), (1024, 768, 1024, 1, 0), (300, 200, 333, 0, 0),
+                                            (512, 512, 2048, 1, 1), (2304, 1280, 640, 1, 0), (256, 256, 4096, 1, 1)])
+def test_cta_pair_gemm_bit_identical(tc, m, n, k, ex, lower):
+    """k_gemm_tc2 (tcgen05 cta_group::2, 256x256 tiles over a CTA pair) gives
+    the single-CTA kernel's results bit for bit: the same K order per output
+    element, only the tiling and the operand staging differ"""
+    import torch
+
+    def run(pair_min):
+        tc.set_global_option("tc_pair_min_tiles", pair_min)
+        g = torch.Generator(device="cuda").manual_seed(m + n + k)
+        R = m + n
+        ldw = ((k + n + 63) // 64) * 64
+        b16 = (torch.rand((R, ldw), device="cuda", generator=g) * 2 - 1).half()
+        b32 = torch.rand((R, ldw), device="cuda", generator=g) * 2 - 1
+        tc.gemm_problem_device("tc16", b16, b32, None, ldw, m, n, k, 0, 0, 0 if lower else m, 0, 0, k, ex, lower,
+                               -1.0, 1.0)
+        torch.cuda.synchronize()
+        return (b16 if ex == 0 else b32)[:m, k:k + n].clone()
+
+    try:
+        single = run(0)
+        pair = run(1)
+    finally:
+        tc.set_global_option("tc_pair_min_tiles", 512)
+    assert torch.equal(single.view(torch.int16) if ex == 0 else single.view(torch.int32),
+                       pair.view(torch.int16) if ex == 0 else pair.view(torch.int32))

@@ -48,4 +48,4 @@ for var in args.set or [""]:
                       "med_ms": times[len(times) // 2], "tflops": tc.potrf_flops(args.n) / times[0] / 1e9,
                       "ops": plan.stats()["ops"], "rel_error": rel}), flush=True)
     del plan
-    tc.set_global_option("tc_pair_min_tiles", 0)
+    tc.set_global_option("tc_pair_min_tiles", 512)  # the library default
