@@ -199,7 +199,7 @@ namespace tcb {
 int apply_plan_option(std::unique_ptr<Engine>& eng, const std::string& k, int value, std::string* err) {
     static const char* keys[] = {"use_tc", "use_tc32", "inverse_trsm", "fuse_checks", "mma32_max_log2",
                                  "mma32w_max_log2", "syrk_split_min", "shadow_per_block", "sub32_max_rows",
-                                 "trsm_row_split_min", "lookahead_prio", "fuse_inverse"};
+                                 "trsm_row_split_min", "lookahead_prio", "fuse_inverse", "fuse_shadow"};
     bool known = false;
     for (const char* x : keys) known = known || k == x;
     if (!known) return 0;
@@ -221,6 +221,7 @@ int apply_plan_option(std::unique_ptr<Engine>& eng, const std::string& k, int va
     else if (k == "trsm_row_split_min") po.trsm_row_split_min = value < 0 ? 0 : value;
     else if (k == "lookahead_prio") po.lookahead_prio = value != 0;
     else if (k == "fuse_inverse") po.fuse_inverse = value != 0;
+    else if (k == "fuse_shadow") po.fuse_shadow = value != 0;
     else po.shadow_per_block = value != 0;
     Plan p = Plan::make(e.plan.n, e.plan.b, e.plan.levels, e.plan.quantize, e.plan.leaf_size, po);
     const bool g = e.use_graph, dg = e.dag_graph, pdl = e.use_pdl;

@@ -73,6 +73,10 @@ int tc_batch_create(int n, int b, const int* levels, int nlevels, int quantize, 
         auto* bt = new tc_batch;
         for (int i = 0; i < concurrency; ++i) {
             PlanOptions po;
+            // the leaf shadows stay separate ops in batches: fused into the
+            // leaf POTRF, 16 concurrent plans ran bimodally (264-430 vs a
+            // steady 433-435 TF/s, profiles/r02_c4_fuse_shadow_ab.txt)
+            po.fuse_shadow = false;
             bt->eng.push_back(std::make_unique<Engine>(
                 Plan::make(n, b, std::vector<int>(levels, levels + nlevels), quantize != 0, 0, po)));
         }

@@ -136,9 +136,11 @@ __device__ __forceinline__ void tri_tile_ab(int k, int& a, int& b) {
     b = k - ((a * (a + 1)) >> 1);
 }
 // tiles -> global, whole tiles as 16-byte row chunks (a diagonal tile's
-// strict upper part goes back as loaded)
+// strict upper part goes back as loaded); g16 (F32 tiles only, may be null):
+// also the binary16-rounded copy at the same coordinates (a fused OP_SHADOW)
 template <typename T, int NTHREADS>
-__device__ __forceinline__ void tri_store_vec(const float* S, T* g, long long ld, int nt, int off, int tid) {
+__device__ __forceinline__ void tri_store_vec(const float* S, T* g, long long ld, int nt, int off, int tid,
+                                              __half* g16 = nullptr) {
     constexpr int VEC = 16 / int(sizeof(T)), CPR = 32 / VEC, CPT = 32 * CPR, KSTEP = NTHREADS / CPT;
     const int ntile = (nt * (nt + 1)) >> 1;
     const int row = (tid % CPT) / CPR, col = (tid % CPR) * VEC;
@@ -151,7 +153,15 @@ __device__ __forceinline__ void tri_store_vec(const float* S, T* g, long long ld
         T* e = reinterpret_cast<T*>(&w);
 #pragma unroll
         for (int u = 0; u < VEC; ++u) e[u] = from_float<T>(t[tri_sw(row, col + u)]);
-        *reinterpret_cast<uint4*>(g + (long long)((off + a) * 32 + row) * ld + (off + b) * 32 + col) = w;
+        const long long o = (long long)((off + a) * 32 + row) * ld + (off + b) * 32 + col;
+        *reinterpret_cast<uint4*>(g + o) = w;
+        if constexpr (VEC == 4) {
+            if (g16) {
+                const float* f = reinterpret_cast<const float*>(&w);
+                __half2 h[2] = {__floats2half2_rn(f[0], f[1]), __floats2half2_rn(f[2], f[3])};
+                *reinterpret_cast<uint2*>(g16 + o) = *reinterpret_cast<const uint2*>(h);
+            }
+        }
     }
 }
 __device__ __forceinline__ bool vec16_ok(const void* g, long long ld_bytes) {

@@ -229,7 +229,9 @@ void Engine::launch_op(int i, cudaStream_t s) {
             launch_dequant(ctx_, op.level, r.r0, r.c0, r.m, r.n, op.slot, op.check_seq,
                            op.check_seq ? r.r0 - op.chk.r0 : 0, op.check_seq ? r.c0 - op.chk.c0 : 0, s);
             break;
-        case OP_POTRF: launch_potrf_leaf(ctx_, op.level, r.r0, r.m, op.seq, op.check_seq, s, op.inv_seq, op.fuse_inv); break;
+        case OP_POTRF:
+            launch_potrf_leaf(ctx_, op.level, r.r0, r.m, op.seq, op.check_seq, s, op.inv_seq, op.fuse_inv, op.shadow16);
+            break;
         case OP_TRSM:
             launch_trsm_leaf(ctx_, op.level, r.r0, r.c0, r.m, r.n, op.lrect.r0, op.seq, op.check_seq, op.chk.r0,
                              op.chk.c0, s);

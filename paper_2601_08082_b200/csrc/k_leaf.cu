@@ -626,8 +626,8 @@ void init_leaf_attributes() {
 constexpr size_t kLeafSmemCap = 220 * 1024;
 
 void launch_potrf_leaf(const DevCtx& c, int lv, int r0, int n, uint32_t seq, uint32_t chk, cudaStream_t s,
-                       uint32_t inv_seq, int fuse_inv) {
-    if (potrf_v2_ok(lv, n)) return launch_potrf_v2(c, lv, r0, n, seq, chk, s, inv_seq, fuse_inv);
+                       uint32_t inv_seq, int fuse_inv, int shadow16) {
+    if (potrf_v2_ok(lv, n)) return launch_potrf_v2(c, lv, r0, n, seq, chk, s, inv_seq, fuse_inv, shadow16);
     if (leaf_cm_ok(lv, n)) return launch_potrf_cm(c, lv, r0, n, seq, chk, s);
     const bool d = lv == LV_F64;
     if (d && n % 32 == 0 && n > 128 && n <= 256 && (c.ldw % 2) == 0 && (r0 % 2) == 0) {

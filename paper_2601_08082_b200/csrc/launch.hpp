@@ -47,7 +47,7 @@ void init_tc_attributes();
 
 // leaves (k_leaf.cu)
 void launch_potrf_leaf(const DevCtx& c, int lv, int r0, int n, uint32_t seq, uint32_t chk_seq, cudaStream_t s,
-                       uint32_t inv_seq = 0, int fuse_inv = 0);
+                       uint32_t inv_seq = 0, int fuse_inv = 0, int shadow16 = 0);
 void launch_trsm_leaf(const DevCtx& c, int lv, int br0, int bc0, int m, int n, int lr0, uint32_t seq,
                       uint32_t chk_seq, int chk_r0, int chk_c0, cudaStream_t s);
 // latency-optimised F16/F32 leaves, n % 32 == 0, n <= 256 (k_leaf_cm.cu)
@@ -66,8 +66,9 @@ bool potrf_v2_ok(int lv, int n);
 void init_potrf_v2_attributes();
 // fuse_inv (F32 leaves): also W = inv(L) into the FP32 inverse workspace,
 // reporting a singular diagonal under inv_seq (the leaf's OP_INVERSE)
+// shadow16 (F32 leaves): also the binary16 copy into the F16 level buffer
 void launch_potrf_v2(const DevCtx& c, int lv, int r0, int n, uint32_t seq, uint32_t chk, cudaStream_t s,
-                     uint32_t inv_seq = 0, int fuse_inv = 0);
+                     uint32_t inv_seq = 0, int fuse_inv = 0, int shadow16 = 0);
 
 // grouped GEMM (k_gemm_simt.cu / k_gemm_tc.cu)
 // problems must already be in device memory with tile0 / tiles_n filled by

@@ -558,6 +558,32 @@ void Plan::fuse_leaf_inverses() {
     }
 }
 
+// an F32 leaf's F16 shadow (the rn16 copy the F16 panel solves read,
+// kernels.cpp:29/78) is written by its POTRF kernel next to the factor: the
+// leaf's OP_SHADOW disappears from the chain
+void Plan::fuse_leaf_shadows() {
+    if (!opt.fuse_shadow) return;
+    std::vector<char> drop(ops.size(), 0);
+    for (size_t i = 0; i < ops.size(); ++i) {
+        Op& sh = ops[i];
+        if (sh.type != OP_SHADOW || sh.level != LV_F16 || sh.blocks.size() != 1) continue;
+        const Block& blk = blocks[sh.blocks[0]];
+        if (!blk.leaf || blk.level != LV_F32) continue;
+        for (Op& pf : ops)
+            if (pf.type == OP_POTRF && pf.level == LV_F32 && pf.rect.r0 == blk.rect.r0 && pf.rect.m == blk.rect.m &&
+                potrf_v2_ok(pf.level, pf.rect.m)) {
+                pf.shadow16 = 1;
+                drop[i] = 1;
+                break;
+            }
+    }
+    std::vector<Op> kept;
+    kept.reserve(ops.size());
+    for (size_t i = 0; i < ops.size(); ++i)
+        if (!drop[i]) kept.push_back(std::move(ops[i]));
+    ops.swap(kept);
+}
+
 void Plan::finalize_accesses() {
     for (Op& op : ops) {
         op.acc.clear();
@@ -595,6 +621,7 @@ void Plan::finalize_accesses() {
             case OP_POTRF:
                 op.acc.push_back({op.level, op.rect, true});
                 if (op.fuse_inv) op.acc.push_back({BUF_W32, {op.rect.r0, 0, op.rect.m, kW32Ld}, true});
+                if (op.shadow16) op.acc.push_back({LV_F16, op.rect, true});
                 break;
             case OP_INVERSE:
                 if (op.fused) break;  // no accesses: nothing waits on it
@@ -769,6 +796,7 @@ Plan Plan::make(int n, int b, const std::vector<int>& levels, bool quantize, int
         }
     P.emit_potrf(0);
     P.fuse_leaf_inverses();
+    P.fuse_leaf_shadows();
     for (int i : order) {
         Op exp;
         exp.type = OP_EXPORT;

@@ -144,6 +144,7 @@ struct Op {
     int fuse_inv = 0;
     uint32_t inv_seq = 0;
     int fused = 0;         // OP_INVERSE done by the leaf's POTRF
+    int shadow16 = 0;      // OP_POTRF of an F32 leaf: also writes the leaf's F16 shadow (its OP_SHADOW removed)
 };
 
 // a require_finite point of the reference (tree.cpp:108, 114, 121): a
@@ -171,6 +172,7 @@ struct PlanOptions {
     int sub32_max_rows = 0;  // F32 leaf solves of at most this many rows by substitution (k_trsm_cm) instead of inverse + GEMM
     bool lookahead_prio = true;   // with the splits below: the first row part / the diag1 chain of a split SYRK at high priority, the rest low
     int trsm_row_split_min = 0;   // off-diagonal panels with at least this many rows: TRSM ops split at diag2's first split (lookahead: diag2.diag1's SYRK and factorization start after the first row part)
+    bool fuse_shadow = true;      // F32 leaves: their F16 shadow written by the leaf POTRF's store phase
     bool fuse_inverse = false;    // F32 leaves: W = inv(L) inside the leaf POTRF kernel (no separate inverse launch on the chain); measured slower: 99.5k extra cycles per leaf on one SM vs the 8-CTA inverse's 25 us (N=16384 11.7 vs 9.3 ms)
     bool shadow_per_block = true;  // one OP_SHADOW per block of L (pipelines the lower-level TRSM with the factorization it reads)
     int syrk_split_min = 1 << 30; // tree_syrk nodes at least this large launch per region (lookahead; off by default: it shortens the critical path but adds launches, a net loss for batches)
@@ -264,6 +266,7 @@ struct Plan {
     // flops and sequence numbers stay one per call
     using RowSplit = std::vector<std::pair<int, int>>;
     void fuse_leaf_inverses();
+    void fuse_leaf_shadows();
     void emit_panel(int block, int lnode, int ext_slot, int d2node = -1);
     void emit_trsm(Rect brect, int p, int lnode, const RowSplit* rows = nullptr);
     void emit_syrk(int cnode, Rect arect, int p, bool critical = true, bool via_split = false);
