@@ -225,11 +225,13 @@ int apply_plan_option(std::unique_ptr<Engine>& eng, const std::string& k, int va
     else po.shadow_per_block = value != 0;
     Plan p = Plan::make(e.plan.n, e.plan.b, e.plan.levels, e.plan.quantize, e.plan.leaf_size, po);
     const bool g = e.use_graph, dg = e.dag_graph, pdl = e.use_pdl;
+    const int pmt = e.pair_min_tiles;
     const int s = e.n_streams, bt = e.bulk_tiles_per_cta, bm = e.bulk_max_ctas;
     eng = std::make_unique<Engine>(std::move(p));
     eng->use_graph = g;
     eng->dag_graph = dg;
     eng->use_pdl = pdl;
+    eng->pair_min_tiles = pmt;
     eng->n_streams = s;
     eng->bulk_tiles_per_cta = bt;
     eng->bulk_max_ctas = bm;

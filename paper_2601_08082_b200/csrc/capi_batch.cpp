@@ -79,6 +79,10 @@ int tc_batch_create(int n, int b, const int* levels, int nlevels, int quantize, 
             po.fuse_shadow = false;
             bt->eng.push_back(std::make_unique<Engine>(
                 Plan::make(n, b, std::vector<int>(levels, levels + nlevels), quantize != 0, 0, po)));
+            // no CTA-pair GEMMs in batches: with 16 plans side by side their
+            // clusters (two free SMs of one TPC) were starved now and then
+            // (C4 98-438 vs a steady 423-429 TF/s, profiles/r02_c4_pair_ab.txt)
+            bt->eng.back()->pair_min_tiles = 0;
         }
         *out = bt;
         return TC_OK;

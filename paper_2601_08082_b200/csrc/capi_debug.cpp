@@ -78,9 +78,9 @@ extern "C" int tc_debug_gemm(int gclass, int m, int n, int k, int lower, double 
     int pair = 0;
     if (tc) {
         tiles = tc_build_probs(c, gclass == GC_TC32 ? KIND_TF32X3 : KIND_F16, v, host, &err);
-        if (gclass == GC_TC16 && tc_pair_min_tiles() > 0 && tiles >= tc_pair_min_tiles()) {
+        if (tc_pair_min_tiles() > 0 && tiles >= tc_pair_min_tiles()) {
             std::vector<unsigned char> h2;
-            const int t2 = tc_build_probs(c, KIND_F16, v, h2, nullptr, 1);
+            const int t2 = tc_build_probs(c, gclass == GC_TC32 ? KIND_TF32X3 : KIND_F16, v, h2, nullptr, 1);
             if (t2 > 0) {
                 host.swap(h2);
                 tiles = t2;
@@ -98,7 +98,7 @@ extern "C" int tc_debug_gemm(int gclass, int m, int n, int k, int lower, double 
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     auto launch = [&] {
-        if (pair) launch_gemm_tc_pair(c, dprob, 1, tiles, nullptr);
+        if (pair) launch_gemm_tc_pair(c, gclass == GC_TC32 ? KIND_TF32X3 : KIND_F16, dprob, 1, tiles, nullptr);
         else if (tc) launch_gemm_tc(c, gclass == GC_TC32 ? KIND_TF32X3 : KIND_F16, dprob, 1, tiles, nullptr);
         else launch_gemm_simt(c, gclass, static_cast<DevProb*>(dprob), 1, tiles, nullptr);
     };
@@ -111,7 +111,7 @@ extern "C" int tc_debug_gemm(int gclass, int m, int n, int k, int lower, double 
     cudaGraphExec_t ge = nullptr;
     cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
     for (int i = 0; i < iters; ++i) {
-        if (pair) launch_gemm_tc_pair(c, dprob, 1, tiles, cs);
+        if (pair) launch_gemm_tc_pair(c, gclass == GC_TC32 ? KIND_TF32X3 : KIND_F16, dprob, 1, tiles, cs);
         else if (tc) launch_gemm_tc(c, gclass == GC_TC32 ? KIND_TF32X3 : KIND_F16, dprob, 1, tiles, cs);
         else launch_gemm_simt(c, gclass, static_cast<DevProb*>(dprob), 1, tiles, cs);
     }
@@ -195,9 +195,9 @@ extern "C" int tc_gemm_problem_device(int gclass, void* b16, void* b32, void* b6
             set_last_error("tc_build_probs: " + err);
             return TC_INVALID_ARGUMENT;
         }
-        if (gclass == GC_TC16 && tc_pair_min_tiles() > 0 && tiles >= tc_pair_min_tiles()) {
+        if (tc_pair_min_tiles() > 0 && tiles >= tc_pair_min_tiles()) {
             std::vector<unsigned char> h2;
-            const int t2 = tc_build_probs(c, KIND_F16, v, h2, nullptr, 1);
+            const int t2 = tc_build_probs(c, gclass == GC_TC32 ? KIND_TF32X3 : KIND_F16, v, h2, nullptr, 1);
             if (t2 > 0) {
                 host.swap(h2);
                 tiles = t2;
@@ -211,7 +211,7 @@ extern "C" int tc_gemm_problem_device(int gclass, void* b16, void* b32, void* b6
     void* dprob = nullptr;
     if (cudaMallocAsync(&dprob, host.size(), s) != cudaSuccess) return TC_CUDA_ERROR;
     cudaMemcpyAsync(dprob, host.data(), host.size(), cudaMemcpyHostToDevice, s);
-    if (pair) launch_gemm_tc_pair(c, dprob, 1, tiles, s);
+    if (pair) launch_gemm_tc_pair(c, gclass == GC_TC32 ? KIND_TF32X3 : KIND_F16, dprob, 1, tiles, s);
     else if (tc) launch_gemm_tc(c, gclass == GC_TC32 ? KIND_TF32X3 : KIND_F16, dprob, 1, tiles, s);
     else launch_gemm_simt(c, gclass, static_cast<DevProb*>(dprob), 1, tiles, s);
     cudaFreeAsync(dprob, s);

@@ -176,10 +176,11 @@ bool Engine::prepare(std::string* err) {
                 std::vector<unsigned char> tp;
                 L.tiles = tc_build_probs(ctx_, op.gclass == GC_TC32 ? KIND_TF32X3 : KIND_F16, dp, tp, err);
                 if (L.tiles < 0) return false;
-                if (op.gclass == GC_TC16 && tc_pair_min_tiles() > 0 && L.tiles >= tc_pair_min_tiles()) {
-                    // a large FP16-kind list: 256x256 tiles on CTA pairs
+                const int pmin = pair_min_tiles >= 0 ? pair_min_tiles : tc_pair_min_tiles();
+                if (pmin > 0 && L.tiles >= pmin) {
+                    // a large list: 256x256 tiles on CTA pairs
                     std::vector<unsigned char> tp2;
-                    const int t2 = tc_build_probs(ctx_, KIND_F16, dp, tp2, nullptr, 1);
+                    const int t2 = tc_build_probs(ctx_, op.gclass == GC_TC32 ? KIND_TF32X3 : KIND_F16, dp, tp2, nullptr, 1);
                     if (t2 > 0) {
                         tp.swap(tp2);
                         L.tiles = t2;
@@ -243,7 +244,8 @@ void Engine::launch_op(int i, cudaStream_t s) {
             break;
         case OP_GEMM:
             if (L.pair)
-                launch_gemm_tc_pair(ctx_, tab, L.count, L.tiles, s, op.bulk ? bulk_tiles_per_cta : 0);
+                launch_gemm_tc_pair(ctx_, op.gclass == GC_TC32 ? KIND_TF32X3 : KIND_F16, tab, L.count, L.tiles, s,
+                                    op.bulk ? bulk_tiles_per_cta : 0);
             else if (op.gclass == GC_TC16 || op.gclass == GC_TC32)
                 launch_gemm_tc(ctx_, op.gclass == GC_TC32 ? KIND_TF32X3 : KIND_F16, tab, L.count, L.tiles, s,
                                op.bulk ? bulk_max_ctas : 0, op.bulk ? bulk_tiles_per_cta : 0);

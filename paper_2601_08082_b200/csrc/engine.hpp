@@ -52,6 +52,9 @@ class Engine {
     // dependent launch (PDL) on the edges into the chain's ops: the kernel
     // is launched while its producer finishes and waits in
     // griddepcontrol.wait (every factorization kernel starts with it)
+    // CTA-pair GEMM threshold for this engine (-1: the process-wide
+    // tc_pair_min_tiles; 0: never)
+    int pair_min_tiles = -1;
     bool use_pdl = false;  // measured no faster (N=16384 12.62 -> 12.80 ms, C4 425 -> 420 TF/s): off
     bool pdl_src_ok(int i) const;
     int bulk_tiles_per_cta = 1;  // trailing-update GEMMs: 0 persistent, else tiles per CTA (1: SMs free up after every tile, so concurrent work -- other systems of a batch, the factorization chain -- gets them)

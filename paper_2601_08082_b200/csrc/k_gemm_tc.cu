@@ -853,16 +853,31 @@ __global__ void __launch_bounds__(Cfg<KIND>::NTHREADS, 1) k_gemm_tc(DevCtx c, co
 // (the leader's commits multicast), tempty in the leader (both CTAs'
 // epilogue warps arrive).  Epilogue as in k_gemm_tc (TMA-staged C only).
 // ---------------------------------------------------------------------------
-constexpr int P_STAGES = 6;
+// per operand kind: FP16 (6 stages of A + half B) or TF32X3 (3 stages of A +
+// half B + their lo halves, converter warps 10-13 in both CTAs)
+template <int KIND> struct PairCfg;
+template <> struct PairCfg<KIND_F16> {
+    static constexpr int STAGES = 6, NTHREADS = 320, PASSES = 1, BK = 64;
+    static constexpr uint32_t FMT = 0;
+};
+template <> struct PairCfg<KIND_TF32X3> {
+    static constexpr int STAGES = 3, NTHREADS = 448, PASSES = 3, BK = 32;
+    static constexpr uint32_t FMT = 2;
+};
 constexpr int P_BN = 256;                       // pair tile columns (N of the MMA)
 constexpr int P_A_BYTES = BM * 128;             // this CTA's A rows, one k-block
 constexpr int P_B_BYTES = BM * 128;             // this CTA's half of B
-constexpr int P_STAGE_BYTES = P_A_BYTES + P_B_BYTES;
+constexpr int P_TILE_BYTES = P_A_BYTES + P_B_BYTES;
 constexpr int P_STG_BYTES = 2 * BM * 128;
-constexpr int P_SMEM_BYTES = P_STAGES * P_STAGE_BYTES + P_STG_BYTES + 1024 + 256;
+template <int KIND> struct PairGeo {
+    using C = PairCfg<KIND>;
+    static constexpr int STAGE_BYTES = P_TILE_BYTES * (C::PASSES > 1 ? 2 : 1);
+    static constexpr int SMEM_BYTES = C::STAGES * STAGE_BYTES + P_STG_BYTES + 1024 + 256;
+    static constexpr uint32_t IDESC = (1u << 4) | (C::FMT << 7) | (C::FMT << 10) | (uint32_t(P_BN >> 3) << 17) |
+                                      (uint32_t((2 * BM) >> 4) << 24);
+    static_assert(SMEM_BYTES <= 227 * 1024, "pair shared memory");
+};
 constexpr uint32_t P_TMEM_COLS = 2 * P_BN;
-constexpr uint32_t P_IDESC = (1u << 4) | (uint32_t(P_BN >> 3) << 17) | (uint32_t((2 * BM) >> 4) << 24);
-static_assert(P_SMEM_BYTES <= 227 * 1024, "pair shared memory");
 
 __device__ __forceinline__ uint32_t cluster_rank() {
     uint32_t r;
@@ -885,14 +900,24 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m
         "l"(reinterpret_cast<uint64_t>(map)), "r"(mbar_cluster), "r"(x), "r"(y)
         : "memory");
 }
+template <int KIND>
 __device__ __forceinline__ void mma_pair(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accum) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "setp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
-        "}\n" ::"r"(tmem_d),
-        "l"(da), "l"(db), "r"(P_IDESC), "r"(accum));
+    if constexpr (KIND == KIND_F16)
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "setp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+            "}\n" ::"r"(tmem_d),
+            "l"(da), "l"(db), "r"(PairGeo<KIND>::IDESC), "r"(accum));
+    else
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "setp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
+            "}\n" ::"r"(tmem_d),
+            "l"(da), "l"(db), "r"(PairGeo<KIND>::IDESC), "r"(accum));
 }
 // arrive on the barrier at this offset in both CTAs of the pair once the
 // leader's MMAs so far have completed
@@ -909,16 +934,25 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 
-__global__ void __launch_bounds__(320, 1) k_gemm_tc2(DevCtx c, const TcProb* __restrict__ probs, int np, int tiles) {
+template <int KIND>
+__global__ void __launch_bounds__(PairCfg<KIND>::NTHREADS, 1) k_gemm_tc2(DevCtx c, const TcProb* __restrict__ probs,
+                                                                         int np, int tiles) {
+    using G = PairGeo<KIND>;
+    constexpr int P_STAGES = PairCfg<KIND>::STAGES, BKK = PairCfg<KIND>::BK;
+    constexpr bool SPLIT = PairCfg<KIND>::PASSES > 1;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                            ~uintptr_t(1023));
-    auto sA = [&](int st) { return smem + st * P_STAGE_BYTES; };
-    auto sB = [&](int st) { return smem + st * P_STAGE_BYTES + P_A_BYTES; };
-    unsigned char* stg = smem + P_STAGES * P_STAGE_BYTES;
+    // stage: A | B half [| A lo | B half lo]
+    auto sA = [&](int st) { return smem + st * G::STAGE_BYTES; };
+    auto sB = [&](int st) { return smem + st * G::STAGE_BYTES + P_A_BYTES; };
+    auto sAl = [&](int st) { return smem + st * G::STAGE_BYTES + P_TILE_BYTES; };
+    auto sBl = [&](int st) { return smem + st * G::STAGE_BYTES + P_TILE_BYTES + P_A_BYTES; };
+    unsigned char* stg = smem + P_STAGES * G::STAGE_BYTES;
     uint64_t* full = reinterpret_cast<uint64_t*>(stg + P_STG_BYTES);
     uint64_t* empty = full + P_STAGES;
-    uint64_t* tfull = empty + P_STAGES;
+    uint64_t* split = empty + P_STAGES;  // TF32X3: both CTAs' lo halves written (leader's copy)
+    uint64_t* tfull = split + P_STAGES;
     uint64_t* tempty = tfull + 2;
     uint64_t* cfull = tempty + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cfull + 1);
@@ -932,6 +966,7 @@ __global__ void __launch_bounds__(320, 1) k_gemm_tc2(DevCtx c, const TcProb* __r
         for (int st = 0; st < P_STAGES; ++st) {
             mbar_init(&full[st], 1);
             mbar_init(&empty[st], 1);
+            mbar_init(&split[st], 8);  // 4 converter warps x 2 CTAs
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
@@ -962,15 +997,24 @@ __global__ void __launch_bounds__(320, 1) k_gemm_tc2(DevCtx c, const TcProb* __r
                 prefetch_map(&p->ta);
                 prefetch_map(&p->tbh);
                 prefetch_map(&p->tcm);
-                const int nk = (p->k + 63) / 64;
+                const int nk = (p->k + BKK - 1) / BKK;
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    if (leader) mbar_expect_tx(&full[stage], 2 * P_STAGE_BYTES);
-                    const uint32_t fb = mapa_rank(smem_u32(&full[stage]), 0);
-                    const int ka = p->a_kwrap ? (kb * 64) % p->a_kwrap : kb * 64;
-                    tma_load_2d_pair(sA(stage), &p->ta, fb, p->a_c0 + ka, p->a_r0 - p->ya + tm * 2 * BM + int(rank) * BM);
-                    tma_load_2d_pair(sB(stage), &p->tbh, fb, p->b_c0 + kb * 64,
-                                     p->b_r0 - p->yb + tn * P_BN + int(rank) * BM);
+                    const int ka = p->a_kwrap ? (kb * BKK) % p->a_kwrap : kb * BKK;
+                    const int ya = p->a_r0 - p->ya + tm * 2 * BM + int(rank) * BM;
+                    const int yb = p->b_r0 - p->yb + tn * P_BN + int(rank) * BM;
+                    if constexpr (SPLIT) {
+                        // each CTA's loads complete on its own barrier: its
+                        // converter warps need them before the leader's MMA
+                        mbar_expect_tx(&full[stage], P_TILE_BYTES);
+                        tma_load_2d(sA(stage), &p->ta, &full[stage], p->a_c0 + ka, ya);
+                        tma_load_2d(sB(stage), &p->tbh, &full[stage], p->b_c0 + kb * BKK, yb);
+                    } else {
+                        if (leader) mbar_expect_tx(&full[stage], 2 * P_TILE_BYTES);
+                        const uint32_t fb = mapa_rank(smem_u32(&full[stage]), 0);
+                        tma_load_2d_pair(sA(stage), &p->ta, fb, p->a_c0 + ka, ya);
+                        tma_load_2d_pair(sB(stage), &p->tbh, fb, p->b_c0 + kb * BKK, yb);
+                    }
                     if (++stage == P_STAGES) {
                         stage = 0;
                         phase ^= 1;
@@ -988,12 +1032,12 @@ __global__ void __launch_bounds__(320, 1) k_gemm_tc2(DevCtx c, const TcProb* __r
             for (int t = pair; t < tiles; t += npairs) {
                 int pi, tm, tn;
                 if (!tile_coords<P_BN, 2 * BM>(probs, np, t, pi, tm, tn)) continue;
-                const int nk = (probs[pi].k + 63) / 64;
+                const int nk = (probs[pi].k + BKK - 1) / BKK;
                 mbar_wait(&tempty[as], aphase ^ 1);
                 tc_fence_after();
                 const uint32_t dcol = tmem + uint32_t(as * P_BN);
                 for (int kb = 0; kb < nk; ++kb) {
-                    mbar_wait(&full[stage], phase);
+                    mbar_wait(SPLIT ? &split[stage] : &full[stage], phase);
                     tc_fence_after();
                     if (lane == 0) {
                         const uint64_t da = sdesc(sA(stage));
@@ -1001,7 +1045,15 @@ __global__ void __launch_bounds__(320, 1) k_gemm_tc2(DevCtx c, const TcProb* __r
 #pragma unroll
                         for (int k = 0; k < 4; ++k) {
                             const uint64_t o = uint64_t(2 * k);
-                            mma_pair(dcol, da + o, db + o, (kb | k) != 0);
+                            if constexpr (SPLIT) {
+                                // small terms first: lo*hi + hi*lo + hi*hi
+                                const uint64_t dal = sdesc(sAl(stage)), dbl = sdesc(sBl(stage));
+                                mma_pair<KIND>(dcol, dal + o, db + o, (kb | k) != 0);
+                                mma_pair<KIND>(dcol, da + o, dbl + o, 1);
+                                mma_pair<KIND>(dcol, da + o, db + o, 1);
+                            } else {
+                                mma_pair<KIND>(dcol, da + o, db + o, (kb | k) != 0);
+                            }
                         }
                         mma_commit_pair(&empty[stage]);
                         if (kb == nk - 1) mma_commit_pair(&tfull[as]);
@@ -1015,6 +1067,31 @@ __global__ void __launch_bounds__(320, 1) k_gemm_tc2(DevCtx c, const TcProb* __r
                 if (++as == 2) {
                     as = 0;
                     aphase ^= 1;
+                }
+            }
+        }
+    } else if (warp >= 10) {
+        // ---------------- lo halves (TF32X3, both CTAs) ----------------
+        if constexpr (SPLIT) {
+            const int t128 = threadIdx.x - 10 * 32;
+            const uint32_t split_leader = mapa_rank(smem_u32(&split[0]), 0);
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = pair; t < tiles; t += npairs) {
+                int pi, tm, tn;
+                if (!tile_coords<P_BN, 2 * BM>(probs, np, t, pi, tm, tn)) continue;
+                const int nk = (probs[pi].k + BKK - 1) / BKK;
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    split_tf32(sA(stage), sAl(stage), P_A_BYTES, t128);
+                    split_tf32(sB(stage), sBl(stage), P_B_BYTES, t128);
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster(split_leader + uint32_t(stage) * 8u);
+                    if (++stage == P_STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
                 }
             }
         }
@@ -1252,7 +1329,7 @@ int tc_build_probs(const DevCtx& c, int kind, const std::vector<DevProb>& probs,
         const bool bf32 = d.b_buf == BUF_W32 || (f32 && d.b_buf != BUF_W16);
         p.yb = bw ? 0 : ylo;
         if (!make_map(&p.tb, bbuf, bf32, bld, d.b_r0 + d.n - p.yb, d.b_c0 + d.k, BN, err)) return -1;
-        if (!f32 && !make_map(&p.tbh, bbuf, bf32, bld, d.b_r0 + d.n - p.yb, d.b_c0 + d.k, BM, err)) return -1;
+        if (!make_map(&p.tbh, bbuf, bf32, bld, d.b_r0 + d.n - p.yb, d.b_c0 + d.k, BM, err)) return -1;
         {
             const bool cf32 = d.exec_level == LV_F32;
             const void* cbuf = cf32 ? static_cast<const void*>(c.b32) : static_cast<const void*>(c.b16);
@@ -1284,7 +1361,7 @@ int tc_build_probs(const DevCtx& c, int kind, const std::vector<DevProb>& probs,
         p.alpha = d.alpha;
         p.beta = d.beta;
         p.tile0 = tiles;
-        p.tiles_n = (d.n + BN - 1) / BN;
+        p.tiles_n = (d.n + (pair ? P_BN : BN) - 1) / (pair ? P_BN : BN);
         {
             const int bk = f32 ? Cfg<KIND_TF32X3>::BK : Cfg<KIND_F16>::BK;
             const int kc = (g_tc_kchunk / bk) * bk;
@@ -1293,7 +1370,7 @@ int tc_build_probs(const DevCtx& c, int kind, const std::vector<DevProb>& probs,
         }
         const int bmt = pair ? 2 * BM : BM;  // CTA pairs: 256-row tiles
         tiles += ((d.m + bmt - 1) / bmt) * p.tiles_n;
-        if (pair && (f32 || !p.c_tma || p.nkc != 1)) return -2;  // the pair kernel: FP16 kind, TMA-staged C, one K chunk
+        if (pair && (!p.c_tma || p.nkc != 1)) return -2;  // the pair kernel: TMA-staged C, one K chunk
     }
     return tiles;
 }
@@ -1322,7 +1399,9 @@ void init_tc_attributes() {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(k_gemm_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM_BYTES);
+    cudaFuncSetAttribute(k_gemm_tc2<KIND_F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, PairGeo<KIND_F16>::SMEM_BYTES);
+    cudaFuncSetAttribute(k_gemm_tc2<KIND_TF32X3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         PairGeo<KIND_TF32X3>::SMEM_BYTES);
     cudaFuncSetAttribute(k_gemm_tc<KIND_F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo<KIND_F16>::SMEM_BYTES);
     cudaFuncSetAttribute(k_gemm_tc<KIND_TF32X3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          Geo<KIND_TF32X3>::SMEM_BYTES);
@@ -1348,7 +1427,7 @@ void launch_gemm_tc(const DevCtx& c, int kind, const void* d_probs, int nprob, i
 
 // CTA-pair launch (k_gemm_tc2): problem table built with pair = 1; persistent
 // pairs (one per two SMs, or fewer when there are fewer tiles)
-void launch_gemm_tc_pair(const DevCtx& c, const void* d_probs, int nprob, int tiles, cudaStream_t s,
+void launch_gemm_tc_pair(const DevCtx& c, int kind, const void* d_probs, int nprob, int tiles, cudaStream_t s,
                          int tiles_per_pair) {
     if (tiles <= 0) return;
     // persistent (tiles_per_pair = 0) or a bounded number of tiles per pair,
@@ -1357,8 +1436,9 @@ void launch_gemm_tc_pair(const DevCtx& c, const void* d_probs, int nprob, int ti
     if (pairs > tiles) pairs = tiles;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(2 * pairs, 1, 1);
-    cfg.blockDim = dim3(320, 1, 1);
-    cfg.dynamicSmemBytes = P_SMEM_BYTES;
+    const bool tf = kind == KIND_TF32X3;
+    cfg.blockDim = dim3(tf ? PairCfg<KIND_TF32X3>::NTHREADS : PairCfg<KIND_F16>::NTHREADS, 1, 1);
+    cfg.dynamicSmemBytes = tf ? PairGeo<KIND_TF32X3>::SMEM_BYTES : PairGeo<KIND_F16>::SMEM_BYTES;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1367,7 +1447,8 @@ void launch_gemm_tc_pair(const DevCtx& c, const void* d_probs, int nprob, int ti
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k_gemm_tc2, c, static_cast<const TcProb*>(d_probs), nprob, tiles);
+    if (tf) cudaLaunchKernelEx(&cfg, k_gemm_tc2<KIND_TF32X3>, c, static_cast<const TcProb*>(d_probs), nprob, tiles);
+    else cudaLaunchKernelEx(&cfg, k_gemm_tc2<KIND_F16>, c, static_cast<const TcProb*>(d_probs), nprob, tiles);
 }
 
 }  // namespace tcb

@@ -156,12 +156,16 @@ def test_gemm_class_matches_gemm_mixed(tc, oracle, gclass, lvl, lower, m, n, k):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("m,n,k,ex,lower", [(512, 512, 512, 0, 0), (1024, 768, 1024, 1, 0), (300, 200, 333, 0, 0),
-                                            (512, 512, 2048, 1, 1), (2304, 1280, 640, 1, 0), (256, 256, 4096, 1, 1)])
-def test_cta_pair_gemm_bit_identical(tc, m, n, k, ex, lower):
-    """k_gemm_tc2 (tcgen05 cta_group::2, 256x256 tiles over a CTA pair) gives
-    the single-CTA kernel's results bit for bit: the same K order per output
-    element, only the tiling and the operand staging differ"""
+@pytest.mark.parametrize("cls,m,n,k,ex,lower", [("tc16", 512, 512, 512, 0, 0), ("tc16", 1024, 768, 1024, 1, 0),
+                                                ("tc16", 300, 200, 333, 0, 0), ("tc16", 512, 512, 2048, 1, 1),
+                                                ("tc16", 2304, 1280, 640, 1, 0), ("tc16", 256, 256, 4096, 1, 1),
+                                                ("tc32", 512, 512, 512, 1, 0), ("tc32", 300, 200, 333, 1, 0),
+                                                ("tc32", 512, 512, 2048, 1, 1), ("tc32", 1024, 768, 1024, 1, 0)])
+def test_cta_pair_gemm_bit_identical(tc, cls, m, n, k, ex, lower):
+    """k_gemm_tc2 (tcgen05 cta_group::2, 256x256 tiles over a CTA pair; FP16
+    kind and three-pass TF32) gives the single-CTA kernel's results bit for
+    bit: the same K order per output element, only the tiling and the operand
+    staging differ"""
     import torch
 
     def run(pair_min):
@@ -171,7 +175,7 @@ def test_cta_pair_gemm_bit_identical(tc, m, n, k, ex, lower):
         ldw = ((k + n + 63) // 64) * 64
         b16 = (torch.rand((R, ldw), device="cuda", generator=g) * 2 - 1).half()
         b32 = torch.rand((R, ldw), device="cuda", generator=g) * 2 - 1
-        tc.gemm_problem_device("tc16", b16, b32, None, ldw, m, n, k, 0, 0, 0 if lower else m, 0, 0, k, ex, lower,
+        tc.gemm_problem_device(cls, b16, b32, None, ldw, m, n, k, 0, 0, 0 if lower else m, 0, 0, k, ex, lower,
                                -1.0, 1.0)
         torch.cuda.synchronize()
         return (b16 if ex == 0 else b32)[:m, k:k + n].clone()

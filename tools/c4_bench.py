@@ -1,6 +1,6 @@
 """development: C4 as the bench runs it, under plan options.
     python tools/c4_bench.py [conc,in_flight[,key=value...]] ..."""
-import json, sys
+import json, os, sys
 sys.path.insert(0, ".")
 from paper_2601_08082_b200.batch import run_batch_on_rank
 for arg in sys.argv[1:] or ["16,32"]:
@@ -8,7 +8,7 @@ for arg in sys.argv[1:] or ["16,32"]:
     conc, fl = int(parts[0]), int(parts[1])
     opts = {kv.split("=")[0]: int(kv.split("=")[1]) for kv in parts[2:] if not kv.startswith("g:")}
     import paper_2601_08082_b200 as tc
-    tc.set_global_option("tc_pair_min_tiles", 512)  # the library default
+    tc.set_global_option("tc_pair_min_tiles", int(os.environ.get("TC_PAIR_MIN", "512")))
     for kv in parts[2:]:
         if kv.startswith("g:"):
             tc.set_global_option(kv[2:].split("=")[0], int(kv.split("=")[1]))
