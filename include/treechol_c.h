@@ -129,6 +129,10 @@ int tc_plan_timeline_host(tc_plan* plan, double* host, int lda, void* stream, fl
  * order; -1 = not run) */
 int tc_plan_trace_host(tc_plan* plan, double* host, int lda, void* stream, float* t_ops, int cap_ops, float* t_h2d,
                        int cap_h2d, float* t_d2h, int cap_d2h);
+/* development: the same for the device entry point's DAG graph: completion
+ * time of every op in ms from the graph's root (-1e9 = not run) */
+int tc_plan_trace_device(tc_plan* plan, const double* dA_in, int lda_in, double* dL_out, int lda_out, void* stream,
+                         float* t_ops, int cap_ops);
 /* op i of the plan: type (0 import, 1 export, 2 check, 3 quant, 4 dequant,
  * 5 shadow, 6 potrf leaf, 7 trsm leaf, 8 gemm), gemm class (0 = tcgen05
  * FP16, 1..5 SIMT classes, -1 otherwise), level, algorithmic flops, rect */

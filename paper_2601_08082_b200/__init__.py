@@ -120,6 +120,7 @@ def _load():
         "tc_plan_status": (I, [P, C.POINTER(_Info)]),
         "tc_plan_op_probs": (I, [P, I, C.POINTER(C.c_int), I]),
         "tc_plan_timeline": (I, [P, P, I, P, I, P, C.POINTER(C.c_float), C.POINTER(C.c_float), I]),
+        "tc_plan_trace_device": (I, [P, P, I, P, I, P, C.POINTER(C.c_float), I]),
         "tc_plan_trace_host": (I, [P, P, I, P, C.POINTER(C.c_float), I, C.POINTER(C.c_float), I,
                                    C.POINTER(C.c_float), I]),
         "tc_plan_timeline_host": (I, [P, P, I, P, C.POINTER(C.c_float), C.POINTER(C.c_float), I,
@@ -581,6 +582,16 @@ class Plan:
                                      _ptr(l_out), _check_dev(l_out, self.rows, "l_out", self.cols),
                                      _stream_ptr(stream), t0, t1, n_ops))
         return list(t0), list(t1)
+
+    def trace(self, a_in, l_out, stream=None):
+        """development: one run of the DAG graph with a timer stamp after
+        every op; per-op completion ms from the graph's root"""
+        n_ops = self.stats()["ops"]
+        out = (C.c_float * n_ops)()
+        _raise(_lib.tc_plan_trace_device(self._h, _ptr(a_in), _check_dev(a_in, self.rows, "a_in", self.cols),
+                                         _ptr(l_out), _check_dev(l_out, self.rows, "l_out", self.cols),
+                                         _stream_ptr(stream), out, n_ops))
+        return list(out)
 
     def profile(self, a_in, l_out, stream=None):
         """serialized eager run; per-op device milliseconds"""

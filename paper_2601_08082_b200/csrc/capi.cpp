@@ -227,6 +227,8 @@ int apply_plan_option(std::unique_ptr<Engine>& eng, const std::string& k, int va
     const bool g = e.use_graph, dg = e.dag_graph, pdl = e.use_pdl;
     const int pmt = e.pair_min_tiles;
     const int s = e.n_streams, bt = e.bulk_tiles_per_cta, bm = e.bulk_max_ctas;
+    const int ct = e.crit_tiles_per_cta, cm = e.crit_max_ctas, pl = e.prio_levels;
+    const bool np = e.node_prio, il = e.import_low;
     eng = std::make_unique<Engine>(std::move(p));
     eng->use_graph = g;
     eng->dag_graph = dg;
@@ -235,6 +237,11 @@ int apply_plan_option(std::unique_ptr<Engine>& eng, const std::string& k, int va
     eng->n_streams = s;
     eng->bulk_tiles_per_cta = bt;
     eng->bulk_max_ctas = bm;
+    eng->crit_tiles_per_cta = ct;
+    eng->crit_max_ctas = cm;
+    eng->prio_levels = pl;
+    eng->node_prio = np;
+    eng->import_low = il;
     return 1;
 }
 }  // namespace tcb
@@ -254,9 +261,18 @@ int tc_plan_set_option(tc_plan* plan, const char* key, int value) {
         e.dag_graph = value != 0;
         return TC_OK;
     }
-    if (k == "bulk_tiles_per_cta" || k == "bulk_max_ctas") {
+    if (k == "bulk_tiles_per_cta" || k == "bulk_max_ctas" || k == "crit_tiles_per_cta" || k == "crit_max_ctas" ||
+        k == "prio_levels" || k == "node_prio" || k == "import_low") {
         if (e.ready() && e.use_graph) return fail(TC_INVALID_ARGUMENT, k + " must be set before the first run");
-        (k == "bulk_tiles_per_cta" ? e.bulk_tiles_per_cta : e.bulk_max_ctas) = value < 0 ? 0 : value;
+        if (k == "node_prio" || k == "import_low") {
+            (k == "node_prio" ? e.node_prio : e.import_low) = value != 0;
+            return TC_OK;
+        }
+        (k == "bulk_tiles_per_cta" ? e.bulk_tiles_per_cta
+         : k == "bulk_max_ctas"    ? e.bulk_max_ctas
+         : k == "crit_tiles_per_cta" ? e.crit_tiles_per_cta
+         : k == "crit_max_ctas"    ? e.crit_max_ctas
+                                   : e.prio_levels) = value < 0 ? 0 : value;
         return TC_OK;
     }
     if (k == "use_pdl") {
@@ -532,6 +548,17 @@ int tc_plan_timeline_host(tc_plan* plan, double* host, int lda, void* stream, fl
     }
     for (int i = 0; i < cap_h2d && i < int(h.size()); ++i) t_h2d[i] = h[i];
     for (int i = 0; i < cap_d2h && i < int(d.size()); ++i) t_d2h[i] = d[i];
+    return TC_OK;
+}
+
+int tc_plan_trace_device(tc_plan* plan, const double* dA_in, int lda_in, double* dL_out, int lda_out, void* stream,
+                         float* t_ops, int cap_ops) {
+    if (!plan || !dA_in || !dL_out || !t_ops) return fail(TC_INVALID_ARGUMENT, "null argument");
+    std::vector<float> a;
+    std::string err;
+    if (!plan->eng->trace_device(dA_in, lda_in, dL_out, lda_out, static_cast<cudaStream_t>(stream), a, &err))
+        return fail(TC_CUDA_ERROR, err);
+    for (int i = 0; i < cap_ops && i < int(a.size()); ++i) t_ops[i] = a[i];
     return TC_OK;
 }
 

@@ -107,9 +107,15 @@ int tc_batch_set_option(tc_batch* bt, const char* key, int value) {
         if (r < 0) return bfail(TC_INVALID_ARGUMENT, err);
         if (r == 1) continue;
         if (k == "bulk_tiles_per_cta") e->bulk_tiles_per_cta = value < 0 ? 0 : value;
+        else if (k == "crit_tiles_per_cta") e->crit_tiles_per_cta = value < 0 ? 0 : value;
+        else if (k == "crit_max_ctas") e->crit_max_ctas = value < 0 ? 0 : value;
+        else if (k == "prio_levels") e->prio_levels = value;
+        else if (k == "node_prio") e->node_prio = value != 0;
+        else if (k == "import_low") e->import_low = value != 0;
         else if (k == "dag_graph") e->dag_graph = value != 0;
         else if (k == "use_pdl") e->use_pdl = value != 0;
         else if (k == "use_graph") e->use_graph = value != 0;
+        else if (k == "dev_skip") e->dev_skip = value;  // development: see Engine::dev_skip
         else return bfail(TC_INVALID_ARGUMENT, "unknown option '" + k + "'");
     }
     return TC_OK;

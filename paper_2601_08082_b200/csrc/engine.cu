@@ -245,10 +245,12 @@ void Engine::launch_op(int i, cudaStream_t s) {
         case OP_GEMM:
             if (L.pair)
                 launch_gemm_tc_pair(ctx_, op.gclass == GC_TC32 ? KIND_TF32X3 : KIND_F16, tab, L.count, L.tiles, s,
-                                    op.bulk ? bulk_tiles_per_cta : 0);
+                                    op.bulk ? bulk_tiles_per_cta : crit_tiles_per_cta,
+                                    op.bulk ? bulk_max_ctas : crit_max_ctas);
             else if (op.gclass == GC_TC16 || op.gclass == GC_TC32)
                 launch_gemm_tc(ctx_, op.gclass == GC_TC32 ? KIND_TF32X3 : KIND_F16, tab, L.count, L.tiles, s,
-                               op.bulk ? bulk_max_ctas : 0, op.bulk ? bulk_tiles_per_cta : 0);
+                               op.bulk ? bulk_max_ctas : crit_max_ctas,
+                               op.bulk ? bulk_tiles_per_cta : crit_tiles_per_cta);
             else launch_gemm_simt(ctx_, op.gclass, reinterpret_cast<DevProb*>(tab), L.count, L.tiles, s);
             break;
     }
@@ -453,7 +455,7 @@ bool Engine::enqueue(const double* a_in, long long lda_in, double* l_out, long l
     if (use_graph) {
         if (!gexec_ && dag_graph) {
             if (!build_dag_graph(&graph_, -1, err)) return false;
-            TC_TRY(cudaGraphInstantiate(&gexec_, graph_, 0));
+            TC_TRY(cudaGraphInstantiate(&gexec_, graph_, inst_flags()));
         }
         if (!gexec_) {
             cudaStream_t cap;
@@ -495,8 +497,12 @@ bool Engine::build_dag_graph(cudaGraph_t* out, int phase, std::string* err) {
     TC_TRY(cudaGraphCreate(&g, 0));
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    cudaStream_t cap_hi = nullptr, cap_lo = nullptr;
-    TC_TRY(cudaStreamCreateWithPriority(&cap_hi, cudaStreamNonBlocking, hi));
+    // prio_levels 3: the leaf chain above the critical GEMMs (numerically
+    // lower = greater priority)
+    const int mid = prio_levels >= 3 && hi < lo ? hi + 1 : hi;
+    cudaStream_t cap_top = nullptr, cap_hi = nullptr, cap_lo = nullptr;
+    TC_TRY(cudaStreamCreateWithPriority(&cap_top, cudaStreamNonBlocking, hi));
+    TC_TRY(cudaStreamCreateWithPriority(&cap_hi, cudaStreamNonBlocking, mid));
     TC_TRY(cudaStreamCreateWithPriority(&cap_lo, cudaStreamNonBlocking, lo));
     bool ok = true;
     std::string e2;
@@ -517,7 +523,7 @@ bool Engine::build_dag_graph(cudaGraph_t* out, int phase, std::string* err) {
         // the scheduling priority of the capture stream, made explicit on
         // every kernel node: the chain's CTAs go first when SMs free up
         cudaKernelNodeAttrValue pv{};
-        pv.priority = s == cap_hi ? hi : lo;
+        pv.priority = s == cap_top ? hi : s == cap_hi ? mid : lo;
         size_t nn = 0;
         cudaGraphGetNodes(child, nullptr, &nn);
         std::vector<cudaGraphNode_t> kids(nn);
@@ -560,7 +566,9 @@ bool Engine::build_dag_graph(cudaGraph_t* out, int phase, std::string* err) {
         if (!d_trace_ || !ok || !after) return;
         cudaGraphNode_t sn = nullptr;
         unsigned long long* slot = d_trace_ + k;
-        ok = add(cap_lo, {after}, [&](cudaStream_t s) { launch_stamp(slot, s); }, &sn);
+        // greatest priority: a stamp queued behind bulk CTAs would report
+        // their dispatch, not the op's end (one thread, co-resides anywhere)
+        ok = add(cap_top, {after}, [&](cudaStream_t s) { launch_stamp(slot, s); }, &sn);
     };
     stamp(root, 0);
     std::vector<cudaGraphNode_t> node(size_t(N), nullptr);
@@ -583,12 +591,15 @@ bool Engine::build_dag_graph(cudaGraph_t* out, int phase, std::string* err) {
             pdl.push_back(0);
         }
         bool kn = false;
-        ok = add(op.bulk ? cap_lo : cap_hi, deps, [&](cudaStream_t s) { launch_op(i, s); }, &node[size_t(i)], &pdl,
+        const bool chain = prio_levels >= 3 && !op.bulk && !(op.type == OP_GEMM && op.gclass == GC_TC16);
+        const bool low = op.bulk || (import_low && op.type == OP_IMPORT);
+        ok = add(low ? cap_lo : chain ? cap_top : cap_hi, deps, [&](cudaStream_t s) { launch_op(i, s); }, &node[size_t(i)], &pdl,
                  &kn);
         is_kernel[size_t(i)] = kn;
     }
     if (d_trace_)
         for (int i = 0; i < N; ++i) stamp(node[size_t(i)], 1 + i);
+    cudaStreamDestroy(cap_top);
     cudaStreamDestroy(cap_hi);
     cudaStreamDestroy(cap_lo);
     if (!ok) {
@@ -739,7 +750,7 @@ bool Engine::build_host_phases(std::string* err) {
         cudaGraph_t g = nullptr;
         if (!build_dag_graph(&g, p, err)) return false;
         cudaGraphExec_t x = nullptr;
-        const cudaError_t e = cudaGraphInstantiate(&x, g, 0);
+        const cudaError_t e = cudaGraphInstantiate(&x, g, inst_flags());
         cudaGraphDestroy(g);
         TC_TRY(e);
         hph_exec_.push_back(x);
@@ -1010,6 +1021,42 @@ bool Engine::timeline_host(double* host, long long lda, cudaStream_t stream, std
     rd(ed, td2h);
     cudaEventDestroy(origin_ev);
     cudaFreeHost(flag);
+    return true;
+}
+
+bool Engine::trace_device(const double* a_in, long long lda_in, double* l_out, long long lda_out,
+                          cudaStream_t stream, std::vector<float>& top, std::string* err) {
+    if (!prepare(err)) return false;
+    if (!use_graph || !dag_graph) {
+        if (err) *err = "trace_device needs the DAG graph (use_graph, dag_graph)";
+        return false;
+    }
+    const int N = int(plan.ops.size());
+    const size_t slots = 1 + size_t(N);
+    TC_TRY(cudaMalloc(&d_trace_, slots * sizeof(unsigned long long)));
+    TC_TRY(cudaMemset(d_trace_, 0, slots * sizeof(unsigned long long)));
+    auto drop = [&] {
+        if (gexec_) cudaGraphExecDestroy(gexec_);
+        if (graph_) cudaGraphDestroy(graph_);
+        gexec_ = nullptr;
+        graph_ = nullptr;
+    };
+    drop();  // rebuild with stamp nodes
+    const bool ok = enqueue(a_in, lda_in, l_out, lda_out, stream, err);
+    std::vector<unsigned long long> h(slots, 0);
+    const bool ok2 = ok && cudaStreamSynchronize(stream) == cudaSuccess &&
+                     cudaMemcpy(h.data(), d_trace_, slots * sizeof(unsigned long long), cudaMemcpyDeviceToHost) ==
+                         cudaSuccess;
+    drop();
+    cudaFree(d_trace_);
+    d_trace_ = nullptr;
+    if (!ok2) {
+        if (err && err->empty()) *err = "trace run failed";
+        return false;
+    }
+    top.assign(size_t(N), 0.f);
+    for (int i = 0; i < N; ++i)
+        top[size_t(i)] = h[size_t(1 + i)] ? float(double((long long)(h[size_t(1 + i)] - h[0])) * 1e-6) : -1e9f;
     return true;
 }
 

@@ -59,6 +59,18 @@ class Engine {
     bool pdl_src_ok(int i) const;
     int bulk_tiles_per_cta = 1;  // trailing-update GEMMs: 0 persistent, else tiles per CTA (1: SMs free up after every tile, so concurrent work -- other systems of a batch, the factorization chain -- gets them)
     int bulk_max_ctas = 0;       // persistent trailing-update GEMMs: CTA cap (0 = one per SM)
+    int crit_tiles_per_cta = 0;  // the other (critical) tensor-core GEMMs: 0 persistent, else tiles per CTA
+    int crit_max_ctas = 0;       // persistent critical GEMMs: CTA cap (0 = one per SM)
+    // DAG-graph scheduling priorities: 2 = {chain + critical GEMMs, bulk};
+    // 3 = {leaf chain, critical FP16 GEMMs, bulk}: the chain's small kernels
+    // are dispatched before the queued CTAs of a big critical GEMM
+    int prio_levels = 2;
+    // DAG graphs instantiated with cudaGraphInstantiateFlagUseNodePriority:
+    // without it a graph launch ignores the per-node priorities above and
+    // runs every kernel at the launching stream's priority
+    bool node_prio = false;
+    bool import_low = false;  // imports at the bulk (lowest) priority
+    unsigned long long inst_flags() const { return node_prio ? cudaGraphInstantiateFlagUseNodePriority : 0; }
     bool dag_graph = true;       // explicit DAG graph (else: captured multi-stream enqueue)
 
     // enqueue one factorization (import .. export) on `stream`
@@ -169,6 +181,10 @@ class Engine {
     // global-timer stamp after the root, every op and every H2D / D2H copy
     // chunk: completion times (ms from the root) -- ops in op order, H2D
     // chunks in issue order, D2H chunks in issue order
+    // development: one run of the device-path DAG graph with a global-timer
+    // stamp after every op; completion times in ms from the root
+    bool trace_device(const double* a_in, long long lda_in, double* l_out, long long lda_out, cudaStream_t stream,
+                      std::vector<float>& top, std::string* err);
     bool trace_host(double* host, long long lda, cudaStream_t stream, std::vector<float>& top,
                     std::vector<float>& th2d, std::vector<float>& td2h, std::string* err);
 };

@@ -1428,11 +1428,13 @@ void launch_gemm_tc(const DevCtx& c, int kind, const void* d_probs, int nprob, i
 // CTA-pair launch (k_gemm_tc2): problem table built with pair = 1; persistent
 // pairs (one per two SMs, or fewer when there are fewer tiles)
 void launch_gemm_tc_pair(const DevCtx& c, int kind, const void* d_probs, int nprob, int tiles, cudaStream_t s,
-                         int tiles_per_pair) {
+                         int tiles_per_pair, int max_ctas) {
     if (tiles <= 0) return;
-    // persistent (tiles_per_pair = 0) or a bounded number of tiles per pair,
-    // so SMs free up between tiles for concurrent work (the chain)
+    // persistent (tiles_per_pair = 0; at most max_ctas / 2 pairs when
+    // max_ctas > 0, leaving SMs to the chain) or a bounded number of tiles
+    // per pair, so SMs free up between tiles for concurrent work
     int pairs = tiles_per_pair > 0 ? (tiles + tiles_per_pair - 1) / tiles_per_pair : g_sms / 2;
+    if (tiles_per_pair == 0 && max_ctas > 1 && pairs > max_ctas / 2) pairs = max_ctas / 2;
     if (pairs > tiles) pairs = tiles;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(2 * pairs, 1, 1);

@@ -92,7 +92,7 @@ int tc_build_probs(const DevCtx& c, int kind, const std::vector<DevProb>& probs,
 // built with tc_build_probs(..., pair = 1)
 int tc_pair_min_tiles();
 void launch_gemm_tc_pair(const DevCtx& c, int kind, const void* d_probs, int nprob, int tiles, cudaStream_t s,
-                         int tiles_per_pair = 0);
+                         int tiles_per_pair = 0, int max_ctas = 0);
 void launch_gemm_tc(const DevCtx& c, int kind, const void* d_probs, int nprob, int tiles, cudaStream_t s,
                     int max_ctas = 0, int tiles_per_cta = 0);
 bool tc_supported();
