@@ -75,18 +75,9 @@ extern "C" int tc_debug_gemm(int gclass, int m, int n, int k, int lower, double 
     int tiles = 0;
     const bool tc = gclass == GC_TC16 || gclass == GC_TC32;
     std::string err;
-    int pair = 0;
+    int pair = 0, kind = KIND_F16;
     if (tc) {
-        tiles = tc_build_probs(c, gclass == GC_TC32 ? KIND_TF32X3 : KIND_F16, v, host, &err);
-        if (tc_pair_min_tiles() > 0 && tiles >= tc_pair_min_tiles()) {
-            std::vector<unsigned char> h2;
-            const int t2 = tc_build_probs(c, gclass == GC_TC32 ? KIND_TF32X3 : KIND_F16, v, h2, nullptr, 1);
-            if (t2 > 0) {
-                host.swap(h2);
-                tiles = t2;
-                pair = 1;
-            }
-        }
+        tiles = tc_select_tables(c, gclass == GC_TC32, v, host, &err, tc_pair_min_tiles(), -1, &kind, &pair);
     } else {
         tiles = gclass == GC_MMA32W ? simt_tiles(v, M32W_ROWS, 256) : simt_tiles(v, gclass == GC_MMA32 ? M32_TILE : 0);
         host.assign(reinterpret_cast<unsigned char*>(v.data()), reinterpret_cast<unsigned char*>(v.data() + 1));
@@ -98,8 +89,8 @@ extern "C" int tc_debug_gemm(int gclass, int m, int n, int k, int lower, double 
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     auto launch = [&] {
-        if (pair) launch_gemm_tc_pair(c, gclass == GC_TC32 ? KIND_TF32X3 : KIND_F16, dprob, 1, tiles, nullptr);
-        else if (tc) launch_gemm_tc(c, gclass == GC_TC32 ? KIND_TF32X3 : KIND_F16, dprob, 1, tiles, nullptr);
+        if (pair) launch_gemm_tc_pair(c, kind, dprob, 1, tiles, nullptr);
+        else if (tc) launch_gemm_tc(c, kind, dprob, 1, tiles, nullptr);
         else launch_gemm_simt(c, gclass, static_cast<DevProb*>(dprob), 1, tiles, nullptr);
     };
     launch();  // warm
@@ -111,8 +102,8 @@ extern "C" int tc_debug_gemm(int gclass, int m, int n, int k, int lower, double 
     cudaGraphExec_t ge = nullptr;
     cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
     for (int i = 0; i < iters; ++i) {
-        if (pair) launch_gemm_tc_pair(c, gclass == GC_TC32 ? KIND_TF32X3 : KIND_F16, dprob, 1, tiles, cs);
-        else if (tc) launch_gemm_tc(c, gclass == GC_TC32 ? KIND_TF32X3 : KIND_F16, dprob, 1, tiles, cs);
+        if (pair) launch_gemm_tc_pair(c, kind, dprob, 1, tiles, cs);
+        else if (tc) launch_gemm_tc(c, kind, dprob, 1, tiles, cs);
         else launch_gemm_simt(c, gclass, static_cast<DevProb*>(dprob), 1, tiles, cs);
     }
     cudaStreamEndCapture(cs, &g);
@@ -187,22 +178,13 @@ extern "C" int tc_gemm_problem_device(int gclass, void* b16, void* b32, void* b6
     int tiles = 0;
     const bool tc = gclass == GC_TC16 || gclass == GC_TC32;
     std::string err;
-    int pair = 0;
+    int pair = 0, kind = KIND_F16;
     if (tc) {
-        tiles = tc_build_probs(c, gclass == GC_TC32 ? KIND_TF32X3 : KIND_F16, v, host, &err);
+        tiles = tc_select_tables(c, gclass == GC_TC32, v, host, &err, tc_pair_min_tiles(), -1, &kind, &pair);
         if (tiles <= 0) {
             cudaFreeAsync(words, s);
             set_last_error("tc_build_probs: " + err);
             return TC_INVALID_ARGUMENT;
-        }
-        if (tc_pair_min_tiles() > 0 && tiles >= tc_pair_min_tiles()) {
-            std::vector<unsigned char> h2;
-            const int t2 = tc_build_probs(c, gclass == GC_TC32 ? KIND_TF32X3 : KIND_F16, v, h2, nullptr, 1);
-            if (t2 > 0) {
-                host.swap(h2);
-                tiles = t2;
-                pair = 1;
-            }
         }
     } else {
         tiles = gclass == GC_MMA32W ? simt_tiles(v, M32W_ROWS, 256) : simt_tiles(v, gclass == GC_MMA32 ? M32_TILE : 0);
@@ -211,8 +193,8 @@ extern "C" int tc_gemm_problem_device(int gclass, void* b16, void* b32, void* b6
     void* dprob = nullptr;
     if (cudaMallocAsync(&dprob, host.size(), s) != cudaSuccess) return TC_CUDA_ERROR;
     cudaMemcpyAsync(dprob, host.data(), host.size(), cudaMemcpyHostToDevice, s);
-    if (pair) launch_gemm_tc_pair(c, gclass == GC_TC32 ? KIND_TF32X3 : KIND_F16, dprob, 1, tiles, s);
-    else if (tc) launch_gemm_tc(c, gclass == GC_TC32 ? KIND_TF32X3 : KIND_F16, dprob, 1, tiles, s);
+    if (pair) launch_gemm_tc_pair(c, kind, dprob, 1, tiles, s);
+    else if (tc) launch_gemm_tc(c, kind, dprob, 1, tiles, s);
     else launch_gemm_simt(c, gclass, static_cast<DevProb*>(dprob), 1, tiles, s);
     cudaFreeAsync(dprob, s);
     cudaFreeAsync(words, s);

@@ -174,19 +174,10 @@ bool Engine::prepare(std::string* err) {
             L.count = int(dp.size());
             if (op.gclass == GC_TC16 || op.gclass == GC_TC32) {
                 std::vector<unsigned char> tp;
-                L.tiles = tc_build_probs(ctx_, op.gclass == GC_TC32 ? KIND_TF32X3 : KIND_F16, dp, tp, err);
-                if (L.tiles < 0) return false;
                 const int pmin = pair_min_tiles >= 0 ? pair_min_tiles : tc_pair_min_tiles();
-                if (pmin > 0 && L.tiles >= pmin) {
-                    // a large list: 256x256 tiles on CTA pairs
-                    std::vector<unsigned char> tp2;
-                    const int t2 = tc_build_probs(ctx_, op.gclass == GC_TC32 ? KIND_TF32X3 : KIND_F16, dp, tp2, nullptr, 1);
-                    if (t2 > 0) {
-                        tp.swap(tp2);
-                        L.tiles = t2;
-                        L.pair = 1;
-                    }
-                }
+                L.tiles = tc_select_tables(ctx_, op.gclass == GC_TC32, dp, tp, err, pmin, narrow_max_tiles, &L.kind,
+                                           &L.pair);
+                if (L.tiles < 0) return false;
                 L.offset = append(tp.data(), tp.size());
             } else {
                 L.tiles = op.gclass == GC_MMA32W ? simt_tiles(dp, M32W_ROWS, 256)
@@ -244,12 +235,11 @@ void Engine::launch_op(int i, cudaStream_t s) {
             break;
         case OP_GEMM:
             if (L.pair)
-                launch_gemm_tc_pair(ctx_, op.gclass == GC_TC32 ? KIND_TF32X3 : KIND_F16, tab, L.count, L.tiles, s,
+                launch_gemm_tc_pair(ctx_, L.kind, tab, L.count, L.tiles, s,
                                     op.bulk ? bulk_tiles_per_cta : crit_tiles_per_cta,
                                     op.bulk ? bulk_max_ctas : crit_max_ctas);
             else if (op.gclass == GC_TC16 || op.gclass == GC_TC32)
-                launch_gemm_tc(ctx_, op.gclass == GC_TC32 ? KIND_TF32X3 : KIND_F16, tab, L.count, L.tiles, s,
-                               op.bulk ? bulk_max_ctas : crit_max_ctas,
+                launch_gemm_tc(ctx_, L.kind, tab, L.count, L.tiles, s, op.bulk ? bulk_max_ctas : crit_max_ctas,
                                op.bulk ? bulk_tiles_per_cta : crit_tiles_per_cta);
             else launch_gemm_simt(ctx_, op.gclass, reinterpret_cast<DevProb*>(tab), L.count, L.tiles, s);
             break;

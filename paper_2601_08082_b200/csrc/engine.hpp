@@ -22,6 +22,7 @@ struct OpLaunch {
     int tiles = 0;
     int count = 0;
     int pair = 0;       // tcgen05 FP16 kind on CTA pairs (k_gemm_tc2)
+    int kind = 0;       // tcgen05 kind (KIND_*)
     size_t offset = 0;  // into the table arena
 };
 
@@ -55,6 +56,9 @@ class Engine {
     // CTA-pair GEMM threshold for this engine (-1: the process-wide
     // tc_pair_min_tiles; 0: never)
     int pair_min_tiles = -1;
+    // narrow (128x128) FP16 tiles below this many 128x256 tiles (-1: the
+    // process-wide tc_narrow_max_tiles)
+    int narrow_max_tiles = -1;
     bool use_pdl = false;  // measured no faster (N=16384 12.62 -> 12.80 ms, C4 425 -> 420 TF/s): off
     bool pdl_src_ok(int i) const;
     int bulk_tiles_per_cta = 1;  // trailing-update GEMMs: 0 persistent, else tiles per CTA (1: SMs free up after every tile, so concurrent work -- other systems of a batch, the factorization chain -- gets them)

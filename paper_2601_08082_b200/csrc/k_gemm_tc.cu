@@ -103,6 +103,13 @@ template <> struct Cfg<KIND_F16> {
                          STG_BOXES = TC_F16_STG;
     static constexpr uint32_t FMT = 0;
 };
+// the FP16 kind on 128x128 tiles: twice the CTAs of a 128x256 tiling for the
+// skinny TRSM updates (m x 256 x 512 and the like), whose 64-128 tiles leave
+// most SMs idle; same K order per element as KIND_F16 (bit-identical)
+template <> struct Cfg<KIND_F16N> {
+    static constexpr int BN = 128, ESZ = 2, BK = 64, STAGES = 6, NTHREADS = 320, PASSES = 1, STG_BOXES = 2;
+    static constexpr uint32_t FMT = 0;
+};
 template <> struct Cfg<KIND_TF32X3> {
     static constexpr int BN = 128, ESZ = 4, BK = 32, STAGES = 3, NTHREADS = 448, PASSES = 3, STG_BOXES = 2;
     static constexpr uint32_t FMT = 2;
@@ -185,7 +192,7 @@ __device__ __forceinline__ uint64_t sdesc(const void* p) {
 
 template <int KIND>
 __device__ __forceinline__ void mma_issue(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accum) {
-    if constexpr (KIND == KIND_F16)
+    if constexpr (KIND != KIND_TF32X3)
         asm volatile(
             "{\n"
             ".reg .pred p;\n"
@@ -1304,7 +1311,7 @@ int tc_build_probs(const DevCtx& c, int kind, const std::vector<DevProb>& probs,
     out.assign(probs.size() * sizeof(TcProb), 0);
     TcProb* tp = reinterpret_cast<TcProb*>(out.data());
     const bool f32 = kind == KIND_TF32X3;
-    const int BN = f32 ? Cfg<KIND_TF32X3>::BN : Cfg<KIND_F16>::BN;
+    const int BN = f32 ? Cfg<KIND_TF32X3>::BN : kind == KIND_F16N ? Cfg<KIND_F16N>::BN : Cfg<KIND_F16>::BN;
     const void* obuf = f32 ? static_cast<const void*>(c.b32) : static_cast<const void*>(c.b16);
     int tiles = 0;
     for (size_t i = 0; i < probs.size(); ++i) {
@@ -1380,6 +1387,46 @@ int tc_build_probs(const DevCtx& c, int kind, const std::vector<DevProb>& probs,
 // waves the pair's 256x256 tiles leave SMs idle (8192x1024x1024: 22 -> 26 us)
 static int g_tc_pair_min_tiles = 512;
 int tc_pair_min_tiles() { return g_tc_pair_min_tiles; }
+static int g_tc_narrow_max_tiles = 0;
+int tc_narrow_max_tiles() { return g_tc_narrow_max_tiles; }
+
+int tc_select_tables(const DevCtx& c, bool tf32, const std::vector<DevProb>& probs, std::vector<unsigned char>& out,
+                     std::string* err, int pair_min, int narrow_max, int* kind, int* pair) {
+    *kind = tf32 ? KIND_TF32X3 : KIND_F16;
+    *pair = 0;
+    int tiles = tc_build_probs(c, *kind, probs, out, err);
+    if (tiles < 0) return tiles;
+    if (pair_min > 0 && tiles >= pair_min) {
+        std::vector<unsigned char> t2;
+        const int n2 = tc_build_probs(c, *kind, probs, t2, nullptr, 1);
+        if (n2 > 0) {
+            out.swap(t2);
+            *pair = 1;
+            return n2;
+        }
+    }
+    // narrow tiles pay off for short K (latency-bound launches: 2048..8192 x
+    // 256 x 512 12.8 -> 9.2 us); at K >= 2048 or >= 128 wide tiles they lose
+    // (4096 x 2048 x 2048 37 -> 52 us: A is read twice per output column)
+    const int nmax = narrow_max >= 0 ? narrow_max : g_tc_narrow_max_tiles;
+    // never for in-place inverse solves (a_kwrap: C overwrites A, so one tile
+    // must cover every column of its rows)
+    int kmax = 0;
+    bool inplace = false;
+    for (const DevProb& d : probs) {
+        kmax = d.k > kmax ? d.k : kmax;
+        inplace |= d.a_kwrap != 0;
+    }
+    if (!tf32 && nmax > 0 && tiles < nmax && kmax <= 1024 && !inplace) {
+        std::vector<unsigned char> t2;
+        const int n2 = tc_build_probs(c, KIND_F16N, probs, t2, err);
+        if (n2 < 0) return n2;
+        out.swap(t2);
+        *kind = KIND_F16N;
+        return n2;
+    }
+    return tiles;
+}
 
 static int g_sms = 148;
 
@@ -1390,6 +1437,10 @@ bool tc_set_option(const std::string& key, int value) {
     }
     if (key == "tc_pair_min_tiles") {
         g_tc_pair_min_tiles = value < 0 ? 0 : value;
+        return true;
+    }
+    if (key == "tc_narrow_max_tiles") {
+        g_tc_narrow_max_tiles = value < 0 ? 0 : value;
         return true;
     }
     return false;
@@ -1403,6 +1454,8 @@ void init_tc_attributes() {
     cudaFuncSetAttribute(k_gemm_tc2<KIND_TF32X3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          PairGeo<KIND_TF32X3>::SMEM_BYTES);
     cudaFuncSetAttribute(k_gemm_tc<KIND_F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo<KIND_F16>::SMEM_BYTES);
+    cudaFuncSetAttribute(k_gemm_tc<KIND_F16N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Geo<KIND_F16N>::SMEM_BYTES);
     cudaFuncSetAttribute(k_gemm_tc<KIND_TF32X3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          Geo<KIND_TF32X3>::SMEM_BYTES);
 }
@@ -1421,6 +1474,8 @@ void launch_gemm_tc(const DevCtx& c, int kind, const void* d_probs, int nprob, i
     if (kind == KIND_TF32X3)
         k_gemm_tc<KIND_TF32X3><<<grid, Cfg<KIND_TF32X3>::NTHREADS, Geo<KIND_TF32X3>::SMEM_BYTES, s>>>(c, p, nprob,
                                                                                                     tiles);
+    else if (kind == KIND_F16N)
+        k_gemm_tc<KIND_F16N><<<grid, Cfg<KIND_F16N>::NTHREADS, Geo<KIND_F16N>::SMEM_BYTES, s>>>(c, p, nprob, tiles);
     else
         k_gemm_tc<KIND_F16><<<grid, Cfg<KIND_F16>::NTHREADS, Geo<KIND_F16>::SMEM_BYTES, s>>>(c, p, nprob, tiles);
 }

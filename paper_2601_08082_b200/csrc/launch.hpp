@@ -84,13 +84,23 @@ struct TcProb;  // defined in k_gemm_tc.cu (holds TMA descriptors)
 size_t tc_prob_size();
 // fills host-side TcProb records (tensor maps over the F16 buffer)
 // operand kinds of the tensor-core GEMM (k_gemm_tc.cu)
-enum { KIND_F16 = 0, KIND_TF32X3 = 1 };
+// tcgen05 GEMM kinds: FP16 (128x256 tiles), three-pass TF32 (128x128),
+// FP16 on 128x128 tiles (lists too small to fill the SMs with 128x256 ones)
+enum { KIND_F16 = 0, KIND_TF32X3 = 1, KIND_F16N = 2 };
 int tc_build_probs(const DevCtx& c, int kind, const std::vector<DevProb>& probs, std::vector<unsigned char>& out,
                    std::string* err,
                    int pair = 0);
 // FP16 kind on CTA pairs (tcgen05 cta_group::2, 256x256 tiles); the table
 // built with tc_build_probs(..., pair = 1)
 int tc_pair_min_tiles();
+// FP16 lists of fewer 128x256 tiles than this run on 128x128 tiles (0 = never)
+int tc_narrow_max_tiles();
+// the kernel variant and table for one problem list (tf32: the three-pass
+// kind): CTA pairs at >= pair_min tiles (0 = never), the narrow FP16 kind
+// below narrow_max tiles (-1: the process-wide tc_narrow_max_tiles); returns
+// the tile count (< 0: error) and sets *kind, *pair
+int tc_select_tables(const DevCtx& c, bool tf32, const std::vector<DevProb>& probs, std::vector<unsigned char>& out,
+                     std::string* err, int pair_min, int narrow_max, int* kind, int* pair);
 void launch_gemm_tc_pair(const DevCtx& c, int kind, const void* d_probs, int nprob, int tiles, cudaStream_t s,
                          int tiles_per_pair = 0, int max_ctas = 0);
 void launch_gemm_tc(const DevCtx& c, int kind, const void* d_probs, int nprob, int tiles, cudaStream_t s,

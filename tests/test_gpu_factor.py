@@ -451,3 +451,19 @@ def test_fused_leaf_inverse_matches_oracle(tc, oracle):
     rel = tc.factorization_error_device(tc.to_device(a), tc.to_device(l))
     torch.cuda.synchronize()
     assert rel <= 2 * rel_o + FLOOR, (rel, rel_o)
+
+
+def test_narrow_fp16_tiles_keep_the_factor_bit_identical(tc, oracle):
+    """with the narrow FP16 kind enabled for every eligible list, L is
+    bit-identical to the default plan's (in-place inverse solves stay on
+    full-width tiles: a 128-column tile would overwrite A columns another
+    tile still reads)"""
+    a = oracle.spd_generate(2048, 21)
+    st0, l0, _ = _run_opts(tc, a, 128, "[F16, F16, F16, F32]", {})
+    tc.set_global_option("tc_narrow_max_tiles", 1 << 20)
+    try:
+        st1, l1, _ = _run_opts(tc, a, 128, "[F16, F16, F16, F32]", {})
+    finally:
+        tc.set_global_option("tc_narrow_max_tiles", 0)
+    assert st0.status == st1.status == "ok"
+    assert np.array_equal(np.tril(l0).view(np.uint64), np.tril(l1).view(np.uint64))

@@ -187,3 +187,31 @@ def test_cta_pair_gemm_bit_identical(tc, cls, m, n, k, ex, lower):
         tc.set_global_option("tc_pair_min_tiles", 512)
     assert torch.equal(single.view(torch.int16) if ex == 0 else single.view(torch.int32),
                        pair.view(torch.int16) if ex == 0 else pair.view(torch.int32))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,n,k,ex,lower", [(512, 512, 512, 0, 0), (1024, 768, 1024, 1, 0), (300, 200, 333, 0, 0),
+                                            (512, 512, 1024, 1, 1), (8192, 256, 512, 1, 0), (1000, 136, 200, 0, 0)])
+def test_narrow_fp16_gemm_bit_identical(tc, m, n, k, ex, lower):
+    """KIND_F16N (the FP16 kind on 128x128 tiles, option tc_narrow_max_tiles)
+    gives the 128x256 kernel's results bit for bit"""
+    import torch
+
+    def run(narrow):
+        tc.set_global_option("tc_narrow_max_tiles", 1 << 30 if narrow else 0)
+        g = torch.Generator(device="cuda").manual_seed(m + n + k)
+        ldw = ((k + n + 63) // 64) * 64
+        b16 = (torch.rand((m + n, ldw), device="cuda", generator=g) * 2 - 1).half()
+        b32 = torch.rand((m + n, ldw), device="cuda", generator=g) * 2 - 1
+        tc.gemm_problem_device("tc16", b16, b32, None, ldw, m, n, k, 0, 0, 0 if lower else m, 0, 0, k, ex, lower,
+                               -1.0, 1.0)
+        torch.cuda.synchronize()
+        return (b16 if ex == 0 else b32)[:m, k:k + n].clone()
+
+    try:
+        wide = run(False)
+        narrow = run(True)
+    finally:
+        tc.set_global_option("tc_narrow_max_tiles", 0)
+    assert torch.equal(wide.view(torch.int16) if ex == 0 else wide.view(torch.int32),
+                       narrow.view(torch.int16) if ex == 0 else narrow.view(torch.int32))
