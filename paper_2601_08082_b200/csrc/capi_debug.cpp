@@ -209,7 +209,7 @@ extern "C" int tc_gemm_problem_device(int gclass, void* b16, void* b32, void* b6
 // process-wide kernel settings (development / A-B measurements)
 extern "C" int tc_set_global_option(const char* key, int value) {
     if (!key) return TC_INVALID_ARGUMENT;
-    if (tc_set_option(key, value) || potrs_set_option(key, value)) return TC_OK;
+    if (tc_set_option(key, value) || potrs_set_option(key, value) || elem_set_option(key, value)) return TC_OK;
     set_last_error(std::string("unknown global option '") + key + "'");
     return TC_INVALID_ARGUMENT;
 }

@@ -439,7 +439,19 @@ int make_block_table(const std::vector<BlockDescHost>& in, std::vector<BlockDesc
     return tiles;
 }
 
-static int tile_grid(int tiles) { return tiles < 148 * 8 ? tiles : 148 * 8; }
+// grid of the tiled copy kernels: grid-stride over at most 8 CTAs per SM
+// (default), or a fixed number of tiles per CTA (option elem_tiles_per_cta),
+// so their CTAs turn over and higher-priority work gets SMs between tiles
+static int g_elem_tiles_per_cta = 0;
+bool elem_set_option(const std::string& key, int value) {
+    if (key != "elem_tiles_per_cta") return false;
+    g_elem_tiles_per_cta = value < 0 ? 0 : value;
+    return true;
+}
+static int tile_grid(int tiles) {
+    if (g_elem_tiles_per_cta > 0) return (tiles + g_elem_tiles_per_cta - 1) / g_elem_tiles_per_cta;
+    return tiles < 148 * 8 ? tiles : 148 * 8;
+}
 void launch_import(const DevCtx& c, const BlockDesc* d_blocks, int nb, int tiles, cudaStream_t s) {
     if (tiles > 0) k_import<<<tile_grid(tiles), 256, 0, s>>>(c, d_blocks, nb, tiles);
 }

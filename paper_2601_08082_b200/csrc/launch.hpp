@@ -93,6 +93,8 @@ int tc_build_probs(const DevCtx& c, int kind, const std::vector<DevProb>& probs,
 // FP16 kind on CTA pairs (tcgen05 cta_group::2, 256x256 tiles); the table
 // built with tc_build_probs(..., pair = 1)
 int tc_pair_min_tiles();
+// process-wide copy-kernel setting ("elem_tiles_per_cta"); false: unknown key
+bool elem_set_option(const std::string& key, int value);
 // FP16 lists of fewer 128x256 tiles than this run on 128x128 tiles (0 = never)
 int tc_narrow_max_tiles();
 // the kernel variant and table for one problem list (tf32: the three-pass

@@ -20,7 +20,10 @@ ap.add_argument("--json", default="")
 args = ap.parse_args()
 plan = tc.Plan(args.n, 256, "[F16, F16, F16, F32]")
 for kv in args.opt:
-    plan.set_option(kv.split("=")[0], int(kv.split("=")[1]))
+    if kv.startswith("g:"):  # process-wide kernel option
+        tc.set_global_option(kv[2:].split("=")[0], int(kv.split("=")[1]))
+    else:
+        plan.set_option(kv.split("=")[0], int(kv.split("=")[1]))
 a = tc.spd_generate_device(args.n, 42)
 l = torch.empty_like(a)
 plan.factor_device(a, l)
