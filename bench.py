@@ -251,7 +251,7 @@ def run_ours(args):
     # slower of its flops at the tensor peak and its algorithmic bytes (A, B
     # read once, C written -- and read when beta != 0) at the HBM peak; the
     # small-K trailing updates are HBM-bound on their C traffic
-    t_bound, n_hbm = 0.0, 0
+    t_bound, n_hbm, alg_bytes = 0.0, 0, 0.0
     by_type = {}
     for i, t in enumerate(op_ms):
         info = plan.op_info(i)
@@ -269,6 +269,7 @@ def run_ours(args):
                 celems = pr["m"] * pr["n"] / (2.0 if pr["lower"] else 1.0)
                 nbytes += 2.0 * pr["m"] * (pr["a_kwrap"] or pr["k"]) + 2.0 * pr["n"] * pr["k"]
                 nbytes += celems * (2.0 if pr["exec_level"] == 0 else 4.0) * (1 + beta)
+            alg_bytes += nbytes
             tb_t = info["flops"] / (peaks["bf16_tflops"] * 1e12) * 1e3
             tb_h = nbytes / (peaks["hbm_gbs"] * 1e9) * 1e3
             t_bound += max(tb_t, tb_h)
@@ -281,12 +282,16 @@ def run_ours(args):
     if os.path.exists(tpath):
         with open(tpath) as f:
             traffic = json.load(f).get("dram_bytes_per_launch")
-    roofline = {"bound": "tensor", "kernel": "k_gemm_tc (tcgen05 kind::f16, FP32 accumulate)",
+    roofline = {"bound": "tensor",
+                "kernel": "k_gemm_tc / k_gemm_tc2 (tcgen05 kind::f16, FP32 accumulate; CTA pairs for >= 512 tiles)",
                 "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
                 "frac": achieved / peaks["bf16_tflops"], "traffic": traffic, "traffic_unit": "bytes/launch (ncu)",
                 "peak_kind": f"{peak_kind} bf16 burst (MEASURED_PEAKS.json)",
                 "share_of_step": tc_ms / tot_ms if tot_ms else None,
                 "launches": by_type.get("gemm/tc16", [0, 0, 0])[2],
+                # A, B read once, C written (and read when beta != 0): what the
+                # ncu `traffic` figure is compared against
+                "algorithmic_bytes_per_launch": alg_bytes / max(1, by_type.get("gemm/tc16", [0, 0, 0])[2]),
                 "per_launch_bound": {"frac": t_bound / tc_ms if tc_ms else None, "hbm_bound_launches": n_hbm,
                                      "note": "sum over launches of max(flops / tensor peak, algorithmic bytes / "
                                              "HBM peak) / sum of measured launch times"}}
