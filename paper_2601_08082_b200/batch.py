@@ -91,8 +91,11 @@ def run_batch_on_rank(count: int, n: int, b: int, config, seed0: int = 0, nrhs: 
     batch = tc.Batch(n, b, config, True, concurrency)
     for k, v in (options or {}).items():
         batch.set_option(k, v)
-    # warm-up (untimed): builds every plan's workspace and CUDA graph
+    # warm-up (untimed): builds every plan's workspace and CUDA graph, and
+    # sizes the per-call buffers (status words, POTRS workspace and pointer
+    # tables) for in_flight systems, so no allocation lands in a timed call
     warm = [synthetic_spd_device(n, seed0 + 10 ** 6 + k) for k in range(concurrency)]
+    warm += [warm[k % concurrency].clone() for k in range(concurrency, min(in_flight, len(mine)))]
     wb = [a.sum(dim=0, keepdim=True).repeat(nrhs, 1).contiguous() for a in warm]
     batch.run(warm, wb)  # the solve path too (its workspace, first kernel loads)
     del warm, wb
