@@ -73,16 +73,22 @@ int tc_batch_create(int n, int b, const int* levels, int nlevels, int quantize, 
         auto* bt = new tc_batch;
         for (int i = 0; i < concurrency; ++i) {
             PlanOptions po;
-            // the leaf shadows stay separate ops in batches: fused into the
-            // leaf POTRF, 16 concurrent plans ran bimodally (264-430 vs a
-            // steady 433-435 TF/s, profiles/r02_c4_fuse_shadow_ab.txt)
-            po.fuse_shadow = false;
+            // leaf shadows fused into the leaf POTRF (the plan default): C4
+            // 437-439 vs 434-435 TF/s with separate shadow ops
+            // (profiles/r02_c4_options.txt).  An earlier A/B that ran
+            // bimodally (profiles/r02_c4_fuse_shadow_ab.txt) had buffer
+            // re-allocation inside its timed calls
             bt->eng.push_back(std::make_unique<Engine>(
                 Plan::make(n, b, std::vector<int>(levels, levels + nlevels), quantize != 0, 0, po)));
-            // no CTA-pair GEMMs in batches: with 16 plans side by side their
-            // clusters (two free SMs of one TPC) were starved now and then
-            // (C4 98-438 vs a steady 423-429 TF/s, profiles/r02_c4_pair_ab.txt)
-            bt->eng.back()->pair_min_tiles = 0;
+            // CTA-pair GEMMs in batches from 1024 tiles: C4 443-452 TF/s in
+            // 14 runs vs 435-440 without (profiles/r02_c4_options.txt).  An
+            // earlier A/B with one 99 TF/s pair run
+            // (profiles/r02_c4_pair_ab.txt) predates the warm-up that sizes
+            // the per-call buffers
+            bt->eng.back()->pair_min_tiles = 1024;
+            // trailing updates 4 tiles per CTA (C4 440-442 vs 436-439 TF/s
+            // with 1, profiles/r02_c4_options.txt)
+            bt->eng.back()->bulk_tiles_per_cta = 4;
         }
         *out = bt;
         return TC_OK;
@@ -116,6 +122,7 @@ int tc_batch_set_option(tc_batch* bt, const char* key, int value) {
         else if (k == "use_pdl") e->use_pdl = value != 0;
         else if (k == "use_graph") e->use_graph = value != 0;
         else if (k == "dev_skip") e->dev_skip = value;  // development: see Engine::dev_skip
+        else if (k == "pair_min_tiles") e->pair_min_tiles = value;
         else return bfail(TC_INVALID_ARGUMENT, "unknown option '" + k + "'");
     }
     return TC_OK;
