@@ -586,6 +586,18 @@ bool Engine::build_dag_graph(cudaGraph_t* out, int phase, std::string* err) {
         ok = add(low ? cap_lo : chain ? cap_top : cap_hi, deps, [&](cudaStream_t s) { launch_op(i, s); }, &node[size_t(i)], &pdl,
                  &kn);
         is_kernel[size_t(i)] = kn;
+        // host phases: an event after each export, which the copy pipeline
+        // polls to start that block's D2H
+        if (ok && phase >= 0 && op.type == OP_EXPORT && size_t(i) < ev_ex_.size() && ev_ex_[size_t(i)]) {
+            cudaGraphNode_t en = nullptr;
+            ok = cudaGraphAddEventRecordNode(&en, g, &node[size_t(i)], 1, ev_ex_[size_t(i)]) == cudaSuccess;
+        }
+        // host phases: an event after each export, which the copy pipeline
+        // polls to start that block's D2H
+        if (ok && phase >= 0 && op.type == OP_EXPORT && size_t(i) < ev_ex_.size() && ev_ex_[size_t(i)]) {
+            cudaGraphNode_t en = nullptr;
+            ok = cudaGraphAddEventRecordNode(&en, g, &node[size_t(i)], 1, ev_ex_[size_t(i)]) == cudaSuccess;
+        }
     }
     if (d_trace_)
         for (int i = 0; i < N; ++i) stamp(node[size_t(i)], 1 + i);
@@ -722,19 +734,27 @@ bool Engine::build_host_phases(std::string* err) {
     ph_need_.assign(size_t(P), -1);
     for (int p = 0; p < P; ++p)
         if (ph_wait_[size_t(p)] >= 0) ph_need_[size_t(p)] = last_chunk[size_t(ph_wait_[size_t(p)])];
-    std::vector<std::pair<int, Rect>> dl;
+    struct DC {
+        int phase, op;
+        Rect r;
+    };
+    std::vector<DC> dl;
+    ev_ex_.assign(size_t(N), nullptr);
     for (int i = 0; i < N; ++i)
         if (plan.ops[size_t(i)].type == OP_EXPORT) {
             std::vector<Rect> rs;
             chunk_rect(plan.ops[size_t(i)].rect, rs);
-            for (const Rect& r : rs) dl.push_back({ph_op_[size_t(i)], r});
+            for (const Rect& r : rs) dl.push_back({ph_op_[size_t(i)], i, r});
+            if (export_events) TC_TRY(cudaEventCreateWithFlags(&ev_ex_[size_t(i)], cudaEventDisableTiming));
         }
-    std::stable_sort(dl.begin(), dl.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+    std::stable_sort(dl.begin(), dl.end(), [](const DC& x, const DC& y) { return x.phase < y.phase; });
     dc_rect_.clear();
     dc_phase_.clear();
+    dc_op_.clear();
     for (auto& x : dl) {
-        dc_phase_.push_back(x.first);
-        dc_rect_.push_back(x.second);
+        dc_phase_.push_back(x.phase);
+        dc_op_.push_back(x.op);
+        dc_rect_.push_back(x.r);
     }
     for (int p = 0; p < P; ++p) {
         cudaGraph_t g = nullptr;
@@ -754,8 +774,11 @@ bool Engine::build_host_phases(std::string* err) {
 void Engine::drop_host_phases() {
     for (auto x : hph_exec_) cudaGraphExecDestroy(x);
     for (auto e : ev_ph_) cudaEventDestroy(e);
+    for (auto e : ev_ex_)
+        if (e) cudaEventDestroy(e);
     hph_exec_.clear();
     ev_ph_.clear();
+    ev_ex_.clear();
 }
 
 
@@ -825,7 +848,16 @@ bool Engine::run_host_pipeline(const HostIO& io, cudaStream_t stream, std::strin
             moved = true;
         }
         while (d_done < d_iss && done(ev_dc_[size_t(d_done)], &ok)) ++d_done, moved = true;
-        while (ok && d_iss < D && d_iss - d_done < kDepth && p_done > dc_phase_[size_t(d_iss)]) {
+        // a D2H chunk goes once its phase has finished, or (export_events)
+        // once its phase is running and its export op's event has fired
+        auto d2h_ready = [&](int d) {
+            const int ph = dc_phase_[size_t(d)];
+            if (p_done > ph) return true;
+            if (p_iss <= ph || ev_ex_.empty()) return false;
+            const cudaEvent_t e = ev_ex_[size_t(dc_op_[size_t(d)])];
+            return e != nullptr && done(e, &ok);
+        };
+        while (ok && d_iss < D && d_iss - d_done < kDepth && d2h_ready(d_iss)) {
             const Rect& r = dc_rect_[size_t(d_iss)];
             TC_TRY(cudaMemcpy2DAsync(io.host + size_t(r.c0) * io.lda + r.r0, esz * io.lda,
                                      d_stage_ + size_t(r.c0) * n + r.r0, esz * n, esz * size_t(r.m), size_t(r.n),

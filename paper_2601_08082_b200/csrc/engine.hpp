@@ -74,6 +74,12 @@ class Engine {
     // runs every kernel at the launching stream's priority
     bool node_prio = false;
     bool import_low = false;  // imports at the bulk (lowest) priority
+    // host path: an exported block's D2H starts when its export op has run
+    // (an event-record node after it in the phase graph), not when its
+    // whole phase has finished.  Measured neutral at C3 (0.533-0.536 s both
+    // ways, profiles/r02_e2e_export_events.txt): the D2H tail is the L21
+    // panel, which cannot be solved before all of A21 has landed
+    bool export_events = false;
     unsigned long long inst_flags() const { return node_prio ? cudaGraphInstantiateFlagUseNodePriority : 0; }
     bool dag_graph = true;       // explicit DAG graph (else: captured multi-stream enqueue)
 
@@ -145,6 +151,8 @@ class Engine {
     bool run_host_pipeline(const HostIO& io, cudaStream_t stream, std::string* err);
     std::vector<Rect> hc_rect_, dc_rect_;      // H2D chunks (block order), D2H chunks (by phase)
     std::vector<int> dc_phase_, ph_need_;      // phase of each D2H chunk; last H2D chunk a phase reads
+    std::vector<int> dc_op_;                   // export op of each D2H chunk
+    std::vector<cudaEvent_t> ev_ex_;           // per op: event recorded in its phase graph after an export
     std::vector<cudaEvent_t> ev_hc_, ev_dc_;   // per chunk: copy done
     unsigned long long* d_trace_ = nullptr;  // trace_host: stamp slots (null: no stamp nodes)
     cudaGraph_t hgraph_ = nullptr;
