@@ -399,7 +399,7 @@ def run_ours(args):
                            "ranks_per_gpu": (ws + ndev - 1) // ndev,
                            "n": n, "b": b, "precision_tree": CFG,
                            "parallelism": f"independent systems x{ws}" if ws > 1 else "single",
-                           "l2": "inputs (34 GB) larger than L2; no flush needed"},
+                           "l2": f"inputs ({n * n * 8 / 1e9:.1f} GB) larger than the 126 MB L2; no flush needed"},
                 "status": st.status, "rel_error": rel, "digits": -math.log10(rel) if rel > 0 else None,
                 "clocks": clk.summary(), "gpu_launches": stats["launches"] * args.steps,
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "c4": c4, "c5": c5, "variants": variants,
