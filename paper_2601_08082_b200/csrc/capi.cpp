@@ -228,7 +228,8 @@ int apply_plan_option(std::unique_ptr<Engine>& eng, const std::string& k, int va
     const int pmt = e.pair_min_tiles;
     const int s = e.n_streams, bt = e.bulk_tiles_per_cta, bm = e.bulk_max_ctas;
     const int ct = e.crit_tiles_per_cta, cm = e.crit_max_ctas, pl = e.prio_levels;
-    const bool np = e.node_prio, il = e.import_low, ee = e.export_events;
+    const bool np = e.node_prio, il = e.import_low, ee = e.export_events, so = e.startup_order;
+    const int ic = e.import_chain;
     eng = std::make_unique<Engine>(std::move(p));
     eng->use_graph = g;
     eng->dag_graph = dg;
@@ -243,6 +244,8 @@ int apply_plan_option(std::unique_ptr<Engine>& eng, const std::string& k, int va
     eng->node_prio = np;
     eng->import_low = il;
     eng->export_events = ee;
+    eng->startup_order = so;
+    eng->import_chain = ic;
     return 1;
 }
 }  // namespace tcb
@@ -263,10 +266,14 @@ int tc_plan_set_option(tc_plan* plan, const char* key, int value) {
         return TC_OK;
     }
     if (k == "bulk_tiles_per_cta" || k == "bulk_max_ctas" || k == "crit_tiles_per_cta" || k == "crit_max_ctas" ||
-        k == "prio_levels" || k == "node_prio" || k == "import_low" || k == "export_events") {
+        k == "prio_levels" || k == "node_prio" || k == "import_low" || k == "export_events" ||
+        k == "startup_order") {
         if (e.ready() && e.use_graph) return fail(TC_INVALID_ARGUMENT, k + " must be set before the first run");
-        if (k == "node_prio" || k == "import_low" || k == "export_events") {
-            (k == "node_prio" ? e.node_prio : k == "import_low" ? e.import_low : e.export_events) = value != 0;
+        if (k == "node_prio" || k == "import_low" || k == "export_events" || k == "startup_order") {
+            (k == "node_prio"       ? e.node_prio
+             : k == "import_low"    ? e.import_low
+             : k == "export_events" ? e.export_events
+                                    : e.startup_order) = value != 0;
             return TC_OK;
         }
         (k == "bulk_tiles_per_cta" ? e.bulk_tiles_per_cta
@@ -274,6 +281,11 @@ int tc_plan_set_option(tc_plan* plan, const char* key, int value) {
          : k == "crit_tiles_per_cta" ? e.crit_tiles_per_cta
          : k == "crit_max_ctas"    ? e.crit_max_ctas
                                    : e.prio_levels) = value < 0 ? 0 : value;
+        return TC_OK;
+    }
+    if (k == "import_chain") {
+        if (e.ready() && e.use_graph) return fail(TC_INVALID_ARGUMENT, k + " must be set before the first run");
+        e.import_chain = value < 0 ? 0 : value;
         return TC_OK;
     }
     if (k == "use_pdl") {

@@ -118,6 +118,8 @@ int tc_batch_set_option(tc_batch* bt, const char* key, int value) {
         else if (k == "prio_levels") e->prio_levels = value;
         else if (k == "node_prio") e->node_prio = value != 0;
         else if (k == "import_low") e->import_low = value != 0;
+        else if (k == "startup_order") e->startup_order = value != 0;
+        else if (k == "import_chain") e->import_chain = value < 0 ? 0 : value;
         else if (k == "dag_graph") e->dag_graph = value != 0;
         else if (k == "use_pdl") e->use_pdl = value != 0;
         else if (k == "use_graph") e->use_graph = value != 0;

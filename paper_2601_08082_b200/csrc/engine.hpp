@@ -80,6 +80,8 @@ class Engine {
     // ways, profiles/r02_e2e_export_events.txt): the D2H tail is the L21
     // panel, which cannot be solved before all of A21 has landed
     bool export_events = false;
+    bool startup_order = false;  // see build_dag_graph
+    int import_chain = 0;        // device graph: at most this many imports in flight (0 = all at once)
     unsigned long long inst_flags() const { return node_prio ? cudaGraphInstantiateFlagUseNodePriority : 0; }
     bool dag_graph = true;       // explicit DAG graph (else: captured multi-stream enqueue)
 
